@@ -1,0 +1,179 @@
+"""Pins for oracle steps O5/O6 (Toeplitz product, CG) and the whole of Algorithm a1 (O8): dense
+Phi^*Phi, LAPACK solves, the weight/function-space equivalence (Lemma l:equiv), the exact-GP error
+bounds and the special cases the paper and SPEC state."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from efgp_data import CONFIGS
+
+
+def _small_problem(d=2, N=400, m=5, h=0.6, seed=0):
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(0, 1, (N, d))
+    D = O.spectral_weights("matern", 0.1, d, h, m, 1.5)
+    return rng, x, D
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_toeplitz_apply_equals_dense_FstarF(d):
+    # T beta = F^*F beta with F_{n,p} = exp(+2 pi i h j_p.x_n) built explicitly (eq 223).
+    # Pins the sign convention (G1) and the index/extraction convention of Alg a:FF.
+    m = {1: 7, 2: 4, 3: 2}[d]
+    rng, x, _ = _small_problem(d=d, N=300, m=m)
+    h = 0.6
+    v = O.toeplitz_vector(x, h, m)
+    F = O.design_matrix(x, h, m, np.ones((2 * m + 1,) * d))
+    beta = rng.normal(size=(2 * m + 1,) * d) + 1j * rng.normal(size=(2 * m + 1,) * d)
+    ref = (F.conj().T @ (F @ beta.reshape(-1))).reshape(beta.shape)
+    np.testing.assert_allclose(O.toeplitz_apply(v, beta), ref, rtol=1e-12, atol=1e-10)
+    T = O.toeplitz_matrix(v, m)
+    np.testing.assert_allclose(O.toeplitz_apply(v, beta, T), ref, rtol=1e-12, atol=1e-10)
+
+
+def test_toeplitz_column_and_structure():
+    rng, x, _ = _small_problem()
+    h, m = 0.6, 5
+    v = O.toeplitz_vector(x, h, m)
+    e0 = np.zeros((11, 11), complex)
+    e0[m, m] = 1
+    np.testing.assert_allclose(O.toeplitz_apply(v, e0), v[m:3 * m + 1, m:3 * m + 1], atol=0)
+    a = rng.normal(size=(11, 11)) + 1j * rng.normal(size=(11, 11))
+    b = rng.normal(size=(11, 11)) + 1j * rng.normal(size=(11, 11))
+    Ta, Tb = O.toeplitz_apply(v, a), O.toeplitz_apply(v, b)
+    assert np.vdot(Ta, b) == pytest.approx(np.vdot(a, Tb), rel=1e-12)                   # Hermitian
+    assert np.vdot(a, Ta).real >= -1e-10 * 400 * np.vdot(a, a).real                      # PSD
+    np.testing.assert_array_equal(O.toeplitz_apply(np.zeros_like(v), a), 0)             # N = 0
+
+
+def test_system_apply_equals_dense_weight_space_matrix():
+    rng, x, D = _small_problem()
+    h, m = 0.6, 5
+    v = O.toeplitz_vector(x, h, m)
+    Phi = O.design_matrix(x, h, m, D)
+    beta = rng.normal(size=(11, 11)) + 1j * rng.normal(size=(11, 11))
+    ref = Phi.conj().T @ (Phi @ beta.reshape(-1)) + 0.01 * beta.reshape(-1)
+    np.testing.assert_allclose(O.system_apply(v, D, 0.01, beta).reshape(-1), ref, rtol=1e-12, atol=1e-10)
+    # D = 0 degenerate kernel -> sigma^2 beta
+    np.testing.assert_allclose(O.system_apply(v, 0 * D, 0.3, beta), 0.3 * beta)
+
+
+def test_cg_matches_lapack_solve():
+    rng, x, D = _small_problem(N=500)
+    h, m, sigma = 0.6, 5, 0.2
+    y = rng.normal(size=500)
+    v = O.toeplitz_vector(x, h, m)
+    b = O.rhs(x, y, h, m, D)
+    beta, iters, hist = O.cg(lambda p: O.system_apply(v, D, sigma ** 2, p), b, 1e-13, 2000)
+    Phi = O.design_matrix(x, h, m, D)
+    A = Phi.conj().T @ Phi + sigma ** 2 * np.eye(Phi.shape[1])
+    ref = np.linalg.solve(A, Phi.conj().T @ y)
+    np.testing.assert_allclose(beta.reshape(-1), ref, rtol=1e-9, atol=1e-9 * np.abs(ref).max())
+    assert hist[iters] <= 1e-13 and all(hh > 1e-13 for hh in hist[:iters])   # first crossing
+    assert len(hist) == iters + 1
+
+
+def test_cg_zero_rhs_and_cap():
+    rng, x, D = _small_problem()
+    v = O.toeplitz_vector(x, 0.6, 5)
+    beta, iters, hist = O.cg(lambda p: O.system_apply(v, D, 0.01, p), np.zeros((11, 11), complex), 1e-8, 50)
+    assert iters == 0 and np.all(beta == 0)                                    # y = 0 -> beta = 0
+    b = O.rhs(x, rng.normal(size=len(x)), 0.6, 5, D)
+    _, iters, hist = O.cg(lambda p: O.system_apply(v, D, 0.01, p), b, 1e-30, 7)
+    assert iters == 7 and len(hist) == 8
+
+
+@pytest.mark.parametrize("kernel,nu,ell,sigma,d", [("se", 0.0, 0.1, 0.3, 1), ("matern", 1.5, 0.1, 0.1, 2),
+                                                    ("matern", 0.5, 0.2, 0.1, 3)])
+def test_lemma_equiv_weight_space_equals_function_space_k_tilde(kernel, nu, ell, sigma, d):
+    # Lemma l:equiv with Prop a2b/magic: EFGP's mu equals the dense
+    # function-space GP mean with the approximate kernel k~ = Phi Phi^* (eq 110).  Exact identity;
+    # the primary whole-pipeline pin.
+    rng = np.random.default_rng(1)
+    N = {1: 600, 2: 500, 3: 300}[d]
+    x = rng.uniform(0, 1, (N, d))
+    y = np.sin(6 * x[:, 0]) + sigma * rng.normal(size=N)
+    xt = rng.uniform(0, 1, (50, d))
+    eps = {1: 1e-4, 2: 1e-3, 3: 1e-2}[d]
+    fit = O.efgp_fit(x, y, kernel, ell, sigma, eps, nu=nu, cg_tol=1e-14, max_iter=20000,
+                     m=None if d < 3 else 4, h=None if d < 3 else 0.5)
+    mu = O.efgp_predict(fit, xt)
+    kt = lambda a, b: O.kernel_tilde_matrix(a, b, fit.h, fit.m, fit.D)
+    mu_fs, alpha = O.dense_gp_mean(x, y, xt, kt, sigma)
+    np.testing.assert_allclose(mu, mu_fs, rtol=1e-9, atol=1e-9 * np.abs(mu_fs).max())
+    Phi = O.design_matrix(x, fit.h, fit.m, fit.D)
+    np.testing.assert_allclose(fit.beta.reshape(-1), Phi.conj().T @ alpha, atol=1e-8 * np.abs(fit.beta).max())  # a2b
+    np.testing.assert_allclose(alpha, (y - (Phi @ fit.beta.reshape(-1)).real) / sigma ** 2,
+                               atol=1e-7 * np.abs(alpha).max())                                   # magic
+
+
+def test_se_efgp_matches_exact_gp_within_eps():
+    # For SE the (h, m) rule is rigorous; tight-CG EFGP vs the exact (true-kernel) GP is within a
+    # small multiple of eps (SURVEY P7 / A.8 measured 0.2 eps on c1).  Gate: 10 eps.
+    c = CONFIGS["c1"]
+    rng = np.random.default_rng(2)
+    x = rng.uniform(0, 1, (1500, 1))
+    y = np.sin(6 * math.pi * x[:, 0]) + np.cos(2 * math.pi * x[:, 0]) ** 2 + 0.1 * rng.normal(size=1500)
+    xt = np.linspace(0, 1, 200)[:, None]
+    fit = O.efgp_fit(x, y, "se", c.ell, c.sigma, c.eps, cg_tol=1e-13, max_iter=50000)
+    mu = O.efgp_predict(fit, xt)
+    kfun = lambda a, b: O.kernel_value("se", np.abs(a[:, None, 0] - b[None, :, 0]), c.ell)
+    mu_ex, _ = O.dense_gp_mean(x, y, xt, kfun, c.sigma)
+    assert np.linalg.norm(mu - mu_ex) / np.linalg.norm(mu_ex) <= 10 * c.eps
+
+
+def test_matern_stability_theorem_374():
+    # Theorem t:muerr (i), eq 374: ||mu~ - mu|| / ||y|| <= ||K~ - K||_2 / sigma^2 at the
+    # data points; Prop p:Kerr eq Kerr: ||K~-K|| <= ||K~-K||_F.
+    c = CONFIGS["c5"]
+    rng = np.random.default_rng(11)
+    N = 800
+    x = rng.uniform(0, 1, (N, 2))
+    y = np.sin(6 * math.pi * x[:, 0]) * np.cos(4 * math.pi * x[:, 1]) + 0.1 * rng.normal(size=N)
+    fit = O.efgp_fit(x, y, c.kernel, c.ell, c.sigma, c.eps, nu=c.nu, cg_tol=1e-12, max_iter=50000)
+    mu_t = O.efgp_predict(fit, x)
+    K = O.kernel_value("matern", np.linalg.norm(x[:, None] - x[None], axis=-1), c.ell, c.nu)
+    mu, _ = O.dense_gp_mean(x, y, x, lambda a, b: K, c.sigma)
+    Kt = O.kernel_tilde_matrix(x, x, fit.h, fit.m, fit.D)
+    lhs = np.linalg.norm(mu_t - mu) / np.linalg.norm(y)
+    spec = np.linalg.norm(Kt - K, 2)
+    assert lhs <= spec / c.sigma ** 2
+    assert spec <= np.linalg.norm(Kt - K) + 1e-12
+
+
+def test_single_point_special_case():
+    # N=1, x=0.5, y=1, sigma=1, SE l=0.1, eps=1e-10 -> mu(0.5) = k~(0)/(k~(0)+1) ~ 0.5
+    fit = O.efgp_fit(np.array([[0.5]]), np.array([1.0]), "se", 0.1, 1.0, 1e-10, cg_tol=1e-14)
+    mu = O.efgp_predict(fit, np.array([[0.5]]))[0]
+    k0 = float(np.sum(fit.D ** 2))                 # k~(0) = sum_j h k^(h j)
+    assert mu == pytest.approx(k0 / (k0 + 1.0), rel=1e-12)
+    assert mu == pytest.approx(0.5, abs=1e-8)
+
+
+def test_zero_data_gives_zero_weights():
+    x = np.random.default_rng(0).uniform(0, 1, (100, 2))
+    fit = O.efgp_fit(x, np.zeros(100), "matern", 0.1, 0.1, 1e-3, nu=1.5)
+    assert fit.iters == 0 and np.all(fit.beta == 0)
+
+
+def test_condition_number_bound_and_fig3_point():
+    # Prop p:cond eq 361: kappa(K + sigma^2 I) <= N/sigma^2 + 1; Fig. fig:cond1:
+    # SE l=0.1, sigma=0.3, uniform points in [0,1], N=1e4 -> log10 kappa_WS = 4.43.
+    rng = np.random.default_rng(0)
+    N, sigma = 10_000, 0.3
+    x = rng.uniform(0, 1, (N, 1))
+    h, m = O.choose_params_se(0.1, 1, 1e-10)
+    D = O.spectral_weights("se", 0.1, 1, h, m)
+    v = O.toeplitz_vector(x, h, m)
+    A = D.reshape(-1)[:, None] * O.toeplitz_matrix(v, m) * D.reshape(-1)[None, :] + sigma ** 2 * np.eye(2 * m + 1)
+    ev = np.linalg.eigvalsh(A)
+    kappa = ev[-1] / ev[0]
+    assert kappa <= N / sigma ** 2 + 1
+    assert math.log10(kappa) == pytest.approx(4.43, abs=0.05)
+
+
+def test_default_max_iter_formula():
+    # k <= log(1/eps) sqrt(N) / (2 sigma)
+    assert O.default_max_iter(10_000, 0.1, 1e-6) == math.ceil(math.log(1e6) * 100 / 0.2)
