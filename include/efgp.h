@@ -1,0 +1,143 @@
+/*
+ * efgp.h — C ABI of the B200 (sm_100a) EFGP hot path.
+ *
+ * Equispaced-Fourier GP regression (Greengard, Rachh, Barnett et al., arXiv 2210.10210), Algorithm
+ * "a1": type-1 NUFFTs build the Toeplitz generating vector v (eq "88",
+ * P:816-818) and the right-hand side Phi^* y = D F^* y (eq "rhs"); conjugate gradients
+ * solve (D F^*F D + sigma^2 I) beta = Phi^* y (eqs "be"/"97") with the padded-FFT
+ * Toeplitz product of Algorithm "a:FF"; a type-2 NUFFT evaluates the posterior mean
+ * mu(x*) = sum_j D_j beta_j exp(2 pi i h j.x*) (eq "muws"; steps 5-6).
+ *
+ * Sign convention (reading G1): v_j = sum_n exp(-2 pi i h j.x_n),
+ * (F^* y)_j = sum_n exp(-2 pi i h j.x_n) y_n, mu(x) = Re sum_j D_j beta_j exp(+2 pi i h j.x).
+ *
+ * Conventions for every entry point:
+ *  - Points are (N, d) row-major fp64 (x_n in [0,1]^d), observations N fp64.
+ *  - Pointers may be device memory (cudaMalloc / torch CUDA tensors) or host memory; the library
+ *    detects which with cudaPointerGetAttributes.  Host inputs are streamed to the device in
+ *    chunks inside the call (pinned memory gives overlapped copies).  The caller owns all of them;
+ *    the library keeps no pointer after a call returns.
+ *  - All device work is enqueued on options.stream (NULL = legacy default stream).  efgp_fit and
+ *    efgp_predict return after their work is complete (they synchronise that stream).
+ *  - The handle owns every internal buffer and the cuFFT plans.  A handle is not thread-safe.
+ *  - Errors are reported by the status code; efgp_last_error() gives a message.  After an
+ *    EFGP_ERR_CUDA the handle should be destroyed.
+ *  - There is no CPU fallback: every step of the path runs in this library's sm_100a kernels and
+ *    cuFFT; if no CUDA device is present, efgp_setup returns EFGP_ERR_CUDA.
+ */
+#ifndef EFGP_H
+#define EFGP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EFGP_ABI_VERSION 1
+
+typedef struct efgp_plan *efgp_handle;
+
+typedef enum { EFGP_SE = 0, EFGP_MATERN = 1 } efgp_kernel;
+
+typedef enum {
+  EFGP_OK = 0,
+  EFGP_ERR_NOCONVERGE = 1, /* CG hit max_iter; beta and the residual history stay readable */
+  EFGP_ERR_INVALID = 2,    /* bad argument or input data                                 */
+  EFGP_ERR_RESOURCE = 3,   /* a grid or buffer does not fit in device memory                       */
+  EFGP_ERR_CUDA = 4,       /* CUDA runtime / cuFFT failure                                          */
+  EFGP_ERR_NCCL = 5        /* reserved for the collective path                                      */
+} efgp_status;
+
+/* Matérn eps rescaling (§7.1; reading G3). */
+typedef enum { EFGP_RESCALE_NONE = 0, EFGP_RESCALE_L2 = 1, EFGP_RESCALE_PRINTED = 2 } efgp_rescale;
+
+/* Spreading strategy for the type-1 step. AUTO picks the fastest valid one. */
+typedef enum { EFGP_SPREAD_AUTO = 0, EFGP_SPREAD_GLOBAL = 1, EFGP_SPREAD_SMEM = 2, EFGP_SPREAD_SORTED = 3 } efgp_spread_method;
+
+typedef struct {
+  double h;            /* grid spacing override when m > 0                        */
+  int64_t m;           /* modes per dimension override (2m+1 per dim), 0 = rule (Alg a1 step 1) */
+  double cg_tol;       /* CG relative-residual stop, 0 = eps                      */
+  int64_t max_iter;    /* CG cap, 0 = ceil(log(1/tol) sqrt(N)/(2 sigma))           */
+  double nufft_tol;    /* NUFFT tolerance, 0 = eps/10                                   */
+  int matern_rescale;  /* efgp_rescale, default EFGP_RESCALE_L2                                  */
+  int spread_method;   /* efgp_spread_method                                                     */
+  int graph_iters;     /* CG iterations per CUDA-graph launch, 0 = default                        */
+  void *stream;        /* cudaStream_t for all device work (NULL = default stream)               */
+} efgp_options;
+
+typedef struct {
+  double h;             /* frequency grid spacing                                 */
+  int64_t m, M, d;      /* half-width, number of modes (2m+1)^d, dimension          */
+  int64_t N;            /* number of points of the last fit (sum over shards)      */
+  int64_t iters;        /* CG iterations of the last fit                            */
+  double rel_resid;     /* last recursive relative residual ||r||/||b||            */
+  double cg_tol;        /* tolerance used                                           */
+  int64_t max_iter;     /* cap used                                                 */
+  int64_t nf1, nf2, L;  /* type-1 v-grid, rhs/type-2 grid and Toeplitz box sizes per dim */
+  int64_t w;            /* ES kernel width (cells per dimension)                   */
+  double beta_es;       /* ES kernel shape parameter                               */
+  double nufft_tol;
+  int spread_method;    /* method actually used by the last fit                   */
+  double t_spread_ms, t_modes_ms, t_solve_ms, t_predict_ms; /* device time of the last calls */
+} efgp_info;
+
+/* Fill *opt with defaults (all zero / automatic). */
+void efgp_default_options(efgp_options *opt);
+
+/* Step 1 of Alg a1: choose (h, m) (Cor c:SEparams P:1113-1124 for SE; Remark r:heur eqs mheur/hheur
+ * P:1305-1337 with the §7.1 rescaling for Matérn), tabulate D_j = sqrt(h^d k^(h|j|)) (eq 117,
+ * P:783-794), size the NUFFT grids and the Toeplitz box, build the cuFFT plans and allocate device
+ * buffers.  nu is used only for EFGP_MATERN (nu >= 1/2).  Returns EFGP_ERR_INVALID for sigma <= 0,
+ * ell <= 0, eps outside [1e-14, 1e-1], d not in {1,2,3}, nu < 1/2; EFGP_ERR_RESOURCE if buffers do
+ * not fit; EFGP_ERR_CUDA if there is no usable device.  opt may be NULL. */
+efgp_status efgp_setup(efgp_handle *out, efgp_kernel kernel, double nu, double ell, double sigma,
+                       double eps, int d, const efgp_options *opt);
+
+/* Steps 2-4 of Alg a1 on one process: type-1 spreading of the N points, FFT + deconvolution to v
+ * and F^*y, Toeplitz precompute, CG.  x: (N, d), y: (N).  Returns EFGP_ERR_INVALID if N < 1 or any
+ * coordinate is outside [0,1] or non-finite, or any y is non-finite; EFGP_ERR_NOCONVERGE if CG hits
+ * max_iter (beta is still usable). */
+efgp_status efgp_fit(efgp_handle, const double *x, const double *y, int64_t N);
+
+/* Multi-process split of efgp_fit.  efgp_fit_local spreads this rank's
+ * shard and writes its partial modes (the Hermitian halves of v and F^*y, efgp_modes_count doubles)
+ * to modes_out (device pointer).  The caller sums modes_out over ranks (one allreduce) and calls
+ * efgp_fit_solve with the summed buffer and the global N.  Linearity of the type-1 sums in the
+ * points (eqs 88, rhs) makes the sum of partial modes equal the modes of the union of shards. */
+int64_t efgp_modes_count(efgp_handle);
+efgp_status efgp_fit_local(efgp_handle, const double *x, const double *y, int64_t N, double *modes_out);
+efgp_status efgp_fit_solve(efgp_handle, const double *modes, int64_t N_total);
+
+/* Steps 5-6 of Alg a1: mu at q targets xt (q, d) written to mu_out (q).  EFGP_ERR_INVALID before a
+ * successful fit/load or for targets outside [0,1]^d (their mu is set to NaN). q = 0 is a no-op. */
+efgp_status efgp_predict(efgp_handle, const double *xt, int64_t q, double *mu_out);
+
+/* Model state (SPEC S:369 serialisation).  beta is the Hermitian-half weight vector: for j in J_m
+ * with j_d >= 0, row-major over (j_1+m, ..., j_{d-1}+m, j_d), interleaved (re, im) doubles;
+ * efgp_weights_count() doubles.  Pointers may be host or device. */
+int64_t efgp_weights_count(efgp_handle);
+efgp_status efgp_get_weights(efgp_handle, double *beta_out);
+efgp_status efgp_load_weights(efgp_handle, const double *beta_in);
+
+/* Intermediate vectors of the last fit, Hermitian halves as interleaved complex doubles:
+ * which = 0: v over J_{2m} (j_d in [0,2m]; (4m+1)^{d-1} (2m+1) complex);
+ * which = 1: the right-hand side Phi^* y = D F^* y over J_m half (weights layout);
+ * which = 2: beta (same as efgp_get_weights).  Returns the number of doubles written, or -1. */
+int64_t efgp_copy_vector(efgp_handle, int which, double *out, int64_t cap_doubles);
+
+efgp_status efgp_get_info(efgp_handle, efgp_info *out);
+
+/* Recursive relative residuals ||r_k||/||b||, k = 0..iters of the last fit, into host_out (cap
+ * entries); *n receives the number available. */
+efgp_status efgp_get_residual_history(efgp_handle, double *host_out, int64_t cap, int64_t *n);
+
+const char *efgp_last_error(efgp_handle);
+void efgp_destroy(efgp_handle);
+int efgp_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EFGP_H */

@@ -1,0 +1,332 @@
+// K4-K7 + F2: conjugate gradients on (D F^*F D + sigma^2 I) beta = D F^*y (eq "be", P:570;
+// Alg a1 step 4; stop at relative residual cg_tol), with the Toeplitz
+// product of Alg a:FF done by real transforms:
+//
+//   A p = D . extract_{J_m}( R2C( C2R(pad_L(D . p)) * vhat ) ) + sigma^2 p,   vhat = C2R(v)/L^d (real)
+//
+// Vectors live on the Hermitian half j_d >= 0 (Mh entries); Hermitian inner products become
+// sum_q w_q Re(conj(a_q) b_q) with w_q = 2 for j_d > 0 and 1 for j_d = 0.
+// One iteration = C2R, k_mul, R2C, k_cg_apply, k_cg_xr, k_cg_p; a CUDA graph captures
+// graph_iters iterations; the host polls a device-side "done" flag after each graph launch, so the
+// reported iteration count is exact (kernels of iterations after convergence return at entry).
+// Block reductions are deterministic (fixed order, no atomics).
+#include <cmath>
+#include <cstring>
+
+#include "efgp_internal.cuh"
+
+namespace efgp {
+
+struct CGState {
+  double rr;        // current ||r||^2 (weighted)
+  double rr_old;    // ||r||^2 of the previous iteration (for beta_cg)
+  double bnorm;     // ||b||
+  double tol;
+  double sigma2;
+  long long iter;
+  long long max_iter;
+  int done;         // 1: converged, 2: hit max_iter
+  int pad_;
+};
+
+constexpr int kCGThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  return t;  // valid in thread 0
+}
+
+// every block reduces the same partials in the same order -> identical value everywhere
+__device__ __forceinline__ double reduce_partials(const double *__restrict__ part, int n, double *sh) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v += part[i];
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) sh[32] = v;
+  __syncthreads();
+  return sh[32];
+}
+
+__global__ void k_cg_init(const double2 *__restrict__ b, double2 *__restrict__ x, double2 *__restrict__ r,
+                          double2 *__restrict__ p, int64_t Mh, int m, double *__restrict__ part) {
+  __shared__ double sh[40];
+  double acc = 0.0;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 bb = b[q];
+    x[q] = make_double2(0.0, 0.0);
+    r[q] = bb;
+    p[q] = bb;
+    const double wq = (q % (m + 1)) ? 2.0 : 1.0;
+    acc += wq * (bb.x * bb.x + bb.y * bb.y);
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void k_cg_init2(CGState *st, const double *__restrict__ part, int nblk, double *hist) {
+  __shared__ double sh[40];
+  const double rr = reduce_partials(part, nblk, sh);
+  if (threadIdx.x == 0) {
+    st->rr = rr;
+    st->rr_old = rr;
+    st->bnorm = sqrt(rr);
+    st->iter = 0;
+    st->done = (rr == 0.0) ? 1 : 0;
+    hist[0] = rr == 0.0 ? 0.0 : 1.0;
+  }
+}
+
+// pad: Xbox = D . p at the J_m bins of the L-box, 0 elsewhere (the C2R input; cuFFT may overwrite
+// it, so it is rewritten in full every iteration)
+template <int D>
+__device__ __forceinline__ void pad_box(const double2 *__restrict__ p, const double *__restrict__ Dh, int m,
+                                        int64_t L, double2 *__restrict__ X, int64_t box) {
+  const int64_t nh = L / 2 + 1;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < box;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rem = idx;
+    const int64_t kd = rem % nh;
+    rem /= nh;
+    bool ok = kd <= m;
+    int64_t q = kd, stride = m + 1;
+#pragma unroll
+    for (int k = D - 2; k >= 0; --k) {
+      const int64_t kk = rem % L;
+      rem /= L;
+      int64_t j;
+      ok = ok && bin_to_mode(kk, L, m, j);
+      q += (j + m) * stride;
+      stride *= (2 * m + 1);
+    }
+    double2 val = make_double2(0.0, 0.0);
+    if (ok) {
+      const double2 pp = p[q];
+      const double dq = Dh[q];
+      val = make_double2(dq * pp.x, dq * pp.y);
+    }
+    X[idx] = val;
+  }
+}
+
+template <int D>
+__global__ void k_cg_pad0(const double2 *__restrict__ p, const double *__restrict__ Dh, int m, int64_t L,
+                          double2 *__restrict__ X, int64_t box) {
+  pad_box<D>(p, Dh, m, L, X, box);
+}
+
+__global__ void k_mul(double *__restrict__ Y, const double *__restrict__ vhat, int64_t n, const CGState *st) {
+  if (st->done) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    Y[i] *= vhat[i];
+}
+
+// Ap = D . Z[J_m] + sigma^2 p ; partial <p, Ap>
+template <int D>
+__global__ void k_cg_apply(const double2 *__restrict__ Z, const double2 *__restrict__ p, const double *__restrict__ Dh,
+                           double2 *__restrict__ Ap, int64_t Mh, int m, int64_t L, const CGState *st,
+                           double *__restrict__ part) {
+  __shared__ double sh[40];
+  if (st->done) return;
+  const double s2 = st->sigma2;
+  double acc = 0.0;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rem = q;
+    const int64_t jd = rem % (m + 1);
+    rem /= (m + 1);
+    int64_t zi = jd, stride = L / 2 + 1;
+#pragma unroll
+    for (int k = D - 2; k >= 0; --k) {
+      int64_t j = rem % (2 * m + 1) - m;
+      rem /= (2 * m + 1);
+      zi += (j < 0 ? j + L : j) * stride;
+      stride *= L;
+    }
+    const double2 z = Z[zi], pp = p[q];
+    const double dq = Dh[q];
+    const double2 a = make_double2(dq * z.x + s2 * pp.x, dq * z.y + s2 * pp.y);
+    Ap[q] = a;
+    const double wq = jd ? 2.0 : 1.0;
+    acc += wq * (pp.x * a.x + pp.y * a.y);
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+// alpha = rr / <p,Ap>; x += alpha p; r -= alpha Ap; partial ||r||^2
+__global__ void k_cg_xr(double2 *__restrict__ x, double2 *__restrict__ r, const double2 *__restrict__ p,
+                        const double2 *__restrict__ Ap, int64_t Mh, int m, CGState *st,
+                        const double *__restrict__ part_pAp, double *__restrict__ part_rr, int nblk) {
+  __shared__ double sh[40];
+  if (st->done) return;
+  const double pAp = reduce_partials(part_pAp, nblk, sh);
+  const double rr = st->rr;
+  const double alpha = rr / pAp;
+  double acc = 0.0;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 pp = p[q], a = Ap[q];
+    double2 xx = x[q], rq = r[q];
+    xx.x += alpha * pp.x;
+    xx.y += alpha * pp.y;
+    rq.x -= alpha * a.x;
+    rq.y -= alpha * a.y;
+    x[q] = xx;
+    r[q] = rq;
+    const double wq = (q % (m + 1)) ? 2.0 : 1.0;
+    acc += wq * (rq.x * rq.x + rq.y * rq.y);
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) {
+    part_rr[blockIdx.x] = acc;
+    if (blockIdx.x == 0) st->rr_old = rr;
+  }
+}
+
+// beta_cg = rr_new / rr_old; p = r + beta_cg p; pad; bookkeeping (block 0)
+template <int D>
+__global__ void k_cg_p(const double2 *__restrict__ r, double2 *__restrict__ p, const double *__restrict__ Dh,
+                       int64_t Mh, int m, int64_t L, double2 *__restrict__ X, int64_t box, CGState *st,
+                       const double *__restrict__ part_rr, int nblk, double *__restrict__ hist) {
+  __shared__ double sh[40];
+  if (st->done) return;
+  const double rr_new = reduce_partials(part_rr, nblk, sh);
+  const double bcg = rr_new / st->rr_old;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 rq = r[q], pp = p[q];
+    p[q] = make_double2(rq.x + bcg * pp.x, rq.y + bcg * pp.y);
+  }
+  // grid-wide dependency: the pad below reads p written by other blocks -> separate kernel
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->rr = rr_new;
+    const long long it = st->iter + 1;
+    st->iter = it;
+    const double rel = sqrt(rr_new) / st->bnorm;
+    hist[it] = rel;
+    if (rel <= st->tol) st->done = 1;
+    else if (it >= st->max_iter) st->done = 2;
+  }
+}
+
+template <int D>
+__global__ void k_cg_pad(const double2 *__restrict__ p, const double *__restrict__ Dh, int m, int64_t L,
+                         double2 *__restrict__ X, int64_t box, const CGState *st) {
+  // runs even when done was just set: harmless (the next C2R input is never used)
+  pad_box<D>(p, Dh, m, L, X, box);
+}
+
+static unsigned nblocks(int64_t n, int sms) {
+  int64_t b = (n + kCGThreads - 1) / kCGThreads;
+  const int64_t cap = (int64_t)sms * 4;
+  if (b > cap) b = cap;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+template <int D>
+static efgp_status enqueue_iteration(efgp_plan *pl, cudaStream_t s, CGState *st, int64_t box, int64_t Ld,
+                                     unsigned nb, unsigned nbox) {
+  const Params &P = pl->P;
+  double *part_pAp = pl->partials, *part_rr = pl->partials + pl->cg_blocks;
+  EFGP_CUFFT(cufftExecZ2D(pl->plan_c2r_L, pl->Xbox, pl->Yr));
+  k_mul<<<nblocks(Ld, pl->num_sms), kCGThreads, 0, s>>>(pl->Yr, pl->vhat, Ld, st);
+  EFGP_CUFFT(cufftExecD2Z(pl->plan_r2c_L, pl->Yr, pl->Zbox));
+  k_cg_apply<D><<<nb, kCGThreads, 0, s>>>(pl->Zbox, pl->p, pl->D_half, pl->Ap, P.Mh, (int)P.m, P.L, st, part_pAp);
+  k_cg_xr<<<nb, kCGThreads, 0, s>>>(pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp, part_rr, (int)nb);
+  k_cg_p<D><<<nb, kCGThreads, 0, s>>>(pl->r, pl->p, pl->D_half, P.Mh, (int)P.m, P.L, pl->Xbox, box, st, part_rr,
+                                      (int)nb, pl->hist);
+  k_cg_pad<D><<<nbox, kCGThreads, 0, s>>>(pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box, st);
+  EFGP_CUDA(cudaGetLastError());
+  return EFGP_OK;
+}
+
+template <int D>
+static efgp_status cg_solve_d(efgp_plan *pl, int64_t N_total) {
+  const Params &P = pl->P;
+  cudaStream_t s = pl->stream;
+  int64_t box = P.L / 2 + 1, Ld = P.L;
+  for (int k = 0; k < D - 1; ++k) {
+    box *= P.L;
+    Ld *= P.L;
+  }
+  const unsigned nb = nblocks(P.Mh, pl->num_sms);
+  const unsigned nbox = nblocks(box, pl->num_sms);
+  if ((int)nb > pl->cg_blocks) {
+    pl->err = "internal: cg partials too small";
+    return EFGP_ERR_INVALID;
+  }
+  int64_t max_iter = P.max_iter_opt;
+  if (max_iter <= 0) {
+    const double Nd = (double)(N_total > 0 ? N_total : 1);
+    max_iter = (int64_t)std::ceil(std::log(1.0 / P.cg_tol) * std::sqrt(Nd) / (2.0 * P.sigma));
+    if (max_iter < 10) max_iter = 10;
+  }
+  pl->max_iter_used = max_iter;
+  if (max_iter + 1 > pl->hist_cap) {
+    if (pl->hist) cudaFree(pl->hist);
+    pl->hist = nullptr;
+    pl->hist_cap = 0;
+    EFGP_CUDA(cudaMalloc(&pl->hist, sizeof(double) * (max_iter + 1)));
+    pl->hist_cap = max_iter + 1;
+  }
+  CGState *st = reinterpret_cast<CGState *>(pl->scal);
+  CGState init{};
+  init.tol = P.cg_tol;
+  init.sigma2 = P.sigma * P.sigma;
+  init.max_iter = max_iter;
+  EFGP_CUDA(cudaMemcpyAsync(st, &init, sizeof(CGState), cudaMemcpyHostToDevice, s));
+  k_cg_init<<<nb, kCGThreads, 0, s>>>(pl->b, pl->x, pl->r, pl->p, P.Mh, (int)P.m, pl->partials);
+  k_cg_init2<<<1, kCGThreads, 0, s>>>(st, pl->partials, (int)nb, pl->hist);
+  k_cg_pad0<D><<<nbox, kCGThreads, 0, s>>>(pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box);
+  EFGP_CUDA(cudaGetLastError());
+  EFGP_CUFFT(cufftSetStream(pl->plan_c2r_L, s));
+  EFGP_CUFFT(cufftSetStream(pl->plan_r2c_L, s));
+
+  const int G = P.graph_iters;
+  if (!pl->cg_exec || pl->cg_exec_iters != G) {
+    if (pl->cg_exec) cudaGraphExecDestroy(pl->cg_exec);
+    pl->cg_exec = nullptr;
+    cudaGraph_t graph;
+    EFGP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    for (int it = 0; it < G; ++it) {
+      efgp_status e = enqueue_iteration<D>(pl, s, st, box, Ld, nb, nbox);
+      if (e != EFGP_OK) {
+        cudaStreamEndCapture(s, &graph);
+        return e;
+      }
+    }
+    EFGP_CUDA(cudaStreamEndCapture(s, &graph));
+    EFGP_CUDA(cudaGraphInstantiate(&pl->cg_exec, graph, 0));
+    cudaGraphDestroy(graph);
+    pl->cg_exec_iters = G;
+  }
+  CGState host{};
+  for (;;) {
+    EFGP_CUDA(cudaGraphLaunch(pl->cg_exec, s));
+    EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned, st, sizeof(CGState), cudaMemcpyDeviceToHost, s));
+    EFGP_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(&host, pl->h_pinned, sizeof(CGState));
+    if (host.done) break;
+  }
+  pl->iters = host.iter;
+  pl->rel_resid = host.bnorm > 0 ? std::sqrt(host.rr) / host.bnorm : 0.0;
+  return host.done == 2 ? EFGP_ERR_NOCONVERGE : EFGP_OK;
+}
+
+efgp_status cg_solve(efgp_plan *pl, int64_t N_total) {
+  switch (pl->P.d) {
+    case 1: return cg_solve_d<1>(pl, N_total);
+    case 2: return cg_solve_d<2>(pl, N_total);
+    case 3: return cg_solve_d<3>(pl, N_total);
+  }
+  return EFGP_ERR_INVALID;
+}
+
+}  // namespace efgp

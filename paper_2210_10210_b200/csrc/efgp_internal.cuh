@@ -1,0 +1,175 @@
+// Internal declarations of the EFGP sm_100a library (not part of the C ABI; see include/efgp.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/efgp.h"
+
+namespace efgp {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr int kMaxW = 16;  // ES kernel width for nufft_tol down to 1e-15
+
+// Host-side parameter record.
+struct Params {
+  int kernel = EFGP_SE;
+  double nu = 0, ell = 0, sigma = 0, eps = 0;
+  int d = 1;
+  double h = 0;
+  int64_t m = 0;
+  int64_t M = 0;        // (2m+1)^d
+  int64_t Mh = 0;       // (2m+1)^(d-1) (m+1): Hermitian half of J_m (j_d >= 0)
+  int64_t Kvh = 0;      // (4m+1)^(d-1) (2m+1): Hermitian half of J_2m
+  double cg_tol = 0;
+  int64_t max_iter_opt = 0;
+  double nufft_tol = 0;
+  int w = 0;            // ES width in cells
+  double beta_es = 0;   // ES shape
+  int64_t n1 = 0;       // type-1 fine grid for v (modes J_2m), per dim
+  int64_t n2 = 0;       // type-1 fine grid for F^*y and type-2 grid (modes J_m), per dim
+  int64_t L = 0;        // Toeplitz FFT box per dim (>= 4m+1)
+  int rescale = EFGP_RESCALE_L2;
+  int spread_method = EFGP_SPREAD_AUTO;
+  int graph_iters = 8;
+};
+
+// host_setup.cu
+std::string validate_and_choose(Params &p, const efgp_options &opt);
+double khat_host(const Params &p, double xi_norm);
+int64_t next_smooth(int64_t n);                              // smallest 2^a 3^b 5^c 7^d >= n
+void gauss_legendre(int n, std::vector<double> &x, std::vector<double> &w);
+// phihat[k] = alpha * int_{-1}^{1} exp(beta (sqrt(1 - z^2) - 1)) cos(k alpha z) dz, alpha = w pi / n
+std::vector<double> es_fourier_table(int w, double beta, int64_t n, int64_t kmax);
+
+struct DevBuf {
+  void *ptr = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace efgp
+
+struct efgp_plan {
+  efgp::Params P;
+  cudaStream_t stream = nullptr;       // internal non-blocking stream: all library work (capturable)
+  cudaStream_t ustream = nullptr;      // caller's stream (options.stream): ordering at entry/exit only
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  int device = 0;
+  int num_sms = 148;
+  std::string err;
+
+  // tables
+  double *D_half = nullptr;   // Mh spectral weights (eq 117) on the J_m half
+  double *psi1 = nullptr;     // ES Fourier transform, grid n1, k = 0..2m
+  double *psi2 = nullptr;     // grid n2, k = 0..m
+
+  // type-1 grids and spectra
+  double *g1 = nullptr;       // n1^d real
+  double *g2 = nullptr;       // n2^d real
+  double2 *G1h = nullptr;     // n1^(d-1) (n1/2+1)
+  double2 *G2h = nullptr;     // n2^(d-1) (n2/2+1)
+  double *modes = nullptr;    // local partial modes: v half (Kvh cplx) | F^*y half (Mh cplx)
+  double *modes_sum = nullptr;
+
+  // Toeplitz operator and CG state
+  double2 *Xbox = nullptr;    // L^(d-1) (L/2+1) complex, C2R input
+  double *Yr = nullptr;       // L^d real
+  double *vhat = nullptr;     // L^d real, C2R(v)/L^d
+  double2 *Zbox = nullptr;    // R2C output
+  double2 *b = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *Ap = nullptr;  // Mh each
+  double *partials = nullptr; // 2 * cg_blocks
+  double *scal = nullptr;     // device scalars (see cg.cu)
+  double *hist = nullptr;     // residual history, hist_cap entries
+  int64_t hist_cap = 0;
+  int cg_blocks = 1;
+  int *dflags = nullptr;      // [0] invalid-input flag
+  double *h_pinned = nullptr; // small pinned host mirror of scalars/flags
+
+  // type-2
+  double2 *T2box = nullptr;   // n2^(d-1) (n2/2+1)
+  double *t2grid = nullptr;   // n2^d real
+  bool t2_valid = false;
+
+  // host-input staging
+  double *stage[2] = {nullptr, nullptr};
+  int64_t stage_pts = 0;
+
+  cufftHandle plan_g1 = 0, plan_g2 = 0, plan_c2r_L = 0, plan_r2c_L = 0, plan_t2 = 0;
+  cudaGraphExec_t cg_exec = nullptr;
+  int cg_exec_iters = 0;
+
+  // state of the last fit
+  bool fitted = false;
+  int64_t N_last = 0;
+  int64_t iters = 0;
+  double rel_resid = 0;
+  int64_t max_iter_used = 0;
+  int spread_used = 0;
+  double t_spread = 0, t_modes = 0, t_solve = 0, t_predict = 0;
+  cudaEvent_t ev[8] = {};
+};
+
+namespace efgp {
+// spread.cu
+efgp_status spread_points(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s);
+efgp_status spread_begin(efgp_plan *pl, cudaStream_t s);
+efgp_status spread_end(efgp_plan *pl, cudaStream_t s);
+// modes.cu
+efgp_status type1_modes(efgp_plan *pl, double *modes_out, cudaStream_t s);
+efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s);
+efgp_status type2_grid(efgp_plan *pl, cudaStream_t s);
+// cg.cu
+efgp_status cg_solve(efgp_plan *pl, int64_t N_total);
+// interp.cu
+efgp_status interp_targets(efgp_plan *pl, const double *xt, int64_t q, double *mu, cudaStream_t s);
+}  // namespace efgp
+
+#define EFGP_CUDA(call)                                                                  \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      pl->err = std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + __FILE__ + \
+                ":" + std::to_string(__LINE__);                                          \
+      return e_ == cudaErrorMemoryAllocation ? EFGP_ERR_RESOURCE : EFGP_ERR_CUDA;        \
+    }                                                                                    \
+  } while (0)
+
+#define EFGP_CUFFT(call)                                                                 \
+  do {                                                                                   \
+    cufftResult r_ = (call);                                                             \
+    if (r_ != CUFFT_SUCCESS) {                                                           \
+      pl->err = std::string("cuFFT error ") + std::to_string((int)r_) + " at " + __FILE__ + \
+                ":" + std::to_string(__LINE__);                                          \
+      return r_ == CUFFT_ALLOC_FAILED ? EFGP_ERR_RESOURCE : EFGP_ERR_CUDA;               \
+    }                                                                                    \
+  } while (0)
+
+#define EFGP_TRY(call)                 \
+  do {                                 \
+    efgp_status s_ = (call);           \
+    if (s_ != EFGP_OK) return s_;      \
+  } while (0)
+
+// ---- device helpers shared by the kernels ------------------------------------------------
+namespace efgp {
+
+// ES kernel phi(z) = exp(beta (sqrt(1 - z^2) - 1)) on |z| <= 1 (FINUFFT's exponential of
+// semicircle).  Evaluated directly in fp64.
+__device__ __forceinline__ double es_kernel(double z, double beta) {
+  double a = fma(-z, z, 1.0);
+  a = a > 0.0 ? a : 0.0;
+  return exp(beta * (sqrt(a) - 1.0));
+}
+
+// Signed mode index of FFT bin k in a length-n transform whose modes satisfy |j| <= jmax
+// (jmax < n/2): returns true and j if bin k holds a mode.
+__device__ __forceinline__ bool bin_to_mode(int64_t k, int64_t n, int64_t jmax, int64_t &j) {
+  if (k <= jmax) { j = k; return true; }
+  if (k >= n - jmax) { j = k - n; return true; }
+  return false;
+}
+
+}  // namespace efgp

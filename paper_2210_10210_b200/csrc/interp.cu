@@ -1,0 +1,171 @@
+// K9: type-2 interpolation mu(x*) = sum_{cells l near theta*} b_l prod_k phi((l_k - t_k) 2/W),
+// t = h x* n2, b = C2R(c') the real type-2 fine grid (Alg a1 steps 5-6; eq "muws"
+// P:557).  One thread per target.  SMEM variant: each CTA stages the occupied part of the grid
+// (cells reachable from x* in [0,1]^d) in shared memory once, then gathers from it; GLOBAL
+// variant gathers from L2.  Targets outside [0,1]^d or non-finite give mu = NaN and raise
+// dflags[1].
+#include <cmath>
+
+#include "efgp_internal.cuh"
+
+namespace efgp {
+
+#define EFGP_W_CASES2(MACRO) \
+  MACRO(2) MACRO(3) MACRO(4) MACRO(5) MACRO(6) MACRO(7) MACRO(8) MACRO(9) MACRO(10) MACRO(11) MACRO(12) MACRO(13) MACRO(14) MACRO(15) MACRO(16)
+
+struct Occ2 {
+  int lo, A;
+};
+static inline Occ2 occupied2(double h, int n, int W) {
+  const int lo = -(W / 2);
+  const int hi0 = (int)std::ceil(h * n - 0.5 * W);
+  return Occ2{lo, hi0 + W - 1 - lo + 1};
+}
+
+__device__ __forceinline__ int wrapn(int i, int n) {
+  i %= n;
+  return i < 0 ? i + n : i;
+}
+
+template <int D, int W, bool SMEM>
+__global__ void __launch_bounds__(256) k_interp(const double *__restrict__ xt, int64_t q,
+                                                const double *__restrict__ grid, int n, double h, double beta,
+                                                int lo, int A, double *__restrict__ mu, int *__restrict__ err) {
+  extern __shared__ double sgrid[];
+  if constexpr (SMEM) {
+    int64_t cells = A;
+    for (int k = 1; k < D; ++k) cells *= A;
+    for (int64_t c = threadIdx.x; c < cells; c += blockDim.x) {
+      int64_t rem = c, gi = 0;
+      int idx[D];
+#pragma unroll
+      for (int k = D - 1; k >= 0; --k) {
+        idx[k] = (int)(rem % A);
+        rem /= A;
+      }
+#pragma unroll
+      for (int k = 0; k < D; ++k) gi = gi * n + wrapn(idx[k] + lo, n);
+      sgrid[c] = __ldg(grid + gi);
+    }
+    __syncthreads();
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q; i += (int64_t)gridDim.x * blockDim.x) {
+    double xc[D];
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      xc[k] = __ldg(xt + i * D + k);
+      ok = ok && xc[k] >= 0.0 && xc[k] <= 1.0;
+    }
+    if (!ok) {
+      mu[i] = __longlong_as_double(0x7ff8000000000000LL);
+      atomicOr(err + 1, 1);
+      continue;
+    }
+    int base[D];
+    double wt[D][W];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const double t = h * xc[k] * (double)n;
+      const int i0 = (int)ceil(t - 0.5 * W);
+      base[k] = i0;
+#pragma unroll
+      for (int a = 0; a < W; ++a) wt[k][a] = es_kernel(((double)(i0 + a) - t) * (2.0 / W), beta);
+    }
+    double acc = 0.0;
+    if constexpr (D == 1) {
+#pragma unroll
+      for (int a = 0; a < W; ++a) {
+        const double g = SMEM ? sgrid[base[0] + a - lo] : __ldg(grid + wrapn(base[0] + a, n));
+        acc = fma(g, wt[0][a], acc);
+      }
+    } else if constexpr (D == 2) {
+#pragma unroll
+      for (int a = 0; a < W; ++a) {
+        double ra = 0.0;
+        if (SMEM) {
+          const double *row = sgrid + (int64_t)(base[0] + a - lo) * A + (base[1] - lo);
+#pragma unroll
+          for (int b = 0; b < W; ++b) ra = fma(row[b], wt[1][b], ra);
+        } else {
+          const double *row = grid + (int64_t)wrapn(base[0] + a, n) * n;
+#pragma unroll
+          for (int b = 0; b < W; ++b) ra = fma(__ldg(row + wrapn(base[1] + b, n)), wt[1][b], ra);
+        }
+        acc = fma(ra, wt[0][a], acc);
+      }
+    } else {
+#pragma unroll 1
+      for (int a = 0; a < W; ++a) {
+        double ra = 0.0;
+#pragma unroll
+        for (int b = 0; b < W; ++b) {
+          double rb = 0.0;
+          if (SMEM) {
+            const double *row = sgrid + ((int64_t)(base[0] + a - lo) * A + (base[1] + b - lo)) * A + (base[2] - lo);
+#pragma unroll
+            for (int e = 0; e < W; ++e) rb = fma(row[e], wt[2][e], rb);
+          } else {
+            const double *row = grid + ((int64_t)wrapn(base[0] + a, n) * n + wrapn(base[1] + b, n)) * n;
+#pragma unroll
+            for (int e = 0; e < W; ++e) rb = fma(__ldg(row + wrapn(base[2] + e, n)), wt[2][e], rb);
+          }
+          ra = fma(rb, wt[1][b], ra);
+        }
+        acc = fma(ra, wt[0][a], acc);
+      }
+    }
+    mu[i] = acc;
+  }
+}
+
+template <int D, int W>
+static efgp_status launch_interp(efgp_plan *pl, const double *xt, int64_t q, double *mu, cudaStream_t s) {
+  const Params &P = pl->P;
+  const Occ2 o = occupied2(P.h, (int)P.n2, W);
+  size_t cells = o.A;
+  for (int k = 1; k < D; ++k) cells *= o.A;
+  const size_t sb = cells * sizeof(double);
+  int64_t blocks = (q + 255) / 256;
+  if (sb <= 160 * 1024) {
+    // one wave of persistent CTAs so the staged grid is reused across many targets
+    const int64_t cap = (int64_t)pl->num_sms * (sb <= 48 * 1024 ? 4 : (sb <= 100 * 1024 ? 2 : 1));
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    EFGP_CUDA(cudaFuncSetAttribute(k_interp<D, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    k_interp<D, W, true><<<(unsigned)blocks, 256, sb, s>>>(xt, q, pl->t2grid, (int)P.n2, P.h, P.beta_es, o.lo, o.A,
+                                                           mu, pl->dflags);
+  } else {
+    const int64_t cap = (int64_t)pl->num_sms * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    k_interp<D, W, false><<<(unsigned)blocks, 256, 0, s>>>(xt, q, pl->t2grid, (int)P.n2, P.h, P.beta_es, o.lo, o.A,
+                                                           mu, pl->dflags);
+  }
+  EFGP_CUDA(cudaGetLastError());
+  return EFGP_OK;
+}
+
+template <int D>
+static efgp_status interp_d(efgp_plan *pl, const double *xt, int64_t q, double *mu, cudaStream_t s) {
+  switch (pl->P.w) {
+#define EFGP_CASE(WW) \
+  case WW:            \
+    return launch_interp<D, WW>(pl, xt, q, mu, s);
+    EFGP_W_CASES2(EFGP_CASE)
+#undef EFGP_CASE
+  }
+  return EFGP_ERR_INVALID;
+}
+
+efgp_status interp_targets(efgp_plan *pl, const double *xt, int64_t q, double *mu, cudaStream_t s) {
+  if (q <= 0) return EFGP_OK;
+  switch (pl->P.d) {
+    case 1: return interp_d<1>(pl, xt, q, mu, s);
+    case 2: return interp_d<2>(pl, xt, q, mu, s);
+    case 3: return interp_d<3>(pl, xt, q, mu, s);
+  }
+  return EFGP_ERR_INVALID;
+}
+
+}  // namespace efgp

@@ -1,0 +1,54 @@
+"""The C-ABI library loads and exports every symbol include/efgp.h declares (no GPU needed; no
+compute calls).  Also: the binding refuses to run without the library (no CPU fallback)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "efgp.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(efgp_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for n in ("efgp_setup", "efgp_fit", "efgp_predict", "efgp_get_info", "efgp_destroy", "efgp_fit_local",
+              "efgp_fit_solve", "efgp_load_weights", "efgp_get_residual_history", "efgp_last_error"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2210_10210_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_2210_10210_b200 import build
+        build.build()
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(declared_functions()) <= set(_lib.SIGNATURES)
+    assert _lib.load().efgp_abi_version() == 1
+
+
+def test_library_is_sm100a_only():
+    from paper_2210_10210_b200 import _lib
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out and "sm_90" not in out
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    from paper_2210_10210_b200 import _lib
+    saved = _lib._lib
+    try:
+        _lib._lib = None
+        with pytest.raises(RuntimeError, match="no CPU fallback"):
+            _lib.load(str(tmp_path / "nope.so"))
+    finally:
+        _lib._lib = saved

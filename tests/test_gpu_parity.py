@@ -1,0 +1,271 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded inputs.
+
+Gates:
+  * (h, m) exactly equal to the oracle's rules;
+  * type-1 outputs v and Phi^*y: relative l2 <= 5 nufft_tol (the NUFFT tolerance contract, SPEC
+    S:226, with the 0.6-1.8x spread measured in SURVEY A.5);
+  * type-2 (predict from given weights): relative l2 <= 5 nufft_tol;
+  * whole path in parity mode (CG to eps/1000 on both sides, reading G9): mu relative l2 <= 10 eps
+    (BASELINE north_star), CG iteration count within +-2 of the oracle or inside the oracle's
+    [2 eps, eps/2] crossing window (reading G10).
+Sizes: reduced N (and, where the oracle's O(M^2) Toeplitz product would take minutes, reduced m)
+so that the oracle finishes in seconds while the GPU grids still span many tiles / CTAs.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from _util import CONFIGS, O, dev, generate, gpu_beta_full, gpu_rhs_full, gpu_v_full, model, rel
+
+pytestmark = pytest.mark.gpu
+
+# (N for type-1 checks, m override or None)
+T1_SIZES = {"c1": (10_000, None), "c2": (20_000, None), "c3": (20_000, None), "c4": (1_000, None),
+            "c5": (50_000, None)}
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_setup_parameters_match_oracle(name):
+    c = CONFIGS[name]
+    g = model(c)
+    inf = g.info()
+    h, m = O.choose_params(c.kernel, c.ell, c.d, c.eps, c.nu)
+    assert inf["m"] == m and inf["h"] == pytest.approx(h, rel=1e-15, abs=0)
+    assert inf["M"] == (2 * m + 1) ** c.d and inf["nufft_tol"] == pytest.approx(c.eps / 10)
+    g.close()
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_type1_v_and_rhs(name):
+    c = CONFIGS[name]
+    N, _ = T1_SIZES[name]
+    x, y, _ = generate(c, N=N, q=1)
+    g = model(c, max_iter=1)
+    g.fit(dev(x), dev(y))
+    inf = g.info()
+    h, m = inf["h"], inf["m"]
+    v_ref = O.toeplitz_vector(x, h, m)
+    D = O.spectral_weights(c.kernel, c.ell, c.d, h, m, c.nu)
+    b_ref = O.rhs(x, y, h, m, D)
+    v = gpu_v_full(m, g)
+    b = gpu_rhs_full(g)
+    tol = 5 * inf["nufft_tol"]
+    assert rel(v, v_ref) <= tol, (rel(v, v_ref), tol)
+    assert rel(b, b_ref) <= tol, (rel(b, b_ref), tol)
+    assert abs(v[(2 * m,) * c.d] - N) <= tol * N          # v_0 = N
+    g.close()
+
+
+def test_spread_strategies_agree():
+    c = CONFIGS["c5"]
+    x, y, _ = generate(c, N=200_000, q=1)
+    out = {}
+    for method in ("global", "smem"):
+        g = model(c, max_iter=1, spread=method)
+        g.fit(dev(x), dev(y))
+        assert g.info()["spread_method"] == method
+        out[method] = (g.vector("v"), g.vector("rhs"))
+        g.close()
+    assert rel(out["smem"][0], out["global"][0]) < 1e-12
+    assert rel(out["smem"][1], out["global"][1]) < 1e-12
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_type2_predict_from_loaded_weights(name):
+    c = CONFIGS[name]
+    g = model(c)
+    inf = g.info()
+    m, d, h = inf["m"], c.d, inf["h"]
+    rng = np.random.default_rng(100 + c.id)
+    full = rng.normal(size=(2 * m + 1,) * d) + 1j * rng.normal(size=(2 * m + 1,) * d)
+    full = 0.5 * (full + np.conj(full[(slice(None, None, -1),) * d]))       # Hermitian
+    from paper_2210_10210_b200 import full_to_half
+    g.load_weights(full_to_half(full))
+    q = {1: 1000, 2: 3000, 3: 500}[d]
+    _, _, xt = generate(c, N=1, q=q)
+    xt = np.concatenate([xt, np.zeros((1, d)), np.ones((1, d))])          # domain corners
+    mu = g.predict(dev(xt)).cpu().numpy()
+    D = O.spectral_weights(c.kernel, c.ell, d, h, m, c.nu)
+    ref = O.posterior_mean(full, D, h, xt)
+    assert rel(mu, ref) <= 5 * inf["nufft_tol"], rel(mu, ref)
+    g.close()
+
+
+# (N, m override or None, h override) for the whole-path parity runs
+CG_SIZES = {"c1": (10_000, None), "c2": (20_000, 20), "c3": (5_000, None), "c4": (3_000, 6), "c5": (50_000, None)}
+
+
+def _window_ok(k_g, k_o, hist_o, eps_cg):
+    lo = next((k for k, r in enumerate(hist_o) if r <= 2 * eps_cg), len(hist_o))
+    hi = next((k for k, r in enumerate(hist_o) if r <= eps_cg / 2), len(hist_o) + 10)
+    return abs(k_g - k_o) <= 2 or lo <= k_g <= hi
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_whole_path_parity_mode(name):
+    c = CONFIGS[name]
+    N, m_over = CG_SIZES[name]
+    x, y, xt = generate(c, N=N, q=min(c.q, 2000))
+    cg_tol = c.eps / 1000
+    kw = {}
+    if m_over is not None:
+        h0, _ = O.choose_params(c.kernel, c.ell, c.d, c.eps, c.nu)
+        kw = dict(h=h0, m=m_over)
+    g = model(c, cg_tol=cg_tol, **kw)
+    g.fit(dev(x), dev(y))
+    mu = g.predict(dev(xt)).cpu().numpy()
+    inf = g.info()
+    fit = O.efgp_fit(x, y, c.kernel, c.ell, c.sigma, c.eps, nu=c.nu, cg_tol=cg_tol,
+                     h=kw.get("h"), m=kw.get("m"))
+    ref = O.efgp_predict(fit, xt)
+    err = rel(mu, ref)
+    assert err <= 10 * c.eps, (err, 10 * c.eps)
+    hist_g = g.residual_history()
+    assert len(hist_g) == inf["iters"] + 1 and hist_g[-1] <= cg_tol
+    assert _window_ok(inf["iters"], fit.iters, fit.history, cg_tol), (inf["iters"], fit.iters)
+    # the trajectories agree to NUFFT accuracy before roundoff decorrelates them
+    k = min(10, fit.iters, inf["iters"])
+    np.testing.assert_allclose(hist_g[:k + 1], fit.history[:k + 1], rtol=1e-2)
+    g.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c5"])
+def test_production_mode_iterations(name):
+    # CG stopped at eps (what the bench times): iteration count within +-2 / window of the oracle.
+    c = CONFIGS[name]
+    N = 10_000 if name == "c1" else 100_000
+    x, y, xt = generate(c, N=N, q=1000)
+    g = model(c)
+    g.fit(dev(x), dev(y))
+    mu = g.predict(dev(xt)).cpu().numpy()
+    fit = O.efgp_fit(x, y, c.kernel, c.ell, c.sigma, c.eps, nu=c.nu)
+    inf = g.info()
+    assert _window_ok(inf["iters"], fit.iters, fit.history, c.eps), (inf["iters"], fit.iters)
+    assert rel(mu, O.efgp_predict(fit, xt)) <= 10 * c.eps
+    g.close()
+
+
+# ------------------------------------------------------------------------------- edge cases
+def test_single_point_at_origin_gives_unit_v():
+    c = CONFIGS["c5"]
+    g = model(c, max_iter=2)
+    g.fit(dev(np.zeros((1, 2))), dev(np.ones(1)))
+    v = gpu_v_full(None, g)
+    assert np.max(np.abs(v - 1.0)) <= 5 * c.eps / 10 * math.sqrt(v.size)
+    g.close()
+
+
+def test_boundary_and_identical_points():
+    c = CONFIGS["c2"]
+    rng = np.random.default_rng(0)
+    x = np.concatenate([np.zeros((50, 2)), np.ones((50, 2)), np.full((300, 2), 0.37), rng.uniform(0, 1, (600, 2)),
+                        np.array([[0.0, 1.0], [1.0, 0.0]])])
+    y = rng.normal(size=len(x))
+    g = model(c, max_iter=1)
+    g.fit(dev(x), dev(y))
+    inf = g.info()
+    v_ref = O.toeplitz_vector(x, inf["h"], inf["m"])
+    assert rel(gpu_v_full(None, g), v_ref) <= 5 * inf["nufft_tol"]
+    g.close()
+
+
+def test_zero_observations_give_zero_mean():
+    c = CONFIGS["c5"]
+    x, _, xt = generate(c, N=5000, q=100)
+    g = model(c)
+    g.fit(dev(x), dev(np.zeros(5000)))
+    assert g.info()["iters"] == 0
+    assert np.all(g.weights() == 0)
+    assert np.all(g.predict(dev(xt)).cpu().numpy() == 0)
+    g.close()
+
+
+def test_invalid_inputs_rejected():
+    from paper_2210_10210_b200 import EFGPError
+    c = CONFIGS["c5"]
+    g = model(c)
+    with pytest.raises(EFGPError, match="INVALID"):
+        g.predict(dev(np.full((3, 2), 0.5)))                       # predict before fit
+    x = np.random.default_rng(1).uniform(0, 1, (100, 2))
+    for bad in (1.5, -0.1, np.nan):
+        xb = x.copy()
+        xb[7, 1] = bad
+        with pytest.raises(EFGPError, match="INVALID"):
+            g.fit(dev(xb), dev(np.ones(100)))
+    yb = np.ones(100)
+    yb[3] = np.inf
+    with pytest.raises(EFGPError, match="INVALID"):
+        g.fit(dev(x), dev(yb))
+    with pytest.raises(EFGPError, match="INVALID"):
+        g.fit(dev(x[:0]), dev(np.ones(0)))
+    g.fit(dev(x), dev(np.ones(100)))
+    out = g.predict(dev(np.zeros((0, 2))))                          # q = 0
+    assert out.numel() == 0
+    with pytest.raises(EFGPError, match="INVALID"):
+        g.predict(dev(np.array([[0.5, 2.0]])))
+    g.close()
+    from paper_2210_10210_b200 import EFGP
+    for args in [("se", 0.1, 0.0, 1e-6, 1), ("se", -1.0, 0.1, 1e-6, 1), ("se", 0.1, 0.1, 1.0, 1),
+                 ("se", 0.1, 0.1, 1e-6, 4), ("matern", 0.1, 0.1, 1e-3, 2, 0.25)]:
+        with pytest.raises(EFGPError, match="INVALID"):
+            EFGP(*args)
+
+
+def test_noconvergence_keeps_state():
+    c = CONFIGS["c5"]
+    x, y, xt = generate(c, N=20_000, q=10)
+    g = model(c, max_iter=5)
+    with pytest.warns(RuntimeWarning, match="max_iter"):
+        g.fit(dev(x), dev(y))
+    assert g.last_status == 1
+    inf = g.info()
+    assert inf["iters"] == 5 and len(g.residual_history()) == 6 and inf["rel_resid"] > c.eps
+    assert np.all(np.isfinite(g.predict(dev(xt)).cpu().numpy()))
+    g.close()
+
+
+def test_host_inputs_match_device_inputs():
+    c = CONFIGS["c3"]
+    x, y, xt = generate(c, N=30_000, q=500)
+    g = model(c, cg_tol=1e-8)
+    g.fit(dev(x), dev(y))
+    mu_d = g.predict(dev(xt)).cpu().numpy()
+    beta_d = g.weights()
+    g.fit(x, y)                                   # numpy host arrays: streamed by the library
+    mu_h = g.predict(xt).numpy()
+    assert rel(g.weights(), beta_d) < 1e-10 and rel(mu_h, mu_d) < 1e-10
+    g.close()
+
+
+def test_shard_linearity_of_partial_modes():
+    # the multi-GPU decomposition on one GPU: partial modes of two shards sum to the modes of all
+    import torch
+    c = CONFIGS["c5"]
+    x, y, xt = generate(c, N=40_000, q=200)
+    g = model(c)
+    full = g.fit_local(dev(x), dev(y)).clone()
+    a = g.fit_local(dev(x[:15_000]), dev(y[:15_000])).clone()
+    b = g.fit_local(dev(x[15_000:]), dev(y[15_000:])).clone()
+    assert rel((a + b).cpu().numpy(), full.cpu().numpy()) < 1e-12
+    g.fit_solve(a + b, 40_000)
+    mu_s = g.predict(dev(xt)).cpu().numpy()
+    g.fit(dev(x), dev(y))
+    assert rel(mu_s, g.predict(dev(xt)).cpu().numpy()) < 1e-9
+    g.close()
+
+
+def test_device_generator_matches_host_generator():
+    import torch
+    from efgp_data import gpu as G
+    for name in ("c1", "c3", "c4", "c5"):
+        c = CONFIGS[name]
+        xh, yh, th = generate(c, N=4096, q=512, start=123_456)
+        xd, yd = G.generate_points(c, 123_456, 4096)
+        td = G.generate_targets(c, 0, 512)
+        if c.points == "uniform":
+            np.testing.assert_array_equal(xd.cpu().numpy(), xh)        # integer arithmetic: bitwise
+        else:
+            np.testing.assert_allclose(xd.cpu().numpy(), xh, rtol=0, atol=1e-14)
+        np.testing.assert_allclose(yd.cpu().numpy(), yh, rtol=0, atol=1e-13)
+        np.testing.assert_array_equal(td.cpu().numpy(), th)
