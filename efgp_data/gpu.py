@@ -55,8 +55,9 @@ def generate_points(cfg, start: int, count: int, x=None, y=None, device=None):
 def generate_targets(cfg, start: int, count: int, out=None, device=None):
     import torch
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
-    if cfg.targets == "equispaced":
-        return (torch.arange(start, start + count, dtype=torch.float64, device=dev) / (cfg.q - 1))[:, None].contiguous()
+    if cfg.targets == "equispaced":   # tiny: take the host recipe verbatim (same rounding)
+        from .configs import targets
+        return torch.from_numpy(targets(cfg, start, start + count)).to(dev)
     if out is None:
         out = torch.empty((count, cfg.d), dtype=torch.float64, device=dev)
     st = torch.cuda.current_stream(dev).cuda_stream
