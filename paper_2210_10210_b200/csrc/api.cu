@@ -55,8 +55,9 @@ efgp_status build(efgp_plan *pl) {
     }
     Dh[q] = std::sqrt(std::pow(P.h, d) * khat_host(P, P.h * std::sqrt(r2)));
   }
-  const std::vector<double> psi1 = es_fourier_table(P.w, P.beta_es, P.n1, 2 * P.m);
-  const std::vector<double> psi2 = es_fourier_table(P.w, P.beta_es, P.n2, P.m);
+  // deconvolution tables of the piecewise-polynomial kernel the kernels actually use
+  const std::vector<double> psi1 = es_fourier_table_poly(P.poly, P.w, P.n1, 2 * P.m);
+  const std::vector<double> psi2 = es_fourier_table_poly(P.poly, P.w, P.n2, P.m);
   EFGP_TRY(dalloc(pl, &pl->D_half, P.Mh));
   EFGP_TRY(dalloc(pl, &pl->psi1, psi1.size()));
   EFGP_TRY(dalloc(pl, &pl->psi2, psi2.size()));
@@ -64,13 +65,20 @@ efgp_status build(efgp_plan *pl) {
   EFGP_CUDA(cudaMemcpy(pl->psi1, psi1.data(), sizeof(double) * psi1.size(), cudaMemcpyHostToDevice));
   EFGP_CUDA(cudaMemcpy(pl->psi2, psi2.data(), sizeof(double) * psi2.size(), cudaMemcpyHostToDevice));
 
-  const int64_t g1 = ipow(P.n1, d), g2 = ipow(P.n2, d);
+  const int64_t g1 = ipow(P.n1, d), g2 = ipow(P.n2, d), gr = ipow(P.n_rhs, d);
   const int64_t G1h = ipow(P.n1, d - 1) * (P.n1 / 2 + 1), G2h = ipow(P.n2, d - 1) * (P.n2 / 2 + 1);
+  const int64_t Grh = ipow(P.n_rhs, d - 1) * (P.n_rhs / 2 + 1);
   const int64_t Ld = ipow(P.L, d), box = ipow(P.L, d - 1) * (P.L / 2 + 1);
   EFGP_TRY(dalloc(pl, &pl->g1, g1));
-  EFGP_TRY(dalloc(pl, &pl->g2, g2));
+  EFGP_TRY(dalloc(pl, &pl->g2, gr));
   EFGP_TRY(dalloc(pl, &pl->G1h, G1h));
-  EFGP_TRY(dalloc(pl, &pl->G2h, G2h));
+  EFGP_TRY(dalloc(pl, &pl->G2h, Grh));
+  if (P.spread_method == EFGP_SPREAD_SORTED) {
+    const int64_t nbmax = (P.chunk + P.bin_batch - 1) / P.bin_batch;
+    EFGP_TRY(dalloc(pl, &pl->rec_x, nbmax * P.bin_batch));
+    EFGP_TRY(dalloc(pl, &pl->rec_y, nbmax * P.bin_batch));
+    EFGP_TRY(dalloc(pl, &pl->seg, (int64_t)P.ntile1 * P.ntile1 * nbmax));
+  }
   EFGP_TRY(dalloc(pl, &pl->modes, 2 * (P.Kvh + P.Mh)));
   EFGP_TRY(dalloc(pl, &pl->modes_sum, 2 * (P.Kvh + P.Mh)));
   EFGP_TRY(dalloc(pl, &pl->Xbox, box));
@@ -89,7 +97,7 @@ efgp_status build(efgp_plan *pl) {
   EFGP_TRY(dalloc(pl, &pl->T2box, G2h));
   EFGP_TRY(dalloc(pl, &pl->t2grid, g2));
   EFGP_TRY(make_plan(pl, &pl->plan_g1, d, P.n1, CUFFT_D2Z));
-  EFGP_TRY(make_plan(pl, &pl->plan_g2, d, P.n2, CUFFT_D2Z));
+  EFGP_TRY(make_plan(pl, &pl->plan_g2, d, P.n_rhs, CUFFT_D2Z));
   EFGP_TRY(make_plan(pl, &pl->plan_c2r_L, d, P.L, CUFFT_Z2D));
   EFGP_TRY(make_plan(pl, &pl->plan_r2c_L, d, P.L, CUFFT_D2Z));
   EFGP_TRY(make_plan(pl, &pl->plan_t2, d, P.n2, CUFFT_Z2D));
@@ -434,7 +442,8 @@ void efgp_destroy(efgp_handle pl) {
     if (h) cufftDestroy(h);
   void *bufs[] = {pl->D_half, pl->psi1, pl->psi2, pl->g1, pl->g2, pl->G1h, pl->G2h, pl->modes, pl->modes_sum,
                   pl->Xbox, pl->Yr, pl->vhat, pl->Zbox, pl->b, pl->x, pl->r, pl->p, pl->Ap, pl->partials,
-                  pl->scal, pl->hist, pl->dflags, pl->T2box, pl->t2grid, pl->stage[0], pl->stage[1]};
+                  pl->scal, pl->hist, pl->dflags, pl->T2box, pl->t2grid, pl->stage[0], pl->stage[1],
+                  pl->rec_x, pl->rec_y, pl->seg};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (pl->h_pinned) cudaFreeHost(pl->h_pinned);

@@ -13,6 +13,13 @@ namespace efgp {
 constexpr double kPi = 3.14159265358979323846;
 constexpr int kMaxW = 16;  // ES kernel width for nufft_tol down to 1e-15
 
+// Piecewise-polynomial ES kernel weights (degree w+2 in s = 2u-1 per cell offset a), passed to the
+// kernels by value (lives in the constant bank).
+struct EsPoly {
+  double c[kMaxW][kMaxW + 3];
+  int deg;
+};
+
 // Host-side parameter record.
 struct Params {
   int kernel = EFGP_SE;
@@ -31,9 +38,16 @@ struct Params {
   int64_t n1 = 0;       // type-1 fine grid for v (modes J_2m), per dim
   int64_t n2 = 0;       // type-1 fine grid for F^*y and type-2 grid (modes J_m), per dim
   int64_t L = 0;        // Toeplitz FFT box per dim (>= 4m+1)
+  int64_t n_rhs = 0;    // grid of the strength-y spread: n1 (SORTED) or n2
   int rescale = EFGP_RESCALE_L2;
-  int spread_method = EFGP_SPREAD_AUTO;
+  int spread_method = EFGP_SPREAD_AUTO;  // resolved at setup (never AUTO afterwards)
   int graph_iters = 8;
+  EsPoly poly{};
+  // SORTED spreading geometry (2D)
+  int s_lo = 0, s_count = 0;   // start cells i0 in [s_lo, s_lo + s_count) per dim
+  int tile = 16, ntile1 = 0;   // tile side (start cells) and tiles per dim
+  int64_t chunk = 0;           // points per chunk
+  int bin_batch = 2048;        // points per bin CTA
 };
 
 // host_setup.cu
@@ -43,6 +57,11 @@ int64_t next_smooth(int64_t n);                              // smallest 2^a 3^b
 void gauss_legendre(int n, std::vector<double> &x, std::vector<double> &w);
 // phihat[k] = alpha * int_{-1}^{1} exp(beta (sqrt(1 - z^2) - 1)) cos(k alpha z) dz, alpha = w pi / n
 std::vector<double> es_fourier_table(int w, double beta, int64_t n, int64_t kmax);
+void es_poly_fit(int w, double beta, EsPoly &out);
+double es_poly_eval(const EsPoly &P, int a, double u);
+std::vector<double> es_fourier_table_poly(const EsPoly &P, int w, int64_t n, int64_t kmax);
+// spread.cu: choose the spreading strategy and its geometry (sets spread_method, n_rhs, tiles)
+void resolve_spread_method(Params &p);
 
 struct DevBuf {
   void *ptr = nullptr;
@@ -96,6 +115,11 @@ struct efgp_plan {
   // host-input staging
   double *stage[2] = {nullptr, nullptr};
   int64_t stage_pts = 0;
+
+  // SORTED spreading: per-chunk binned records and the (tile x batch) segment table
+  double2 *rec_x = nullptr;   // chunk records (x1, x2)
+  double *rec_y = nullptr;    // chunk records y
+  int2 *seg = nullptr;        // [tile][batch] -> (offset within batch, count)
 
   cufftHandle plan_g1 = 0, plan_g2 = 0, plan_c2r_L = 0, plan_r2c_L = 0, plan_t2 = 0;
   cudaGraphExec_t cg_exec = nullptr;
@@ -157,11 +181,28 @@ efgp_status interp_targets(efgp_plan *pl, const double *xt, int64_t q, double *m
 namespace efgp {
 
 // ES kernel phi(z) = exp(beta (sqrt(1 - z^2) - 1)) on |z| <= 1 (FINUFFT's exponential of
-// semicircle).  Evaluated directly in fp64.
+// semicircle).  Evaluated directly in fp64 (reference; the kernels use es_weights).
 __device__ __forceinline__ double es_kernel(double z, double beta) {
   double a = fma(-z, z, 1.0);
   a = a > 0.0 ? a : 0.0;
   return exp(beta * (sqrt(a) - 1.0));
+}
+
+// Weights of the W cells i0 .. i0+W-1 for a point at grid coordinate t: i0 = ceil(t - W/2),
+// u = i0 - (t - W/2) in [0,1), w[a] = phi~_a(u) by Horner (degree W+2) in s = 2u - 1.
+template <int W>
+__device__ __forceinline__ int es_weights(double t, const EsPoly &P, double (&w)[W]) {
+  const double tm = t - 0.5 * W;
+  const double i0 = ceil(tm);
+  const double s = 2.0 * (i0 - tm) - 1.0;
+#pragma unroll
+  for (int a = 0; a < W; ++a) {
+    double acc = P.c[a][W + 2];
+#pragma unroll
+    for (int k = W + 1; k >= 0; --k) acc = fma(acc, s, P.c[a][k]);
+    w[a] = acc;
+  }
+  return (int)i0;
 }
 
 // Signed mode index of FFT bin k in a length-n transform whose modes satisfy |j| <= jmax

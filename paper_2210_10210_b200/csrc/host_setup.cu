@@ -2,6 +2,7 @@
 // Written independently of oracle/ (which uses quadrature where this file uses closed forms).
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 
 #include "efgp_internal.cuh"
 
@@ -70,6 +71,78 @@ void gauss_legendre(int n, std::vector<double> &x, std::vector<double> &w) {
     x[n - 1 - i] = z;
     w[i] = w[n - 1 - i] = 2.0 / ((1.0 - z * z) * pp * pp);
   }
+}
+
+// Piecewise-polynomial ES kernel: for cell offset a in [0, w) and
+// u in [0, 1), phi_a(u) = phi((2(a+u) - w)/w) is approximated by a degree-(w+2) polynomial in
+// s = 2u - 1 from Chebyshev interpolation, stored as monomial coefficients c[a][k].
+void es_poly_fit(int w, double beta, EsPoly &out) {
+  std::memset(&out, 0, sizeof(out));
+  const int p = w + 2;  // degree
+  out.deg = p;
+  const int nn = p + 1;
+  for (int a = 0; a < w; ++a) {
+    std::vector<double> fs(nn), cheb(nn, 0.0);
+    for (int j = 0; j < nn; ++j) {
+      const double s = std::cos(kPi * (j + 0.5) / nn);
+      const double u = 0.5 * (s + 1.0);
+      const double z = (2.0 * (a + u) - w) / w;
+      const double q = 1.0 - z * z;
+      fs[j] = std::exp(beta * (std::sqrt(q > 0 ? q : 0.0) - 1.0));
+    }
+    for (int k = 0; k < nn; ++k) {
+      double sacc = 0.0;
+      for (int j = 0; j < nn; ++j) sacc += fs[j] * std::cos(kPi * k * (j + 0.5) / nn);
+      cheb[k] = (k == 0 ? 1.0 : 2.0) * sacc / nn;
+    }
+    // Chebyshev -> monomial: T_0 = 1, T_1 = s, T_{k+1} = 2 s T_k - T_{k-1}
+    std::vector<double> Tm1(nn, 0.0), T0(nn, 0.0), T1(nn, 0.0), mono(nn, 0.0);
+    T0[0] = 1.0;
+    for (int i = 0; i < nn; ++i) mono[i] += cheb[0] * T0[i];
+    if (nn > 1) {
+      T1[1] = 1.0;
+      for (int i = 0; i < nn; ++i) mono[i] += cheb[1] * T1[i];
+    }
+    for (int k = 2; k < nn; ++k) {
+      std::vector<double> T2(nn, 0.0);
+      for (int i = 0; i < nn; ++i) {
+        if (i > 0) T2[i] += 2.0 * T1[i - 1];
+        T2[i] -= T0[i];
+      }
+      for (int i = 0; i < nn; ++i) mono[i] += cheb[k] * T2[i];
+      T0 = T1;
+      T1 = T2;
+    }
+    for (int k = 0; k < nn; ++k) out.c[a][k] = mono[k];
+  }
+}
+
+double es_poly_eval(const EsPoly &P, int a, double u) {
+  const double s = 2.0 * u - 1.0;
+  double acc = P.c[a][P.deg];
+  for (int k = P.deg - 1; k >= 0; --k) acc = acc * s + P.c[a][k];
+  return acc;
+}
+
+// phihat[k] = int phi~(t) cos(k t) dt over the support [-alpha, alpha], alpha = w pi / n, with phi~
+// the piecewise polynomial actually used by the kernels (so deconvolution and spreading agree):
+// = alpha (2/w) sum_a int_0^1 phi~_a(u) cos(k alpha (2(a+u) - w)/w) du, Gauss-Legendre per piece.
+std::vector<double> es_fourier_table_poly(const EsPoly &P, int w, int64_t n, int64_t kmax) {
+  const double alpha = w * kPi / (double)n;
+  const int nq = 2 * P.deg + 40;
+  std::vector<double> z, wq;
+  gauss_legendre(nq, z, wq);
+  std::vector<double> t(kmax + 1, 0.0);
+  for (int a = 0; a < w; ++a) {
+    for (int i = 0; i < nq; ++i) {
+      const double u = 0.5 * (z[i] + 1.0), wu = 0.5 * wq[i];
+      const double f = es_poly_eval(P, a, u);
+      const double zz = (2.0 * (a + u) - w) / w;
+      for (int64_t k = 0; k <= kmax; ++k) t[k] += wu * f * std::cos(k * alpha * zz);
+    }
+  }
+  for (auto &v : t) v *= alpha * 2.0 / w;
+  return t;
 }
 
 std::vector<double> es_fourier_table(int w, double beta, int64_t n, int64_t kmax) {
@@ -141,6 +214,8 @@ std::string validate_and_choose(Params &p, const efgp_options &opt) {
   p.L = next_smooth(4 * p.m + 1);
   p.spread_method = opt.spread_method;
   p.graph_iters = opt.graph_iters > 0 ? opt.graph_iters : 8;
+  es_poly_fit(p.w, p.beta_es, p.poly);
+  resolve_spread_method(p);
   return "";
 }
 

@@ -29,7 +29,7 @@ __device__ __forceinline__ int wrapn(int i, int n) {
 
 template <int D, int W, bool SMEM>
 __global__ void __launch_bounds__(256) k_interp(const double *__restrict__ xt, int64_t q,
-                                                const double *__restrict__ grid, int n, double h, double beta,
+                                                const double *__restrict__ grid, int n, double h, EsPoly P,
                                                 int lo, int A, double *__restrict__ mu, int *__restrict__ err) {
   extern __shared__ double sgrid[];
   if constexpr (SMEM) {
@@ -65,13 +65,7 @@ __global__ void __launch_bounds__(256) k_interp(const double *__restrict__ xt, i
     int base[D];
     double wt[D][W];
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      const double t = h * xc[k] * (double)n;
-      const int i0 = (int)ceil(t - 0.5 * W);
-      base[k] = i0;
-#pragma unroll
-      for (int a = 0; a < W; ++a) wt[k][a] = es_kernel(((double)(i0 + a) - t) * (2.0 / W), beta);
-    }
+    for (int k = 0; k < D; ++k) base[k] = es_weights<W>(h * xc[k] * (double)n, P, wt[k]);
     double acc = 0.0;
     if constexpr (D == 1) {
 #pragma unroll
@@ -133,13 +127,13 @@ static efgp_status launch_interp(efgp_plan *pl, const double *xt, int64_t q, dou
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     EFGP_CUDA(cudaFuncSetAttribute(k_interp<D, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-    k_interp<D, W, true><<<(unsigned)blocks, 256, sb, s>>>(xt, q, pl->t2grid, (int)P.n2, P.h, P.beta_es, o.lo, o.A,
+    k_interp<D, W, true><<<(unsigned)blocks, 256, sb, s>>>(xt, q, pl->t2grid, (int)P.n2, P.h, P.poly, o.lo, o.A,
                                                            mu, pl->dflags);
   } else {
     const int64_t cap = (int64_t)pl->num_sms * 16;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    k_interp<D, W, false><<<(unsigned)blocks, 256, 0, s>>>(xt, q, pl->t2grid, (int)P.n2, P.h, P.beta_es, o.lo, o.A,
+    k_interp<D, W, false><<<(unsigned)blocks, 256, 0, s>>>(xt, q, pl->t2grid, (int)P.n2, P.h, P.poly, o.lo, o.A,
                                                            mu, pl->dflags);
   }
   EFGP_CUDA(cudaGetLastError());

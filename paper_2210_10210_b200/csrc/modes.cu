@@ -143,14 +143,17 @@ efgp_status type1_modes(efgp_plan *pl, double *modes_out, cudaStream_t s) {
   EFGP_CUFFT(cufftSetStream(pl->plan_g2, s));
   EFGP_CUFFT(cufftExecD2Z(pl->plan_g1, pl->g1, pl->G1h));
   EFGP_CUFFT(cufftExecD2Z(pl->plan_g2, pl->g2, pl->G2h));
-  const double s1 = std::pow(2.0 * kPi / (double)P.n1, P.d), s2 = std::pow(2.0 * kPi / (double)P.n2, P.d);
+  // the strength-y grid is n_rhs (= n1 for SORTED spreading, else n2); psi1 covers k <= 2m on n1
+  const int64_t nr = P.n_rhs;
+  const double *psir = (nr == P.n1) ? pl->psi1 : pl->psi2;
+  const double s1 = std::pow(2.0 * kPi / (double)P.n1, P.d), s2 = std::pow(2.0 * kPi / (double)nr, P.d);
   double2 *vh = reinterpret_cast<double2 *>(modes_out);
   double2 *fyh = vh + P.Kvh;
   const unsigned g = grid_for(P.Kvh + P.Mh, 256, pl->num_sms);
   switch (P.d) {
-    case 1: k_deconv<1><<<g, 256, 0, s>>>(pl->G1h, P.n1, pl->G2h, P.n2, (int)P.m, pl->psi1, pl->psi2, s1, s2, vh, fyh, P.Kvh, P.Mh); break;
-    case 2: k_deconv<2><<<g, 256, 0, s>>>(pl->G1h, P.n1, pl->G2h, P.n2, (int)P.m, pl->psi1, pl->psi2, s1, s2, vh, fyh, P.Kvh, P.Mh); break;
-    case 3: k_deconv<3><<<g, 256, 0, s>>>(pl->G1h, P.n1, pl->G2h, P.n2, (int)P.m, pl->psi1, pl->psi2, s1, s2, vh, fyh, P.Kvh, P.Mh); break;
+    case 1: k_deconv<1><<<g, 256, 0, s>>>(pl->G1h, P.n1, pl->G2h, nr, (int)P.m, pl->psi1, psir, s1, s2, vh, fyh, P.Kvh, P.Mh); break;
+    case 2: k_deconv<2><<<g, 256, 0, s>>>(pl->G1h, P.n1, pl->G2h, nr, (int)P.m, pl->psi1, psir, s1, s2, vh, fyh, P.Kvh, P.Mh); break;
+    case 3: k_deconv<3><<<g, 256, 0, s>>>(pl->G1h, P.n1, pl->G2h, nr, (int)P.m, pl->psi1, psir, s1, s2, vh, fyh, P.Kvh, P.Mh); break;
   }
   EFGP_CUDA(cudaGetLastError());
   return EFGP_OK;

@@ -61,14 +61,18 @@ def test_spread_strategies_agree():
     c = CONFIGS["c5"]
     x, y, _ = generate(c, N=200_000, q=1)
     out = {}
-    for method in ("global", "smem"):
+    for method in ("global", "smem", "sorted"):
         g = model(c, max_iter=1, spread=method)
         g.fit(dev(x), dev(y))
         assert g.info()["spread_method"] == method
         out[method] = (g.vector("v"), g.vector("rhs"))
         g.close()
+    # v: same grid and kernel, different summation order -> roundoff
     assert rel(out["smem"][0], out["global"][0]) < 1e-12
+    assert rel(out["sorted"][0], out["global"][0]) < 1e-12
     assert rel(out["smem"][1], out["global"][1]) < 1e-12
+    # SORTED spreads y on the n1 grid (finer) instead of n2: agree within the NUFFT tolerance
+    assert rel(out["sorted"][1], out["global"][1]) < 2 * c.eps / 10
 
 
 @pytest.mark.parametrize("name", list(CONFIGS))
