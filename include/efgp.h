@@ -81,6 +81,7 @@ typedef struct {
   double nufft_tol;
   int spread_method;    /* method actually used by the last fit                   */
   double t_spread_ms, t_modes_ms, t_solve_ms, t_predict_ms; /* device time of the last calls */
+  int64_t sorted_tile, sorted_parts, sorted_chunk;           /* SORTED geometry (0 otherwise)  */
 } efgp_info;
 
 /* Fill *opt with defaults (all zero / automatic). */

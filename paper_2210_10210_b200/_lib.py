@@ -28,7 +28,8 @@ class Info(C.Structure):
                 ("max_iter", C.c_int64), ("nf1", C.c_int64), ("nf2", C.c_int64), ("L", C.c_int64),
                 ("w", C.c_int64), ("beta_es", C.c_double), ("nufft_tol", C.c_double),
                 ("spread_method", C.c_int), ("t_spread_ms", C.c_double), ("t_modes_ms", C.c_double),
-                ("t_solve_ms", C.c_double), ("t_predict_ms", C.c_double)]
+                ("t_solve_ms", C.c_double), ("t_predict_ms", C.c_double), ("sorted_tile", C.c_int64),
+                ("sorted_parts", C.c_int64), ("sorted_chunk", C.c_int64)]
 
 
 # every symbol include/efgp.h declares, with (restype, argtypes)

@@ -74,10 +74,17 @@ efgp_status build(efgp_plan *pl) {
   EFGP_TRY(dalloc(pl, &pl->G1h, G1h));
   EFGP_TRY(dalloc(pl, &pl->G2h, Grh));
   if (P.spread_method == EFGP_SPREAD_SORTED) {
+    sorted_geometry(pl->P, pl->num_sms);
     const int64_t nbmax = (P.chunk + P.bin_batch - 1) / P.bin_batch;
-    EFGP_TRY(dalloc(pl, &pl->rec_x, nbmax * P.bin_batch));
-    EFGP_TRY(dalloc(pl, &pl->rec_y, nbmax * P.bin_batch));
-    EFGP_TRY(dalloc(pl, &pl->seg, (int64_t)P.ntile1 * P.ntile1 * nbmax));
+    for (int k = 0; k < 2; ++k) {
+      EFGP_TRY(dalloc(pl, &pl->rec_x[k], nbmax * P.bin_batch));
+      EFGP_TRY(dalloc(pl, &pl->rec_y[k], nbmax * P.bin_batch));
+      EFGP_TRY(dalloc(pl, &pl->seg[k], (int64_t)P.ntile1 * P.ntile1 * nbmax));
+      EFGP_CUDA(cudaEventCreateWithFlags(&pl->ev_bin[k], cudaEventDisableTiming));
+      EFGP_CUDA(cudaEventCreateWithFlags(&pl->ev_tiles[k], cudaEventDisableTiming));
+    }
+    EFGP_CUDA(cudaEventCreateWithFlags(&pl->ev_sp, cudaEventDisableTiming));
+    EFGP_CUDA(cudaStreamCreateWithFlags(&pl->bin_stream, cudaStreamNonBlocking));
   }
   EFGP_TRY(dalloc(pl, &pl->modes, 2 * (P.Kvh + P.Mh)));
   EFGP_TRY(dalloc(pl, &pl->modes_sum, 2 * (P.Kvh + P.Mh)));
@@ -419,6 +426,11 @@ efgp_status efgp_get_info(efgp_handle pl, efgp_info *o) {
   o->t_modes_ms = pl->t_modes;
   o->t_solve_ms = pl->t_solve;
   o->t_predict_ms = pl->t_predict;
+  if (P.spread_method == EFGP_SPREAD_SORTED) {
+    o->sorted_tile = P.tile;
+    o->sorted_parts = P.tile_parts;
+    o->sorted_chunk = P.chunk;
+  }
   return EFGP_OK;
 }
 
@@ -443,9 +455,12 @@ void efgp_destroy(efgp_handle pl) {
   void *bufs[] = {pl->D_half, pl->psi1, pl->psi2, pl->g1, pl->g2, pl->G1h, pl->G2h, pl->modes, pl->modes_sum,
                   pl->Xbox, pl->Yr, pl->vhat, pl->Zbox, pl->b, pl->x, pl->r, pl->p, pl->Ap, pl->partials,
                   pl->scal, pl->hist, pl->dflags, pl->T2box, pl->t2grid, pl->stage[0], pl->stage[1],
-                  pl->rec_x, pl->rec_y, pl->seg};
+                  pl->rec_x[0], pl->rec_y[0], pl->seg[0], pl->rec_x[1], pl->rec_y[1], pl->seg[1]};
   for (void *b : bufs)
     if (b) cudaFree(b);
+  for (cudaEvent_t e : {pl->ev_bin[0], pl->ev_bin[1], pl->ev_tiles[0], pl->ev_tiles[1], pl->ev_sp})
+    if (e) cudaEventDestroy(e);
+  if (pl->bin_stream) cudaStreamDestroy(pl->bin_stream);
   if (pl->h_pinned) cudaFreeHost(pl->h_pinned);
   for (auto &e : pl->ev)
     if (e) cudaEventDestroy(e);

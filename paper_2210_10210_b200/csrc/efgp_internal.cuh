@@ -46,6 +46,7 @@ struct Params {
   // SORTED spreading geometry (2D)
   int s_lo = 0, s_count = 0;   // start cells i0 in [s_lo, s_lo + s_count) per dim
   int tile = 16, ntile1 = 0;   // tile side (start cells) and tiles per dim
+  int tile_parts = 1;          // work items per tile per chunk
   int64_t chunk = 0;           // points per chunk
   int bin_batch = 2048;        // points per bin CTA
 };
@@ -60,8 +61,10 @@ std::vector<double> es_fourier_table(int w, double beta, int64_t n, int64_t kmax
 void es_poly_fit(int w, double beta, EsPoly &out);
 double es_poly_eval(const EsPoly &P, int a, double u);
 std::vector<double> es_fourier_table_poly(const EsPoly &P, int w, int64_t n, int64_t kmax);
-// spread.cu: choose the spreading strategy and its geometry (sets spread_method, n_rhs, tiles)
+// spread.cu: choose the spreading strategy (sets spread_method, n_rhs)
 void resolve_spread_method(Params &p);
+// spread_sorted.cu: tile geometry of the SORTED strategy
+void sorted_geometry(Params &p, int num_sms);
 
 struct DevBuf {
   void *ptr = nullptr;
@@ -117,9 +120,12 @@ struct efgp_plan {
   int64_t stage_pts = 0;
 
   // SORTED spreading: per-chunk binned records and the (tile x batch) segment table
-  double2 *rec_x = nullptr;   // chunk records (x1, x2)
-  double *rec_y = nullptr;    // chunk records y
-  int2 *seg = nullptr;        // [tile][batch] -> (offset within batch, count)
+  // (double-buffered: binning of chunk k+1 on bin_stream overlaps accumulation of chunk k)
+  double2 *rec_x[2] = {nullptr, nullptr};  // chunk records (x1, x2)
+  double *rec_y[2] = {nullptr, nullptr};   // chunk records y
+  int2 *seg[2] = {nullptr, nullptr};       // [tile][batch] -> (offset within batch, count)
+  cudaStream_t bin_stream = nullptr;
+  cudaEvent_t ev_bin[2] = {nullptr, nullptr}, ev_tiles[2] = {nullptr, nullptr}, ev_sp = nullptr;
 
   cufftHandle plan_g1 = 0, plan_g2 = 0, plan_c2r_L = 0, plan_r2c_L = 0, plan_t2 = 0;
   cudaGraphExec_t cg_exec = nullptr;
@@ -141,6 +147,7 @@ namespace efgp {
 efgp_status spread_points(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s);
 efgp_status spread_begin(efgp_plan *pl, cudaStream_t s);
 efgp_status spread_end(efgp_plan *pl, cudaStream_t s);
+efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s);
 // modes.cu
 efgp_status type1_modes(efgp_plan *pl, double *modes_out, cudaStream_t s);
 efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s);
