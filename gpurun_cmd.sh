@@ -1,2 +1,5 @@
-python tools/spread_sweep.py --N 2e8 --variants '[{}, {"EFGP_SORTED_TILE": 8, "EFGP_SORTED_Q": 2}, {"EFGP_SORTED_TILE": 10, "EFGP_SORTED_Q": 2}, {"EFGP_SORTED_TILE": 11, "EFGP_SORTED_Q": 1}, {"EFGP_SORTED_TILE": 11, "EFGP_SORTED_Q": 2}, {"EFGP_SORTED_TILE": 11, "EFGP_SORTED_Q": 4}, {"EFGP_SORTED_TILE": 12, "EFGP_SORTED_Q": 2}, {"EFGP_SORTED_TILE": 16, "EFGP_SORTED_Q": 2}, {"EFGP_SORTED_TILE": 11, "EFGP_SORTED_Q": 2, "EFGP_SORTED_CHUNK": 1048576}, {"EFGP_SORTED_TILE": 11, "EFGP_SORTED_Q": 4, "EFGP_SORTED_CHUNK": 4194304}]' > gpurun_out/sweep2.log 2>&1; cat gpurun_out/sweep2.log
-timeout 600 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+for CH in 4194304 16777216 67108864; do
+python tools/spread_once.py --N 1.34e8 --fits 2 --weights mixed > gpurun_out/plain_$CH.log 2>&1
+EFGP_SORTED_CHUNK=$CH ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_ch$CH.csv -k regex:"k_bin5|k_tiles4" python tools/spread_once.py --N 1.34e8 --fits 1 --weights mixed > gpurun_out/ncu_$CH.log 2>&1
+done
+for W in fp64 fp32; do EFGP_SORTED_CHUNK=16777216 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_w$W.csv -k regex:"k_bin5|k_tiles4" python tools/spread_once.py --N 1.34e8 --fits 1 --weights $W > gpurun_out/ncu_w$W.log 2>&1; done

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define EFGP_ABI_VERSION 1
+#define EFGP_ABI_VERSION 2
 
 typedef struct efgp_plan *efgp_handle;
 
@@ -55,6 +55,16 @@ typedef enum { EFGP_RESCALE_NONE = 0, EFGP_RESCALE_L2 = 1, EFGP_RESCALE_PRINTED 
 /* Spreading strategy for the type-1 step. AUTO picks the fastest valid one. */
 typedef enum { EFGP_SPREAD_AUTO = 0, EFGP_SPREAD_GLOBAL = 1, EFGP_SPREAD_SMEM = 2, EFGP_SPREAD_SORTED = 3 } efgp_spread_method;
 
+/* Arithmetic of the SORTED spreader (DESIGN.md §7 "K1 precision").  FFTs, CG, deconvolution, the
+ * fine grids and all outputs are fp64 in every mode.
+ *   FP64 : kernel weights and accumulation in fp64 (default).
+ *   FP32 : kernel weights evaluated in fp32 from the fp64 reduced coordinate (relative error ~1e-7),
+ *          fp64 accumulation.
+ *   MIXED: fp32 weights; each start cell's window sums one shared-memory round (<= ~40 points) in
+ *          fp32 (packed FFMA2) and adds it to its fp64 window.
+ * FP32 and MIXED are refused (EFGP_ERR_INVALID) for nufft_tol < 1e-6. */
+typedef enum { EFGP_WEIGHTS_FP64 = 0, EFGP_WEIGHTS_FP32 = 1, EFGP_WEIGHTS_MIXED = 2 } efgp_weights;
+
 typedef struct {
   double h;            /* grid spacing override when m > 0                        */
   int64_t m;           /* modes per dimension override (2m+1 per dim), 0 = rule (Alg a1 step 1) */
@@ -64,6 +74,7 @@ typedef struct {
   int matern_rescale;  /* efgp_rescale, default EFGP_RESCALE_L2                                  */
   int spread_method;   /* efgp_spread_method                                                     */
   int graph_iters;     /* CG iterations per CUDA-graph launch, 0 = default                        */
+  int spread_weights;  /* efgp_weights, default EFGP_WEIGHTS_FP64                                  */
   void *stream;        /* cudaStream_t for all device work (NULL = default stream)               */
 } efgp_options;
 
@@ -81,7 +92,8 @@ typedef struct {
   double nufft_tol;
   int spread_method;    /* method actually used by the last fit                   */
   double t_spread_ms, t_modes_ms, t_solve_ms, t_predict_ms; /* device time of the last calls */
-  int64_t sorted_tile, sorted_parts, sorted_chunk;           /* SORTED geometry (0 otherwise)  */
+  int64_t sorted_t1, sorted_t2, sorted_chunk, sorted_round;   /* SORTED geometry (0 otherwise)  */
+  int64_t spread_precision;                                   /* efgp_weights of the SORTED path */
 } efgp_info;
 
 /* Fill *opt with defaults (all zero / automatic). */

@@ -58,6 +58,8 @@ efgp_status build(efgp_plan *pl) {
   // deconvolution tables of the piecewise-polynomial kernel the kernels actually use
   const std::vector<double> psi1 = es_fourier_table_poly(P.poly, P.w, P.n1, 2 * P.m);
   const std::vector<double> psi2 = es_fourier_table_poly(P.poly, P.w, P.n2, P.m);
+  EFGP_TRY(dalloc(pl, &pl->poly_dev, 1));
+  EFGP_CUDA(cudaMemcpy(pl->poly_dev, &P.poly, sizeof(EsPoly), cudaMemcpyHostToDevice));
   EFGP_TRY(dalloc(pl, &pl->D_half, P.Mh));
   EFGP_TRY(dalloc(pl, &pl->psi1, psi1.size()));
   EFGP_TRY(dalloc(pl, &pl->psi2, psi2.size()));
@@ -75,11 +77,10 @@ efgp_status build(efgp_plan *pl) {
   EFGP_TRY(dalloc(pl, &pl->G2h, Grh));
   if (P.spread_method == EFGP_SPREAD_SORTED) {
     sorted_geometry(pl->P, pl->num_sms);
-    const int64_t nbmax = (P.chunk + P.bin_batch - 1) / P.bin_batch;
     for (int k = 0; k < 2; ++k) {
-      EFGP_TRY(dalloc(pl, &pl->rec_x[k], nbmax * P.bin_batch));
-      EFGP_TRY(dalloc(pl, &pl->rec_y[k], nbmax * P.bin_batch));
-      EFGP_TRY(dalloc(pl, &pl->seg[k], (int64_t)P.ntile1 * P.ntile1 * nbmax));
+      // + 2 records of slack: the bulk copies read an aligned superset of each round
+      EFGP_TRY(dalloc(pl, &pl->rec[k], ((int64_t)P.ntiles * P.cap + 2) * 3));
+      EFGP_TRY(dalloc(pl, &pl->tcnt[k], P.ntiles));
       EFGP_CUDA(cudaEventCreateWithFlags(&pl->ev_bin[k], cudaEventDisableTiming));
       EFGP_CUDA(cudaEventCreateWithFlags(&pl->ev_tiles[k], cudaEventDisableTiming));
     }
@@ -427,9 +428,11 @@ efgp_status efgp_get_info(efgp_handle pl, efgp_info *o) {
   o->t_solve_ms = pl->t_solve;
   o->t_predict_ms = pl->t_predict;
   if (P.spread_method == EFGP_SPREAD_SORTED) {
-    o->sorted_tile = P.tile;
-    o->sorted_parts = P.tile_parts;
+    o->sorted_t1 = P.T1;
+    o->sorted_t2 = P.T2;
     o->sorted_chunk = P.chunk;
+    o->sorted_round = P.round;
+    o->spread_precision = P.spread_mode;
   }
   return EFGP_OK;
 }
@@ -452,10 +455,10 @@ void efgp_destroy(efgp_handle pl) {
   if (pl->cg_exec) cudaGraphExecDestroy(pl->cg_exec);
   for (cufftHandle h : {pl->plan_g1, pl->plan_g2, pl->plan_c2r_L, pl->plan_r2c_L, pl->plan_t2})
     if (h) cufftDestroy(h);
-  void *bufs[] = {pl->D_half, pl->psi1, pl->psi2, pl->g1, pl->g2, pl->G1h, pl->G2h, pl->modes, pl->modes_sum,
+  void *bufs[] = {pl->poly_dev, pl->D_half, pl->psi1, pl->psi2, pl->g1, pl->g2, pl->G1h, pl->G2h, pl->modes, pl->modes_sum,
                   pl->Xbox, pl->Yr, pl->vhat, pl->Zbox, pl->b, pl->x, pl->r, pl->p, pl->Ap, pl->partials,
                   pl->scal, pl->hist, pl->dflags, pl->T2box, pl->t2grid, pl->stage[0], pl->stage[1],
-                  pl->rec_x[0], pl->rec_y[0], pl->seg[0], pl->rec_x[1], pl->rec_y[1], pl->seg[1]};
+                  pl->rec[0], pl->tcnt[0], pl->rec[1], pl->tcnt[1]};
   for (void *b : bufs)
     if (b) cudaFree(b);
   for (cudaEvent_t e : {pl->ev_bin[0], pl->ev_bin[1], pl->ev_tiles[0], pl->ev_tiles[1], pl->ev_sp})

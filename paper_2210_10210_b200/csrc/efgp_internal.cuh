@@ -19,6 +19,9 @@ struct EsPoly {
   double c[kMaxW][kMaxW + 3];
   int deg;
 };
+struct EsPolyF {  // the same coefficients rounded to fp32 (fp32-weight spreading)
+  float c[kMaxW][kMaxW + 3];
+};
 
 // Host-side parameter record.
 struct Params {
@@ -43,12 +46,17 @@ struct Params {
   int spread_method = EFGP_SPREAD_AUTO;  // resolved at setup (never AUTO afterwards)
   int graph_iters = 8;
   EsPoly poly{};
+  EsPolyF polyf{};
+  int spread_mode = 0;         // SORTED precision: 0 fp64, 1 fp32 weights, 2 fp32 weights + round sums
   // SORTED spreading geometry (2D)
   int s_lo = 0, s_count = 0;   // start cells i0 in [s_lo, s_lo + s_count) per dim
-  int tile = 16, ntile1 = 0;   // tile side (start cells) and tiles per dim
-  int tile_parts = 1;          // work items per tile per chunk
+  int T1 = 16, T2 = 16;        // tile of T1 x T2 start cells (T1 T2 <= 256)
+  int nt1 = 0, nt2 = 0, ntiles = 0;
+  int cap = 0;                 // records per tile list per chunk
+  int round = 0;               // records per shared-memory round
+  int tiles_grid = 0;          // CTAs of the accumulation kernel
+  int bin_grid = 0;            // CTAs of the binning kernel
   int64_t chunk = 0;           // points per chunk
-  int bin_batch = 2048;        // points per bin CTA
 };
 
 // host_setup.cu
@@ -87,6 +95,7 @@ struct efgp_plan {
   double *D_half = nullptr;   // Mh spectral weights (eq 117) on the J_m half
   double *psi1 = nullptr;     // ES Fourier transform, grid n1, k = 0..2m
   double *psi2 = nullptr;     // grid n2, k = 0..m
+  efgp::EsPoly *poly_dev = nullptr;  // the kernel-weight polynomial in global memory
 
   // type-1 grids and spectra
   double *g1 = nullptr;       // n1^d real
@@ -119,11 +128,10 @@ struct efgp_plan {
   double *stage[2] = {nullptr, nullptr};
   int64_t stage_pts = 0;
 
-  // SORTED spreading: per-chunk binned records and the (tile x batch) segment table
+  // SORTED spreading: per-chunk tile lists of (x1, x2, y) records and their counts
   // (double-buffered: binning of chunk k+1 on bin_stream overlaps accumulation of chunk k)
-  double2 *rec_x[2] = {nullptr, nullptr};  // chunk records (x1, x2)
-  double *rec_y[2] = {nullptr, nullptr};   // chunk records y
-  int2 *seg[2] = {nullptr, nullptr};       // [tile][batch] -> (offset within batch, count)
+  double *rec[2] = {nullptr, nullptr};     // ntiles x cap x 3 doubles
+  int *tcnt[2] = {nullptr, nullptr};       // ntiles
   cudaStream_t bin_stream = nullptr;
   cudaEvent_t ev_bin[2] = {nullptr, nullptr}, ev_tiles[2] = {nullptr, nullptr}, ev_sp = nullptr;
 
@@ -199,7 +207,7 @@ __device__ __forceinline__ double es_kernel(double z, double beta) {
 // u = i0 - (t - W/2) in [0,1), w[a] = phi~_a(u) by Horner (degree W+2) in s = 2u - 1.
 template <int W>
 __device__ __forceinline__ int es_weights(double t, const EsPoly &P, double (&w)[W]) {
-  const double tm = t - 0.5 * W;
+  const double tm = __dsub_rn(t, 0.5 * W);  // no FMA contraction: the SORTED binning must agree
   const double i0 = ceil(tm);
   const double s = 2.0 * (i0 - tm) - 1.0;
 #pragma unroll

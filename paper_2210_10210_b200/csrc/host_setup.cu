@@ -215,6 +215,15 @@ std::string validate_and_choose(Params &p, const efgp_options &opt) {
   p.spread_method = opt.spread_method;
   p.graph_iters = opt.graph_iters > 0 ? opt.graph_iters : 8;
   es_poly_fit(p.w, p.beta_es, p.poly);
+  for (int a = 0; a < kMaxW; ++a)
+    for (int k = 0; k < kMaxW + 3; ++k) p.polyf.c[a][k] = (float)p.poly.c[a][k];
+  // fp32 kernel weights (fp64 accumulation) only when asked for, and only where fp32 rounding of the
+  // weights (~1e-7 relative) sits well below the NUFFT tolerance (DESIGN.md §7 "K1 weights")
+  if (opt.spread_weights < EFGP_WEIGHTS_FP64 || opt.spread_weights > EFGP_WEIGHTS_MIXED)
+    return "unknown spread_weights";
+  if (opt.spread_weights != EFGP_WEIGHTS_FP64 && p.nufft_tol < 1e-6)
+    return "fp32 spreading weights need nufft_tol >= 1e-6";
+  p.spread_mode = opt.spread_weights;
   resolve_spread_method(p);
   return "";
 }

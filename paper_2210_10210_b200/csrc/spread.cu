@@ -205,7 +205,8 @@ static size_t smem_bytes(const Params &P) {
 
 void resolve_spread_method(Params &p) {
   int m = p.spread_method;
-  const bool sorted_ok = p.d == 2 && p.w <= 6;
+  // SORTED: 2D, register windows up to 6 x 6, start-cell lookup tables up to 2048 per dimension
+  const bool sorted_ok = p.d == 2 && p.w <= 6 && p.h * p.n1 + p.w < 2048;
   const bool smem_ok = smem_bytes(p) <= 200 * 1024;
   if (m == EFGP_SPREAD_AUTO) m = sorted_ok ? EFGP_SPREAD_SORTED : (smem_ok ? EFGP_SPREAD_SMEM : EFGP_SPREAD_GLOBAL);
   if (m == EFGP_SPREAD_SORTED && !sorted_ok) m = smem_ok ? EFGP_SPREAD_SMEM : EFGP_SPREAD_GLOBAL;
@@ -267,8 +268,10 @@ efgp_status spread_points(efgp_plan *pl, const double *x, const double *y, int64
   if (N <= 0) return EFGP_OK;
   int method = pl->P.spread_method;
   if (method == EFGP_SPREAD_SORTED) {
-    // the binning loads points as 16-byte pairs; an unaligned x falls back to GLOBAL (same grids)
-    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) return spread_sorted2(pl, x, y, N, s);
+    // the binning bulk-copies x and y (16-byte alignment); unaligned inputs fall back to GLOBAL
+    // (same grids, same kernel)
+    if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0)
+      return spread_sorted2(pl, x, y, N, s);
     method = EFGP_SPREAD_GLOBAL;
   }
   switch (pl->P.d) {

@@ -69,13 +69,13 @@ class EFGP:
 
     kernel: "se" or "matern" (nu >= 1/2); ell, sigma, eps as in the paper (Alg a1); d in {1,2,3}.
     Optional overrides: h and m (both), cg_tol (default eps), max_iter, nufft_tol (default eps/10),
-    matern_rescale ("A" true L2 norm, "B" none, "P" printed), spread ("auto"/"global"/"smem").
+    matern_rescale ("A" true L2 norm, "B" none, "P" printed), spread ("auto"/"global"/"smem"/"sorted"), weights ("fp64"/"fp32"/"mixed": SORTED spreading arithmetic, include/efgp.h).
     """
 
     def __init__(self, kernel: str, ell: float, sigma: float, eps: float, d: int, nu: float = 0.0, *,
                  h: float | None = None, m: int | None = None, cg_tol: float | None = None,
                  max_iter: int | None = None, nufft_tol: float | None = None, matern_rescale: str = "A",
-                 spread: str = "auto", graph_iters: int | None = None, stream=None, device=None):
+                 spread: str = "auto", weights: str = "fp64", graph_iters: int | None = None, stream=None, device=None):
         import torch
         self._lib = L.load()
         self._torch = torch
@@ -97,6 +97,7 @@ class EFGP:
             opt.nufft_tol = float(nufft_tol)
         opt.matern_rescale = _RESCALE[matern_rescale]
         opt.spread_method = _SPREAD[spread]
+        opt.spread_weights = {"fp64": 0, "fp32": 1, "mixed": 2}[weights]
         if graph_iters is not None:
             opt.graph_iters = int(graph_iters)
         opt.stream = C.c_void_p(stream.cuda_stream)

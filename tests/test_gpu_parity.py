@@ -75,6 +75,71 @@ def test_spread_strategies_agree():
     assert rel(out["sorted"][1], out["global"][1]) < 2 * c.eps / 10
 
 
+@pytest.mark.parametrize("weights", ["fp32", "mixed"])
+@pytest.mark.parametrize("name", ["c2", "c5"])
+def test_type1_fp32_weights(name, weights):
+    # SORTED with fp32 kernel-weight evaluation (fp64 or per-round fp32 accumulation): same NUFFT
+    # tolerance gate as the fp64 path
+    c = CONFIGS[name]
+    N, _ = T1_SIZES[name]
+    x, y, _ = generate(c, N=N, q=1)
+    g = model(c, max_iter=1, spread="sorted", weights=weights)
+    g.fit(dev(x), dev(y))
+    inf = g.info()
+    assert inf["spread_method"] == "sorted" and inf["spread_precision"] == {"fp32": 1, "mixed": 2}[weights]
+    h, m = inf["h"], inf["m"]
+    v_ref = O.toeplitz_vector(x, h, m)
+    b_ref = O.rhs(x, y, h, m, O.spectral_weights(c.kernel, c.ell, c.d, h, m, c.nu))
+    tol = 5 * inf["nufft_tol"]
+    assert rel(gpu_v_full(m, g), v_ref) <= tol
+    assert rel(gpu_rhs_full(g), b_ref) <= tol
+    g.close()
+
+
+def test_fp32_weights_refused_below_1e_6():
+    from paper_2210_10210_b200 import EFGPError
+    c = CONFIGS["c1"]                      # nufft_tol 1e-7
+    with pytest.raises(EFGPError, match="INVALID"):
+        model(c, spread="sorted", weights="fp32")
+
+
+@pytest.mark.parametrize("weights", ["fp64", "fp32", "mixed"])
+def test_sorted_chunks_ragged_and_overflow(weights, monkeypatch):
+    # many chunks with a ragged tail (small chunk), and a point cloud concentrated in one tile so the
+    # tile lists overflow into the direct RED path: SORTED equals GLOBAL to roundoff
+    c = CONFIGS["c5"]
+    rng = np.random.default_rng(7)
+    x_u, y_u, _ = generate(c, N=300_001, q=1)
+    x_c = 0.3 + 0.004 * rng.uniform(size=(150_000, 2))
+    for x, y in ((x_u, y_u), (np.concatenate([x_c, x_u[:1000]]), rng.normal(size=151_000))):
+        monkeypatch.setenv("EFGP_SORTED_CHUNK", "65536")
+        gs = model(c, max_iter=1, spread="sorted", weights=weights)
+        monkeypatch.delenv("EFGP_SORTED_CHUNK")
+        assert gs.info()["sorted_chunk"] == 65536
+        gg = model(c, max_iter=1, spread="global")
+        gs.fit(dev(x), dev(y))
+        gg.fit(dev(x), dev(y))
+        tol = 1e-12 if weights == "fp64" else 1e-6
+        assert rel(gs.vector("v"), gg.vector("v")) < tol
+        assert rel(gs.vector("rhs"), gg.vector("rhs")) < 2 * c.eps / 10   # y on n1 vs n2 grid
+        gs.close()
+        gg.close()
+
+
+@pytest.mark.parametrize("weights", ["fp32", "mixed"])
+def test_whole_path_parity_fp32_weights(weights):
+    c = CONFIGS["c5"]
+    N, _ = CG_SIZES["c5"]
+    x, y, xt = generate(c, N=N, q=2000)
+    cg_tol = c.eps / 1000
+    g = model(c, cg_tol=cg_tol, spread="sorted", weights=weights)
+    g.fit(dev(x), dev(y))
+    mu = g.predict(dev(xt)).cpu().numpy()
+    ref = O.efgp_predict(O.efgp_fit(x, y, c.kernel, c.ell, c.sigma, c.eps, nu=c.nu, cg_tol=cg_tol), xt)
+    assert rel(mu, ref) <= 10 * c.eps
+    g.close()
+
+
 @pytest.mark.parametrize("name", list(CONFIGS))
 def test_type2_predict_from_loaded_weights(name):
     c = CONFIGS[name]

@@ -18,10 +18,10 @@ from efgp_data import CONFIGS
 from efgp_data import gpu as G
 from paper_2210_10210_b200 import EFGP
 c = CONFIGS['c5']
-N = int(float(%r)); runs = int(%r); method = %r
+N = int(float(%r)); runs = int(%r); method = %r; weights = %r
 x, y = G.generate_points(c, 0, N)
 torch.cuda.synchronize()
-g = EFGP(c.kernel, c.ell, c.sigma, c.eps, c.d, c.nu, max_iter=1, spread=method)
+g = EFGP(c.kernel, c.ell, c.sigma, c.eps, c.d, c.nu, max_iter=1, spread=method, weights=weights)
 ts = []
 for r in range(runs + 1):
     import warnings
@@ -30,7 +30,8 @@ for r in range(runs + 1):
         g.fit(x, y)
     ts.append(g.info()['t_spread_ms'])
 inf = g.info()
-print(json.dumps({'method': method, 'tile': inf['sorted_tile'], 'Q': inf['sorted_parts'], 'chunk': inf['sorted_chunk'],
+print(json.dumps({'method': method, 'weights': weights, 'T1': inf['sorted_t1'], 'T2': inf['sorted_t2'],
+                  'R': inf['sorted_round'], 'chunk': inf['sorted_chunk'],
                   'spread_ms': min(ts[1:]), 'pts_per_s': N / (min(ts[1:]) / 1e3)}))
 """
 
@@ -47,8 +48,9 @@ def main():
     for v in variants:
         env = dict(os.environ)
         method = v.pop("method", "sorted")
+        weights = v.pop("weights", "fp64")
         env.update({k: str(val) for k, val in v.items()})
-        code = CHILD % (ROOT, a.N, a.runs, method)
+        code = CHILD % (ROOT, a.N, a.runs, method, weights)
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
         line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-500:]
         print(json.dumps(v), line, flush=True)
