@@ -146,6 +146,11 @@ efgp_status efgp_get_info(efgp_handle, efgp_info *out);
  * entries); *n receives the number available. */
 efgp_status efgp_get_residual_history(efgp_handle, double *host_out, int64_t cap, int64_t *n);
 
+/* Diagnostics: with EFGP_SORTED_TRACE set at setup, the SORTED spreader records globaltimer stamps
+ * [chunk][cta][4] = (binned, acc waits, acc starts, acc done) of the last fit; copies up to cap of
+ * them to host_out and returns how many exist (0 if tracing is off). */
+int64_t efgp_debug_trace(efgp_handle, unsigned long long *host_out, int64_t cap);
+
 const char *efgp_last_error(efgp_handle);
 void efgp_destroy(efgp_handle);
 int efgp_abi_version(void);

@@ -50,6 +50,7 @@ SIGNATURES = {
     "efgp_copy_vector": (C.c_int64, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64]),
     "efgp_get_info": (C.c_int, [C.c_void_p, C.POINTER(Info)]),
     "efgp_get_residual_history": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
+    "efgp_debug_trace": (C.c_int64, [C.c_void_p, C.c_void_p, C.c_int64]),
     "efgp_last_error": (C.c_char_p, [C.c_void_p]),
     "efgp_destroy": (None, [C.c_void_p]),
 }

@@ -77,15 +77,8 @@ efgp_status build(efgp_plan *pl) {
   EFGP_TRY(dalloc(pl, &pl->G2h, Grh));
   if (P.spread_method == EFGP_SPREAD_SORTED) {
     sorted_geometry(pl->P, pl->num_sms);
-    for (int k = 0; k < 2; ++k) {
-      // + 2 records of slack: the bulk copies read an aligned superset of each round
-      EFGP_TRY(dalloc(pl, &pl->rec[k], ((int64_t)P.ntiles * P.cap + 2) * 3));
-      EFGP_TRY(dalloc(pl, &pl->tcnt[k], P.ntiles));
-      EFGP_CUDA(cudaEventCreateWithFlags(&pl->ev_bin[k], cudaEventDisableTiming));
-      EFGP_CUDA(cudaEventCreateWithFlags(&pl->ev_tiles[k], cudaEventDisableTiming));
-    }
-    EFGP_CUDA(cudaEventCreateWithFlags(&pl->ev_sp, cudaEventDisableTiming));
-    EFGP_CUDA(cudaStreamCreateWithFlags(&pl->bin_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < P.nbuf; ++k)
+      EFGP_TRY(dalloc(pl, &pl->rec[k], (int64_t)P.ntiles * P.tiles_grid * P.cap));
   }
   EFGP_TRY(dalloc(pl, &pl->modes, 2 * (P.Kvh + P.Mh)));
   EFGP_TRY(dalloc(pl, &pl->modes_sum, 2 * (P.Kvh + P.Mh)));
@@ -428,7 +421,7 @@ efgp_status efgp_get_info(efgp_handle pl, efgp_info *o) {
   o->t_solve_ms = pl->t_solve;
   o->t_predict_ms = pl->t_predict;
   if (P.spread_method == EFGP_SPREAD_SORTED) {
-    o->sorted_t1 = P.T1;
+    o->sorted_t1 = P.T1;  // (the SORTED kernel is one cooperative launch per fit)
     o->sorted_t2 = P.T2;
     o->sorted_chunk = P.chunk;
     o->sorted_round = P.round;
@@ -447,6 +440,13 @@ efgp_status efgp_get_residual_history(efgp_handle pl, double *host_out, int64_t 
   return EFGP_OK;
 }
 
+int64_t efgp_debug_trace(efgp_handle pl, unsigned long long *host_out, int64_t cap) {
+  if (!pl || !pl->trace) return 0;
+  const int64_t n = std::min<int64_t>(cap, (int64_t)pl->trace_n);
+  if (host_out && n > 0 && cudaMemcpy(host_out, pl->trace, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return (int64_t)pl->trace_n;
+}
+
 const char *efgp_last_error(efgp_handle pl) { return pl ? pl->err.c_str() : "null handle"; }
 
 void efgp_destroy(efgp_handle pl) {
@@ -458,12 +458,10 @@ void efgp_destroy(efgp_handle pl) {
   void *bufs[] = {pl->poly_dev, pl->D_half, pl->psi1, pl->psi2, pl->g1, pl->g2, pl->G1h, pl->G2h, pl->modes, pl->modes_sum,
                   pl->Xbox, pl->Yr, pl->vhat, pl->Zbox, pl->b, pl->x, pl->r, pl->p, pl->Ap, pl->partials,
                   pl->scal, pl->hist, pl->dflags, pl->T2box, pl->t2grid, pl->stage[0], pl->stage[1],
-                  pl->rec[0], pl->tcnt[0], pl->rec[1], pl->tcnt[1]};
+                  pl->rec[0], pl->rec[1], pl->rec[2], pl->trace,
+                  pl->sync_buf};
   for (void *b : bufs)
     if (b) cudaFree(b);
-  for (cudaEvent_t e : {pl->ev_bin[0], pl->ev_bin[1], pl->ev_tiles[0], pl->ev_tiles[1], pl->ev_sp})
-    if (e) cudaEventDestroy(e);
-  if (pl->bin_stream) cudaStreamDestroy(pl->bin_stream);
   if (pl->h_pinned) cudaFreeHost(pl->h_pinned);
   for (auto &e : pl->ev)
     if (e) cudaEventDestroy(e);

@@ -22,6 +22,9 @@ struct EsPoly {
 struct EsPolyF {  // the same coefficients rounded to fp32 (fp32-weight spreading)
   float c[kMaxW][kMaxW + 3];
 };
+struct EsPolyP {  // fp32 coefficients of cell offsets (2q, 2q+1) as pairs (pad offset W: 0); W <= 6
+  float2 c[3][9 + 1];
+};
 
 // Host-side parameter record.
 struct Params {
@@ -47,15 +50,16 @@ struct Params {
   int graph_iters = 8;
   EsPoly poly{};
   EsPolyF polyf{};
+  EsPolyP polyp{};
   int spread_mode = 0;         // SORTED precision: 0 fp64, 1 fp32 weights, 2 fp32 weights + round sums
   // SORTED spreading geometry (2D)
   int s_lo = 0, s_count = 0;   // start cells i0 in [s_lo, s_lo + s_count) per dim
-  int T1 = 16, T2 = 16;        // tile of T1 x T2 start cells (T1 T2 <= 256)
+  int T1 = 8, T2 = 16;         // tile of T1 x T2 start cells (T1 T2 <= 128)
   int nt1 = 0, nt2 = 0, ntiles = 0;
-  int cap = 0;                 // records per tile list per chunk
+  int cap = 0;                 // records per (tile, binner CTA) segment per chunk
   int round = 0;               // records per shared-memory round
-  int tiles_grid = 0;          // CTAs of the accumulation kernel
-  int bin_grid = 0;            // CTAs of the binning kernel
+  int tiles_grid = 0;          // CTAs of the fused spreading kernel (<= one per SM)
+  int nbuf = 2;                // tile-list buffers in flight
   int64_t chunk = 0;           // points per chunk
 };
 
@@ -128,12 +132,13 @@ struct efgp_plan {
   double *stage[2] = {nullptr, nullptr};
   int64_t stage_pts = 0;
 
-  // SORTED spreading: per-chunk tile lists of (x1, x2, y) records and their counts
-  // (double-buffered: binning of chunk k+1 on bin_stream overlaps accumulation of chunk k)
-  double *rec[2] = {nullptr, nullptr};     // ntiles x cap x 3 doubles
-  int *tcnt[2] = {nullptr, nullptr};       // ntiles
-  cudaStream_t bin_stream = nullptr;
-  cudaEvent_t ev_bin[2] = {nullptr, nullptr}, ev_tiles[2] = {nullptr, nullptr}, ev_sp = nullptr;
+  // SORTED spreading: per-chunk tile lists (nbuf buffers) of x pairs and y, and the per-call
+  // list lengths + handshake counters of the fused kernel
+  double4 *rec[3] = {nullptr, nullptr, nullptr};  // ntiles x grid x segcap records (x1, x2, y, key)
+  int *sync_buf = nullptr;
+  size_t sync_cap = 0;
+  unsigned long long *trace = nullptr;  // EFGP_SORTED_TRACE: per-chunk, per-CTA role timestamps
+  size_t trace_cap = 0, trace_n = 0;
 
   cufftHandle plan_g1 = 0, plan_g2 = 0, plan_c2r_L = 0, plan_r2c_L = 0, plan_t2 = 0;
   cudaGraphExec_t cg_exec = nullptr;

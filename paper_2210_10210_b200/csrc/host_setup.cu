@@ -217,6 +217,12 @@ std::string validate_and_choose(Params &p, const efgp_options &opt) {
   es_poly_fit(p.w, p.beta_es, p.poly);
   for (int a = 0; a < kMaxW; ++a)
     for (int k = 0; k < kMaxW + 3; ++k) p.polyf.c[a][k] = (float)p.poly.c[a][k];
+  for (int q = 0; q < 3; ++q)
+    for (int k = 0; k < 10; ++k) {
+      const int a0 = 2 * q, a1 = 2 * q + 1;
+      p.polyp.c[q][k] = make_float2(a0 < p.w && k <= p.poly.deg ? (float)p.poly.c[a0][k] : 0.f,
+                                    a1 < p.w && k <= p.poly.deg ? (float)p.poly.c[a1][k] : 0.f);
+    }
   // fp32 kernel weights (fp64 accumulation) only when asked for, and only where fp32 rounding of the
   // weights (~1e-7 relative) sits well below the NUFFT tolerance (DESIGN.md §7 "K1 weights")
   if (opt.spread_weights < EFGP_WEIGHTS_FP64 || opt.spread_weights > EFGP_WEIGHTS_MIXED)

@@ -1,4 +1,5 @@
-// K1, SORTED strategy (d = 2, W <= 6): tile-binned spreading with register accumulation.
+// K1, SORTED strategy (d = 2, W <= 6): tile-binned spreading with register accumulation, as ONE
+// persistent warp-specialised kernel (type-1 of eqs "88" and "rhs").
 //
 // Why: a 2D point touches W^2 cells per strength; accumulating each touch with an atomic is bounded
 // by the atomic units (shared fp64 atomicAdd is a CAS loop on sm_100a), far below HBM speed
@@ -7,23 +8,27 @@
 // its points in registers and pays the window update once per tile segment.
 //
 // The start cells reachable from x in [0,1]^2 form an S x S square (S = s_count); it is cut into
-// tiles of T1 x T2 start cells (T1 T2 <= 256, one thread per start cell).  Per chunk of C points
-// (double-buffered on two streams, so binning of chunk k+1 overlaps accumulation of chunk k):
-//   k_bin3  : each CTA streams 2048 points from HBM (evict-first), validates them, ranks them per
-//             tile in shared memory, reserves room in each tile's list with ONE global atomic per
-//             (CTA, tile), and writes the (x1, x2, y) records contiguously per tile (the chunk's
-//             records, 24 B per point, stay in L2).  A tile list that would exceed its capacity
-//             spills the point to direct fp64 RED spreading (correct for any data, fast for spread data).
-//   k_tiles3: persistent; CTA b takes the b-th equal share of the concatenated tile lists.  Per round
-//             of R records: one bulk async copy (cp.async.bulk + mbarrier, double-buffered) stages the
-//             raw records in shared memory; phase A (thread per record, balanced) computes the start
-//             cell, its rank (shared int atomics) and, for fp32 weights, the 2W kernel weights; phase B
-//             scans the per-cell counts into a sorted index; phase C (thread per start cell)
-//             accumulates its records into two W x W fp64 register windows (strength 1 and y, both
-//             on the n1 grid).  At a tile change the windows are summed in shared memory in W^2
-//             conflict-free steps and flushed with one RED per cell.
-// Weights: WF = double evaluates the piecewise polynomial in fp64 (in phase C);  WF = float
-// evaluates it in fp32 (phase A) from the fp64 reduced coordinate; accumulation is fp64 in both.
+// tiles of T1 x T2 start cells (T1 T2 <= 128, one accumulator thread per start cell).  The points
+// are processed in chunks of C points; the chunk's records go through L2-resident per-tile lists
+// (NBUF buffers).  One CTA per SM (cooperative launch, all CTAs co-resident), 12 warps:
+//   binner warps 8-11  : stream batches of 1024 points from HBM by bulk async copy (TMA engine, a
+//                        3-stage mbarrier ring that runs ahead across chunks), validate, rank per
+//                        tile (shared int atomics; start cell -> tile by lookup table), reserve room
+//                        in each tile's list with ONE global atomic per (batch, tile), and write the
+//                        records tile-contiguously with coalesced stores: x pairs (16 B) and y (8 B).
+//                        A full list spills the point to direct fp64 RED spreading (correct for any
+//                        data, fast for spread-out data).  Chunk k is written once all CTAs have
+//                        finished accumulating chunk k - NBUF (global counters).
+//   accumulator warps 0-7 (one thread per start cell): once all CTAs have binned chunk k, CTA b
+//                        takes the b-th equal share of the concatenated tile lists, in rounds of R
+//                        records: bulk copy into shared memory; pass 1 (thread per record) start
+//                        cell + rank (shared int atomics); scan; pass 2 (thread per record) writes the
+//                        record (FP64 mode) or its fp32 kernel weights (FP32 / MIXED) at its
+//                        cell-sorted slot; phase C (thread per start cell) accumulates into two
+//                        W x W register windows (strength 1 and y, both on the n1 grid).  At the end
+//                        of a tile segment the windows are summed in shared memory in W^2
+//                        conflict-free steps and flushed with one RED per cell.
+// Register budget: setmaxnreg moves registers from the binner warpgroup to the accumulators.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -32,8 +37,13 @@
 
 namespace efgp {
 
-constexpr int kBinThreads = 256, kBinPPT = 8, kBinBatch = kBinThreads * kBinPPT;  // 2048 points / CTA
-constexpr int kTileThreads = 256;                                                  // T1 T2 <= 256
+constexpr int kAccThreads = 256;                  // warps 0-7
+constexpr int kBinThreads = 128;                  // warps 8-11
+constexpr int kFusedThreads = kAccThreads + kBinThreads;
+constexpr int kBarAcc = 1, kBarBin = 2, kBarAcc2 = 3;  // named barriers (0 = __syncthreads)
+constexpr int kModeF64 = 0;   // fp64 weights (evaluated per record in phase C), fp64 accumulation
+constexpr int kModeW32 = 1;   // fp32 weights (pass 2), fp64 accumulation
+[[maybe_unused]] constexpr int kModeA32 = 2;   // fp32 weights, fp32 (packed FFMA2) sums within a round, fp64 across
 
 __device__ __forceinline__ int wrap_s(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
 
@@ -45,57 +55,65 @@ __device__ __forceinline__ int start_cell(double t) {
   return (int)ceil(__dsub_rn(t, 0.5 * W));
 }
 
-// exclusive scan of n ints in shared memory by a whole block (n arbitrary, blockDim multiple of 32)
-__device__ void block_exclusive_scan(int *a, int n, int *total, int *warp_sums) {
-  const int per = (n + blockDim.x - 1) / blockDim.x;
-  const int beg = threadIdx.x * per, end = min(n, beg + per);
-  int s = 0;
-  for (int i = beg; i < end; ++i) s += a[i];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-  int v = s;
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// named barrier that also returns whether the predicate held in any participating thread
+__device__ __forceinline__ bool named_sync_or(int id, int n, bool pred) {
+  unsigned r;
+  asm volatile(
+      "{\n .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n bar.red.or.pred q, %2, %3, p;\n selp.u32 %0, 1, 0, q;\n}"
+      : "=r"(r)
+      : "r"((unsigned)pred), "r"(id), "r"(n)
+      : "memory");
+  return r != 0;
+}
+
+// exclusive scan of one int per thread over a group of NW warps (group thread index g, named
+// barrier id); returns the exclusive prefix, *total gets the sum
+template <int NW>
+__device__ __forceinline__ int group_scan(int v, int g, int *wsum, int bar, int *total) {
+  const int lane = g & 31, wid = g >> 5;
+  int s = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += t;
+    const int t = __shfl_up_sync(0xffffffffu, s, o);
+    if (lane >= o) s += t;
   }
-  if (lane == 31) warp_sums[wid] = v;
-  __syncthreads();
+  if (lane == 31) wsum[wid] = s;
+  named_sync(bar, NW * 32);
   if (wid == 0) {
-    int w = lane < nw ? warp_sums[lane] : 0;
+    int w = lane < NW ? wsum[lane] : 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
+    for (int o = 1; o < NW; o <<= 1) {
       const int t = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += t;
     }
-    if (lane < nw) warp_sums[lane] = w;
+    if (lane < NW) wsum[lane] = w;
   }
-  __syncthreads();
-  int run = v - s + (wid > 0 ? warp_sums[wid - 1] : 0);
+  named_sync(bar, NW * 32);
+  if (total && g == 0) *total = wsum[NW - 1];
+  const int r = s - v + (wid > 0 ? wsum[wid - 1] : 0);
+  named_sync(bar, NW * 32);  // wsum reusable, *total visible
+  return r;
+}
+
+// exclusive scan in place of n ints in shared memory by a group of NW warps
+template <int NW>
+__device__ void group_scan_array(int *a, int n, int g, int *wsum, int bar, int *total) {
+  const int per = (n + NW * 32 - 1) / (NW * 32);
+  const int beg = g * per, end = min(n, beg + per);
+  int s = 0;
+  for (int i = beg; i < end; ++i) s += a[i];
+  int run = group_scan<NW>(s, g, wsum, bar, total);
   for (int i = beg; i < end; ++i) {
     const int c = a[i];
     a[i] = run;
     run += c;
   }
-  if (threadIdx.x == blockDim.x - 1) *total = run;
-  __syncthreads();
+  named_sync(bar, NW * 32);
 }
 
-// fp32 kernel weights from the fp64 grid coordinate: the reduced coordinate s = 2(i0 - t + W/2) - 1
-// in [-1, 1] is formed in fp64, the polynomial is evaluated in fp32.
-template <int W>
-__device__ __forceinline__ void es_weights_f32(double t, const EsPolyF &P, float (&w)[W]) {
-  const double tm = __dsub_rn(t, 0.5 * W);
-  const float s = (float)(2.0 * (ceil(tm) - tm) - 1.0);
-#pragma unroll
-  for (int a = 0; a < W; ++a) {
-    float acc = P.c[a][W + 2];
-#pragma unroll
-    for (int k = W + 1; k >= 0; --k) acc = fmaf(acc, s, P.c[a][k]);
-    w[a] = acc;
-  }
-}
-
-// the same for both coordinates of a 2D point at once, with packed fp32x2 FMAs (FFMA2)
+// fp32 kernel weights of both coordinates of a 2D point, packed fp32x2 Horner (FFMA2); the reduced
+// coordinate s = 2(i0 - t + W/2) - 1 in [-1, 1] is formed in fp64
 template <int W>
 __device__ __forceinline__ void es_weights_f32x2(double t1, double t2, const EsPolyF &P, float (&w1)[W],
                                                  float (&w2)[W]) {
@@ -111,8 +129,24 @@ __device__ __forceinline__ void es_weights_f32x2(double t1, double t2, const EsP
   }
 }
 
-// direct fp64 RED spreading of one point (overflow path; the polynomial is read from global memory so
-// the kernel parameters are not copied to the stack)
+// fp32 kernel weights of one coordinate as W/2 (rounded up) pairs (w[2p], w[2p+1]) by packed Horner
+// (FFMA2: pair accumulator x scalar s + coefficient pair); the pad weight w[W] (W odd) is 0
+template <int W>
+__device__ __forceinline__ void es_weights_pairs(double t, const EsPolyP &P, float2 (&w)[(W + 1) / 2]) {
+  const double tm = __dsub_rn(t, 0.5 * W);
+  const float s = (float)(2.0 * (ceil(tm) - tm) - 1.0);
+  const float2 s2 = make_float2(s, s);
+#pragma unroll
+  for (int q = 0; q < (W + 1) / 2; ++q) {
+    float2 acc = P.c[q][W + 2];
+#pragma unroll
+    for (int k = W + 1; k >= 0; --k) acc = __ffma2_rn(acc, s2, P.c[q][k]);
+    w[q] = acc;
+  }
+}
+
+// direct fp64 RED spreading of one point (list overflow path; the polynomial is read from global
+// memory so the kernel parameters are not copied to the stack)
 template <int W>
 __device__ __noinline__ void spread_point_red(double x1, double x2, double yv, double h, int n1,
                                               const EsPoly *__restrict__ Pg, double *__restrict__ g1,
@@ -133,15 +167,15 @@ __device__ __noinline__ void spread_point_red(double x1, double x2, double yv, d
   }
 }
 
-// ---- bulk async copy global -> shared with an mbarrier (TMA engine, 1D) -----------------------
+// ---- bulk async copies global -> shared with mbarriers (TMA engine, 1D) ------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
+__device__ __forceinline__ void mbar_expect(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
@@ -154,430 +188,625 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-
-// exclusive scan of one int per thread over the block (blockDim = 256); returns the exclusive prefix
-__device__ __forceinline__ int block_scan_256(int v, int *wsum) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int s = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, s, o);
-    if (lane >= o) s += t;
-  }
-  if (lane == 31) wsum[wid] = s;
-  __syncthreads();
-  if (wid == 0) {
-    int w = lane < 8 ? wsum[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += t;
-    }
-    if (lane < 8) wsum[lane] = w;
-  }
-  __syncthreads();
-  return s - v + (wid > 0 ? wsum[wid - 1] : 0);
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
-
-// K1a: bin the chunk's points by tile.  Persistent CTAs (2 per SM) walk the chunk's batches of
-// kBinBatch points; the next batch's x and y arrive by bulk async copy (TMA engine, mbarrier) while
-// the current one is processed, so HBM reads stay in flight without holding registers.  Per batch:
-// validate, start cells -> tile (shared lookup tables, no integer division), rank per tile (shared
-// int atomics), ONE global atomic per non-empty tile reserves room in its list, then the records
-// (x1, x2, y) are written tile-contiguously with coalesced stores (24 B per point, into L2).
-constexpr int kBinMaxS = 8192;  // start cells per dimension supported by the lookup tables
-
-template <int W>
-__global__ void __launch_bounds__(kBinThreads, 2)
-    k_bin5(const double *__restrict__ x, const double *__restrict__ y, int64_t n, double h, int n1, int s_lo, int S,
-           int T1, int T2, int nt2, int ntiles, int cap, double *__restrict__ rec, int *__restrict__ gcnt,
-           const EsPoly *__restrict__ Pg, double *__restrict__ g1, double *__restrict__ gy, int *__restrict__ err) {
-  extern __shared__ __align__(16) unsigned char bsm[];
-  double *xin = reinterpret_cast<double *>(bsm);                     // [2][kBinBatch * 2]
-  double *yin = xin + 2 * 2 * kBinBatch;                             // [2][kBinBatch]
-  int *perm = reinterpret_cast<int *>(yin + 2 * kBinBatch);          // [kBinBatch] slot -> j | t << 16
-  int *cnt = perm + kBinBatch;                                       // ntiles
-  int *loc = cnt + ntiles;                                           // ntiles
-  int *base = loc + ntiles;                                          // ntiles
-  int *rowt = base + ntiles;                                         // S: (c1 / T1) * nt2
-  int *colt = rowt + S;                                              // S: c2 / T2
-  __shared__ int wsum[32], total;
-  __shared__ __align__(8) uint64_t bar[2];
-  const int tid = threadIdx.x;
-  const int64_t nbatch = (n + kBinBatch - 1) / kBinBatch;
-  for (int c = tid; c < S; c += kBinThreads) {
-    rowt[c] = (c / T1) * nt2;
-    colt[c] = c / T2;
-  }
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  auto issue = [&](int64_t b, int buf) {
-    if (tid == 0 && b < nbatch) {
-      const int64_t i0 = b * kBinBatch;
-      const int nb = (int)(n - i0 < (int64_t)kBinBatch ? n - i0 : (int64_t)kBinBatch);
-      const int ne = nb & ~1;  // y copies need a multiple of 16 bytes; an odd tail is loaded below
-      const uint32_t bytes = (uint32_t)(nb * 16 + ne * 8);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[buf])), "r"(bytes)
-                   : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_u32(xin + buf * 2 * kBinBatch)),
-          "l"(x + 2 * i0), "r"((uint32_t)(nb * 16)), "r"(smem_u32(&bar[buf]))
-          : "memory");
-      if (ne > 0)
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(yin + buf * kBinBatch)),
-            "l"(y + i0), "r"((uint32_t)(ne * 8)), "r"(smem_u32(&bar[buf]))
-            : "memory");
-    }
-  };
-  uint32_t phase[2] = {0u, 0u};
-  int buf = 0;
-  issue(blockIdx.x, 0);
-  issue(blockIdx.x + gridDim.x, 1);
-  for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x, buf ^= 1) {
-    const int64_t i0 = b * kBinBatch;
-    const int nb = (int)(n - i0 < (int64_t)kBinBatch ? n - i0 : (int64_t)kBinBatch);
-    for (int t = tid; t < ntiles; t += kBinThreads) cnt[t] = 0;
-    mbar_wait(&bar[buf], phase[buf]);
-    phase[buf] ^= 1u;
-    const double *xs = xin + buf * 2 * kBinBatch;
-    double *ys = yin + buf * kBinBatch;
-    if ((nb & 1) && tid == 0) ys[nb - 1] = y[i0 + nb - 1];
-    __syncthreads();
-    int tl[kBinPPT], rk[kBinPPT];
-#pragma unroll
-    for (int k = 0; k < kBinPPT; ++k) {
-      const int j = k * kBinThreads + tid;
-      tl[k] = -1;
-      if (j >= nb) continue;
-      const double2 p = *reinterpret_cast<const double2 *>(xs + 2 * j);
-      const double yv = ys[j];
-      const bool ok = p.x >= 0.0 && p.x <= 1.0 && p.y >= 0.0 && p.y <= 1.0 && isfinite(yv);
-      if (!ok) {
-        atomicOr(err, 1);
-        continue;
-      }
-      const int c1 = start_cell<W>(grid_t(h, p.x, n1)) - s_lo;
-      const int c2 = start_cell<W>(grid_t(h, p.y, n1)) - s_lo;
-      const int t = rowt[c1] + colt[c2];
-      tl[k] = t;
-      rk[k] = atomicAdd(&cnt[t], 1);
-    }
-    __syncthreads();
-    for (int t = tid; t < ntiles; t += kBinThreads) {
-      const int c = cnt[t];
-      loc[t] = c;
-      base[t] = c ? atomicAdd(gcnt + t, c) : 0;
-    }
-    __syncthreads();
-    block_exclusive_scan(loc, ntiles, &total, wsum);
-#pragma unroll
-    for (int k = 0; k < kBinPPT; ++k)
-      if (tl[k] >= 0) perm[loc[tl[k]] + rk[k]] = (k * kBinThreads + tid) | (tl[k] << 16);
-    __syncthreads();
-    const int nv = total;
-    for (int e = tid; e < 3 * nv; e += kBinThreads) {
-      const int slot = e / 3, comp = e - 3 * slot;
-      const int v = perm[slot];
-      const int j = v & 0xFFFF, t = v >> 16;
-      const int p = base[t] + slot - loc[t];
-      const double val = comp < 2 ? xs[2 * j + comp] : ys[j];
-      if (p < cap) {
-        rec[((int64_t)t * cap + p) * 3 + comp] = val;
-      } else if (comp == 0) {
-        spread_point_red<W>(xs[2 * j], xs[2 * j + 1], ys[j], h, n1, Pg, g1, gy);
-      }
-    }
-    __syncthreads();  // this buffer is consumed: refill it with the batch after next
-    issue(b + 2 * (int64_t)gridDim.x, buf);
-  }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
-
-// Spreading modes of the accumulation kernel
-constexpr int kModeF64 = 0;   // fp64 weights (evaluated per record in phase C), fp64 accumulation
-constexpr int kModeW32 = 1;   // fp32 weights (phase A), fp64 accumulation
-constexpr int kModeA32 = 2;   // fp32 weights, fp32 (packed FFMA2) accumulation within a round, fp64 across
+__device__ __forceinline__ void stamp(const unsigned long long *base, int k, int slot) {
+  if (base) const_cast<unsigned long long *>(base)[((size_t)k * gridDim.x + blockIdx.x) * 4 + slot] = gtimer();
+}
+__device__ __forceinline__ void spin_until(const unsigned *p, unsigned target) {
+  while (ld_acquire(p) < target) __nanosleep(256);
+}
 
 template <int W, int MODE>
 struct StageRec {
-  // MODE 0: sorted copy of (x1, x2, y); else: w1[W], w2[W] (fp32) then y (fp64), 16-byte padded
-  static constexpr int kBytes = MODE == kModeF64 ? 24 : ((8 * W + 8) + 15) / 16 * 16;
+  // MODE F64: sorted copy of (x1, x2, y).  Otherwise the fp32 weights of each coordinate padded to an
+  // even count WE (pad weight 0): w1e[WE], w2e[WE]; then y: MIXED stores it as fp32 in the pad slot
+  // w1e[W] (W odd) or after w2e (W even); W32 stores it as fp64 after w2e.  16-byte padded.
+  static constexpr int WE = (W + 1) / 2 * 2;
+  static constexpr int kYSlot = (W & 1) ? W : 2 * WE;  // MIXED: float index of y
+  static constexpr int kBytes = MODE == kModeF64 ? 24
+                                : MODE == kModeW32 ? (8 * WE + 8 + 15) / 16 * 16
+                                                   : (4 * (2 * WE + ((W & 1) ? 0 : 1)) + 15) / 16 * 16;
 };
 
-template <int W, int MODE>
-__device__ __forceinline__ void load_stage_w(const unsigned char *sp, float (&w1)[W], float (&w2)[W], double &yv) {
-  constexpr int NF = 2 * W, NV = (NF + 3) / 4;
-  float f[NV * 4];
+// NB bytes of a stage record as floats (16-byte vector loads)
+template <int NB>
+__device__ __forceinline__ void load_floats(const unsigned char *sp, float (&f)[NB / 4]) {
   const float4 *q = reinterpret_cast<const float4 *>(sp);
 #pragma unroll
-  for (int i = 0; i < NV; ++i) {
+  for (int i = 0; i < NB / 16; ++i) {
     const float4 v = q[i];
     f[4 * i] = v.x;
     f[4 * i + 1] = v.y;
     f[4 * i + 2] = v.z;
     f[4 * i + 3] = v.w;
   }
-#pragma unroll
-  for (int a = 0; a < W; ++a) {
-    w1[a] = f[a];
-    w2[a] = f[W + a];
-  }
-  yv = *reinterpret_cast<const double *>(sp + 8 * W);
 }
 
-// K1b: persistent accumulation.  CTA b takes the b-th equal share of the concatenated tile lists.
-template <int W, int MODE>
-__global__ void __launch_bounds__(kTileThreads, 1)
-    k_tiles4(const double *__restrict__ rec, const int *__restrict__ gcnt, int cap, int ntiles, int T1, int T2,
-             int nt2, int R, double h, int n1, int s_lo, EsPoly P, EsPolyF PF, double *__restrict__ g1,
-             double *__restrict__ gy) {
-  constexpr int SB = StageRec<W, MODE>::kBytes;
-  extern __shared__ __align__(16) unsigned char tsm[];
-  // layout: raw[(R + 2) * 3] doubles | stage[R * SB] | kr[R] | cnt[256] | tpre[ntiles + 1]
-  double *raw = reinterpret_cast<double *>(tsm);
-  unsigned char *stage = tsm + sizeof(double) * (size_t)(R + 2) * 3;
-  int *kr = reinterpret_cast<int *>(stage + (size_t)R * SB);
-  int *cnt = kr + R;
-  int *tpre = cnt + kTileThreads;
-  __shared__ int wsum[32];
-  __shared__ int total;
-  __shared__ __align__(8) uint64_t bar;
+// All kernel arguments (passed by value; lives in the constant bank).
+struct FusedArgs {
+  const double *x, *y;
+  int64_t N, chunk;
+  int nchunks, nbuf;
+  double h;
+  int n1, s_lo, S, T1, T2, nt2, ntiles;
+  int segcap;          // records per (tile, binner CTA) segment per chunk
+  int R;               // records per accumulator round
+  double4 *rec[3];     // [buf][tile][cta][segcap] records (x1, x2, y, key bits)
+  int *segcnt;         // [nchunks][tile][cta] segment lengths
+  int *tilecnt;        // [nchunks][tile] list lengths (sum over CTAs)
+  unsigned *bin_done;  // [nchunks] CTAs that finished binning chunk k
+  unsigned *acc_done;  // [nchunks] CTAs that finished accumulating chunk k
+  unsigned long long *trace;  // optional [nchunks][grid][4] globaltimer stamps (EFGP_SORTED_TRACE)
+  const EsPoly *poly_dev;
+  double *g1, *gy;
+  int *err;
+};
 
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    mbar_init(&bar, 1);
+constexpr int kWBatch = 256;                      // points per binner-warp batch
+constexpr int kWStages = 3;                       // TMA ring depth per binner warp
+constexpr int kBinWarps = kBinThreads / 32;       // 4
+
+template <int W, int MODE>
+struct FusedSmem {
+  // binner: per warp a TMA ring (x pairs + y), per-tile count / offset / base, perm; shared: the
+  // CTA's running segment lengths and the start-cell tables
+  __host__ __device__ static size_t bin_warp_bytes(int ntiles) {
+    return (size_t)kWStages * kWBatch * 24 + 4 * (size_t)kWBatch + 4 * 3 * (size_t)ntiles;
+  }
+  __host__ __device__ static size_t bin_bytes(int ntiles, int S) {
+    return kBinWarps * ((bin_warp_bytes(ntiles) + 15) / 16 * 16) + 4 * ((size_t)ntiles + 2 * (size_t)S);
+  }
+};
+
+// ------------------------------------------------------------------------------- binner role
+// Four independent binner warps (no CTA barrier per batch).  Each warp streams batches of 256
+// points through its own TMA ring, ranks them per tile with warp-private shared counters, reserves
+// room in the CTA's segment of each tile with one shared atomic per (batch, tile), and writes the
+// records tile-contiguously.  Per-segment and per-tile lengths are published at each chunk's end.
+template <int W>
+__device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..127 */) {
+  const int lane = g & 31, wid = g >> 5, ntiles = A.ntiles, G = gridDim.x;
+  const size_t wbytes = (FusedSmem<W, 0>::bin_warp_bytes(ntiles) + 15) / 16 * 16;
+  unsigned char *wsm = sm + wid * wbytes;
+  double *xin = reinterpret_cast<double *>(wsm);                      // [stage][kWBatch * 2]
+  double *yin = xin + kWStages * 2 * kWBatch;                         // [stage][kWBatch]
+  int *perm = reinterpret_cast<int *>(yin + kWStages * kWBatch);      // kWBatch
+  int *wcnt = perm + kWBatch;                                         // ntiles
+  int *wloc = wcnt + ntiles;                                          // ntiles
+  int *wbase = wloc + ntiles;                                         // ntiles
+  int *off = reinterpret_cast<int *>(sm + kBinWarps * wbytes);        // ntiles (CTA-shared)
+  int *rowt = off + ntiles;                                           // S
+  int *colt = rowt + A.S;                                             // S
+  __shared__ __align__(8) uint64_t bar[kBinWarps][kWStages];
+  for (int c = g; c < A.S; c += kBinThreads) {
+    rowt[c] = ((c / A.T1) * A.nt2) << 16 | (c % A.T1) * A.T2;
+    colt[c] = (c / A.T2) << 16 | (c % A.T2);
+  }
+  for (int t = g; t < ntiles; t += kBinThreads) off[t] = 0;
+  for (int t = lane; t < ntiles; t += 32) wcnt[t] = 0;
+  if (lane == 0) {
+    for (int s = 0; s < kWStages; ++s) mbar_init(&bar[wid][s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int t = tid; t < ntiles; t += kTileThreads) tpre[t] = min(gcnt[t], cap);
-  __syncthreads();
-  block_exclusive_scan(tpre, ntiles, &total, wsum);
-  if (tid == 0) tpre[ntiles] = total;
-  __syncthreads();
-  const int all = tpre[ntiles];
-  const int gb = (int)((int64_t)blockIdx.x * all / gridDim.x), ge = (int)((int64_t)(blockIdx.x + 1) * all / gridDim.x);
-  if (gb >= ge) return;
-  int t_first = 0;  // last tile with tpre[t] <= gb (binary search; identical in all threads)
-  {
-    int lo = 0, hi = ntiles;
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (tpre[mid] <= gb) lo = mid;
-      else hi = mid;
+  named_sync(kBarBin, kBinThreads);
+  const int64_t nbatch = (A.N + kWBatch - 1) / kWBatch;
+  const int64_t bpc = A.chunk / kWBatch;  // batches per chunk
+  const int64_t nw = (int64_t)G * kBinWarps, gw = (int64_t)blockIdx.x * kBinWarps + wid;
+  auto issue = [&](int64_t i) {  // i-th batch of this warp: global batch gw + i nw
+    const int64_t b = gw + i * nw;
+    if (lane != 0 || b >= nbatch) return;
+    const int s = (int)(i % kWStages);
+    const int64_t i0 = b * kWBatch;
+    const int nb = (int)(A.N - i0 < kWBatch ? A.N - i0 : kWBatch);
+    const int ne = nb & ~1;  // y copies need a multiple of 16 bytes; an odd tail is loaded by hand
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect(&bar[wid][s], (uint32_t)(nb * 16 + ne * 8));
+    bulk_g2s(xin + s * 2 * kWBatch, A.x + 2 * i0, (uint32_t)(nb * 16), &bar[wid][s]);
+    if (ne > 0) bulk_g2s(yin + s * kWBatch, A.y + i0, (uint32_t)(ne * 8), &bar[wid][s]);
+  };
+  for (int i = 0; i < kWStages; ++i) issue(i);
+  uint32_t phases = 0;
+  int cur = -1;  // chunk whose segments this CTA is writing
+  auto enter_chunk = [&](int k) {
+    // publish chunks cur .. k-1, then wait until buffer k % nbuf is free.  Every step is the same
+    // three barriers in all four warps (each warp walks every chunk in order).
+    while (cur < k) {
+      named_sync(kBarBin, kBinThreads);  // all warps are done with chunk cur
+      if (cur >= 0) {
+        int *sc = A.segcnt + (int64_t)cur * ntiles * G;
+        for (int t = g; t < ntiles; t += kBinThreads) {
+          const int c = min(off[t], A.segcap);
+          sc[(int64_t)t * G + blockIdx.x] = c;
+          if (c) atomicAdd(A.tilecnt + (int64_t)cur * ntiles + t, c);
+          off[t] = 0;
+        }
+      }
+      named_sync(kBarBin, kBinThreads);  // published
+      if (g == 0) {
+        if (cur >= 0) {
+          __threadfence();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          atomicAdd(A.bin_done + cur, 1u);
+          stamp(A.trace, cur, 0);
+        }
+        if (cur + 1 < A.nchunks && cur + 1 >= A.nbuf) spin_until(A.acc_done + (cur + 1 - A.nbuf), 2 * G);
+      }
+      ++cur;
+      named_sync(kBarBin, kBinThreads);  // buffer cur % nbuf is free
     }
-    t_first = lo;
-    while (tpre[t_first + 1] <= gb) ++t_first;  // skip empty tiles ending at gb
+  };
+  const int tper = (ntiles + 31) / 32, tb = lane * tper, te = min(ntiles, tb + tper);
+  for (int64_t i = 0;; ++i) {
+    const int64_t b = gw + i * nw;
+    // every warp walks the chunks in order; a warp with no batch left in a chunk still enters it
+    const int k = b < nbatch ? (int)(b / bpc) : A.nchunks;
+    if (k != cur) enter_chunk(k);
+    if (b >= nbatch) break;
+    const int s = (int)(i % kWStages);
+    const int64_t i0 = b * kWBatch;
+    const int nb = (int)(A.N - i0 < kWBatch ? A.N - i0 : kWBatch);
+    double4 *rec = A.rec[k % A.nbuf];
+    mbar_wait(&bar[wid][s], (phases >> s) & 1u);
+    phases ^= 1u << s;
+    const double2 *xs2 = reinterpret_cast<const double2 *>(xin + s * 2 * kWBatch);
+    double *ys = yin + s * kWBatch;
+    if ((nb & 1) && lane == 0) ys[nb - 1] = A.y[i0 + nb - 1];
+    __syncwarp();
+    int tk[kWBatch / 32], rk[kWBatch / 32];  // (tile << 8 | key), rank within the batch's tile
+#pragma unroll
+    for (int q = 0; q < kWBatch / 32; ++q) {
+      const int j = q * 32 + lane;
+      tk[q] = -1;
+      if (j >= nb) continue;
+      const double2 p = xs2[j];
+      const double yv = ys[j];
+      const bool ok = p.x >= 0.0 && p.x <= 1.0 && p.y >= 0.0 && p.y <= 1.0 && isfinite(yv);
+      if (!ok) {
+        atomicOr(A.err, 1);
+        continue;
+      }
+      const int r = rowt[start_cell<W>(grid_t(A.h, p.x, A.n1)) - A.s_lo];
+      const int c = colt[start_cell<W>(grid_t(A.h, p.y, A.n1)) - A.s_lo];
+      const int t = (r >> 16) + (c >> 16);
+      tk[q] = t << 8 | ((r & 0xFFFF) + (c & 0xFFFF));
+      rk[q] = atomicAdd(&wcnt[t], 1);
+    }
+    __syncwarp();
+    // warp scan of the per-tile counts -> slot offsets; reserve room in the CTA's segments
+    int sum = 0;
+    for (int t = tb; t < te; ++t) sum += wcnt[t];
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int nv = __shfl_sync(0xffffffffu, incl, 31);
+    int run = incl - sum;
+    for (int t = tb; t < te; ++t) {
+      const int c = wcnt[t];
+      wloc[t] = run;
+      wbase[t] = c ? atomicAdd(&off[t], c) : 0;
+      wcnt[t] = 0;
+      run += c;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < kWBatch / 32; ++q)
+      if (tk[q] >= 0) perm[wloc[tk[q] >> 8] + rk[q]] = (q * 32 + lane) | (tk[q] << 8);
+    __syncwarp();
+    for (int slot = lane; slot < nv; slot += 32) {
+      const int v = perm[slot];
+      const int j = v & 0xFF, key = (v >> 8) & 0xFF, t = v >> 16;
+      const int p = wbase[t] + slot - wloc[t];
+      const double2 xx = xs2[j];
+      const double yv = ys[j];
+      if (p < A.segcap) {
+        rec[((int64_t)t * G + blockIdx.x) * A.segcap + p] = make_double4(xx.x, xx.y, yv, __longlong_as_double((long long)key));
+      } else {
+        spread_point_red<W>(xx.x, xx.y, yv, A.h, A.n1, A.poly_dev, A.g1, A.gy);
+      }
+    }
+    __syncwarp();  // stage s consumed
+    issue(i + kWStages);
   }
+}
+
+// -------------------------------------------------------------------------- accumulator role
+// Two independent groups of 4 warps (128 threads, one per start cell of a tile of <= 128 cells),
+// each with its own named barrier, shared-memory region and share of the chunk's records (virtual
+// CTA 2 blockIdx + group), so one group's barriers and latencies overlap the other's work.
+constexpr int kAccGroups = 2, kGrpThreads = kAccThreads / kAccGroups;  // 128 threads per group
+
+template <int W, int MODE>
+struct AccSmem {
+  // raw round (32 B records, bulk-copied), cell-sorted stage, per-cell counts, tile prefix, two
+  // segment prefixes, fp64 tile accumulator; all 16-byte multiples
+  __host__ __device__ static size_t bytes(int R, int ntiles, int grid, int T1, int T2) {
+    size_t b = 32 * (size_t)R + (size_t)R * StageRec<W, MODE>::kBytes;
+    b += ((4 * (size_t)(kGrpThreads + ntiles + 1 + 2 * (grid + 1))) + 15) / 16 * 16;
+    b += 16 * (size_t)(T1 + W - 1) * (T2 + W - 1);
+    return b;
+  }
+};
+
+template <int W, int MODE>
+__device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_all, const EsPoly &P,
+                                 const EsPolyP &PF) {
+  constexpr int SB = StageRec<W, MODE>::kBytes;
+  const int gi = tid_all / kGrpThreads, tid = tid_all % kGrpThreads;
+  const int bar_id = gi == 0 ? kBarAcc : kBarAcc2;
+  const int R = A.R, ntiles = A.ntiles, T1 = A.T1, T2 = A.T2, n1 = A.n1, s_lo = A.s_lo, G = gridDim.x;
+  const int VG = G * kAccGroups, vb = blockIdx.x * kAccGroups + gi;  // virtual CTA
+  const double h = A.h;
+  unsigned char *gsm = sm + gi * AccSmem<W, MODE>::bytes(R, ntiles, G, T1, T2);
+  double4 *raw = reinterpret_cast<double4 *>(gsm);                      // R records
+  unsigned char *stage = reinterpret_cast<unsigned char *>(raw + R);    // R * SB, cell-sorted
+  int *cnt = reinterpret_cast<int *>(stage + (size_t)R * SB);           // 128
+  int *tpre = cnt + kGrpThreads;                                        // ntiles + 1
+  int *spre = tpre + ntiles + 1;                                        // [2][G + 1]
+  double *tacc = reinterpret_cast<double *>(
+      gsm + 32 * (size_t)R + (size_t)R * SB + ((4 * (size_t)(kGrpThreads + ntiles + 1 + 2 * (G + 1))) + 15) / 16 * 16);
+  __shared__ int wsum_s[kAccGroups][8], total_s[kAccGroups], spre_tile_s[kAccGroups][2];
+  __shared__ __align__(8) uint64_t bar_s[kAccGroups];
+  int *wsum = wsum_s[gi], *spre_tile = spre_tile_s[gi];
+  int &total = total_s[gi];
+  uint64_t *bar = &bar_s[gi];
   const int NT = T1 * T2;
   const bool own = tid < NT;
   const int my_r = own ? tid / T2 : 0, my_c = own ? tid % T2 : 0;
   const int A1 = T1 + W - 1, A2 = T2 + W - 1;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < 2 * A1 * A2; i += kGrpThreads) tacc[i] = 0.0;
+  named_sync(bar_id, kGrpThreads);
   uint32_t phase = 0u;
-
-  struct Rd {
-    int tile, lo, n;
-  };
-  auto round_at = [&](int t, int lo) -> Rd {
-    const int hi = min(tpre[t + 1], ge) - tpre[t];
-    return Rd{t, lo, min(R, hi - lo)};
-  };
-  auto next_round = [&](Rd r) -> Rd {
-    const int tile_hi = min(tpre[r.tile + 1], ge) - tpre[r.tile];
-    if (r.lo + r.n < tile_hi) return round_at(r.tile, r.lo + r.n);
-    int t = r.tile + 1;
-    while (t < ntiles && tpre[t] < ge && tpre[t + 1] == tpre[t]) ++t;
-    if (t >= ntiles || tpre[t] >= ge) return Rd{-1, 0, 0};
-    return round_at(t, 0);
-  };
-  // bulk copy of round r into raw (aligned superset: records are 24 B, copies need 16 B alignment)
-  auto issue = [&](Rd r) {
-    if (tid == 0 && r.tile >= 0) {
-      const int64_t first = (int64_t)r.tile * cap + r.lo;
-      const int64_t a0 = first & ~int64_t(1), a1 = (first + r.n + 1) & ~int64_t(1);
-      bulk_load(raw, rec + a0 * 3, (uint32_t)((a1 - a0) * 24), &bar);
-    }
-  };
-
+  // register windows of this thread's start cell: fp64 (FP64 / FP32 modes) or fp32 pairs along b
+  // (MIXED); the unused set is eliminated by the compiler
   double a1[W][W], ay[W][W];
 #pragma unroll
   for (int a = 0; a < W; ++a)
 #pragma unroll
     for (int b = 0; b < W; ++b) a1[a][b] = ay[a][b] = 0.0;
+  float2 p1[W][(W + 1) / 2], py[W][(W + 1) / 2];
+  int pend = 0;
+#pragma unroll
+  for (int a = 0; a < W; ++a)
+#pragma unroll
+    for (int b = 0; b < (W + 1) / 2; ++b) p1[a][b] = py[a][b] = make_float2(0.f, 0.f);
 
-  Rd cur = round_at(t_first, gb - tpre[t_first]);
-  issue(cur);
-  while (cur.tile >= 0) {
-    const Rd nxt = next_round(cur);
-    const int r0 = (cur.tile / nt2) * T1, c0 = (cur.tile % nt2) * T2;
-    const int nr = cur.n;
-    const double *rw = raw + 3 * (int)(((int64_t)cur.tile * cap + cur.lo) & 1);
-    cnt[tid] = 0;
-    mbar_wait(&bar, phase);
-    phase ^= 1u;
-    __syncthreads();
-    // pass 1 (thread per record): start cell within the tile and its rank
-    for (int j = tid; j < nr; j += kTileThreads) {
-      const double t1 = grid_t(h, rw[3 * j], n1), t2 = grid_t(h, rw[3 * j + 1], n1);
-      const int key = (start_cell<W>(t1) - s_lo - r0) * T2 + (start_cell<W>(t2) - s_lo - c0);
-      kr[j] = key | (atomicAdd(&cnt[key], 1) << 8);
+  for (int k = 0; k < A.nchunks; ++k) {
+    const double4 *rec = A.rec[k % A.nbuf];
+    const int *segc = A.segcnt + (int64_t)k * ntiles * G;
+    if (tid == 0) {
+      if (gi == 0) stamp(A.trace, k, 1);
+      spin_until(A.bin_done + k, G);
+      if (gi == 0) stamp(A.trace, k, 2);
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      spre_tile[0] = spre_tile[1] = -1;
     }
-    __syncthreads();
-    const int mycnt = cnt[tid];
-    const int myoff = block_scan_256(mycnt, wsum);
-    cnt[tid] = myoff;
-    __syncthreads();
-    // pass 2 (thread per record): write the record (MODE 0) or its fp32 weights at its sorted slot
-    for (int j = tid; j < nr; j += kTileThreads) {
-      const int v = kr[j];
-      const int pos = cnt[v & 255] + (v >> 8);
-      unsigned char *sp = stage + (size_t)pos * SB;
-      if constexpr (MODE == kModeF64) {
-        double *d = reinterpret_cast<double *>(sp);
-        d[0] = rw[3 * j];
-        d[1] = rw[3 * j + 1];
-        d[2] = rw[3 * j + 2];
-      } else {
-        float w1[W], w2[W];
-        es_weights_f32x2<W>(grid_t(h, rw[3 * j], n1), grid_t(h, rw[3 * j + 1], n1), PF, w1, w2);
-        float f[4 * ((2 * W + 3) / 4)];
-#pragma unroll
-        for (int a = 0; a < W; ++a) {
-          f[a] = w1[a];
-          f[W + a] = w2[a];
+    named_sync(bar_id, kGrpThreads);
+    for (int t = tid; t < ntiles; t += kGrpThreads) tpre[t] = __ldcg(A.tilecnt + (int64_t)k * ntiles + t);
+    named_sync(bar_id, kGrpThreads);
+    group_scan_array<4>(tpre, ntiles, tid, wsum, bar_id, &total);
+    if (tid == 0) tpre[ntiles] = total;
+    named_sync(bar_id, kGrpThreads);
+    const int all = tpre[ntiles];
+    const int gb = (int)((int64_t)vb * all / VG), ge = (int)((int64_t)(vb + 1) * all / VG);
+    if (gb < ge) {
+      int t_first;
+      {
+        int lo = 0, hi = ntiles;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (tpre[mid] <= gb) lo = mid;
+          else hi = mid;
         }
-#pragma unroll
-        for (int i = 2 * W; i < 4 * ((2 * W + 3) / 4); ++i) f[i] = 0.f;
-        float4 *q = reinterpret_cast<float4 *>(sp);
-#pragma unroll
-        for (int i = 0; i < (2 * W + 3) / 4; ++i) q[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
-        *reinterpret_cast<double *>(sp + 8 * W) = rw[3 * j + 2];
+        t_first = lo;
+        while (tpre[t_first + 1] <= gb) ++t_first;
       }
-    }
-    __syncthreads();
-    issue(nxt);  // raw is free: the next round's copy lands during phase C
-    // phase C (thread per start cell): register accumulation of its records
-    if (mycnt > 0) {
-      const unsigned char *sp = stage + (size_t)myoff * SB;
-      if constexpr (MODE == kModeF64) {
-        for (int k = 0; k < mycnt; ++k, sp += SB) {
-          const double *d = reinterpret_cast<const double *>(sp);
-          const double yv = d[2];
-          double w1[W], w2[W];
-          es_weights<W>(grid_t(h, d[0], n1), P, w1);
-          es_weights<W>(grid_t(h, d[1], n1), P, w2);
+      struct Rd {
+        int tile, lo, n;
+      };
+      auto round_at = [&](int t, int lo) -> Rd {
+        const int hi = min(tpre[t + 1], ge) - tpre[t];
+        return Rd{t, lo, min(R, hi - lo)};
+      };
+      auto next_round = [&](Rd r) -> Rd {
+        const int tile_hi = min(tpre[r.tile + 1], ge) - tpre[r.tile];
+        if (r.lo + r.n < tile_hi) return round_at(r.tile, r.lo + r.n);
+        int t = r.tile + 1;
+        while (t < ntiles && tpre[t] < ge && tpre[t + 1] == tpre[t]) ++t;
+        if (t >= ntiles || tpre[t] >= ge) return Rd{-1, 0, 0};
+        return round_at(t, 0);
+      };
+      // segment prefix of tile t into slot (t & 1), by the group's first warp (a barrier follows
+      // before it is read)
+      auto seg_prefix = [&](int t) {
+        if (t < 0 || tid >= 32) return;
+        const int sl = t & 1;
+        if (spre_tile[sl] == t) return;
+        int *sp = spre + sl * (G + 1);
+        const int per = (G + 31) / 32, beg = tid * per, end = min(G, beg + per);
+        int s = 0;
+        for (int c = beg; c < end; ++c) s += __ldcg(segc + (int64_t)t * G + c);
+        int incl = s;
 #pragma unroll
-          for (int a = 0; a < W; ++a) {
-            const double ca = w1[a], cy = yv * w1[a];
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (tid >= o) incl += v;
+        }
+        int run = incl - s;
+        for (int c = beg; c < end; ++c) {
+          sp[c] = run;
+          run += __ldcg(segc + (int64_t)t * G + c);
+        }
+        if (tid == 31) sp[G] = incl;
+        __syncwarp();
+        if (tid == 0) spre_tile[sl] = t;
+      };
+      // bulk copies of round r into raw: one per (tile, binner CTA) segment piece it spans
+      auto issue = [&](Rd r) {
+        if (tid != 0 || r.tile < 0) return;
+        const int *sp = spre + (r.tile & 1) * (G + 1);
+        int lo2 = 0, hi2 = G;  // last segment with sp[c] <= r.lo
+        while (hi2 - lo2 > 1) {
+          const int mid = (lo2 + hi2) >> 1;
+          if (sp[mid] <= r.lo) lo2 = mid;
+          else hi2 = mid;
+        }
+        int c = lo2;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect(bar, (uint32_t)(r.n * 32));
+        const double4 *tb = rec + (int64_t)r.tile * G * A.segcap;
+        for (int done = 0; done < r.n; ++c) {
+          const int a0 = r.lo + done - sp[c];
+          const int m = min(sp[c + 1] - sp[c] - a0, r.n - done);
+          if (m > 0) {
+            bulk_g2s(raw + done, tb + (int64_t)c * A.segcap + a0, (uint32_t)(m * 32), bar);
+            done += m;
+          }
+        }
+      };
+      Rd cur = round_at(t_first, gb - tpre[t_first]);
+      seg_prefix(cur.tile);
+      named_sync(bar_id, kGrpThreads);
+      issue(cur);
+      while (cur.tile >= 0) {
+        const Rd nxt = next_round(cur);
+        const int r0 = (cur.tile / A.nt2) * T1, c0 = (cur.tile % A.nt2) * T2;
+        const int nr = cur.n;
+        cnt[tid] = 0;
+        seg_prefix(nxt.tile);  // for issue(nxt) below
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        named_sync(bar_id, kGrpThreads);
+        // pass 1 (thread per record): rank within its start cell (key from the binner), kept in
+        // the record's key slot
+        for (int j = tid; j < nr; j += kGrpThreads) {
+          int *kp = reinterpret_cast<int *>(&raw[j].w);
+          kp[1] = atomicAdd(&cnt[kp[0]], 1);
+        }
+        named_sync(bar_id, kGrpThreads);
+        const int mycnt = cnt[tid];
+        const int myoff = group_scan<4>(mycnt, tid, wsum, bar_id, nullptr);
+        cnt[tid] = myoff;
+        named_sync(bar_id, kGrpThreads);
+        // pass 2 (thread per record): the record (FP64) or its fp32 weights at its sorted slot
+        for (int j = tid; j < nr; j += kGrpThreads) {
+          const double4 rv = raw[j];
+          unsigned char *st = stage + (size_t)(cnt[__double2loint(rv.w)] + __double2hiint(rv.w)) * SB;
+          if constexpr (MODE == kModeF64) {
+            double *d = reinterpret_cast<double *>(st);
+            d[0] = rv.x;
+            d[1] = rv.y;
+            d[2] = rv.z;
+          } else {
+            constexpr int WP = (W + 1) / 2, WE = 2 * WP, NF = SB / 4;
+            float2 w1[WP], w2[WP];
+            es_weights_pairs<W>(grid_t(h, rv.x, n1), PF, w1);
+            es_weights_pairs<W>(grid_t(h, rv.y, n1), PF, w2);
+            float f[NF];
 #pragma unroll
-            for (int b2 = 0; b2 < W; ++b2) {
-              a1[a][b2] = fma(ca, w2[b2], a1[a][b2]);
-              ay[a][b2] = fma(cy, w2[b2], ay[a][b2]);
+            for (int q = 0; q < WP; ++q) {
+              f[2 * q] = w1[q].x;
+              f[2 * q + 1] = w1[q].y;
+              f[WE + 2 * q] = w2[q].x;
+              f[WE + 2 * q + 1] = w2[q].y;
+            }
+#pragma unroll
+            for (int i = 2 * WE; i < NF; ++i) f[i] = 0.f;
+            if constexpr (MODE == kModeA32) {
+              f[StageRec<W, MODE>::kYSlot] = (float)rv.z;
+            } else {
+              f[2 * WE] = __int_as_float(__double2loint(rv.z));
+              f[2 * WE + 1] = __int_as_float(__double2hiint(rv.z));
+            }
+            float4 *q4 = reinterpret_cast<float4 *>(st);
+#pragma unroll
+            for (int i = 0; i < NF / 4; ++i) q4[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+          }
+        }
+        named_sync(bar_id, kGrpThreads);
+        issue(nxt);  // raw is free: the next round's copies land during phase C
+        // phase C (thread per start cell): register accumulation of its records
+        if (mycnt > 0) {
+          const unsigned char *sp = stage + (size_t)myoff * SB;
+          if constexpr (MODE == kModeF64) {
+            for (int q = 0; q < mycnt; ++q, sp += SB) {
+              const double *d = reinterpret_cast<const double *>(sp);
+              const double yv = d[2];
+              double w1[W], w2[W];
+              es_weights<W>(grid_t(h, d[0], n1), P, w1);
+              es_weights<W>(grid_t(h, d[1], n1), P, w2);
+#pragma unroll
+              for (int a = 0; a < W; ++a) {
+                const double ca = w1[a], cy = yv * w1[a];
+#pragma unroll
+                for (int b2 = 0; b2 < W; ++b2) {
+                  a1[a][b2] = fma(ca, w2[b2], a1[a][b2]);
+                  ay[a][b2] = fma(cy, w2[b2], ay[a][b2]);
+                }
+              }
+            }
+          } else if constexpr (MODE == kModeW32) {
+            constexpr int WE = StageRec<W, MODE>::WE, NF = SB / 4;
+            for (int q = 0; q < mycnt; ++q, sp += SB) {
+              float f[NF];
+              load_floats<SB>(sp, f);
+              const double yv = __hiloint2double(__float_as_int(f[2 * WE + 1]), __float_as_int(f[2 * WE]));
+              double w2[W];
+#pragma unroll
+              for (int b2 = 0; b2 < W; ++b2) w2[b2] = (double)f[WE + b2];
+#pragma unroll
+              for (int a = 0; a < W; ++a) {
+                const double ca = (double)f[a], cy = yv * ca;
+#pragma unroll
+                for (int b2 = 0; b2 < W; ++b2) {
+                  a1[a][b2] = fma(ca, w2[b2], a1[a][b2]);
+                  ay[a][b2] = fma(cy, w2[b2], ay[a][b2]);
+                }
+              }
+            }
+          } else {
+            // MIXED: fp32 pairs along b: (acc[a][2p], acc[a][2p+1]) += w1[a] * (w2[2p], w2[2p+1])
+            constexpr int WP = (W + 1) / 2, WE = 2 * WP, NF = SB / 4;
+            for (int q = 0; q < mycnt; ++q, sp += SB) {
+              float f[NF];
+              load_floats<SB>(sp, f);
+              const float yf = f[StageRec<W, MODE>::kYSlot];
+#pragma unroll
+              for (int a = 0; a < W; ++a) {
+                const float c1 = f[a], cy = yf * f[a];
+#pragma unroll
+                for (int pp = 0; pp < WP; ++pp) {
+                  const float2 w2p = make_float2(f[WE + 2 * pp], f[WE + 2 * pp + 1]);
+                  p1[a][pp] = __ffma2_rn(w2p, make_float2(c1, c1), p1[a][pp]);
+                  py[a][pp] = __ffma2_rn(w2p, make_float2(cy, cy), py[a][pp]);
+                }
+              }
             }
           }
         }
-      } else if constexpr (MODE == kModeW32) {
-        for (int k = 0; k < mycnt; ++k, sp += SB) {
-          float w1[W], w2[W];
-          double yv;
-          load_stage_w<W, MODE>(sp, w1, w2, yv);
+        // MIXED: the fp32 windows of one tile segment sum at most 64 points per start cell; past that
+        // (only for very concentrated data) they are folded into the fp64 tile accumulator early
+        bool fold_now = nxt.tile != cur.tile;
+        if constexpr (MODE == kModeA32) {
+          pend += mycnt;
+          fold_now = named_sync_or(bar_id, kGrpThreads, pend >= 64) || fold_now;
+        } else {
+          named_sync(bar_id, kGrpThreads);  // stage and cnt free
+        }
+        if (fold_now) {
+          // add the windows into the fp64 tile accumulator in W^2 conflict-free steps
 #pragma unroll
           for (int a = 0; a < W; ++a) {
-            const double ca = (double)w1[a], cy = yv * (double)w1[a];
 #pragma unroll
             for (int b2 = 0; b2 < W; ++b2) {
-              const double wb = (double)w2[b2];
-              a1[a][b2] = fma(ca, wb, a1[a][b2]);
-              ay[a][b2] = fma(cy, wb, ay[a][b2]);
+              if (own) {
+                const int idx = (my_r + a) * A2 + (my_c + b2);
+                if constexpr (MODE == kModeA32) {
+                  const float2 v1 = p1[a][b2 / 2], vy = py[a][b2 / 2];
+                  tacc[idx] += (double)((b2 & 1) ? v1.y : v1.x);
+                  tacc[A1 * A2 + idx] += (double)((b2 & 1) ? vy.y : vy.x);
+                } else {
+                  tacc[idx] += a1[a][b2];
+                  tacc[A1 * A2 + idx] += ay[a][b2];
+                }
+              }
+              named_sync(bar_id, kGrpThreads);
             }
           }
-        }
-      } else {
-        float2 acc[W][W];
+          if constexpr (MODE == kModeA32) {
 #pragma unroll
-        for (int a = 0; a < W; ++a)
+            for (int a = 0; a < W; ++a)
 #pragma unroll
-          for (int b2 = 0; b2 < W; ++b2) acc[a][b2] = make_float2(0.f, 0.f);
-        for (int k = 0; k < mycnt; ++k, sp += SB) {
-          float w1[W], w2[W];
-          double yv;
-          load_stage_w<W, MODE>(sp, w1, w2, yv);
-          const float yf = (float)yv;
+              for (int pp = 0; pp < (W + 1) / 2; ++pp) p1[a][pp] = py[a][pp] = make_float2(0.f, 0.f);
+            pend = 0;
+          } else {
 #pragma unroll
-          for (int a = 0; a < W; ++a) {
-            const float2 pa = make_float2(w1[a], yf * w1[a]);
+            for (int a = 0; a < W; ++a)
 #pragma unroll
-            for (int b2 = 0; b2 < W; ++b2) acc[a][b2] = __ffma2_rn(pa, make_float2(w2[b2], w2[b2]), acc[a][b2]);
+              for (int b2 = 0; b2 < W; ++b2) a1[a][b2] = ay[a][b2] = 0.0;
           }
         }
-#pragma unroll
-        for (int a = 0; a < W; ++a)
-#pragma unroll
-          for (int b2 = 0; b2 < W; ++b2) {
-            a1[a][b2] += (double)acc[a][b2].x;
-            ay[a][b2] += (double)acc[a][b2].y;
+        // end of a tile segment: one RED per cell of the tile accumulator, which is re-zeroed
+        if (nxt.tile != cur.tile) {
+          for (int i = tid; i < A1 * A2; i += kGrpThreads) {
+            const double v1 = tacc[i], vy = tacc[A1 * A2 + i];
+            const int r = wrap_s(s_lo + r0 + i / A2, n1), c = wrap_s(s_lo + c0 + i % A2, n1);
+            const int64_t gidx = (int64_t)r * n1 + c;
+            if (v1 != 0.0) atomicAdd(A.g1 + gidx, v1);
+            if (vy != 0.0) atomicAdd(A.gy + gidx, vy);
+            tacc[i] = tacc[A1 * A2 + i] = 0.0;
           }
+          named_sync(bar_id, kGrpThreads);
+        }
+        cur = nxt;
       }
     }
-    __syncthreads();  // stage, kr, cnt free
-    // flush the windows at the end of a tile segment: W^2 conflict-free steps into shared memory,
-    // then one RED per cell
-    if (nxt.tile != cur.tile) {
-      double *acc = reinterpret_cast<double *>(stage);
-      for (int i = tid; i < 2 * A1 * A2; i += kTileThreads) acc[i] = 0.0;
-      __syncthreads();
-#pragma unroll
-      for (int a = 0; a < W; ++a) {
-#pragma unroll
-        for (int b2 = 0; b2 < W; ++b2) {
-          if (own) {
-            const int idx = (my_r + a) * A2 + (my_c + b2);
-            acc[idx] += a1[a][b2];
-            acc[A1 * A2 + idx] += ay[a][b2];
-          }
-          a1[a][b2] = ay[a][b2] = 0.0;
-          __syncthreads();
-        }
-      }
-      for (int i = tid; i < A1 * A2; i += kTileThreads) {
-        const double v1 = acc[i], vy = acc[A1 * A2 + i];
-        const int r = wrap_s(s_lo + r0 + i / A2, n1), c = wrap_s(s_lo + c0 + i % A2, n1);
-        const int64_t gi = (int64_t)r * n1 + c;
-        if (v1 != 0.0) atomicAdd(g1 + gi, v1);
-        if (vy != 0.0) atomicAdd(gy + gi, vy);
-      }
-      __syncthreads();
+    // this group is done reading chunk k's lists
+    named_sync(bar_id, kGrpThreads);
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(A.acc_done + k, 1u);
+      if (gi == 0) stamp(A.trace, k, 3);
     }
-    cur = nxt;
   }
 }
 
 template <int W, int MODE>
-static size_t tiles_smem_bytes(int R, int ntiles) {
-  size_t b = sizeof(double) * (size_t)(R + 2) * 3;        // raw
-  b += (size_t)R * StageRec<W, MODE>::kBytes;             // stage
-  b += 4 * (size_t)R;                                     // kr
-  b += 4 * (size_t)(kTileThreads + ntiles + 1);           // cnt, tpre
-  return b;
-}
-static size_t bin_smem_bytes(int ntiles, int S) {
-  return sizeof(double) * 2 * 3 * kBinBatch + sizeof(int) * kBinBatch + sizeof(int) * (3 * (size_t)ntiles + 2 * S);
+__global__ void __launch_bounds__(kFusedThreads, 1) k_spread_fused(const FusedArgs A, const EsPoly P, const EsPolyP PF) {
+  extern __shared__ __align__(16) unsigned char fsm[];
+  const int tid = threadIdx.x;
+  const size_t acc_bytes = 2 * AccSmem<W, MODE>::bytes(A.R, A.ntiles, gridDim.x, A.T1, A.T2);
+  if (tid >= kAccThreads) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+    binner_role<W>(A, fsm + (acc_bytes + 15) / 16 * 16, tid - kAccThreads);
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+    accumulator_role<W, MODE>(A, fsm, tid, P, PF);
+  }
 }
 
-// Tile shape (T1 x T2 start cells, T1 T2 <= 256, least covered area), chunk, capacity, round size.
+template <int W, int MODE>
+static size_t fused_smem_bytes(int R, int ntiles, int S, int grid, int T1, int T2) {
+  return 2 * AccSmem<W, MODE>::bytes(R, ntiles, grid, T1, T2) + FusedSmem<W, MODE>::bin_bytes(ntiles, S);
+}
+
+static size_t fused_smem(int w, int mode, int R, int ntiles, int S, int grid, int T1, int T2) {
+  switch (w) {
+#define EFGP_SZ(WW)                                            \
+  case WW:                                                     \
+    return mode == 0   ? fused_smem_bytes<WW, 0>(R, ntiles, S, grid, T1, T2) \
+           : mode == 1 ? fused_smem_bytes<WW, 1>(R, ntiles, S, grid, T1, T2) \
+                       : fused_smem_bytes<WW, 2>(R, ntiles, S, grid, T1, T2);
+    EFGP_SZ(2) EFGP_SZ(3) EFGP_SZ(4) EFGP_SZ(5) EFGP_SZ(6)
+#undef EFGP_SZ
+  }
+  return ~size_t(0);
+}
+
+// Tile shape (T1 x T2 start cells, T1 T2 <= 128, least covered area), chunk, capacity, round size.
 void sorted_geometry(Params &p, int num_sms) {
   p.s_lo = -(p.w / 2);
   const int hi0 = (int)std::ceil(p.h * p.n1 - 0.5 * p.w);
   p.s_count = hi0 - p.s_lo + 1;
   const int S = p.s_count;
   int64_t best = -1;
-  for (int T2 = 6; T2 <= 64; ++T2) {
-    const int T1 = std::min(kTileThreads / T2, S);
+  for (int T2 = 4; T2 <= 32; ++T2) {
+    const int T1 = std::min(kGrpThreads / T2, S);
     if (T1 < 4) continue;
     const int64_t nt1 = (S + T1 - 1) / T1, nt2 = (S + T2 - 1) / T2;
     const int64_t cover = nt1 * T1 * nt2 * T2;
@@ -591,85 +820,118 @@ void sorted_geometry(Params &p, int num_sms) {
     }
   }
   if (const char *e = std::getenv("EFGP_SORTED_T2")) {
-    p.T2 = std::max(4, std::min(64, std::atoi(e)));
-    p.T1 = std::min(kTileThreads / p.T2, S);
+    p.T2 = std::max(4, std::min(32, std::atoi(e)));
+    p.T1 = std::min(kGrpThreads / p.T2, S);
     p.nt1 = (S + p.T1 - 1) / p.T1;
     p.nt2 = (S + p.T2 - 1) / p.T2;
   }
   p.ntiles = p.nt1 * p.nt2;
-  p.chunk = int64_t(1) << 21;
-  if (const char *e = std::getenv("EFGP_SORTED_CHUNK")) p.chunk = std::max<int64_t>(kBinBatch, std::atoll(e));
-  // capacity per tile list: 2x the uniform share + slack; overflow spills to direct RED spreading
-  const double share = (double)p.chunk * p.T1 * p.T2 / ((double)S * S);
-  p.cap = (int)std::min<double>((double)p.chunk, 2.0 * share + 8192.0);
-  p.cap = (p.cap + 1) & ~1;
+  p.chunk = int64_t(1) << 22;
+  if (const char *e = std::getenv("EFGP_SORTED_CHUNK"))
+    p.chunk = std::max<int64_t>(kWBatch, std::atoll(e) / kWBatch * kWBatch);
+  p.nbuf = 2;
+  if (const char *e = std::getenv("EFGP_SORTED_NBUF")) p.nbuf = std::max(2, std::min(3, std::atoi(e)));
   p.tiles_grid = num_sms;
-  p.bin_grid = 2 * num_sms;
-  if (const char *e = std::getenv("EFGP_BIN_GRID")) p.bin_grid = std::max(1, std::atoi(e));
   if (const char *e = std::getenv("EFGP_SORTED_GRID")) p.tiles_grid = std::max(1, std::atoi(e));
-  // round size: the largest multiple of 256 whose shared memory fits 227 KB
-  const size_t lim = 224 * 1024;
-  int R = 256;
-  for (int r = 256; r <= 16384; r += 256) {
-    size_t need = 0;
-    switch (p.w) {
-#define EFGP_SZ(WW)                                                   \
-  case WW:                                                            \
-    need = p.spread_mode == 0   ? tiles_smem_bytes<WW, 0>(r, p.ntiles) \
-           : p.spread_mode == 1 ? tiles_smem_bytes<WW, 1>(r, p.ntiles) \
-                                : tiles_smem_bytes<WW, 2>(r, p.ntiles); \
-    break;
-      EFGP_SZ(2) EFGP_SZ(3) EFGP_SZ(4) EFGP_SZ(5) EFGP_SZ(6)
-#undef EFGP_SZ
-    }
-    if (need <= lim) R = r;
-  }
-  if (const char *e = std::getenv("EFGP_SORTED_R")) R = std::max(256, std::min(R, std::atoi(e) / 256 * 256));
+  // capacity of a (tile, binner CTA) segment: 2x its uniform share + slack; overflow spills to
+  // direct RED spreading (correct for any data)
+  const double share = (double)p.chunk * p.T1 * p.T2 / ((double)S * S) / p.tiles_grid;
+  p.cap = (int)std::min<double>((double)p.chunk, 2.0 * share + 256.0);
+  // round size: the largest multiple of 128 whose shared memory fits 227 KB
+  const size_t lim = 227 * 1024 - 256;
+  int R = 0;
+  for (int r = 256; r <= 16384; r += 128)
+    if (fused_smem(p.w, p.spread_mode, r, p.ntiles, S, p.tiles_grid, p.T1, p.T2) <= lim) R = r;
+  if (const char *e = std::getenv("EFGP_SORTED_R")) R = std::max(256, std::min(R, std::atoi(e) / 128 * 128));
   p.round = R;
 }
 
-template <int W>
-static efgp_status run_sorted(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s) {
+template <int W, int MODE>
+static efgp_status launch_fused(efgp_plan *pl, const FusedArgs &A, cudaStream_t s) {
   const Params &P = pl->P;
-  const int ntiles = P.ntiles, R = P.round;
-  const size_t bsm = bin_smem_bytes(ntiles, P.s_count);
-  const int mode = P.spread_mode;
-  const size_t tsm = mode == 0 ? tiles_smem_bytes<W, 0>(R, ntiles)
-                     : mode == 1 ? tiles_smem_bytes<W, 1>(R, ntiles) : tiles_smem_bytes<W, 2>(R, ntiles);
-  auto ktiles = mode == 0 ? k_tiles4<W, 0> : mode == 1 ? k_tiles4<W, 1> : k_tiles4<W, 2>;
-  EFGP_CUDA(cudaFuncSetAttribute(k_bin5<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
-  EFGP_CUDA(cudaFuncSetAttribute(ktiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
-  cudaStream_t sb = pl->bin_stream;
-  EFGP_CUDA(cudaEventRecord(pl->ev_sp, s));
-  EFGP_CUDA(cudaStreamWaitEvent(sb, pl->ev_sp, 0));
-  int k = 0;
-  for (int64_t c0 = 0; c0 < N; c0 += P.chunk, ++k) {
-    const int buf = k & 1;
-    const int64_t nc = std::min<int64_t>(P.chunk, N - c0);
-    const int nb = (int)((nc + kBinBatch - 1) / kBinBatch);
-    if (k >= 2) EFGP_CUDA(cudaStreamWaitEvent(sb, pl->ev_tiles[buf], 0));
-    EFGP_CUDA(cudaMemsetAsync(pl->tcnt[buf], 0, sizeof(int) * ntiles, sb));
-    const int bgrid = (int)std::min<int64_t>((int64_t)P.bin_grid, nb);
-    k_bin5<W><<<bgrid, kBinThreads, bsm, sb>>>(x + c0 * 2, y + c0, nc, P.h, (int)P.n1, P.s_lo, P.s_count, P.T1, P.T2,
-                                               P.nt2, ntiles, P.cap, pl->rec[buf], pl->tcnt[buf], pl->poly_dev, pl->g1,
-                                               pl->g2, pl->dflags);
-    EFGP_CUDA(cudaEventRecord(pl->ev_bin[buf], sb));
-    EFGP_CUDA(cudaStreamWaitEvent(s, pl->ev_bin[buf], 0));
-    ktiles<<<P.tiles_grid, kTileThreads, tsm, s>>>(pl->rec[buf], pl->tcnt[buf], P.cap, ntiles, P.T1, P.T2, P.nt2, R,
-                                                   P.h, (int)P.n1, P.s_lo, P.poly, P.polyf, pl->g1, pl->g2);
-    EFGP_CUDA(cudaEventRecord(pl->ev_tiles[buf], s));
+  const size_t sm = fused_smem_bytes<W, MODE>(A.R, A.ntiles, A.S, P.tiles_grid, A.T1, A.T2);
+  auto kern = k_spread_fused<W, MODE>;
+  EFGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int per_sm = 0;
+  EFGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFusedThreads, sm));
+  if (per_sm < 1) {
+    pl->err = "SORTED spreading kernel does not fit on an SM";
+    return EFGP_ERR_RESOURCE;
   }
-  EFGP_CUDA(cudaGetLastError());
+  const int grid = P.tiles_grid;  // the segment layout was sized for exactly this many CTAs
+  if (grid > pl->num_sms * per_sm) {
+    pl->err = "SORTED spreading: not all CTAs can be co-resident";
+    return EFGP_ERR_RESOURCE;
+  }
+  FusedArgs a = A;
+  EsPoly poly = P.poly;
+  EsPolyP polyf = P.polyp;
+  void *args[] = {(void *)&a, (void *)&poly, (void *)&polyf};
+  // cooperative launch: all CTAs are co-resident (they wait on one another through global counters)
+  EFGP_CUDA(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kFusedThreads), args, sm, s));
   return EFGP_OK;
 }
 
 efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s) {
-  switch (pl->P.w) {
-    case 2: return run_sorted<2>(pl, x, y, N, s);
-    case 3: return run_sorted<3>(pl, x, y, N, s);
-    case 4: return run_sorted<4>(pl, x, y, N, s);
-    case 5: return run_sorted<5>(pl, x, y, N, s);
-    case 6: return run_sorted<6>(pl, x, y, N, s);
+  const Params &P = pl->P;
+  FusedArgs A{};
+  A.x = x;
+  A.y = y;
+  A.N = N;
+  A.chunk = P.chunk;
+  A.nchunks = (int)((N + P.chunk - 1) / P.chunk);
+  A.nbuf = P.nbuf;
+  A.h = P.h;
+  A.n1 = (int)P.n1;
+  A.s_lo = P.s_lo;
+  A.S = P.s_count;
+  A.T1 = P.T1;
+  A.T2 = P.T2;
+  A.nt2 = P.nt2;
+  A.ntiles = P.ntiles;
+  A.segcap = P.cap;
+  A.R = P.round;
+  for (int b = 0; b < 3; ++b) A.rec[b] = pl->rec[b];
+  // per-chunk segment and tile lengths and the two handshake counters, zeroed for this call
+  const int G = P.tiles_grid;
+  const size_t need = (size_t)A.nchunks * ((size_t)P.ntiles * G + P.ntiles + 2);
+  if (need > pl->sync_cap) {
+    if (pl->sync_buf) cudaFree(pl->sync_buf);
+    pl->sync_buf = nullptr;
+    pl->sync_cap = 0;
+    EFGP_CUDA(cudaMalloc((void **)&pl->sync_buf, need * sizeof(int)));
+    pl->sync_cap = need;
+  }
+  EFGP_CUDA(cudaMemsetAsync(pl->sync_buf, 0, need * sizeof(int), s));
+  A.segcnt = pl->sync_buf;
+  A.tilecnt = A.segcnt + (size_t)A.nchunks * P.ntiles * G;
+  A.bin_done = reinterpret_cast<unsigned *>(A.tilecnt + (size_t)A.nchunks * P.ntiles);
+  A.acc_done = A.bin_done + A.nchunks;
+  A.trace = nullptr;
+  if (std::getenv("EFGP_SORTED_TRACE")) {
+    const size_t tn = (size_t)A.nchunks * G * 4;
+    if (tn > pl->trace_cap) {
+      if (pl->trace) cudaFree(pl->trace);
+      EFGP_CUDA(cudaMalloc((void **)&pl->trace, tn * sizeof(unsigned long long)));
+      pl->trace_cap = tn;
+    }
+    EFGP_CUDA(cudaMemsetAsync(pl->trace, 0, tn * sizeof(unsigned long long), s));
+    A.trace = pl->trace;
+    pl->trace_n = tn;
+  }
+  A.poly_dev = pl->poly_dev;
+  A.g1 = pl->g1;
+  A.gy = pl->g2;
+  A.err = pl->dflags;
+  const int mode = P.spread_mode;
+  switch (P.w) {
+#define EFGP_CASE(WW)                                  \
+  case WW:                                             \
+    return mode == 0   ? launch_fused<WW, 0>(pl, A, s) \
+           : mode == 1 ? launch_fused<WW, 1>(pl, A, s) \
+                       : launch_fused<WW, 2>(pl, A, s);
+    EFGP_CASE(2) EFGP_CASE(3) EFGP_CASE(4) EFGP_CASE(5) EFGP_CASE(6)
+#undef EFGP_CASE
   }
   pl->err = "internal: SORTED spreading needs w <= 6";
   return EFGP_ERR_INVALID;

@@ -34,6 +34,24 @@ def main():
             g.fit(x, y)
         inf = g.info()
         print(f"spread {inf['t_spread_ms']:.3f} ms  {N / inf['t_spread_ms'] * 1e3:.3e} pts/s", flush=True)
+    if os.environ.get("EFGP_SORTED_TRACE"):
+        import ctypes as C
+        import numpy as np
+        n = g._lib.efgp_debug_trace(g._h, None, 0)
+        buf = np.zeros(n, dtype=np.uint64)
+        g._lib.efgp_debug_trace(g._h, buf.ctypes.data_as(C.c_void_p), n)
+        G = 148
+        tr = buf.reshape(-1, G, 4).astype(np.float64)
+        t0 = tr[tr > 0].min()
+        tr = (tr - t0) / 1e3  # us
+        nch = tr.shape[0]
+        for k in list(range(min(nch, 6))) + [nch - 1]:
+            b, w0, w1, d = tr[k, :, 0], tr[k, :, 1], tr[k, :, 2], tr[k, :, 3]
+            print(f"chunk {k:3d}: binned [{b.min():8.1f} .. {b.max():8.1f}]  acc wait from [{w0.min():8.1f} .. {w0.max():8.1f}] "
+                  f"start [{w1.min():8.1f} .. {w1.max():8.1f}]  done [{d.min():8.1f} .. {d.max():8.1f}] us")
+        waits = (tr[:, :, 2] - tr[:, :, 1]).sum(axis=0)
+        work = (tr[:, :, 3] - tr[:, :, 2]).sum(axis=0)
+        print(f"acc total wait per CTA: mean {waits.mean():.1f} us, acc work per CTA mean {work.mean():.1f} us (max {work.max():.1f})")
     g.close()
 
 
