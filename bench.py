@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-points", type=float, default=1e6, help="cpu_baseline sample size")
     ap.add_argument("--spread", default="auto")
+    ap.add_argument("--weights", default="fp64", choices=["fp64", "fp32", "mixed"],
+                    help="SORTED spreading arithmetic (include/efgp.h efgp_weights); fp64 is the strict default")
     return ap.parse_args()
 
 
@@ -70,7 +72,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "200", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                                          "-lms", "100", "-i", str(self.idx)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -193,7 +195,7 @@ def main():
     xt = G.generate_targets(cfg, qa, qb - qa, device=dev)
     mu = torch.empty(qb - qa, dtype=torch.float64, device=dev)
     torch.cuda.synchronize()
-    model = EFGP(cfg.kernel, cfg.ell, cfg.sigma, cfg.eps, cfg.d, cfg.nu, spread=args.spread)
+    model = EFGP(cfg.kernel, cfg.ell, cfg.sigma, cfg.eps, cfg.d, cfg.nu, spread=args.spread, weights=args.weights)
     graph_iters = 8
 
     def step(xx, yy, tt, out):
@@ -275,12 +277,16 @@ def main():
         alg_bytes = (b - a) * 8 * (d + 1)                      # read x and y once
         sp = statistics.median(spread_ms)
         achieved = alg_bytes / (sp / 1e3) / 1e9
-        traffic = None
+        # DRAM traffic per launch of the spreading kernel: bytes/point from the committed ncu --set full
+        # capture (profiles/traffic.json, written from the capture by hand) x this launch's points
+        traffic, traffic_src = None, None
         try:
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
                 tr = json.load(f)
-            key = f"{cfg.name}_N{N // world}_{inf['spread_method']}"
-            traffic = tr.get(key)
+            ent = tr.get(f"{cfg.name}_{inf['spread_method']}_{args.weights}")
+            if ent:
+                traffic = ent["bytes_per_point"] * (b - a)
+                traffic_src = ent["capture"]
         except Exception:
             pass
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -289,14 +295,15 @@ def main():
                "data": "synthetic (device Philox generator, efgp_data)",
                "config": {"workload": f"{cfg.name}: 2D Matern-3/2 l={cfg.ell} sigma={cfg.sigma} eps={cfg.eps}, "
                                       f"N={N:.0e} uniform points, q={q:.0e} uniform targets, seed {cfg.seed}",
-                          "N": N, "q": q, "m": inf["m"], "M": inf["M"], "cg_iters": statistics.median(iters),
+                          "N": N, "q": q, "spread": inf["spread_method"], "spread_arithmetic": args.weights,
+                          "m": inf["m"], "M": inf["M"], "cg_iters": statistics.median(iters),
                           "l2": "inputs (24 GB/N_gpus) larger than the 126 MB L2; no explicit flush",
                           "parallelism": f"points sharded x{world}, one allreduce of modes, CG replicated"},
                "phases_ms": {"spread": sp, "fft_deconv": statistics.median(modes_ms),
                              "toeplitz+cg": statistics.median(solve_ms), "predict": statistics.median(pred_ms)},
                "roofline": {"kernel": f"k_spread_{inf['spread_method']} (K1)", "bound": "hbm",
                             "achieved": achieved, "peak": peak, "peak_source": src, "unit": "GB/s",
-                            "frac": achieved / peak, "traffic": traffic,
+                            "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                             "alg_bytes_per_launch": alg_bytes},
                "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches}
         if not args.no_cpu_baseline:
