@@ -38,6 +38,11 @@ efgp_status make_plan(efgp_plan *pl, cufftHandle *h, int d, int64_t n, cufftType
 }
 
 efgp_status build(efgp_plan *pl) {
+  if (pl->P.spread_method == EFGP_SPREAD_SORTED && !sorted_geometry(pl->P, pl->num_sms)) {
+    pl->P.sorted_disabled = true;  // e.g. too many tiles for shared memory: SMEM or GLOBAL instead
+    pl->P.spread_method = pl->P.spread_method_requested;
+    resolve_spread_method(pl->P);
+  }
   const Params &P = pl->P;
   const int d = P.d;
   // D_j = sqrt(h^d k^(h|j|)) on the J_m half (eq 117)
@@ -76,7 +81,6 @@ efgp_status build(efgp_plan *pl) {
   EFGP_TRY(dalloc(pl, &pl->G1h, G1h));
   EFGP_TRY(dalloc(pl, &pl->G2h, Grh));
   if (P.spread_method == EFGP_SPREAD_SORTED) {
-    sorted_geometry(pl->P, pl->num_sms);
     for (int k = 0; k < P.nbuf; ++k)
       EFGP_TRY(dalloc(pl, &pl->rec[k], (int64_t)P.ntiles * P.tiles_grid * P.cap));
   }

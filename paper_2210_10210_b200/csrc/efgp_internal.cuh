@@ -13,8 +13,13 @@ namespace efgp {
 constexpr double kPi = 3.14159265358979323846;
 constexpr int kMaxW = 16;  // ES kernel width for nufft_tol down to 1e-15
 
-// Piecewise-polynomial ES kernel weights (degree w+2 in s = 2u-1 per cell offset a), passed to the
-// kernels by value (lives in the constant bank).
+// Degree of the piecewise-polynomial ES kernel per cell offset: degree W already gives the aliasing
+// error of the exact ES kernel to within 2 % for W >= 4 (the deconvolution tables are the
+// polynomial's own Fourier transform); narrower kernels keep W + 2.
+__host__ __device__ constexpr int es_degree(int W) { return W >= 4 ? W : W + 2; }
+
+// Piecewise-polynomial ES kernel weights (degree es_degree(w) in s = 2u-1 per cell offset a), passed
+// to the kernels by value (lives in the constant bank).
 struct EsPoly {
   double c[kMaxW][kMaxW + 3];
   int deg;
@@ -47,6 +52,8 @@ struct Params {
   int64_t n_rhs = 0;    // grid of the strength-y spread: n1 (SORTED) or n2
   int rescale = EFGP_RESCALE_L2;
   int spread_method = EFGP_SPREAD_AUTO;  // resolved at setup (never AUTO afterwards)
+  int spread_method_requested = EFGP_SPREAD_AUTO;
+  bool sorted_disabled = false;          // SORTED geometry does not fit: resolve to another method
   int graph_iters = 8;
   EsPoly poly{};
   EsPolyF polyf{};
@@ -76,7 +83,7 @@ std::vector<double> es_fourier_table_poly(const EsPoly &P, int w, int64_t n, int
 // spread.cu: choose the spreading strategy (sets spread_method, n_rhs)
 void resolve_spread_method(Params &p);
 // spread_sorted.cu: tile geometry of the SORTED strategy
-void sorted_geometry(Params &p, int num_sms);
+bool sorted_geometry(Params &p, int num_sms);  // false: no room for a round
 
 struct DevBuf {
   void *ptr = nullptr;
@@ -209,7 +216,7 @@ __device__ __forceinline__ double es_kernel(double z, double beta) {
 }
 
 // Weights of the W cells i0 .. i0+W-1 for a point at grid coordinate t: i0 = ceil(t - W/2),
-// u = i0 - (t - W/2) in [0,1), w[a] = phi~_a(u) by Horner (degree W+2) in s = 2u - 1.
+// u = i0 - (t - W/2) in [0,1), w[a] = phi~_a(u) by Horner (degree es_degree(W)) in s = 2u - 1.
 template <int W>
 __device__ __forceinline__ int es_weights(double t, const EsPoly &P, double (&w)[W]) {
   const double tm = __dsub_rn(t, 0.5 * W);  // no FMA contraction: the SORTED binning must agree
@@ -217,9 +224,10 @@ __device__ __forceinline__ int es_weights(double t, const EsPoly &P, double (&w)
   const double s = 2.0 * (i0 - tm) - 1.0;
 #pragma unroll
   for (int a = 0; a < W; ++a) {
-    double acc = P.c[a][W + 2];
+    constexpr int D = es_degree(W);
+    double acc = P.c[a][D];
 #pragma unroll
-    for (int k = W + 1; k >= 0; --k) acc = fma(acc, s, P.c[a][k]);
+    for (int k = D - 1; k >= 0; --k) acc = fma(acc, s, P.c[a][k]);
     w[a] = acc;
   }
   return (int)i0;

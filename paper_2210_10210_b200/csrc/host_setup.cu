@@ -74,11 +74,11 @@ void gauss_legendre(int n, std::vector<double> &x, std::vector<double> &w) {
 }
 
 // Piecewise-polynomial ES kernel: for cell offset a in [0, w) and
-// u in [0, 1), phi_a(u) = phi((2(a+u) - w)/w) is approximated by a degree-(w+2) polynomial in
+// u in [0, 1), phi_a(u) = phi((2(a+u) - w)/w) is approximated by a degree-es_degree(w) polynomial in
 // s = 2u - 1 from Chebyshev interpolation, stored as monomial coefficients c[a][k].
 void es_poly_fit(int w, double beta, EsPoly &out) {
   std::memset(&out, 0, sizeof(out));
-  const int p = w + 2;  // degree
+  const int p = es_degree(w);  // degree
   out.deg = p;
   const int nn = p + 1;
   for (int a = 0; a < w; ++a) {
@@ -213,6 +213,7 @@ std::string validate_and_choose(Params &p, const efgp_options &opt) {
   p.n2 = next_smooth(std::max<int64_t>(2 * (2 * p.m + 1), 2 * p.w));
   p.L = next_smooth(4 * p.m + 1);
   p.spread_method = opt.spread_method;
+  p.spread_method_requested = opt.spread_method;
   p.graph_iters = opt.graph_iters > 0 ? opt.graph_iters : 8;
   es_poly_fit(p.w, p.beta_es, p.poly);
   for (int a = 0; a < kMaxW; ++a)

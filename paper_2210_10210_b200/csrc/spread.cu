@@ -206,7 +206,7 @@ static size_t smem_bytes(const Params &P) {
 void resolve_spread_method(Params &p) {
   int m = p.spread_method;
   // SORTED: 2D, register windows up to 6 x 6, start-cell lookup tables up to 2048 per dimension
-  const bool sorted_ok = p.d == 2 && p.w <= 6 && p.h * p.n1 + p.w < 2048;
+  const bool sorted_ok = p.d == 2 && p.w <= 6 && p.h * p.n1 + p.w < 2048 && !p.sorted_disabled;
   const bool smem_ok = smem_bytes(p) <= 200 * 1024;
   if (m == EFGP_SPREAD_AUTO) m = sorted_ok ? EFGP_SPREAD_SORTED : (smem_ok ? EFGP_SPREAD_SMEM : EFGP_SPREAD_GLOBAL);
   if (m == EFGP_SPREAD_SORTED && !sorted_ok) m = smem_ok ? EFGP_SPREAD_SMEM : EFGP_SPREAD_GLOBAL;

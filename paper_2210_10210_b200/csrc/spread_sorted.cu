@@ -121,9 +121,10 @@ __device__ __forceinline__ void es_weights_f32x2(double t1, double t2, const EsP
   const float2 s = make_float2((float)(2.0 * (ceil(tm1) - tm1) - 1.0), (float)(2.0 * (ceil(tm2) - tm2) - 1.0));
 #pragma unroll
   for (int a = 0; a < W; ++a) {
-    float2 acc = make_float2(P.c[a][W + 2], P.c[a][W + 2]);
+    constexpr int D = es_degree(W);
+    float2 acc = make_float2(P.c[a][D], P.c[a][D]);
 #pragma unroll
-    for (int k = W + 1; k >= 0; --k) acc = __ffma2_rn(acc, s, make_float2(P.c[a][k], P.c[a][k]));
+    for (int k = D - 1; k >= 0; --k) acc = __ffma2_rn(acc, s, make_float2(P.c[a][k], P.c[a][k]));
     w1[a] = acc.x;
     w2[a] = acc.y;
   }
@@ -138,9 +139,10 @@ __device__ __forceinline__ void es_weights_pairs(double t, const EsPolyP &P, flo
   const float2 s2 = make_float2(s, s);
 #pragma unroll
   for (int q = 0; q < (W + 1) / 2; ++q) {
-    float2 acc = P.c[q][W + 2];
+    constexpr int D = es_degree(W);
+    float2 acc = P.c[q][D];
 #pragma unroll
-    for (int k = W + 1; k >= 0; --k) acc = __ffma2_rn(acc, s2, P.c[q][k]);
+    for (int k = D - 1; k >= 0; --k) acc = __ffma2_rn(acc, s2, P.c[q][k]);
     w[q] = acc;
   }
 }
@@ -252,7 +254,7 @@ struct FusedArgs {
 };
 
 constexpr int kWBatch = 256;                      // points per binner-warp batch
-constexpr int kWStages = 3;                       // TMA ring depth per binner warp
+constexpr int kWStages = 2;                       // TMA ring depth per binner warp
 constexpr int kBinWarps = kBinThreads / 32;       // 4
 
 template <int W, int MODE>
@@ -433,7 +435,7 @@ struct AccSmem {
   // segment prefixes, fp64 tile accumulator; all 16-byte multiples
   __host__ __device__ static size_t bytes(int R, int ntiles, int grid, int T1, int T2) {
     size_t b = 32 * (size_t)R + (size_t)R * StageRec<W, MODE>::kBytes;
-    b += ((4 * (size_t)(kGrpThreads + ntiles + 1 + 2 * (grid + 1))) + 15) / 16 * 16;
+    b += ((4 * (size_t)(2 * kGrpThreads + ntiles + 1 + 2 * (grid + 1))) + 15) / 16 * 16;
     b += 16 * (size_t)(T1 + W - 1) * (T2 + W - 1);
     return b;
   }
@@ -447,15 +449,17 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
   const int bar_id = gi == 0 ? kBarAcc : kBarAcc2;
   const int R = A.R, ntiles = A.ntiles, T1 = A.T1, T2 = A.T2, n1 = A.n1, s_lo = A.s_lo, G = gridDim.x;
   const int VG = G * kAccGroups, vb = blockIdx.x * kAccGroups + gi;  // virtual CTA
+  if (R <= 0) __trap();  // the host never launches without a round (sorted_geometry checks)
   const double h = A.h;
   unsigned char *gsm = sm + gi * AccSmem<W, MODE>::bytes(R, ntiles, G, T1, T2);
   double4 *raw = reinterpret_cast<double4 *>(gsm);                      // R records
   unsigned char *stage = reinterpret_cast<unsigned char *>(raw + R);    // R * SB, cell-sorted
   int *cnt = reinterpret_cast<int *>(stage + (size_t)R * SB);           // 128
-  int *tpre = cnt + kGrpThreads;                                        // ntiles + 1
+  int *coff = cnt + kGrpThreads;                                        // 128: cell offsets
+  int *tpre = coff + kGrpThreads;                                       // ntiles + 1
   int *spre = tpre + ntiles + 1;                                        // [2][G + 1]
   double *tacc = reinterpret_cast<double *>(
-      gsm + 32 * (size_t)R + (size_t)R * SB + ((4 * (size_t)(kGrpThreads + ntiles + 1 + 2 * (G + 1))) + 15) / 16 * 16);
+      gsm + 32 * (size_t)R + (size_t)R * SB + ((4 * (size_t)(2 * kGrpThreads + ntiles + 1 + 2 * (G + 1))) + 15) / 16 * 16);
   __shared__ int wsum_s[kAccGroups][8], total_s[kAccGroups], spre_tile_s[kAccGroups][2];
   __shared__ __align__(8) uint64_t bar_s[kAccGroups];
   int *wsum = wsum_s[gi], *spre_tile = spre_tile_s[gi];
@@ -600,13 +604,24 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
         }
         named_sync(bar_id, kGrpThreads);
         const int mycnt = cnt[tid];
-        const int myoff = group_scan<4>(mycnt, tid, wsum, bar_id, nullptr);
-        cnt[tid] = myoff;
+        if (tid < 32) {  // cell offsets: warp 0 scans the 128 counts (4 per lane)
+          const int4 c4 = reinterpret_cast<const int4 *>(cnt)[tid];
+          const int sum = c4.x + c4.y + c4.z + c4.w;
+          int incl = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o) incl += v;
+          }
+          const int e = incl - sum;
+          reinterpret_cast<int4 *>(coff)[tid] = make_int4(e, e + c4.x, e + c4.x + c4.y, e + c4.x + c4.y + c4.z);
+        }
         named_sync(bar_id, kGrpThreads);
+        const int myoff = coff[tid];
         // pass 2 (thread per record): the record (FP64) or its fp32 weights at its sorted slot
         for (int j = tid; j < nr; j += kGrpThreads) {
           const double4 rv = raw[j];
-          unsigned char *st = stage + (size_t)(cnt[__double2loint(rv.w)] + __double2hiint(rv.w)) * SB;
+          unsigned char *st = stage + (size_t)(coff[__double2loint(rv.w)] + __double2hiint(rv.w)) * SB;
           if constexpr (MODE == kModeF64) {
             double *d = reinterpret_cast<double *>(st);
             d[0] = rv.x;
@@ -799,7 +814,7 @@ static size_t fused_smem(int w, int mode, int R, int ntiles, int S, int grid, in
 }
 
 // Tile shape (T1 x T2 start cells, T1 T2 <= 128, least covered area), chunk, capacity, round size.
-void sorted_geometry(Params &p, int num_sms) {
+bool sorted_geometry(Params &p, int num_sms) {
   p.s_lo = -(p.w / 2);
   const int hi0 = (int)std::ceil(p.h * p.n1 - 0.5 * p.w);
   p.s_count = hi0 - p.s_lo + 1;
@@ -844,6 +859,7 @@ void sorted_geometry(Params &p, int num_sms) {
     if (fused_smem(p.w, p.spread_mode, r, p.ntiles, S, p.tiles_grid, p.T1, p.T2) <= lim) R = r;
   if (const char *e = std::getenv("EFGP_SORTED_R")) R = std::max(256, std::min(R, std::atoi(e) / 128 * 128));
   p.round = R;
+  return R >= 256;  // otherwise the lists / tables do not leave room for a round: use another method
 }
 
 template <int W, int MODE>
