@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libefgp.so")
+LIB_PATH = os.environ.get("EFGP_LIB", os.path.join(HERE, "libefgp.so"))  # override: A/B builds
 
 EFGP_OK, EFGP_ERR_NOCONVERGE, EFGP_ERR_INVALID, EFGP_ERR_RESOURCE, EFGP_ERR_CUDA, EFGP_ERR_NCCL = range(6)
 STATUS_NAMES = {0: "EFGP_OK", 1: "EFGP_ERR_NOCONVERGE", 2: "EFGP_ERR_INVALID", 3: "EFGP_ERR_RESOURCE",

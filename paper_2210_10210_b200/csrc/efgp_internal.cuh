@@ -216,19 +216,33 @@ __device__ __forceinline__ double es_kernel(double z, double beta) {
 }
 
 // Weights of the W cells i0 .. i0+W-1 for a point at grid coordinate t: i0 = ceil(t - W/2),
-// u = i0 - (t - W/2) in [0,1), w[a] = phi~_a(u) by Horner (degree es_degree(W)) in s = 2u - 1.
+// u = i0 - (t - W/2) in [0,1), w[a] = phi~_a(u) in s = 2u - 1 (degree es_degree(W)).  The ES kernel
+// is even, so piece W-1-a is piece a mirrored, p_{W-1-a}(s) = p_a(-s) (es_poly_fit builds them so):
+// with p_a = E_a(s^2) + s O_a(s^2), one even and one odd Horner in s^2 give both weights, half the
+// FMAs of W separate Horner evaluations.
 template <int W>
 __device__ __forceinline__ int es_weights(double t, const EsPoly &P, double (&w)[W]) {
   const double tm = __dsub_rn(t, 0.5 * W);  // no FMA contraction: the SORTED binning must agree
   const double i0 = ceil(tm);
   const double s = 2.0 * (i0 - tm) - 1.0;
+  const double s2 = s * s;
+  constexpr int D = es_degree(W);
+  constexpr int DE = D & ~1, DO = (D & 1) ? D : D - 1;  // highest even / odd power
 #pragma unroll
-  for (int a = 0; a < W; ++a) {
-    constexpr int D = es_degree(W);
-    double acc = P.c[a][D];
+  for (int a = 0; a < W / 2; ++a) {
+    double e = P.c[a][DE], o = P.c[a][DO];
 #pragma unroll
-    for (int k = D - 1; k >= 0; --k) acc = fma(acc, s, P.c[a][k]);
-    w[a] = acc;
+    for (int k = DE - 2; k >= 0; k -= 2) e = fma(e, s2, P.c[a][k]);
+#pragma unroll
+    for (int k = DO - 2; k >= 1; k -= 2) o = fma(o, s2, P.c[a][k]);
+    w[a] = fma(s, o, e);
+    w[W - 1 - a] = fma(-s, o, e);
+  }
+  if constexpr (W & 1) {
+    double e = P.c[W / 2][DE];
+#pragma unroll
+    for (int k = DE - 2; k >= 0; k -= 2) e = fma(e, s2, P.c[W / 2][k]);
+    w[W / 2] = e;
   }
   return (int)i0;
 }

@@ -115,6 +115,12 @@ void es_poly_fit(int w, double beta, EsPoly &out) {
     }
     for (int k = 0; k < nn; ++k) out.c[a][k] = mono[k];
   }
+  // exact mirror symmetry of the even ES kernel (es_weights relies on it): piece w-1-a is piece a at
+  // -s, the middle piece (w odd) is even
+  for (int a = 0; a < w / 2; ++a)
+    for (int k = 0; k < nn; ++k) out.c[w - 1 - a][k] = (k & 1) ? -out.c[a][k] : out.c[a][k];
+  if (w & 1)
+    for (int k = 1; k < nn; k += 2) out.c[w / 2][k] = 0.0;
 }
 
 double es_poly_eval(const EsPoly &P, int a, double u) {

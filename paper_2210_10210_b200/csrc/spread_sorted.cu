@@ -406,16 +406,24 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     for (int q = 0; q < kWBatch / 32; ++q)
       if (tk[q] >= 0) perm[wloc[tk[q] >> 8] + rk[q]] = (q * 32 + lane) | (tk[q] << 8);
     __syncwarp();
+    bool ovf = false;
     for (int slot = lane; slot < nv; slot += 32) {
       const int v = perm[slot];
       const int j = v & 0xFF, key = (v >> 8) & 0xFF, t = v >> 16;
       const int p = wbase[t] + slot - wloc[t];
       const double2 xx = xs2[j];
       const double yv = ys[j];
-      if (p < A.segcap) {
+      if (p < A.segcap)
         rec[((int64_t)t * G + blockIdx.x) * A.segcap + p] = make_double4(xx.x, xx.y, yv, __longlong_as_double((long long)key));
-      } else {
-        spread_point_red<W>(xx.x, xx.y, yv, A.h, A.n1, A.poly_dev, A.g1, A.gy);
+      else
+        ovf = true;
+    }
+    if (__any_sync(0xffffffffu, ovf)) {  // full segments (concentrated data): direct RED spreading,
+      for (int slot = lane; slot < nv; slot += 32) {  // kept out of the hot loop above
+        const int v = perm[slot];
+        const int j = v & 0xFF, t = v >> 16;
+        if (wbase[t] + slot - wloc[t] >= A.segcap)
+          spread_point_red<W>(xs2[j].x, xs2[j].y, ys[j], A.h, A.n1, A.poly_dev, A.g1, A.gy);
       }
     }
     __syncwarp();  // stage s consumed
@@ -476,6 +484,15 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
   for (int i = tid; i < 2 * A1 * A2; i += kGrpThreads) tacc[i] = 0.0;
   named_sync(bar_id, kGrpThreads);
   uint32_t phase = 0u;
+  // optional phase timing (EFGP_SORTED_TRACE): cycles spent between the PH(i) marks, thread 0 of
+  // each group, summed over the launch into trace[nchunks*G*4 + (blockIdx*2 + group)*8 + i]
+  long long ph_t = clock64(), ph_acc[7] = {0, 0, 0, 0, 0, 0, 0};
+#define PH(i)                                    \
+  if (A.trace && tid == 0) {                     \
+    const long long t_ = clock64();              \
+    ph_acc[(i)] += t_ - ph_t;                    \
+    ph_t = t_;                                   \
+  }
   // register windows of this thread's start cell: fp64 (FP64 / FP32 modes) or fp32 pairs along b
   // (MIXED); the unused set is eliminated by the compiler
   double a1[W][W], ay[W][W];
@@ -593,9 +610,11 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
         const int nr = cur.n;
         cnt[tid] = 0;
         seg_prefix(nxt.tile);  // for issue(nxt) below
+        PH(0);
         mbar_wait(bar, phase);
         phase ^= 1u;
         named_sync(bar_id, kGrpThreads);
+        PH(1);
         // pass 1 (thread per record): rank within its start cell (key from the binner), kept in
         // the record's key slot
         for (int j = tid; j < nr; j += kGrpThreads) {
@@ -617,6 +636,7 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
           reinterpret_cast<int4 *>(coff)[tid] = make_int4(e, e + c4.x, e + c4.x + c4.y, e + c4.x + c4.y + c4.z);
         }
         named_sync(bar_id, kGrpThreads);
+        PH(2);
         const int myoff = coff[tid];
         // pass 2 (thread per record): the record (FP64) or its fp32 weights at its sorted slot
         for (int j = tid; j < nr; j += kGrpThreads) {
@@ -654,6 +674,7 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
           }
         }
         named_sync(bar_id, kGrpThreads);
+        PH(3);
         issue(nxt);  // raw is free: the next round's copies land during phase C
         // phase C (thread per start cell): register accumulation of its records
         if (mycnt > 0) {
@@ -716,6 +737,7 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
         }
         // MIXED: the fp32 windows of one tile segment sum at most 64 points per start cell; past that
         // (only for very concentrated data) they are folded into the fp64 tile accumulator early
+        PH(4);
         bool fold_now = nxt.tile != cur.tile;
         if constexpr (MODE == kModeA32) {
           pend += mycnt;
@@ -756,6 +778,7 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
               for (int b2 = 0; b2 < W; ++b2) a1[a][b2] = ay[a][b2] = 0.0;
           }
         }
+        PH(5);
         // end of a tile segment: one RED per cell of the tile accumulator, which is re-zeroed
         if (nxt.tile != cur.tile) {
           for (int i = tid; i < A1 * A2; i += kGrpThreads) {
@@ -768,9 +791,11 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
           }
           named_sync(bar_id, kGrpThreads);
         }
+        PH(6);
         cur = nxt;
       }
     }
+    PH(0);  // (the chunk hand-off counts as waiting)
     // this group is done reading chunk k's lists
     named_sync(bar_id, kGrpThreads);
     if (tid == 0) {
@@ -779,6 +804,11 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
       if (gi == 0) stamp(A.trace, k, 3);
     }
   }
+  if (A.trace && tid == 0) {
+    unsigned long long *o = A.trace + (size_t)A.nchunks * G * 4 + ((size_t)blockIdx.x * kAccGroups + gi) * 8;
+    for (int i = 0; i < 7; ++i) o[i] = (unsigned long long)ph_acc[i];
+  }
+#undef PH
 }
 
 template <int W, int MODE>
@@ -787,10 +817,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_spread_fused(const FusedAr
   const int tid = threadIdx.x;
   const size_t acc_bytes = 2 * AccSmem<W, MODE>::bytes(A.R, A.ntiles, gridDim.x, A.T1, A.T2);
   if (tid >= kAccThreads) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;" ::: "memory");
     binner_role<W>(A, fsm + (acc_bytes + 15) / 16 * 16, tid - kAccThreads);
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
     accumulator_role<W, MODE>(A, fsm, tid, P, PF);
   }
 }
@@ -925,7 +955,7 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
   A.acc_done = A.bin_done + A.nchunks;
   A.trace = nullptr;
   if (std::getenv("EFGP_SORTED_TRACE")) {
-    const size_t tn = (size_t)A.nchunks * G * 4;
+    const size_t tn = (size_t)A.nchunks * G * 4 + (size_t)G * kAccGroups * 8;
     if (tn > pl->trace_cap) {
       if (pl->trace) cudaFree(pl->trace);
       EFGP_CUDA(cudaMalloc((void **)&pl->trace, tn * sizeof(unsigned long long)));

@@ -41,6 +41,14 @@ def main():
         buf = np.zeros(n, dtype=np.uint64)
         g._lib.efgp_debug_trace(g._h, buf.ctypes.data_as(C.c_void_p), n)
         G = 148
+        nch = (n - G * 2 * 8) // (G * 4)
+        ph = buf[nch * G * 4:].reshape(G * 2, 8).astype(np.float64)[:, :7]
+        names = ["wait/chunk", "tma wait", "pass1+scan", "pass2", "phaseC", "fold", "flush"]
+        tot = ph.sum(axis=1, keepdims=True)
+        frac = (ph / tot).mean(axis=0)
+        print("accumulator phase shares (thread 0 of each group, clock64):",
+              ", ".join(f"{nm} {100 * f:.1f}%" for nm, f in zip(names, frac)))
+        buf = buf[:nch * G * 4]
         tr = buf.reshape(-1, G, 4).astype(np.float64)
         t0 = tr[tr > 0].min()
         tr = (tr - t0) / 1e3  # us
