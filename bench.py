@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--N", type=float, default=None, help="override the number of points")
     ap.add_argument("--q", type=float, default=None, help="override the number of targets")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-interp-n", action="store_true", help="skip the NEXT-1 measurement (mu at the N points)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-points", type=float, default=1e6, help="cpu_baseline sample size")
     ap.add_argument("--spread", default="auto")
@@ -238,6 +239,27 @@ def main():
     inf = model.info()
     value = N / (ms / 1e3)
 
+    # NEXT-1: mu at the N training points (Alg a1 step 7), i.e. K9 at q = N;
+    # reported beside the headline (not part of it), with its own HBM roofline (read x*, write mu)
+    interp_n = None
+    if not args.no_interp_n:
+        try:
+            mu_n = torch.empty(b - a, dtype=torch.float64, device=dev)
+            model.predict(x, out=mu_n)  # warm-up
+            tis = []
+            for _ in range(max(1, min(args.steps, 3))):
+                model.predict(x, out=mu_n)
+                tis.append(model.info()["t_predict_ms"])
+            ti = statistics.median(tis)
+            alg = (b - a) * 8 * (cfg.d + 1)
+            pk, _ = peaks()
+            interp_n = {"q": b - a, "ms": ti, "targets_per_s": (b - a) / (ti / 1e3), "kernel": "k_interp (K9)",
+                        "roofline": {"bound": "hbm", "achieved": alg / (ti / 1e3) / 1e9, "peak": pk, "unit": "GB/s",
+                                     "frac": alg / (ti / 1e3) / 1e9 / pk}}
+            del mu_n
+        except Exception as exc:
+            interp_n = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
     # e2e: same metric through the public API with host (pinned) buffers, copies inside the step
     e2e = None
     if not args.no_e2e:
@@ -305,7 +327,7 @@ def main():
                             "achieved": achieved, "peak": peak, "peak_source": src, "unit": "GB/s",
                             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                             "alg_bytes_per_launch": alg_bytes},
-               "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches}
+               "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "mu_at_training_points": interp_n}
         if not args.no_cpu_baseline:
             try:
                 ns = int(args.oracle_points)

@@ -351,3 +351,58 @@ def test_device_generator_matches_host_generator():
             np.testing.assert_allclose(xd.cpu().numpy(), xh, rtol=0, atol=1e-14)
         np.testing.assert_allclose(yd.cpu().numpy(), yh, rtol=0, atol=1e-13)
         np.testing.assert_array_equal(td.cpu().numpy(), th)
+
+
+# ------------------------------------------------------------------ full size (BASELINE c5, N = 1e9)
+def _uniform_mode_mean(a):
+    """E[exp(-2 pi i a X)], X ~ U[0,1]: (1 - exp(-2 pi i a)) / (2 pi i a) (1 at a = 0)."""
+    a = np.asarray(a, dtype=np.float64)
+    out = np.ones(a.shape, dtype=np.complex128)
+    nz = a != 0
+    out[nz] = (1 - np.exp(-2j * np.pi * a[nz])) / (2j * np.pi * a[nz])
+    return out
+
+
+def _moment(f, a, nodes=400):
+    """int_0^1 f(x) exp(-2 pi i a x) dx by Gauss-Legendre (f smooth)."""
+    z, w = np.polynomial.legendre.leggauss(nodes)
+    x, w = 0.5 * (z + 1), 0.5 * w
+    return (w * f(x)) @ np.exp(-2j * np.pi * np.outer(x, a))
+
+
+def test_full_size_c5_type1_properties():
+    # The bench workload itself (c5, N = 1e9 device-generated uniform points, production options,
+    # the SORTED launch configuration bench.py times).  The oracle's direct sums cannot run at this
+    # size, so the type-1 outputs are checked against what holds at any size: for iid uniform points
+    # E[v_j] = N prod_k E[e^{-2 pi i h j_k X}] and E[(F*y)_j] = N I_sin(h j_1) I_cos(h j_2) for
+    # y = sin(6 pi x1) cos(4 pi x2) + zero-mean noise; deviations are the NUFFT error (<= 5 tol ||v||)
+    # plus sampling noise (~1/sqrt(N)).  v_0 = N up to the NUFFT error.
+    import torch
+    from efgp_data import gpu as G
+    c = CONFIGS["c5"]
+    N = c.N
+    try:
+        x, y = G.generate_points(c, 0, N)
+    except RuntimeError as exc:  # pragma: no cover - needs ~24 GB of free device memory
+        pytest.skip(f"cannot allocate the full c5 input: {exc}")
+    g = model(c, max_iter=1)
+    with pytest.warns(RuntimeWarning):
+        g.fit(x, y)
+    inf = g.info()
+    assert inf["spread_method"] == "sorted"
+    m, h, tol = inf["m"], inf["h"], inf["nufft_tol"]
+    v = gpu_v_full(m, g) / N
+    j = np.arange(-2 * m, 2 * m + 1)
+    ev = np.outer(_uniform_mode_mean(h * j), _uniform_mode_mean(h * j))
+    bound = 5 * tol * np.linalg.norm(v) + 8 / math.sqrt(N)
+    assert abs(v[2 * m, 2 * m] - 1.0) <= 5 * tol
+    assert np.max(np.abs(v - ev)) <= bound, (np.max(np.abs(v - ev)), bound)
+    D = O.spectral_weights(c.kernel, c.ell, c.d, h, m, c.nu)
+    fy = gpu_rhs_full(g) / (D * N)
+    jm = np.arange(-m, m + 1)
+    efy = np.outer(_moment(lambda t: np.sin(6 * np.pi * t), h * jm), _moment(lambda t: np.cos(4 * np.pi * t), h * jm))
+    bound_y = 5 * tol * np.linalg.norm(fy) + 8 / math.sqrt(N)
+    assert np.max(np.abs(fy - efy)) <= bound_y, (np.max(np.abs(fy - efy)), bound_y)
+    g.close()
+    del x, y
+    torch.cuda.empty_cache()
