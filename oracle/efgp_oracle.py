@@ -16,6 +16,8 @@ fast transform replaced by the sum that defines it:
   step 4  CG .................. :func:`cg` on :func:`system_apply`; Toeplitz product by direct
                                  convolution (P:796-825, P:846-848), CG as P:895-901, P:1973-1974
   step 5/6 mu(x*) ............. :func:`posterior_mean`    direct sum, eq ``muws``
+  NEXT-2  s(x*) ............... :func:`posterior_variance` one CG per target on eq ``eta``
+                                 (P:571-575), then the direct sum of eq ``sws``
 
 Readings where the paper is silent, garbled or inconsistent:
   G1  exponent signs: v_j = sum_n exp(-2 pi i h j.x_n), (F^*y)_j = sum_n exp(-2 pi i h j.x_n) y_n,
@@ -44,7 +46,8 @@ __all__ = [
     "round_down_sig", "choose_params_se", "choose_params_matern", "choose_params",
     "mode_indices", "spectral_weights", "toeplitz_vector", "rhs_Fy", "rhs",
     "toeplitz_matrix", "toeplitz_apply", "system_apply", "cg", "default_max_iter",
-    "posterior_mean", "design_matrix", "kernel_tilde_matrix", "dense_gp_mean",
+    "posterior_mean", "posterior_variance", "design_matrix", "kernel_tilde_matrix", "dense_gp_mean",
+    "dense_gp_variance", "features",
     "OracleFit", "efgp_fit", "efgp_predict",
 ]
 
@@ -313,6 +316,46 @@ def posterior_mean(beta, D, h, xt, chunk: int = 1 << 14, return_imag: bool = Fal
     return (mu, imax) if return_imag else mu
 
 
+def features(D, h, xt) -> np.ndarray:
+    """phi_j(x*) = D_j exp(+2 pi i h j.x*) over J_m, shape (q,) + D.shape  (eq ``basis`` P:707)."""
+    xt = np.asarray(xt, dtype=np.float64)
+    d = D.ndim
+    m = (D.shape[0] - 1) // 2
+    j = np.arange(-m, m + 1, dtype=np.float64)
+    E = [np.exp(+1j * TWO_PI * h * np.outer(xt[:, l], j)) for l in range(d)]
+    if d == 1:
+        P = E[0]
+    elif d == 2:
+        P = E[0][:, :, None] * E[1][:, None, :]
+    else:
+        P = E[0][:, :, None, None] * E[1][:, None, :, None] * E[2][:, None, None, :]
+    return D[None] * P
+
+
+def posterior_variance(fit, xt, cg_tol: float | None = None, max_iter: int | None = None,
+                       return_iters: bool = False):
+    """s(x*) = sum_j eta_j phi_j(x*)  (eq ``sws``) where, per target,
+    (Phi^*Phi + sigma^2 I) eta = sigma^2 conj(phi(x*))  (eq ``eta``), solved by the same
+    plain CG and system_apply as the mean ("a new right-hand side ... per target").
+    The exact value is real; the real part is returned."""
+    xt = np.asarray(xt, dtype=np.float64)
+    if xt.ndim == 1:
+        xt = xt[:, None]
+    s2 = fit.sigma ** 2
+    tol = fit.eps if cg_tol is None else cg_tol
+    cap = default_max_iter(max(1, int(round(fit.v[(2 * fit.m,) * fit.d].real))), fit.sigma, tol) \
+        if max_iter is None else max_iter
+    T = toeplitz_matrix(fit.v, fit.m) if fit.M <= 4096 else None
+    Phi = features(fit.D, fit.h, xt)
+    out = np.empty(len(xt))
+    iters = []
+    for t in range(len(xt)):
+        eta, k, _ = cg(lambda p: system_apply(fit.v, fit.D, s2, p, T), s2 * np.conj(Phi[t]), tol, cap)
+        out[t] = np.sum(eta * Phi[t]).real
+        iters.append(k)
+    return (out, iters) if return_iters else out
+
+
 # ----------------------------------------------------------------------------------------------
 # Dense references used by the oracle's own pins (P:58-139, P:550-633, P:751-760)
 # ----------------------------------------------------------------------------------------------
@@ -337,6 +380,16 @@ def dense_gp_mean(x, y, xt, kfun, sigma):
     c = scipy.linalg.cho_factor(K + sigma ** 2 * np.eye(len(x)))
     alpha = scipy.linalg.cho_solve(c, y)
     return kfun(xt, x) @ alpha, alpha
+
+
+def dense_gp_variance(x, xt, kfun, sigma):
+    """Function-space GP variance s(x*) = k(x*,x*) - k(x*,X) (K + sigma^2 I)^{-1} k(X,x*)
+    (eq ``s``) by Cholesky."""
+    K = kfun(x, x)
+    c = scipy.linalg.cho_factor(K + sigma ** 2 * np.eye(len(x)))
+    Kt = kfun(xt, x)
+    kss = np.array([kfun(xt[i:i + 1], xt[i:i + 1])[0, 0] for i in range(len(xt))])
+    return kss - np.einsum("ij,ji->i", Kt, scipy.linalg.cho_solve(c, Kt.T))
 
 
 # ----------------------------------------------------------------------------------------------
