@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define EFGP_ABI_VERSION 2
+#define EFGP_ABI_VERSION 3
 
 typedef struct efgp_plan *efgp_handle;
 
@@ -94,6 +94,8 @@ typedef struct {
   double t_spread_ms, t_modes_ms, t_solve_ms, t_predict_ms; /* device time of the last calls */
   int64_t sorted_t1, sorted_t2, sorted_chunk, sorted_round;   /* SORTED geometry (0 otherwise)  */
   int64_t spread_precision;                                   /* efgp_weights of the SORTED path */
+  double t_var_ms;                                            /* device time of the last predict_var */
+  int64_t var_iters_max, var_batch;                           /* its largest CG count, targets/batch */
 } efgp_info;
 
 /* Fill *opt with defaults (all zero / automatic). */
@@ -126,6 +128,14 @@ efgp_status efgp_fit_solve(efgp_handle, const double *modes, int64_t N_total);
 /* Steps 5-6 of Alg a1: mu at q targets xt (q, d) written to mu_out (q).  EFGP_ERR_INVALID before a
  * successful fit/load or for targets outside [0,1]^d (their mu is set to NaN). q = 0 is a no-op. */
 efgp_status efgp_predict(efgp_handle, const double *xt, int64_t q, double *mu_out);
+
+/* NEXT-2: posterior variance s(x*) = sum_j eta_j phi_j(x*) (eq "sws"), one CG per target
+ * on (Phi^*Phi + sigma^2 I) eta = sigma^2 conj(phi(x*)) (eq "eta"), batched
+ * over targets with the Toeplitz operator of the last fit, each CG stopped at cg_tol (reading G6).
+ * xt: (q, d) row-major; var_out: q doubles (host or device).  Needs a previous successful efgp_fit
+ * or efgp_fit_solve (EFGP_ERR_INVALID otherwise); targets outside [0,1]^d give NaN and
+ * EFGP_ERR_INVALID.  q = 0 is a no-op. */
+efgp_status efgp_predict_var(efgp_handle, const double *xt, int64_t q, double *var_out);
 
 /* Model state (SPEC S:369 serialisation).  beta is the Hermitian-half weight vector: for j in J_m
  * with j_d >= 0, row-major over (j_1+m, ..., j_{d-1}+m, j_d), interleaved (re, im) doubles;

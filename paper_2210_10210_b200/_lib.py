@@ -30,7 +30,8 @@ class Info(C.Structure):
                 ("spread_method", C.c_int), ("t_spread_ms", C.c_double), ("t_modes_ms", C.c_double),
                 ("t_solve_ms", C.c_double), ("t_predict_ms", C.c_double), ("sorted_t1", C.c_int64),
                 ("sorted_t2", C.c_int64), ("sorted_chunk", C.c_int64), ("sorted_round", C.c_int64),
-                ("spread_precision", C.c_int64)]
+                ("spread_precision", C.c_int64), ("t_var_ms", C.c_double), ("var_iters_max", C.c_int64),
+                ("var_batch", C.c_int64)]
 
 
 # every symbol include/efgp.h declares, with (restype, argtypes)
@@ -44,6 +45,7 @@ SIGNATURES = {
     "efgp_fit_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "efgp_fit_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
     "efgp_predict": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "efgp_predict_var": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "efgp_weights_count": (C.c_int64, [C.c_void_p]),
     "efgp_get_weights": (C.c_int, [C.c_void_p, C.c_void_p]),
     "efgp_load_weights": (C.c_int, [C.c_void_p, C.c_void_p]),

@@ -226,6 +226,7 @@ efgp_status fit_solve_impl(efgp_plan *pl, const double *modes, int64_t N_total) 
   EFGP_CUDA(cudaEventRecord(pl->ev[3], s));
   EFGP_CUDA(cudaMemcpyAsync(pl->modes_sum, modes, sizeof(double) * 2 * (P.Kvh + P.Mh), cudaMemcpyDefault, s));
   EFGP_TRY(toeplitz_setup(pl, pl->modes_sum, s));
+  pl->op_valid = true;
   const efgp_status st = cg_solve(pl, N_total);
   EFGP_CUDA(cudaEventRecord(pl->ev[4], s));
   EFGP_CUDA(cudaEventSynchronize(pl->ev[4]));
@@ -356,6 +357,53 @@ efgp_status efgp_predict(efgp_handle pl, const double *xt, int64_t q, double *mu
   return EFGP_OK;
 }
 
+efgp_status efgp_predict_var(efgp_handle pl, const double *xt, int64_t q, double *var_out) {
+  if (!pl) return EFGP_ERR_INVALID;
+  if (!pl->fitted || !pl->op_valid) {
+    pl->err = "predict_var before a successful fit (the variance needs the fit's Toeplitz operator)";
+    return EFGP_ERR_INVALID;
+  }
+  if (q < 0 || (q > 0 && (!xt || !var_out))) {
+    pl->err = "predict_var: bad arguments";
+    return EFGP_ERR_INVALID;
+  }
+  if (q == 0) return EFGP_OK;
+  const int d = pl->P.d;
+  cudaStream_t s = pl->stream;
+  EFGP_TRY(enter(pl));
+  EFGP_CUDA(cudaEventRecord(pl->ev[5], s));
+  EFGP_CUDA(cudaMemsetAsync(pl->dflags + 1, 0, sizeof(int), s));
+  const bool dx = is_device_ptr(xt), dm = is_device_ptr(var_out);
+  if (dx && dm) {
+    EFGP_TRY(variance_targets(pl, xt, q, var_out, s));
+  } else {
+    const int64_t chunk = std::min<int64_t>(q, 1ll << 20);
+    double *dxt = nullptr, *dv = nullptr;
+    EFGP_CUDA(cudaMallocAsync((void **)&dxt, sizeof(double) * chunk * d, s));
+    EFGP_CUDA(cudaMallocAsync((void **)&dv, sizeof(double) * chunk, s));
+    for (int64_t s0 = 0; s0 < q; s0 += chunk) {
+      const int64_t n = std::min(chunk, q - s0);
+      EFGP_CUDA(cudaMemcpyAsync(dxt, xt + s0 * d, sizeof(double) * n * d, cudaMemcpyDefault, s));
+      EFGP_TRY(variance_targets(pl, dxt, n, dv, s));
+      EFGP_CUDA(cudaMemcpyAsync(var_out + s0, dv, sizeof(double) * n, cudaMemcpyDefault, s));
+    }
+    EFGP_CUDA(cudaFreeAsync(dxt, s));
+    EFGP_CUDA(cudaFreeAsync(dv, s));
+  }
+  EFGP_CUDA(cudaEventRecord(pl->ev[6], s));
+  EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned, pl->dflags, sizeof(int) * 4, cudaMemcpyDeviceToHost, s));
+  EFGP_CUDA(cudaStreamSynchronize(s));
+  pl->t_var = elapsed(pl->ev[5], pl->ev[6]);
+  EFGP_TRY(leave(pl));
+  int flags[4];
+  std::memcpy(flags, pl->h_pinned, sizeof(flags));
+  if (flags[1]) {
+    pl->err = "predict_var: a target is outside [0,1]^d or non-finite (its variance is NaN)";
+    return EFGP_ERR_INVALID;
+  }
+  return EFGP_OK;
+}
+
 int64_t efgp_weights_count(efgp_handle pl) { return pl ? 2 * pl->P.Mh : -1; }
 
 efgp_status efgp_get_weights(efgp_handle pl, double *beta_out) {
@@ -431,6 +479,11 @@ efgp_status efgp_get_info(efgp_handle pl, efgp_info *o) {
     o->sorted_round = P.round;
     o->spread_precision = P.spread_mode;
   }
+  {
+    o->t_var_ms = pl->t_var;
+    o->var_iters_max = pl->var_iters_max;
+    o->var_batch = pl->var_B;
+  }
   return EFGP_OK;
 }
 
@@ -457,6 +510,12 @@ void efgp_destroy(efgp_handle pl) {
   if (!pl) return;
   if (pl->stream) cudaStreamSynchronize(pl->stream);
   if (pl->cg_exec) cudaGraphExecDestroy(pl->cg_exec);
+  if (pl->var_exec) cudaGraphExecDestroy(pl->var_exec);
+  for (cufftHandle h : {pl->plan_var_c2r, pl->plan_var_r2c})
+    if (h) cufftDestroy(h);
+  for (void *b : {(void *)pl->var_x, (void *)pl->var_r, (void *)pl->var_p, (void *)pl->var_Ap, (void *)pl->var_X,
+                  (void *)pl->var_Z, (void *)pl->var_Y, pl->var_st})
+    if (b) cudaFree(b);
   for (cufftHandle h : {pl->plan_g1, pl->plan_g2, pl->plan_c2r_L, pl->plan_r2c_L, pl->plan_t2})
     if (h) cufftDestroy(h);
   void *bufs[] = {pl->poly_dev, pl->D_half, pl->psi1, pl->psi2, pl->g1, pl->g2, pl->G1h, pl->G2h, pl->modes, pl->modes_sum,

@@ -149,6 +149,19 @@ struct efgp_plan {
 
   cufftHandle plan_g1 = 0, plan_g2 = 0, plan_c2r_L = 0, plan_r2c_L = 0, plan_t2 = 0;
   cudaGraphExec_t cg_exec = nullptr;
+
+  // posterior variance (NEXT-2, variance.cu): batched CG buffers for var_B targets, created lazily
+  int var_B = 0;
+  double2 *var_x = nullptr, *var_r = nullptr, *var_p = nullptr, *var_Ap = nullptr;
+  double2 *var_X = nullptr, *var_Z = nullptr;
+  double *var_Y = nullptr;
+  void *var_st = nullptr;
+  cufftHandle plan_var_c2r = 0, plan_var_r2c = 0;
+  cudaGraphExec_t var_exec = nullptr;
+  int var_exec_max_iter = 0;
+  int var_iters_max = 0;
+  bool op_valid = false;  // the Toeplitz operator (vhat) of a fit is in place
+  double t_var = 0;
   int cg_exec_iters = 0;
 
   // state of the last fit
@@ -176,6 +189,8 @@ efgp_status type2_grid(efgp_plan *pl, cudaStream_t s);
 efgp_status cg_solve(efgp_plan *pl, int64_t N_total);
 // interp.cu
 efgp_status interp_targets(efgp_plan *pl, const double *xt, int64_t q, double *mu, cudaStream_t s);
+// variance.cu
+efgp_status variance_targets(efgp_plan *pl, const double *xt, int64_t q, double *out, cudaStream_t s);
 }  // namespace efgp
 
 #define EFGP_CUDA(call)                                                                  \

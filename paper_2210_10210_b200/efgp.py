@@ -193,6 +193,19 @@ class EFGP:
                         allow_noconverge=False)
         return out
 
+    def predict_var(self, xt, out=None):
+        """Posterior variance at targets xt (q, d) (NEXT-2, eqs eta/sws).  Device in -> device out."""
+        torch = self._torch
+        q = int(xt.shape[0])
+        if out is None:
+            dev = xt.device if isinstance(xt, torch.Tensor) else torch.device("cpu")
+            out = torch.empty(q, dtype=torch.float64, device=dev)
+        px, kx = _ptr_and_keep(xt)
+        with torch.cuda.device(self.device):
+            self._check(self._lib.efgp_predict_var(self._h, C.c_void_p(px), q, C.c_void_p(out.data_ptr())),
+                        allow_noconverge=False)
+        return out
+
     # ------------------------------------------------------------------ state
     def info(self) -> dict:
         inf = L.Info()

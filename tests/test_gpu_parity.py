@@ -406,3 +406,52 @@ def test_full_size_c5_type1_properties():
     g.close()
     del x, y
     torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------ NEXT-2: posterior variance (eqs eta, sws)
+VAR_SIZES = {"c1": (3000, None), "c2": (5000, 12), "c3": (3000, None), "c4": (1500, 5), "c5": (20_000, None)}
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_posterior_variance_parity(name, monkeypatch):
+    # GPU batched CG (small batches so the batch loop is exercised) against the oracle's per-target
+    # CG on the same fit parameters; both CGs to eps/1000 (parity mode, reading G9).  Gate 10 eps.
+    c = CONFIGS[name]
+    N, m_over = VAR_SIZES[name]
+    x, y, _ = generate(c, N=N, q=1)
+    xt = np.random.default_rng(20 + c.id).uniform(0, 1, (37, c.d))
+    xt[0] = x[0]                                                   # a data point (small variance)
+    cg_tol = c.eps / 1000
+    kw = {}
+    if m_over is not None:
+        h0, _ = O.choose_params(c.kernel, c.ell, c.d, c.eps, c.nu)
+        kw = dict(h=h0, m=m_over)
+    monkeypatch.setenv("EFGP_VAR_BATCH", "16")
+    g = model(c, cg_tol=cg_tol, **kw)
+    g.fit(dev(x), dev(y))
+    var = g.predict_var(dev(xt)).cpu().numpy()
+    inf = g.info()
+    assert inf["var_batch"] == 16 and inf["var_iters_max"] > 0
+    fit = O.efgp_fit(x, y, c.kernel, c.ell, c.sigma, c.eps, nu=c.nu, cg_tol=cg_tol, h=kw.get("h"), m=kw.get("m"))
+    ref = O.posterior_variance(fit, xt, cg_tol=cg_tol)
+    assert rel(var, ref) <= 10 * c.eps, (rel(var, ref), 10 * c.eps)
+    k0 = float(np.sum(fit.D ** 2))
+    assert np.all(var > 0) and np.all(var <= k0 * (1 + 1e-9))
+    g.close()
+
+
+def test_posterior_variance_edge_cases():
+    from paper_2210_10210_b200 import EFGPError
+    c = CONFIGS["c5"]
+    g = model(c)
+    with pytest.raises(EFGPError, match="INVALID"):
+        g.predict_var(dev(np.full((2, 2), 0.5)))                    # before a fit
+    x, y, xt = generate(c, N=2000, q=20)
+    g.fit(dev(x), dev(y))
+    assert g.predict_var(dev(np.zeros((0, 2)))).numel() == 0         # q = 0
+    v_dev = g.predict_var(dev(xt)).cpu().numpy()
+    v_host = g.predict_var(xt).numpy()                               # host arrays
+    np.testing.assert_allclose(v_host, v_dev, rtol=1e-12)
+    with pytest.raises(EFGPError, match="INVALID"):
+        g.predict_var(dev(np.array([[0.5, 1.5]])))
+    g.close()
