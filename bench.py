@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--q", type=float, default=None, help="override the number of targets")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-interp-n", action="store_true", help="skip the NEXT-1 measurement (mu at the N points)")
+    ap.add_argument("--variance", action="store_true",
+                    help="also time NEXT-2 (posterior variance; at N=1e9 its CG needs ~5e4 iterations: minutes)")
+    ap.add_argument("--var-targets", type=float, default=256, help="targets of the NEXT-2 measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-points", type=float, default=1e6, help="cpu_baseline sample size")
     ap.add_argument("--spread", default="auto")
@@ -260,6 +263,25 @@ def main():
         except Exception as exc:
             interp_n = {"error": f"{type(exc).__name__}: {exc}"[:200]}
 
+    # NEXT-2: posterior variance at a sample of the targets (eqs eta/sws, batched CG)
+    variance = None
+    if args.variance:
+        try:
+            qv = min(int(args.var_targets), xt.shape[0])
+            var = torch.empty(qv, dtype=torch.float64, device=dev)
+            model.predict_var(xt[:qv], out=var)  # warm-up (allocates the batched buffers, captures the graph)
+            tv = []
+            for _ in range(2):
+                model.predict_var(xt[:qv], out=var)
+                tv.append(model.info()["t_var_ms"])
+            iv = model.info()
+            variance = {"q": qv, "ms": statistics.median(tv), "targets_per_s": qv / (statistics.median(tv) / 1e3),
+                        "cg_iters_max": iv["var_iters_max"], "batch": iv["var_batch"],
+                        "note": "one CG per target on the fit's Toeplitz operator, batched cuFFT"}
+            del var
+        except Exception as exc:
+            variance = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
     # e2e: same metric through the public API with host (pinned) buffers, copies inside the step
     e2e = None
     if not args.no_e2e:
@@ -327,7 +349,8 @@ def main():
                             "achieved": achieved, "peak": peak, "peak_source": src, "unit": "GB/s",
                             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                             "alg_bytes_per_launch": alg_bytes},
-               "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "mu_at_training_points": interp_n}
+               "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "mu_at_training_points": interp_n,
+               "posterior_variance": variance}
         if not args.no_cpu_baseline:
             try:
                 ns = int(args.oracle_points)

@@ -1,1 +1,5 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -q --timeout 400 -p no:cacheprovider -k "variance" 2>&1 | tail -15
+timeout 1200 python tools/bench_configs.py --configs c1,c2,c3,c5 --c5-N 1e6 --var-targets 256 2>/dev/null | python -c "
+import sys,json
+for l in sys.stdin:
+    d=json.loads(l); print(d['config'], d['N'], 'mean cg', d['cg_iters'], 'var', d.get('variance'))
+"

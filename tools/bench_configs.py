@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--configs", default="c1,c2,c3,c4,c5")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--c5-N", type=float, default=None)
+    ap.add_argument("--var-targets", type=int, default=0, help="also time the posterior variance (NEXT-2)")
     a = ap.parse_args()
     import torch
     from efgp_data import CONFIGS
@@ -55,6 +56,14 @@ def main():
                "cg_us_per_iteration": 1e3 * med("t_solve_ms") / max(1.0, med("iters")),
                "spread_points_per_s": N / (sp / 1e3),
                "spread_hbm_frac": N * 8 * (c.d + 1) / (sp / 1e3) / 1e9 / peak}
+        if a.var_targets:
+            qv = min(a.var_targets, c.q)
+            var = torch.empty(qv, dtype=torch.float64, device=x.device)
+            g.predict_var(xt[:qv], out=var)
+            g.predict_var(xt[:qv], out=var)
+            iv = g.info()
+            out["variance"] = {"q": qv, "ms": iv["t_var_ms"], "targets_per_s": qv / (iv["t_var_ms"] / 1e3),
+                               "cg_iters_max": iv["var_iters_max"]}
         print(json.dumps(out), flush=True)
         g.close()
         del x, y, xt, mu
