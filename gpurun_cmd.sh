@@ -1,5 +1,2 @@
-timeout 1200 python tools/bench_configs.py --configs c1,c2,c3,c5 --c5-N 1e6 --var-targets 256 2>/dev/null | python -c "
-import sys,json
-for l in sys.stdin:
-    d=json.loads(l); print(d['config'], d['N'], 'mean cg', d['cg_iters'], 'var', d.get('variance'))
-"
+timeout 300 python tools/spread_sweep.py --N 2e8 --variants '[{}, {"EFGP_SORTED_DEBUG": 1}]' 2>&1
+timeout 300 python -m pytest tests/test_gpu_parity.py -q --timeout 120 -p no:cacheprovider -x -k "sorted or strategies or invalid" 2>&1 | tail -2

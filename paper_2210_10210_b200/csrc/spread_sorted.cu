@@ -238,6 +238,7 @@ struct FusedArgs {
   const double *x, *y;
   int64_t N, chunk;
   int nchunks, nbuf;
+  int debug;           // diagnostics (EFGP_SORTED_DEBUG): 1 = accumulators skip their work
   double h;
   int n1, s_lo, S, T1, T2, nt2, ntiles;
   int segcap;          // records per (tile, binner CTA) segment per chunk
@@ -253,8 +254,14 @@ struct FusedArgs {
   int *err;
 };
 
-constexpr int kWBatch = 256;                      // points per binner-warp batch
-constexpr int kWStages = 2;                       // TMA ring depth per binner warp
+#ifndef EFGP_WBATCH
+#define EFGP_WBATCH 256
+#endif
+#ifndef EFGP_WSTAGES
+#define EFGP_WSTAGES 2
+#endif
+constexpr int kWBatch = EFGP_WBATCH;              // points per binner-warp batch
+constexpr int kWStages = EFGP_WSTAGES;            // TMA ring depth per binner warp
 constexpr int kBinWarps = kBinThreads / 32;       // 4
 
 template <int W, int MODE>
@@ -364,27 +371,35 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     if ((nb & 1) && lane == 0) ys[nb - 1] = A.y[i0 + nb - 1];
     __syncwarp();
     int tk[kWBatch / 32], rk[kWBatch / 32];  // (tile << 8 | key), rank within the batch's tile
+    // (written as independent predicated steps so the 8 points of a lane overlap their latencies)
+    double2 pv[kWBatch / 32];
+    double yvv[kWBatch / 32];
 #pragma unroll
     for (int q = 0; q < kWBatch / 32; ++q) {
-      const int j = q * 32 + lane;
-      tk[q] = -1;
-      if (j >= nb) continue;
-      const double2 p = xs2[j];
-      const double yv = ys[j];
-      const bool ok = p.x >= 0.0 && p.x <= 1.0 && p.y >= 0.0 && p.y <= 1.0 && isfinite(yv);
-      if (!ok) {
-        atomicOr(A.err, 1);
-        continue;
-      }
+      const int j = min(q * 32 + lane, nb - 1);
+      pv[q] = xs2[j];
+      yvv[q] = ys[j];
+    }
+    bool bad = false;
+    int ci[kWBatch / 32];
+#pragma unroll
+    for (int q = 0; q < kWBatch / 32; ++q) {
+      const bool in = q * 32 + lane < nb;
+      const bool ok = pv[q].x >= 0.0 && pv[q].x <= 1.0 && pv[q].y >= 0.0 && pv[q].y <= 1.0 && isfinite(yvv[q]);
+      bad |= in && !ok;
+      const double2 p = ok ? pv[q] : make_double2(0.0, 0.0);
       const int r = rowt[start_cell<W>(grid_t(A.h, p.x, A.n1)) - A.s_lo];
       const int c = colt[start_cell<W>(grid_t(A.h, p.y, A.n1)) - A.s_lo];
-      const int t = (r >> 16) + (c >> 16);
-      tk[q] = t << 8 | ((r & 0xFFFF) + (c & 0xFFFF));
-      rk[q] = atomicAdd(&wcnt[t], 1);
+      tk[q] = (in && ok) ? (((r >> 16) + (c >> 16)) << 8 | ((r & 0xFFFF) + (c & 0xFFFF))) : -1;
+      ci[q] = (r >> 16) + (c >> 16);
     }
+#pragma unroll
+    for (int q = 0; q < kWBatch / 32; ++q) rk[q] = tk[q] >= 0 ? atomicAdd(&wcnt[ci[q]], 1) : 0;
+    if (bad) atomicOr(A.err, 1);
     __syncwarp();
     // warp scan of the per-tile counts -> slot offsets; reserve room in the CTA's segments
     int sum = 0;
+#pragma unroll 8
     for (int t = tb; t < te; ++t) sum += wcnt[t];
     int incl = sum;
 #pragma unroll
@@ -394,6 +409,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     }
     const int nv = __shfl_sync(0xffffffffu, incl, 31);
     int run = incl - sum;
+#pragma unroll 8
     for (int t = tb; t < te; ++t) {
       const int c = wcnt[t];
       wloc[t] = run;
@@ -407,6 +423,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       if (tk[q] >= 0) perm[wloc[tk[q] >> 8] + rk[q]] = (q * 32 + lane) | (tk[q] << 8);
     __syncwarp();
     bool ovf = false;
+#pragma unroll 4
     for (int slot = lane; slot < nv; slot += 32) {
       const int v = perm[slot];
       const int j = v & 0xFF, key = (v >> 8) & 0xFF, t = v >> 16;
@@ -525,7 +542,7 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
     named_sync(bar_id, kGrpThreads);
     const int all = tpre[ntiles];
     const int gb = (int)((int64_t)vb * all / VG), ge = (int)((int64_t)(vb + 1) * all / VG);
-    if (gb < ge) {
+    if (gb < ge && !(A.debug & 1)) {
       int t_first;
       {
         int lo = 0, hi = ntiles;
@@ -927,6 +944,7 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
   A.chunk = P.chunk;
   A.nchunks = (int)((N + P.chunk - 1) / P.chunk);
   A.nbuf = P.nbuf;
+  A.debug = std::getenv("EFGP_SORTED_DEBUG") ? std::atoi(std::getenv("EFGP_SORTED_DEBUG")) : 0;
   A.h = P.h;
   A.n1 = (int)P.n1;
   A.s_lo = P.s_lo;
