@@ -634,9 +634,20 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
         PH(1);
         // pass 1 (thread per record): rank within its start cell (key from the binner), kept in
         // the record's key slot
-        for (int j = tid; j < nr; j += kGrpThreads) {
-          int *kp = reinterpret_cast<int *>(&raw[j].w);
-          kp[1] = atomicAdd(&cnt[kp[0]], 1);
+        for (int j0 = tid; j0 < nr; j0 += 4 * kGrpThreads) {  // 4 records at a time (latency)
+          int key[4], rnk[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u * kGrpThreads;
+            key[u] = j < nr ? __double2loint(raw[j].w) : -1;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) rnk[u] = key[u] >= 0 ? atomicAdd(&cnt[key[u]], 1) : 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u * kGrpThreads;
+            if (j < nr) reinterpret_cast<int *>(&raw[j].w)[1] = rnk[u];
+          }
         }
         named_sync(bar_id, kGrpThreads);
         const int mycnt = cnt[tid];
@@ -656,6 +667,7 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
         PH(2);
         const int myoff = coff[tid];
         // pass 2 (thread per record): the record (FP64) or its fp32 weights at its sorted slot
+#pragma unroll 2
         for (int j = tid; j < nr; j += kGrpThreads) {
           const double4 rv = raw[j];
           unsigned char *st = stage + (size_t)(coff[__double2loint(rv.w)] + __double2hiint(rv.w)) * SB;
@@ -697,6 +709,7 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
         if (mycnt > 0) {
           const unsigned char *sp = stage + (size_t)myoff * SB;
           if constexpr (MODE == kModeF64) {
+#pragma unroll 2
             for (int q = 0; q < mycnt; ++q, sp += SB) {
               const double *d = reinterpret_cast<const double *>(sp);
               const double yv = d[2];
@@ -715,6 +728,7 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
             }
           } else if constexpr (MODE == kModeW32) {
             constexpr int WE = StageRec<W, MODE>::WE, NF = SB / 4;
+#pragma unroll 2
             for (int q = 0; q < mycnt; ++q, sp += SB) {
               float f[NF];
               load_floats<SB>(sp, f);
@@ -735,6 +749,7 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
           } else {
             // MIXED: fp32 pairs along b: (acc[a][2p], acc[a][2p+1]) += w1[a] * (w2[2p], w2[2p+1])
             constexpr int WP = (W + 1) / 2, WE = 2 * WP, NF = SB / 4;
+#pragma unroll 2
             for (int q = 0; q < mycnt; ++q, sp += SB) {
               float f[NF];
               load_floats<SB>(sp, f);
