@@ -455,3 +455,45 @@ def test_posterior_variance_edge_cases():
     with pytest.raises(EFGPError, match="INVALID"):
         g.predict_var(dev(np.array([[0.5, 1.5]])))
     g.close()
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_full_size_sampled(name):
+    # BASELINE full sizes (c2 1e6, c3 1e7, c4 1e7 points), production options, the launch
+    # configuration bench.py / tools/bench_configs.py time.  Checked one by one where the oracle can:
+    #  * sampled modes of v and Phi^*y against the oracle's direct sums over all N points;
+    #  * the CG answer: true relative residual of beta on the GPU's own (v, b) with the oracle's
+    #    Toeplitz product (c2, c3; c4's M = 4.2e5 is too large for the direct product);
+    #  * mu at sampled targets against the oracle's direct sum with the GPU's beta.
+    from efgp_data import gpu as G
+    c = CONFIGS[name]
+    x_d, y_d = G.generate_points(c, 0, c.N)
+    g = model(c)
+    g.fit(x_d, y_d)
+    inf = g.info()
+    m, h, tol = inf["m"], inf["h"], inf["nufft_tol"]
+    x, y = x_d.cpu().numpy(), y_d.cpu().numpy()
+    rng = np.random.default_rng(30 + c.id)
+    d = c.d
+    v = gpu_v_full(m, g)
+    picks = [tuple([2 * m] * d)] + [tuple(rng.integers(0, 4 * m + 1, d)) for _ in range(7)]
+    for jj in picks:
+        j = np.array(jj) - 2 * m
+        ref = np.exp(-2j * np.pi * h * (x @ j)).sum()
+        assert abs(v[jj] - ref) <= 5 * tol * np.linalg.norm(v), (jj, v[jj], ref)
+    D = O.spectral_weights(c.kernel, c.ell, d, h, m, c.nu)
+    b = gpu_rhs_full(g)
+    for _ in range(6):
+        jj = tuple(rng.integers(0, 2 * m + 1, d))
+        j = np.array(jj) - m
+        ref = D[jj] * (np.exp(-2j * np.pi * h * (x @ j)) * y).sum()
+        assert abs(b[jj] - ref) <= 5 * tol * np.linalg.norm(b), (jj, b[jj], ref)
+    beta = gpu_beta_full(g)
+    if name != "c4":
+        Ab = O.system_apply(v, D, c.sigma ** 2, beta)
+        assert np.linalg.norm(Ab - b) / np.linalg.norm(b) <= 3 * c.eps
+    _, _, xt = generate(c, N=1, q=200)
+    mu = g.predict(dev(xt)).cpu().numpy()
+    ref = O.posterior_mean(beta, D, h, xt)
+    assert rel(mu, ref) <= 5 * tol
+    g.close()
