@@ -80,10 +80,6 @@ efgp_status build(efgp_plan *pl) {
   EFGP_TRY(dalloc(pl, &pl->g2, gr));
   EFGP_TRY(dalloc(pl, &pl->G1h, G1h));
   EFGP_TRY(dalloc(pl, &pl->G2h, Grh));
-  if (P.spread_method == EFGP_SPREAD_SORTED) {
-    for (int k = 0; k < P.nbuf; ++k)
-      EFGP_TRY(dalloc(pl, &pl->rec[k], (int64_t)P.ntiles * P.tiles_grid * P.cap));
-  }
   EFGP_TRY(dalloc(pl, &pl->modes, 2 * (P.Kvh + P.Mh)));
   EFGP_TRY(dalloc(pl, &pl->modes_sum, 2 * (P.Kvh + P.Mh)));
   EFGP_TRY(dalloc(pl, &pl->Xbox, box));

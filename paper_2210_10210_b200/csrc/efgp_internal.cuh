@@ -142,6 +142,7 @@ struct efgp_plan {
   // SORTED spreading: per-chunk tile lists (nbuf buffers) of x pairs and y, and the per-call
   // list lengths + handshake counters of the fused kernel
   double4 *rec[3] = {nullptr, nullptr, nullptr};  // ntiles x grid x segcap records (x1, x2, y, key)
+  size_t rec_cap = 0;                              // records allocated per buffer
   int *sync_buf = nullptr;
   size_t sync_cap = 0;
   unsigned long long *trace = nullptr;  // EFGP_SORTED_TRACE: per-chunk, per-CTA role timestamps

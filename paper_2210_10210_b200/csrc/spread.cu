@@ -270,8 +270,11 @@ efgp_status spread_points(efgp_plan *pl, const double *x, const double *y, int64
   if (method == EFGP_SPREAD_SORTED) {
     // the binning bulk-copies x and y (16-byte alignment); unaligned inputs fall back to GLOBAL
     // (same grids, same kernel)
-    if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0)
-      return spread_sorted2(pl, x, y, N, s);
+    if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0) {
+      const efgp_status st = spread_sorted2(pl, x, y, N, s);
+      if (st != EFGP_ERR_RESOURCE) return st;
+      pl->err.clear();  // co-residency not available now: same grids, direct spreading below
+    }
     method = EFGP_SPREAD_GLOBAL;
   }
   switch (pl->P.d) {

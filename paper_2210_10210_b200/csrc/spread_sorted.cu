@@ -903,7 +903,7 @@ bool sorted_geometry(Params &p, int num_sms) {
     p.nt2 = (S + p.T2 - 1) / p.T2;
   }
   p.ntiles = p.nt1 * p.nt2;
-  p.chunk = int64_t(1) << 22;
+  p.chunk = int64_t(1) << 24;  // 16M points: fewer chunk hand-offs (measured best at 16-32M)
   if (const char *e = std::getenv("EFGP_SORTED_CHUNK"))
     p.chunk = std::max<int64_t>(kWBatch, std::atoll(e) / kWBatch * kWBatch);
   p.nbuf = 2;
@@ -912,8 +912,7 @@ bool sorted_geometry(Params &p, int num_sms) {
   if (const char *e = std::getenv("EFGP_SORTED_GRID")) p.tiles_grid = std::max(1, std::atoi(e));
   // capacity of a (tile, binner CTA) segment: 2x its uniform share + slack; overflow spills to
   // direct RED spreading (correct for any data)
-  const double share = (double)p.chunk * p.T1 * p.T2 / ((double)S * S) / p.tiles_grid;
-  p.cap = (int)std::min<double>((double)p.chunk, 2.0 * share + 256.0);
+  p.cap = 0;  // segment capacity: per call, from the call's effective chunk (sorted_segcap)
   // round size: the largest multiple of 128 whose shared memory fits 227 KB
   const size_t lim = 227 * 1024 - 256;
   int R = 0;
@@ -922,6 +921,13 @@ bool sorted_geometry(Params &p, int num_sms) {
   if (const char *e = std::getenv("EFGP_SORTED_R")) R = std::max(256, std::min(R, std::atoi(e) / 128 * 128));
   p.round = R;
   return R >= 256;  // otherwise the lists / tables do not leave room for a round: use another method
+}
+
+// capacity of a (tile, binner CTA) segment for chunks of `chunk` points: 2x the uniform share +
+// slack; a fuller segment spills its points to direct RED spreading (correct for any data)
+static int sorted_segcap(const Params &p, int64_t chunk) {
+  const double share = (double)chunk * p.T1 * p.T2 / ((double)p.s_count * p.s_count) / p.tiles_grid;
+  return (int)std::min<double>((double)chunk, 2.0 * share + 256.0);
 }
 
 template <int W, int MODE>
@@ -945,8 +951,15 @@ static efgp_status launch_fused(efgp_plan *pl, const FusedArgs &A, cudaStream_t 
   EsPoly poly = P.poly;
   EsPolyP polyf = P.polyp;
   void *args[] = {(void *)&a, (void *)&poly, (void *)&polyf};
-  // cooperative launch: all CTAs are co-resident (they wait on one another through global counters)
-  EFGP_CUDA(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kFusedThreads), args, sm, s));
+  // cooperative launch: all CTAs are co-resident (they wait on one another through global counters).
+  // If the device cannot host them all right now (e.g. SMs taken by other work), report it so the
+  // caller spreads this call with the GLOBAL method instead.
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kFusedThreads), args, sm, s);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {
+    cudaGetLastError();
+    return EFGP_ERR_RESOURCE;
+  }
+  EFGP_CUDA(e);
   return EFGP_OK;
 }
 
@@ -956,8 +969,21 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
   A.x = x;
   A.y = y;
   A.N = N;
-  A.chunk = P.chunk;
-  A.nchunks = (int)((N + P.chunk - 1) / P.chunk);
+  // effective chunk of this call (a small problem is one chunk) and its list buffers
+  const int64_t chunk = std::min<int64_t>(P.chunk, (N + kWBatch - 1) / kWBatch * kWBatch);
+  const int segcap = sorted_segcap(P, chunk);
+  const size_t rec_need = (size_t)P.ntiles * P.tiles_grid * segcap;
+  if (rec_need > pl->rec_cap) {
+    for (int k = 0; k < 3; ++k) {
+      if (pl->rec[k]) cudaFree(pl->rec[k]);
+      pl->rec[k] = nullptr;
+    }
+    pl->rec_cap = 0;
+    for (int k = 0; k < P.nbuf; ++k) EFGP_CUDA(cudaMalloc((void **)&pl->rec[k], rec_need * sizeof(double4)));
+    pl->rec_cap = rec_need;
+  }
+  A.chunk = chunk;
+  A.nchunks = (int)((N + chunk - 1) / chunk);
   A.nbuf = P.nbuf;
   A.debug = std::getenv("EFGP_SORTED_DEBUG") ? std::atoi(std::getenv("EFGP_SORTED_DEBUG")) : 0;
   A.h = P.h;
@@ -968,7 +994,7 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
   A.T2 = P.T2;
   A.nt2 = P.nt2;
   A.ntiles = P.ntiles;
-  A.segcap = P.cap;
+  A.segcap = segcap;
   A.R = P.round;
   for (int b = 0; b < 3; ++b) A.rec[b] = pl->rec[b];
   // per-chunk segment and tile lengths and the two handshake counters, zeroed for this call
