@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -q --timeout 400 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['phases_ms'], d['roofline']['frac'], d['e2e']['value'])"
+timeout 400 python tools/spread_sweep.py --N 4e8 --variants '[{}, {"weights": "mixed"}]' 2>&1 | sed 's/.*"weights": "\([a-z0-9]*\)".*"chunk": \([0-9]*\).*pts_per_s": \([0-9.e+]*\).*/\1 chunk=\2 pts\/s=\3/'
+timeout 300 python -m pytest tests/test_gpu_parity.py -q --timeout 120 -p no:cacheprovider -x -k "sorted or strategies or c5" 2>&1 | tail -1
