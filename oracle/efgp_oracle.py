@@ -18,6 +18,8 @@ fast transform replaced by the sum that defines it:
   step 5/6 mu(x*) ............. :func:`posterior_mean`    direct sum, eq ``muws``
   NEXT-2  s(x*) ............... :func:`posterior_variance` one CG per target on eq ``eta``
                                  (P:571-575), then the direct sum of eq ``sws``
+  NEXT-3  sigma_n ............. :func:`efgp_fit_hetero` CG on (Phi^* S^-1 Phi + I) beta = Phi^* S^-1 y,
+                                 S = diag(sigma_n^2) (reading G11), Phi applied densely
 
 Readings where the paper is silent, garbled or inconsistent:
   G1  exponent signs: v_j = sum_n exp(-2 pi i h j.x_n), (F^*y)_j = sum_n exp(-2 pi i h j.x_n) y_n,
@@ -26,6 +28,10 @@ Readings where the paper is silent, garbled or inconsistent (DESIGN.md "Readings
   G3  Matérn eps rescaling by the true ||k||_{L2(R^d)} (reading A); alternatives B (none), P (printed).
   G4  SE (h, m): Cor c:SEparams literally; h rounded down at the 12th significant digit.
   G6  CG: x0 = 0, unpreconditioned, recursive residual, Hermitian inner products.
+  G11 heteroskedastic noise (P:2759-2763 names it, gives no formula): the weight-space posterior mean
+      for y = Phi beta + e, beta ~ N(0, I), e ~ N(0, S), S = diag(sigma_n^2): beta solves
+      (Phi^* S^-1 Phi + I) beta = Phi^* S^-1 y, mu(x*) = phi(x*) beta.  With sigma_n = sigma it is
+      eq ``be`` divided by sigma^2 (same CG iterates); CG cap P:1766 with sigma = min sigma_n.
 
 Pins: tests/test_oracle_*.py check every function against closed forms, printed values, invariants
 and brute force.  Nothing here is "parity unpinned".
@@ -47,7 +53,7 @@ __all__ = [
     "mode_indices", "spectral_weights", "toeplitz_vector", "rhs_Fy", "rhs",
     "toeplitz_matrix", "toeplitz_apply", "system_apply", "cg", "default_max_iter",
     "posterior_mean", "posterior_variance", "design_matrix", "kernel_tilde_matrix", "dense_gp_mean",
-    "dense_gp_variance", "features",
+    "dense_gp_variance", "features", "hetero_system_apply", "efgp_fit_hetero", "dense_gp_mean_hetero",
     "OracleFit", "efgp_fit", "efgp_predict",
 ]
 
@@ -356,6 +362,46 @@ def posterior_variance(fit, xt, cg_tol: float | None = None, max_iter: int | Non
     return (out, iters) if return_iters else out
 
 
+def hetero_system_apply(x, noise_sd, D, h, m, p, chunk: int = 4096):
+    """(Phi^* S^-1 Phi + I) p with S = diag(noise_sd^2) (reading G11), Phi_{n,j} = D_j exp(+2 pi i h
+    j.x_n) (eq ``205``).  Applied as written: a type-2 sum u = Phi p at the points (P:557's sum at the
+    data points), u / sigma_n^2, then the type-1 sum Phi^* (P:855-862), the BBMM-style product of
+    P:2761-2763; Phi rows are formed chunk by chunk (dense, no fast transform)."""
+    x = np.asarray(x, dtype=np.float64)
+    pv = np.asarray(p).reshape(-1)
+    out = pv.astype(np.complex128).copy()
+    for s in range(0, len(x), chunk):
+        Phi = design_matrix(x[s:s + chunk], h, m, D)
+        u = Phi @ pv
+        out += Phi.conj().T @ (u / np.asarray(noise_sd[s:s + chunk], dtype=np.float64) ** 2)
+    return out.reshape(np.shape(p))
+
+
+def efgp_fit_hetero(x, y, noise_sd, kernel: str, ell: float, eps: float, nu: float = 0.0,
+                    h: float | None = None, m: int | None = None, cg_tol: float | None = None,
+                    max_iter: int | None = None, rescale: str = "A") -> OracleFit:
+    """NEXT-3 (reading G11): per-point noise sigma_n.  Step 1 as Alg a1; right-hand side
+    Phi^* S^-1 y = D F^*(y / sigma_n^2) (eq ``rhs`` with weights y_n / sigma_n^2); CG on
+    hetero_system_apply.  The returned fit's sigma is min sigma_n (used only for the CG cap) and v is
+    None (there is no Toeplitz vector: the structure is gone)."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.ndim == 1:
+        x = x[:, None]
+    N, d = x.shape
+    sd = np.asarray(noise_sd, dtype=np.float64)
+    if h is None or m is None:
+        h0, m0 = choose_params(kernel, ell, d, eps, nu, rescale)
+        h = h0 if h is None else h
+        m = m0 if m is None else m
+    D = spectral_weights(kernel, ell, d, h, m, nu)
+    b = rhs(x, np.asarray(y, dtype=np.float64) / sd ** 2, h, m, D)
+    tol = eps if cg_tol is None else cg_tol
+    smin = float(np.min(sd))
+    cap = default_max_iter(N, smin, tol) if max_iter is None else max_iter
+    beta, iters, hist = cg(lambda p: hetero_system_apply(x, sd, D, h, m, p), b, tol, cap)
+    return OracleFit(kernel, nu, ell, smin, eps, d, h, m, D, None, b, beta, iters, hist)
+
+
 # ----------------------------------------------------------------------------------------------
 # Dense references used by the oracle's own pins (P:58-139, P:550-633, P:751-760)
 # ----------------------------------------------------------------------------------------------
@@ -380,6 +426,14 @@ def dense_gp_mean(x, y, xt, kfun, sigma):
     c = scipy.linalg.cho_factor(K + sigma ** 2 * np.eye(len(x)))
     alpha = scipy.linalg.cho_solve(c, y)
     return kfun(xt, x) @ alpha, alpha
+
+
+def dense_gp_mean_hetero(x, y, xt, kfun, noise_sd):
+    """Function-space GP mean with per-point noise: mu(x*) = k(x*,X) (K + S)^{-1} y, S = diag(sigma_n^2)
+    (eq ``mu`` P:98-115 with sigma^2 I replaced by S), by Cholesky."""
+    K = kfun(x, x)
+    c = scipy.linalg.cho_factor(K + np.diag(np.asarray(noise_sd, dtype=np.float64) ** 2))
+    return kfun(xt, x) @ scipy.linalg.cho_solve(c, y)
 
 
 def dense_gp_variance(x, xt, kfun, sigma):
