@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define EFGP_ABI_VERSION 3
+#define EFGP_ABI_VERSION 4
 
 typedef struct efgp_plan *efgp_handle;
 
@@ -115,6 +115,18 @@ efgp_status efgp_setup(efgp_handle *out, efgp_kernel kernel, double nu, double e
  * coordinate is outside [0,1] or non-finite, or any y is non-finite; EFGP_ERR_NOCONVERGE if CG hits
  * max_iter (beta is still usable). */
 efgp_status efgp_fit(efgp_handle, const double *x, const double *y, int64_t N);
+
+/* NEXT-3: fit with heteroskedastic noise (per-point sigma_n, reading G11).
+ * Solves (Phi^* S^-1 Phi + I) beta = Phi^* S^-1 y, S = diag(noise_sd^2), by CG (reading G6) whose
+ * product is applied with one type-2 and one type-1 NUFFT over the N points per iteration (the
+ * Toeplitz structure is gone); mu(x*) = phi(x*) beta as in efgp_predict.  For
+ * noise_sd_n = sigma it gives efgp_fit's beta (the same system divided by sigma^2).  The sigma given
+ * at setup is not used; the CG cap default is P:1766 with sigma = min noise_sd.
+ * x: (N, d), y: (N), noise_sd: (N); all device or all host (host inputs are copied to the device
+ * for the whole solve: N (d + 2) doubles).  Returns EFGP_ERR_INVALID for N < 1, a non-positive or
+ * non-finite noise_sd, points outside [0,1]^d, non-finite y; EFGP_ERR_NOCONVERGE as efgp_fit.
+ * After it, efgp_predict works; efgp_predict_var is refused (no Toeplitz operator). */
+efgp_status efgp_fit_hetero(efgp_handle, const double *x, const double *y, const double *noise_sd, int64_t N);
 
 /* Multi-process split of efgp_fit.  efgp_fit_local spreads this rank's
  * shard and writes its partial modes (the Hermitian halves of v and F^*y, efgp_modes_count doubles)

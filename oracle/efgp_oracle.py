@@ -398,7 +398,12 @@ def efgp_fit_hetero(x, y, noise_sd, kernel: str, ell: float, eps: float, nu: flo
     tol = eps if cg_tol is None else cg_tol
     smin = float(np.min(sd))
     cap = default_max_iter(N, smin, tol) if max_iter is None else max_iter
-    beta, iters, hist = cg(lambda p: hetero_system_apply(x, sd, D, h, m, p), b, tol, cap)
+    if N * D.size <= 10_000_000:  # small enough to keep Phi: the same product, formed once
+        Phi = design_matrix(x, h, m, D)
+        apply = lambda p: (p.reshape(-1) + Phi.conj().T @ ((Phi @ p.reshape(-1)) / sd ** 2)).reshape(p.shape)
+    else:
+        apply = lambda p: hetero_system_apply(x, sd, D, h, m, p)
+    beta, iters, hist = cg(apply, b, tol, cap)
     return OracleFit(kernel, nu, ell, smin, eps, d, h, m, D, None, b, beta, iters, hist)
 
 

@@ -41,6 +41,7 @@ SIGNATURES = {
     "efgp_setup": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
                              C.c_int, C.POINTER(Options)]),
     "efgp_fit": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
+    "efgp_fit_hetero": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
     "efgp_modes_count": (C.c_int64, [C.c_void_p]),
     "efgp_fit_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "efgp_fit_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),

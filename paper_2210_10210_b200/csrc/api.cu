@@ -289,6 +289,37 @@ efgp_status efgp_fit(efgp_handle pl, const double *x, const double *y, int64_t N
   return fit_solve_impl(pl, pl->modes, N);
 }
 
+efgp_status efgp_fit_hetero(efgp_handle pl, const double *x, const double *y, const double *noise_sd, int64_t N) {
+  if (!pl) return EFGP_ERR_INVALID;
+  if (N < 1 || !x || !y || !noise_sd) {
+    pl->err = "fit_hetero: N must be >= 1 and pointers non-null";
+    return EFGP_ERR_INVALID;
+  }
+  const int d = pl->P.d;
+  cudaStream_t s = pl->stream;
+  const bool dx = is_device_ptr(x), dy = is_device_ptr(y), ds = is_device_ptr(noise_sd);
+  if (!(dx == dy && dy == ds)) {
+    pl->err = "fit_hetero: x, y and noise_sd must all be device or all be host memory";
+    return EFGP_ERR_INVALID;
+  }
+  EFGP_TRY(enter(pl));
+  if (dx) {
+    EFGP_TRY(fit_hetero_device(pl, x, y, noise_sd, N));
+  } else {
+    // every CG iteration reads the points again: stage them on the device for the whole solve
+    double *buf = nullptr;
+    EFGP_CUDA(cudaMallocAsync((void **)&buf, sizeof(double) * N * (d + 2), s));
+    EFGP_CUDA(cudaMemcpyAsync(buf, x, sizeof(double) * N * d, cudaMemcpyHostToDevice, s));
+    EFGP_CUDA(cudaMemcpyAsync(buf + N * d, y, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+    EFGP_CUDA(cudaMemcpyAsync(buf + N * (d + 1), noise_sd, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+    const efgp_status st = fit_hetero_device(pl, buf, buf + N * d, buf + N * (d + 1), N);
+    cudaFreeAsync(buf, s);
+    EFGP_CUDA(cudaStreamSynchronize(s));
+    if (st != EFGP_OK) return st;
+  }
+  return leave(pl);
+}
+
 int64_t efgp_modes_count(efgp_handle pl) { return pl ? 2 * (pl->P.Kvh + pl->P.Mh) : -1; }
 
 efgp_status efgp_fit_local(efgp_handle pl, const double *x, const double *y, int64_t N, double *modes_out) {
@@ -507,7 +538,7 @@ void efgp_destroy(efgp_handle pl) {
   if (pl->stream) cudaStreamSynchronize(pl->stream);
   if (pl->cg_exec) cudaGraphExecDestroy(pl->cg_exec);
   if (pl->var_exec) cudaGraphExecDestroy(pl->var_exec);
-  for (cufftHandle h : {pl->plan_var_c2r, pl->plan_var_r2c})
+  for (cufftHandle h : {pl->plan_var_c2r, pl->plan_var_r2c, pl->plan_het})
     if (h) cufftDestroy(h);
   for (void *b : {(void *)pl->var_x, (void *)pl->var_r, (void *)pl->var_p, (void *)pl->var_Ap, (void *)pl->var_X,
                   (void *)pl->var_Z, (void *)pl->var_Y, pl->var_st})
@@ -518,7 +549,7 @@ void efgp_destroy(efgp_handle pl) {
                   pl->Xbox, pl->Yr, pl->vhat, pl->Zbox, pl->b, pl->x, pl->r, pl->p, pl->Ap, pl->partials,
                   pl->scal, pl->hist, pl->dflags, pl->T2box, pl->t2grid, pl->stage[0], pl->stage[1],
                   pl->rec[0], pl->rec[1], pl->rec[2], pl->trace,
-                  pl->sync_buf};
+                  pl->sync_buf, pl->het_box, pl->het_grid};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (pl->h_pinned) cudaFreeHost(pl->h_pinned);

@@ -223,6 +223,17 @@ __global__ void k_cg_pad(const double2 *__restrict__ p, const double *__restrict
   pad_box<D>(p, Dh, m, L, X, box);
 }
 
+static efgp_status ensure_hist(efgp_plan *pl, int64_t max_iter) {
+  if (max_iter + 1 > pl->hist_cap) {
+    if (pl->hist) cudaFree(pl->hist);
+    pl->hist = nullptr;
+    pl->hist_cap = 0;
+    EFGP_CUDA(cudaMalloc(&pl->hist, sizeof(double) * (max_iter + 1)));
+    pl->hist_cap = max_iter + 1;
+  }
+  return EFGP_OK;
+}
+
 static unsigned nblocks(int64_t n, int sms) {
   int64_t b = (n + kCGThreads - 1) / kCGThreads;
   const int64_t cap = (int64_t)sms * 4;
@@ -269,13 +280,7 @@ static efgp_status cg_solve_d(efgp_plan *pl, int64_t N_total) {
     if (max_iter < 10) max_iter = 10;
   }
   pl->max_iter_used = max_iter;
-  if (max_iter + 1 > pl->hist_cap) {
-    if (pl->hist) cudaFree(pl->hist);
-    pl->hist = nullptr;
-    pl->hist_cap = 0;
-    EFGP_CUDA(cudaMalloc(&pl->hist, sizeof(double) * (max_iter + 1)));
-    pl->hist_cap = max_iter + 1;
-  }
+  EFGP_TRY(ensure_hist(pl, max_iter));
   CGState *st = reinterpret_cast<CGState *>(pl->scal);
   CGState init{};
   init.tol = P.cg_tol;
@@ -318,6 +323,65 @@ static efgp_status cg_solve_d(efgp_plan *pl, int64_t N_total) {
   pl->iters = host.iter;
   pl->rel_resid = host.bnorm > 0 ? std::sqrt(host.rr) / host.bnorm : 0.0;
   return host.done == 2 ? EFGP_ERR_NOCONVERGE : EFGP_OK;
+}
+
+// ---- CG with a caller-applied operator (NEXT-3: the product is a type-2 + type-1 NUFFT pair, not a
+// Toeplitz product).  Same recurrences and stopping rule (reading G6); host-driven, one small
+// device->host read of the state per iteration (each iteration is O(N) work).
+__global__ void k_dot_pAp(const double2 *__restrict__ p, const double2 *__restrict__ Ap, int64_t Mh, int m,
+                          double *__restrict__ part) {
+  __shared__ double sh[40];
+  double acc = 0.0;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 pp = p[q], a = Ap[q];
+    const double wq = (q % (m + 1)) ? 2.0 : 1.0;
+    acc += wq * (pp.x * a.x + pp.y * a.y);
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+template <int D>
+static efgp_status cg_solve_op_d(efgp_plan *pl, int64_t max_iter, CGOp op, void *ctx) {
+  const Params &P = pl->P;
+  cudaStream_t s = pl->stream;
+  const unsigned nb = nblocks(P.Mh, pl->num_sms);
+  pl->max_iter_used = max_iter;
+  EFGP_TRY(ensure_hist(pl, max_iter));
+  CGState *st = reinterpret_cast<CGState *>(pl->scal);
+  CGState init{};
+  init.tol = P.cg_tol;
+  init.max_iter = max_iter;
+  double *part_pAp = pl->partials, *part_rr = pl->partials + pl->cg_blocks;
+  EFGP_CUDA(cudaMemcpyAsync(st, &init, sizeof(CGState), cudaMemcpyHostToDevice, s));
+  k_cg_init<<<nb, kCGThreads, 0, s>>>(pl->b, pl->x, pl->r, pl->p, P.Mh, (int)P.m, pl->partials);
+  k_cg_init2<<<1, kCGThreads, 0, s>>>(st, pl->partials, (int)nb, pl->hist);
+  EFGP_CUDA(cudaGetLastError());
+  CGState host{};
+  for (;;) {
+    EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned, st, sizeof(CGState), cudaMemcpyDeviceToHost, s));
+    EFGP_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(&host, pl->h_pinned, sizeof(CGState));
+    if (host.done) break;
+    EFGP_TRY(op(pl, pl->p, pl->Ap, ctx));
+    k_dot_pAp<<<nb, kCGThreads, 0, s>>>(pl->p, pl->Ap, P.Mh, (int)P.m, part_pAp);
+    k_cg_xr<<<nb, kCGThreads, 0, s>>>(pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp, part_rr, (int)nb);
+    k_cg_p<D><<<nb, kCGThreads, 0, s>>>(pl->r, pl->p, pl->D_half, P.Mh, (int)P.m, P.L, nullptr, 0, st, part_rr,
+                                        (int)nb, pl->hist);
+    EFGP_CUDA(cudaGetLastError());
+  }
+  pl->iters = host.iter;
+  pl->rel_resid = host.bnorm > 0 ? std::sqrt(host.rr) / host.bnorm : 0.0;
+  return host.done == 2 ? EFGP_ERR_NOCONVERGE : EFGP_OK;
+}
+
+efgp_status cg_solve_op(efgp_plan *pl, int64_t max_iter, CGOp op, void *ctx) {
+  switch (pl->P.d) {
+    case 1: return cg_solve_op_d<1>(pl, max_iter, op, ctx);
+    case 2: return cg_solve_op_d<2>(pl, max_iter, op, ctx);
+    case 3: return cg_solve_op_d<3>(pl, max_iter, op, ctx);
+  }
+  return EFGP_ERR_INVALID;
 }
 
 efgp_status cg_solve(efgp_plan *pl, int64_t N_total) {

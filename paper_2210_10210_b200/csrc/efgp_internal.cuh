@@ -165,6 +165,12 @@ struct efgp_plan {
   double t_var = 0;
   int cg_exec_iters = 0;
 
+  // heteroskedastic fit (NEXT-3, hetero.cu): type-2 on the strength-y spreading grid n_rhs when it
+  // differs from n2 (so interpolation is the exact adjoint of spreading), created lazily
+  double2 *het_box = nullptr;
+  double *het_grid = nullptr;
+  cufftHandle plan_het = 0;
+
   // state of the last fit
   bool fitted = false;
   int64_t N_last = 0;
@@ -186,10 +192,20 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
 efgp_status type1_modes(efgp_plan *pl, double *modes_out, cudaStream_t s);
 efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s);
 efgp_status type2_grid(efgp_plan *pl, cudaStream_t s);
+efgp_status type2_grid_from(efgp_plan *pl, const double2 *beta, cudaStream_t s);
+efgp_status type2_grid_on(efgp_plan *pl, const double2 *beta, int64_t n, const double *psi, cufftHandle plan,
+                          double2 *boxbuf, double *grid, cudaStream_t s);
 // cg.cu
 efgp_status cg_solve(efgp_plan *pl, int64_t N_total);
+typedef efgp_status (*CGOp)(efgp_plan *pl, const double2 *p, double2 *Ap, void *ctx);  // Ap = A p
+efgp_status cg_solve_op(efgp_plan *pl, int64_t max_iter, CGOp op, void *ctx);
 // interp.cu
 efgp_status interp_targets(efgp_plan *pl, const double *xt, int64_t q, double *mu, cudaStream_t s);
+// out_n = mu(x_n) / sd_n^2 (sd == nullptr: mu(x_n)) from the real type-2 fine grid `grid` (n^d)
+efgp_status interp_weighted(efgp_plan *pl, const double *grid, int64_t n, const double *xt, int64_t q,
+                            const double *sd, double *out, cudaStream_t s);
+// hetero.cu (NEXT-3): fit with per-point noise; x, y, sd device-resident
+efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, const double *sd, int64_t N);
 // variance.cu
 efgp_status variance_targets(efgp_plan *pl, const double *xt, int64_t q, double *out, cudaStream_t s);
 }  // namespace efgp
@@ -269,6 +285,54 @@ __device__ __forceinline__ bool bin_to_mode(int64_t k, int64_t n, int64_t jmax, 
   if (k <= jmax) { j = k; return true; }
   if (k >= n - jmax) { j = k - n; return true; }
   return false;
+}
+
+// Hermitian-half mode vectors and half-spectrum FFT boxes.
+template <int D>
+__device__ __forceinline__ void decode_half(int64_t loc, int K, int (&j)[D]) {
+  j[D - 1] = (int)(loc % (K + 1));
+  loc /= (K + 1);
+#pragma unroll
+  for (int k = D - 2; k >= 0; --k) {
+    j[k] = (int)(loc % (2 * K + 1)) - K;
+    loc /= (2 * K + 1);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ int64_t encode_half(const int (&j)[D], int K) {
+  int64_t idx = 0;
+#pragma unroll
+  for (int k = 0; k < D - 1; ++k) idx = idx * (2 * K + 1) + (j[k] + K);
+  return idx * (K + 1) + j[D - 1];
+}
+
+// Box index of mode j in an n^(d-1) x (n/2+1) half-spectrum array.
+template <int D>
+__device__ __forceinline__ int64_t box_index(const int (&j)[D], int64_t n) {
+  int64_t idx = 0;
+#pragma unroll
+  for (int k = 0; k < D - 1; ++k) idx = idx * n + (j[k] < 0 ? j[k] + n : j[k]);
+  return idx * (n / 2 + 1) + j[D - 1];
+}
+
+// Inverse: which mode |j_i| <= K sits in box entry idx (false if none).
+template <int D>
+__device__ __forceinline__ bool box_to_mode(int64_t idx, int64_t n, int K, int (&j)[D]) {
+  const int64_t nh = n / 2 + 1;
+  const int64_t kd = idx % nh;
+  idx /= nh;
+  if (kd > K) return false;
+  j[D - 1] = (int)kd;
+#pragma unroll
+  for (int k = D - 2; k >= 0; --k) {
+    const int64_t kk = idx % n;
+    idx /= n;
+    int64_t jj;
+    if (!bin_to_mode(kk, n, K, jj)) return false;
+    j[k] = (int)jj;
+  }
+  return true;
 }
 
 }  // namespace efgp

@@ -30,7 +30,8 @@ __device__ __forceinline__ int wrapn(int i, int n) {
 template <int D, int W, bool SMEM>
 __global__ void __launch_bounds__(256) k_interp(const double *__restrict__ xt, int64_t q,
                                                 const double *__restrict__ grid, int n, double h, EsPoly P,
-                                                int lo, int A, double *__restrict__ mu, int *__restrict__ err) {
+                                                int lo, int A, const double *__restrict__ sd,
+                                                double *__restrict__ mu, int *__restrict__ err) {
   extern __shared__ double sgrid[];
   if constexpr (SMEM) {
     int64_t cells = A;
@@ -109,14 +110,19 @@ __global__ void __launch_bounds__(256) k_interp(const double *__restrict__ xt, i
         acc = fma(ra, wt[0][a], acc);
       }
     }
+    if (sd) {  // NEXT-3: w_n = (Phi p)_n / sigma_n^2 (reading G11)
+      const double sn = __ldg(sd + i);
+      acc /= sn * sn;
+    }
     mu[i] = acc;
   }
 }
 
 template <int D, int W>
-static efgp_status launch_interp(efgp_plan *pl, const double *xt, int64_t q, double *mu, cudaStream_t s) {
+static efgp_status launch_interp(efgp_plan *pl, const double *grid, int n, const double *xt, int64_t q,
+                                 const double *sd, double *mu, cudaStream_t s) {
   const Params &P = pl->P;
-  const Occ2 o = occupied2(P.h, (int)P.n2, W);
+  const Occ2 o = occupied2(P.h, n, W);
   size_t cells = o.A;
   for (int k = 1; k < D; ++k) cells *= o.A;
   const size_t sb = cells * sizeof(double);
@@ -127,25 +133,26 @@ static efgp_status launch_interp(efgp_plan *pl, const double *xt, int64_t q, dou
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     EFGP_CUDA(cudaFuncSetAttribute(k_interp<D, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-    k_interp<D, W, true><<<(unsigned)blocks, 256, sb, s>>>(xt, q, pl->t2grid, (int)P.n2, P.h, P.poly, o.lo, o.A,
-                                                           mu, pl->dflags);
+    k_interp<D, W, true><<<(unsigned)blocks, 256, sb, s>>>(xt, q, grid, n, P.h, P.poly, o.lo, o.A,
+                                                           sd, mu, pl->dflags);
   } else {
     const int64_t cap = (int64_t)pl->num_sms * 16;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    k_interp<D, W, false><<<(unsigned)blocks, 256, 0, s>>>(xt, q, pl->t2grid, (int)P.n2, P.h, P.poly, o.lo, o.A,
-                                                           mu, pl->dflags);
+    k_interp<D, W, false><<<(unsigned)blocks, 256, 0, s>>>(xt, q, grid, n, P.h, P.poly, o.lo, o.A,
+                                                           sd, mu, pl->dflags);
   }
   EFGP_CUDA(cudaGetLastError());
   return EFGP_OK;
 }
 
 template <int D>
-static efgp_status interp_d(efgp_plan *pl, const double *xt, int64_t q, double *mu, cudaStream_t s) {
+static efgp_status interp_d(efgp_plan *pl, const double *grid, int n, const double *xt, int64_t q,
+                            const double *sd, double *mu, cudaStream_t s) {
   switch (pl->P.w) {
 #define EFGP_CASE(WW) \
   case WW:            \
-    return launch_interp<D, WW>(pl, xt, q, mu, s);
+    return launch_interp<D, WW>(pl, grid, n, xt, q, sd, mu, s);
     EFGP_W_CASES2(EFGP_CASE)
 #undef EFGP_CASE
   }
@@ -153,11 +160,16 @@ static efgp_status interp_d(efgp_plan *pl, const double *xt, int64_t q, double *
 }
 
 efgp_status interp_targets(efgp_plan *pl, const double *xt, int64_t q, double *mu, cudaStream_t s) {
+  return interp_weighted(pl, pl->t2grid, pl->P.n2, xt, q, nullptr, mu, s);
+}
+
+efgp_status interp_weighted(efgp_plan *pl, const double *grid, int64_t n, const double *xt, int64_t q,
+                            const double *sd, double *out, cudaStream_t s) {
   if (q <= 0) return EFGP_OK;
   switch (pl->P.d) {
-    case 1: return interp_d<1>(pl, xt, q, mu, s);
-    case 2: return interp_d<2>(pl, xt, q, mu, s);
-    case 3: return interp_d<3>(pl, xt, q, mu, s);
+    case 1: return interp_d<1>(pl, grid, (int)n, xt, q, sd, out, s);
+    case 2: return interp_d<2>(pl, grid, (int)n, xt, q, sd, out, s);
+    case 3: return interp_d<3>(pl, grid, (int)n, xt, q, sd, out, s);
   }
   return EFGP_ERR_INVALID;
 }

@@ -9,53 +9,6 @@
 
 namespace efgp {
 
-template <int D>
-__device__ __forceinline__ void decode_half(int64_t loc, int K, int (&j)[D]) {
-  j[D - 1] = (int)(loc % (K + 1));
-  loc /= (K + 1);
-#pragma unroll
-  for (int k = D - 2; k >= 0; --k) {
-    j[k] = (int)(loc % (2 * K + 1)) - K;
-    loc /= (2 * K + 1);
-  }
-}
-
-template <int D>
-__device__ __forceinline__ int64_t encode_half(const int (&j)[D], int K) {
-  int64_t idx = 0;
-#pragma unroll
-  for (int k = 0; k < D - 1; ++k) idx = idx * (2 * K + 1) + (j[k] + K);
-  return idx * (K + 1) + j[D - 1];
-}
-
-// Box index of mode j in an n^(d-1) x (n/2+1) half-spectrum array.
-template <int D>
-__device__ __forceinline__ int64_t box_index(const int (&j)[D], int64_t n) {
-  int64_t idx = 0;
-#pragma unroll
-  for (int k = 0; k < D - 1; ++k) idx = idx * n + (j[k] < 0 ? j[k] + n : j[k]);
-  return idx * (n / 2 + 1) + j[D - 1];
-}
-
-// Inverse: which mode |j_i| <= K sits in box entry idx (false if none).
-template <int D>
-__device__ __forceinline__ bool box_to_mode(int64_t idx, int64_t n, int K, int (&j)[D]) {
-  const int64_t nh = n / 2 + 1;
-  const int64_t kd = idx % nh;
-  idx /= nh;
-  if (kd > K) return false;
-  j[D - 1] = (int)kd;
-#pragma unroll
-  for (int k = D - 2; k >= 0; --k) {
-    const int64_t kk = idx % n;
-    idx /= n;
-    int64_t jj;
-    if (!bin_to_mode(kk, n, K, jj)) return false;
-    j[k] = (int)jj;
-  }
-  return true;
-}
-
 // K2: v_j = Delta1^d G1^(j) / prod phi^1(j_k), j in J_2m;  (F^*y)_j = Delta2^d G2^(j) / prod phi^2(j_k),
 // j in J_m (type-1 deconvolution; G^ = R2C of the spread grid, e^{-i} sign).
 template <int D>
@@ -184,20 +137,33 @@ efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s) {
 }
 
 efgp_status type2_grid(efgp_plan *pl, cudaStream_t s) {
+  EFGP_TRY(type2_grid_from(pl, pl->x, s));
+  pl->t2_valid = true;
+  return EFGP_OK;
+}
+
+// The type-2 fine grid of an arbitrary Hermitian-half coefficient vector beta (weights layout):
+// t2grid = C2R(c'), c'_j = Delta2^d D_j beta_j / prod phi^2(j_k)  (K8).
+efgp_status type2_grid_from(efgp_plan *pl, const double2 *beta, cudaStream_t s) {
+  return type2_grid_on(pl, beta, pl->P.n2, pl->psi2, pl->plan_t2, pl->T2box, pl->t2grid, s);
+}
+
+// K8 on an n^d grid with deconvolution table psi (k = 0..m at least), C2R plan `plan` (n^d Z2D).
+efgp_status type2_grid_on(efgp_plan *pl, const double2 *beta, int64_t n, const double *psi, cufftHandle plan,
+                          double2 *boxbuf, double *grid, cudaStream_t s) {
   const Params &P = pl->P;
-  int64_t box = P.n2 / 2 + 1;
-  for (int k = 0; k < P.d - 1; ++k) box *= P.n2;
-  const double s2 = std::pow(2.0 * kPi / (double)P.n2, P.d);
+  int64_t box = n / 2 + 1;
+  for (int k = 0; k < P.d - 1; ++k) box *= n;
+  const double sc = std::pow(2.0 * kPi / (double)n, P.d);
   const unsigned g = grid_for(box, 256, pl->num_sms);
   switch (P.d) {
-    case 1: k_place_t2<1><<<g, 256, 0, s>>>(pl->x, pl->D_half, pl->psi2, (int)P.m, P.n2, s2, pl->T2box, box); break;
-    case 2: k_place_t2<2><<<g, 256, 0, s>>>(pl->x, pl->D_half, pl->psi2, (int)P.m, P.n2, s2, pl->T2box, box); break;
-    case 3: k_place_t2<3><<<g, 256, 0, s>>>(pl->x, pl->D_half, pl->psi2, (int)P.m, P.n2, s2, pl->T2box, box); break;
+    case 1: k_place_t2<1><<<g, 256, 0, s>>>(beta, pl->D_half, psi, (int)P.m, n, sc, boxbuf, box); break;
+    case 2: k_place_t2<2><<<g, 256, 0, s>>>(beta, pl->D_half, psi, (int)P.m, n, sc, boxbuf, box); break;
+    case 3: k_place_t2<3><<<g, 256, 0, s>>>(beta, pl->D_half, psi, (int)P.m, n, sc, boxbuf, box); break;
   }
   EFGP_CUDA(cudaGetLastError());
-  EFGP_CUFFT(cufftSetStream(pl->plan_t2, s));
-  EFGP_CUFFT(cufftExecZ2D(pl->plan_t2, pl->T2box, pl->t2grid));
-  pl->t2_valid = true;
+  EFGP_CUFFT(cufftSetStream(plan, s));
+  EFGP_CUFFT(cufftExecZ2D(plan, boxbuf, grid));
   return EFGP_OK;
 }
 

@@ -149,6 +149,17 @@ class EFGP:
             self._check(self._lib.efgp_fit(self._h, C.c_void_p(px), C.c_void_p(py), N))
         return self
 
+    def fit_hetero(self, x, y, noise_sd):
+        """NEXT-3: fit with per-point noise standard deviations noise_sd (N,) (reading G11): solves
+        (Phi^* S^-1 Phi + I) beta = Phi^* S^-1 y with one type-2 + one type-1 NUFFT per CG iteration."""
+        N = int(x.shape[0])
+        px, kx = _ptr_and_keep(x)
+        py, ky = _ptr_and_keep(y)
+        ps, ks = _ptr_and_keep(noise_sd)
+        with self._torch.cuda.device(self.device):
+            self._check(self._lib.efgp_fit_hetero(self._h, C.c_void_p(px), C.c_void_p(py), C.c_void_p(ps), N))
+        return self
+
     def modes_count(self) -> int:
         return int(self._lib.efgp_modes_count(self._h))
 

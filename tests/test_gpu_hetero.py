@@ -1,0 +1,128 @@
+"""NEXT-3 (heteroskedastic noise, reading G11) parity: the GPU NUFFT-pair CG against the
+oracle's dense-Phi CG on the same seeded inputs, plus the homoskedastic limit against the GPU
+Toeplitz path, edge cases, and a large-N property check."""
+import math
+
+import numpy as np
+import pytest
+
+from _util import O, CONFIGS, generate, rel, dev, model, gpu_beta_full
+
+pytestmark = pytest.mark.gpu
+
+# (N, m override or None)
+HET_SIZES = {"c1": (3000, None), "c2": (3000, 12), "c3": (3000, None), "c4": (1500, 5), "c5": (4000, None)}
+
+
+def noise_sd(c, N, seed):
+    # per-point noise: sigma * (0.5 + u), u ~ U[0,1) (DESIGN.md input recipe, NEXT-3)
+    return c.sigma * (0.5 + np.random.default_rng(seed).uniform(0, 1, N))
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_hetero_parity(name):
+    c = CONFIGS[name]
+    N, m_over = HET_SIZES[name]
+    x, y, xt = generate(c, N=N, q=min(c.q, 1000))
+    sd = noise_sd(c, N, 40 + c.id)
+    cg_tol = c.eps / 1000                                          # parity mode (reading G9)
+    kw = {}
+    if m_over is not None:
+        h0, _ = O.choose_params(c.kernel, c.ell, c.d, c.eps, c.nu)
+        kw = dict(h=h0, m=m_over)
+    g = model(c, cg_tol=cg_tol, **kw)
+    g.fit_hetero(dev(x), dev(y), dev(sd))
+    mu = g.predict(dev(xt)).cpu().numpy()
+    inf = g.info()
+    fit = O.efgp_fit_hetero(x, y, sd, c.kernel, c.ell, c.eps, nu=c.nu, h=kw.get("h"), m=kw.get("m"), cg_tol=cg_tol)
+    ref = O.efgp_predict(fit, xt)
+    assert rel(mu, ref) <= 10 * c.eps, (rel(mu, ref), 10 * c.eps)
+    hist = g.residual_history()
+    assert len(hist) == inf["iters"] + 1 and hist[-1] <= cg_tol
+    # reading G10: +-2, or inside the oracle's [2 tol, tol/2] window, or (long parity-mode runs) 10 %
+    lo = next((k for k, r in enumerate(fit.history) if r <= 2 * cg_tol), len(fit.history))
+    hi = next((k for k, r in enumerate(fit.history) if r <= cg_tol / 2), len(fit.history) + 10)
+    assert (abs(inf["iters"] - fit.iters) <= 2 or lo <= inf["iters"] <= hi
+            or abs(inf["iters"] - fit.iters) <= 0.1 * fit.iters), (inf["iters"], fit.iters, lo, hi)
+    k = min(8, fit.iters, inf["iters"])
+    np.testing.assert_allclose(hist[:k + 1], fit.history[:k + 1], rtol=1e-2)
+    # the right-hand side Phi^* S^-1 y to NUFFT accuracy
+    from paper_2210_10210_b200 import half_to_full
+    b = half_to_full(g.vector("rhs"), inf["m"], c.d)
+    assert rel(b, fit.b) <= 5 * inf["nufft_tol"]
+    g.close()
+
+
+@pytest.mark.parametrize("spread", ["sorted", "global"])
+def test_hetero_constant_noise_matches_toeplitz_fit(spread):
+    # sigma_n = sigma: the NUFFT-pair operator and the Toeplitz operator are the same matrix (scaled
+    # by 1/sigma^2), two independent GPU paths; beta agrees to the NUFFT tolerance
+    c = CONFIGS["c5"]
+    x, y, xt = generate(c, N=200_000, q=500)
+    g1 = model(c, cg_tol=c.eps / 1000, spread=spread)
+    g1.fit(dev(x), dev(y))
+    g2 = model(c, cg_tol=c.eps / 1000, spread=spread)
+    g2.fit_hetero(dev(x), dev(y), dev(np.full(len(x), c.sigma)))
+    i1, i2 = g1.info(), g2.info()
+    assert abs(i1["iters"] - i2["iters"]) <= 0.1 * i1["iters"] + 2
+    mu1 = g1.predict(dev(xt)).cpu().numpy()
+    mu2 = g2.predict(dev(xt)).cpu().numpy()
+    assert rel(mu2, mu1) <= 10 * c.eps
+    g1.close()
+    g2.close()
+
+
+def test_hetero_edge_cases():
+    from paper_2210_10210_b200 import EFGPError
+    c = CONFIGS["c5"]
+    x, y, xt = generate(c, N=3000, q=50)
+    sd = noise_sd(c, 3000, 7)
+    g = model(c)
+    for bad in (0.0, -1.0, float("nan"), float("inf")):
+        s2 = sd.copy()
+        s2[123] = bad
+        with pytest.raises(EFGPError, match="INVALID"):
+            g.fit_hetero(dev(x), dev(y), dev(s2))
+    xb = x.copy()
+    xb[5, 1] = 1.5
+    with pytest.raises(EFGPError, match="INVALID"):
+        g.fit_hetero(dev(xb), dev(y), dev(sd))
+    g.fit_hetero(dev(x), dev(y), dev(sd))
+    mu_d = g.predict(dev(xt)).cpu().numpy()
+    b_d = g.vector("rhs")
+    g.fit_hetero(x, y, sd)                                         # host arrays
+    # spreading atomics make runs agree to roundoff; CG amplifies it (as test_host_inputs_match_device_inputs)
+    assert rel(g.vector("rhs"), b_d) < 1e-13
+    assert rel(g.predict(dev(xt)).cpu().numpy(), mu_d) < 10 * c.eps
+    with pytest.raises(EFGPError, match="INVALID"):
+        g.predict_var(dev(xt))                                     # no Toeplitz operator
+    # a single point: closed form mu(x0) = k~(0) y / (k~(0) + sd^2), to the NUFFT tolerance
+    x0 = np.array([[0.3, 0.6]])
+    g.fit_hetero(dev(x0), dev(np.array([2.0])), dev(np.array([0.5])))
+    D = O.spectral_weights(c.kernel, c.ell, 2, g.info()["h"], g.info()["m"], c.nu)
+    k0 = float(np.sum(D ** 2))
+    mu0 = g.predict(dev(x0)).cpu().numpy()[0]
+    assert mu0 == pytest.approx(k0 * 2.0 / (k0 + 0.25), rel=5 * g.info()["nufft_tol"])
+    g.close()
+
+
+def test_hetero_large_n_two_noise_levels():
+    # property at size (N = 2e7, the device generator): with sigma_n = sigma on the first half and 1e6 on
+    # the second, the second half drops out and the fit equals the Toeplitz fit of the first half alone
+    import torch
+    from efgp_data import gpu as G
+    c = CONFIGS["c5"]
+    N = 20_000_000
+    x, y = G.generate_points(c, 0, N)
+    xt = torch.rand(1000, 2, dtype=torch.float64, device="cuda")
+    sd = torch.full((N,), c.sigma, dtype=torch.float64, device="cuda")
+    sd[N // 2:] = 1e6
+    g = model(c, cg_tol=c.eps / 1000)
+    g.fit_hetero(x, y, sd)
+    mu_h = g.predict(xt).cpu().numpy()
+    g2 = model(c, cg_tol=c.eps / 1000)
+    g2.fit(x[:N // 2].contiguous(), y[:N // 2].contiguous())
+    mu_ref = g2.predict(xt).cpu().numpy()
+    assert rel(mu_h, mu_ref) <= 10 * c.eps, rel(mu_h, mu_ref)
+    g.close()
+    g2.close()

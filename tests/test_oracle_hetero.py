@@ -72,3 +72,16 @@ def test_noisy_point_drops_out():
     keep = np.arange(200) != 17
     b = O.efgp_fit_hetero(x[keep], y[keep], sd[keep], "se", 0.1, 1e-8, cg_tol=1e-13)
     np.testing.assert_allclose(O.efgp_predict(a, xt), O.efgp_predict(b, xt), rtol=0, atol=1e-9)
+
+
+def test_dense_and_chunked_products_agree():
+    # the formed-once Phi path of efgp_fit_hetero and hetero_system_apply are the same product
+    rng = np.random.default_rng(15)
+    x = rng.uniform(0, 1, (500, 2))
+    sd = rng.uniform(0.1, 1.0, 500)
+    D = O.spectral_weights("se", 0.2, 2, 0.5, 6)
+    p = rng.standard_normal(D.shape) + 1j * rng.standard_normal(D.shape)
+    Phi = O.design_matrix(x, 0.5, 6, D)
+    dense = p.reshape(-1) + Phi.conj().T @ np.diag(1 / sd ** 2) @ Phi @ p.reshape(-1)
+    np.testing.assert_allclose(O.hetero_system_apply(x, sd, D, 0.5, 6, p, chunk=77).reshape(-1), dense,
+                               rtol=1e-12, atol=1e-12 * np.max(np.abs(dense)))
