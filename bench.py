@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--variance", action="store_true",
                     help="also time NEXT-2 (posterior variance; at N=1e9 its CG needs ~5e4 iterations: minutes)")
     ap.add_argument("--var-targets", type=float, default=256, help="targets of the NEXT-2 measurement")
+    ap.add_argument("--hetero", action="store_true",
+                    help="also time NEXT-3 (heteroskedastic fit: a type-2 + type-1 NUFFT pair per CG iteration)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-points", type=float, default=1e6, help="cpu_baseline sample size")
     ap.add_argument("--spread", default="auto")
@@ -282,6 +284,35 @@ def main():
         except Exception as exc:
             variance = {"error": f"{type(exc).__name__}: {exc}"[:200]}
 
+    # NEXT-3: heteroskedastic fit, sigma_n = sigma (0.5 + u), u ~ U[0,1) (seeded); every
+    # CG iteration is K8 + C2R + K9 (q = N, fused / sigma_n^2) + K1 (N points) + R2C + deconvolution
+    hetero = None
+    if args.hetero:
+        try:
+            gen = torch.Generator(device=dev)
+            gen.manual_seed(1234 + rank)
+            sd = cfg.sigma * (0.5 + torch.rand(b - a, dtype=torch.float64, device=dev, generator=gen))
+            torch.cuda.synchronize()
+            model.fit_hetero(x, y, sd)  # warm-up: grows the handle's memory pool, builds the r2c plan
+            torch.cuda.synchronize()
+            th0 = time.perf_counter()
+            model.fit_hetero(x, y, sd)
+            torch.cuda.synchronize()
+            wall = (time.perf_counter() - th0) * 1e3
+            ih = model.info()
+            per_it = ih["t_solve_ms"] / max(ih["iters"], 1)
+            hetero = {"N": b - a, "iters": ih["iters"], "sorted_path": bool(ih["hetero_sorted"]),
+                      "fit_ms": ih["t_spread_ms"] + ih["t_modes_ms"] + ih["t_solve_ms"], "wall_ms": wall,
+                      "rhs_ms": ih["t_spread_ms"], "sort_ms": ih["t_modes_ms"], "solve_ms": ih["t_solve_ms"],
+                      "ms_per_iteration": per_it, "points_per_s_per_iteration": (b - a) / (per_it / 1e3),
+                      "points_per_s": (b - a) / (wall / 1e3),
+                      "note": "per CG iteration one fused pass over the cell-sorted points: type-2 at each "
+                              "point, / sigma_n^2, type-1 of the result (k_het_apply_sorted), plus two small FFTs"}
+            model.fit(x, y)  # restore the homoskedastic fit for anything after this
+            del sd
+        except Exception as exc:
+            hetero = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
     # e2e: same metric through the public API with host (pinned) buffers, copies inside the step
     e2e = None
     if not args.no_e2e:
@@ -350,7 +381,7 @@ def main():
                             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                             "alg_bytes_per_launch": alg_bytes},
                "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "mu_at_training_points": interp_n,
-               "posterior_variance": variance}
+               "posterior_variance": variance, "hetero_fit": hetero}
         if not args.no_cpu_baseline:
             try:
                 ns = int(args.oracle_points)

@@ -96,6 +96,7 @@ typedef struct {
   int64_t spread_precision;                                   /* efgp_weights of the SORTED path */
   double t_var_ms;                                            /* device time of the last predict_var */
   int64_t var_iters_max, var_batch;                           /* its largest CG count, targets/batch */
+  int64_t hetero_sorted; /* last efgp_fit_hetero: 1 = points sorted once by cell, fused NUFFT-pair pass */
 } efgp_info;
 
 /* Fill *opt with defaults (all zero / automatic). */

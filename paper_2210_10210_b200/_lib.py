@@ -31,7 +31,7 @@ class Info(C.Structure):
                 ("t_solve_ms", C.c_double), ("t_predict_ms", C.c_double), ("sorted_t1", C.c_int64),
                 ("sorted_t2", C.c_int64), ("sorted_chunk", C.c_int64), ("sorted_round", C.c_int64),
                 ("spread_precision", C.c_int64), ("t_var_ms", C.c_double), ("var_iters_max", C.c_int64),
-                ("var_batch", C.c_int64)]
+                ("var_batch", C.c_int64), ("hetero_sorted", C.c_int64)]
 
 
 # every symbol include/efgp.h declares, with (restype, argtypes)

@@ -280,6 +280,15 @@ efgp_status efgp_setup(efgp_handle *out, efgp_kernel kernel, double nu, double e
   EFGP_CUDA(cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking));
   EFGP_CUDA(cudaEventCreateWithFlags(&pl->ev_in, cudaEventDisableTiming));
   EFGP_CUDA(cudaEventCreateWithFlags(&pl->ev_out, cudaEventDisableTiming));
+  {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = pl->device;
+    EFGP_CUDA(cudaMemPoolCreate(&pl->pool, &props));
+    uint64_t keep = UINT64_MAX;
+    EFGP_CUDA(cudaMemPoolSetAttribute(pl->pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   return build(pl);
 }
 
@@ -308,7 +317,7 @@ efgp_status efgp_fit_hetero(efgp_handle pl, const double *x, const double *y, co
   } else {
     // every CG iteration reads the points again: stage them on the device for the whole solve
     double *buf = nullptr;
-    EFGP_CUDA(cudaMallocAsync((void **)&buf, sizeof(double) * N * (d + 2), s));
+    EFGP_PALLOC(&buf, sizeof(double) * N * (d + 2), s);
     EFGP_CUDA(cudaMemcpyAsync(buf, x, sizeof(double) * N * d, cudaMemcpyHostToDevice, s));
     EFGP_CUDA(cudaMemcpyAsync(buf + N * d, y, sizeof(double) * N, cudaMemcpyHostToDevice, s));
     EFGP_CUDA(cudaMemcpyAsync(buf + N * (d + 1), noise_sd, sizeof(double) * N, cudaMemcpyHostToDevice, s));
@@ -359,8 +368,8 @@ efgp_status efgp_predict(efgp_handle pl, const double *xt, int64_t q, double *mu
   } else {
     const int64_t chunk = std::min<int64_t>(q, 1ll << 24);
     double *dxt = nullptr, *dmu = nullptr;
-    EFGP_CUDA(cudaMallocAsync((void **)&dxt, sizeof(double) * chunk * d, s));
-    EFGP_CUDA(cudaMallocAsync((void **)&dmu, sizeof(double) * chunk, s));
+    EFGP_PALLOC(&dxt, sizeof(double) * chunk * d, s);
+    EFGP_PALLOC(&dmu, sizeof(double) * chunk, s);
     for (int64_t s0 = 0; s0 < q; s0 += chunk) {
       const int64_t n = std::min(chunk, q - s0);
       EFGP_CUDA(cudaMemcpyAsync(dxt, xt + s0 * d, sizeof(double) * n * d, cudaMemcpyDefault, s));
@@ -406,8 +415,8 @@ efgp_status efgp_predict_var(efgp_handle pl, const double *xt, int64_t q, double
   } else {
     const int64_t chunk = std::min<int64_t>(q, 1ll << 20);
     double *dxt = nullptr, *dv = nullptr;
-    EFGP_CUDA(cudaMallocAsync((void **)&dxt, sizeof(double) * chunk * d, s));
-    EFGP_CUDA(cudaMallocAsync((void **)&dv, sizeof(double) * chunk, s));
+    EFGP_PALLOC(&dxt, sizeof(double) * chunk * d, s);
+    EFGP_PALLOC(&dv, sizeof(double) * chunk, s);
     for (int64_t s0 = 0; s0 < q; s0 += chunk) {
       const int64_t n = std::min(chunk, q - s0);
       EFGP_CUDA(cudaMemcpyAsync(dxt, xt + s0 * d, sizeof(double) * n * d, cudaMemcpyDefault, s));
@@ -511,6 +520,7 @@ efgp_status efgp_get_info(efgp_handle pl, efgp_info *o) {
     o->var_iters_max = pl->var_iters_max;
     o->var_batch = pl->var_B;
   }
+  o->hetero_sorted = pl->het_path;
   return EFGP_OK;
 }
 
@@ -538,7 +548,7 @@ void efgp_destroy(efgp_handle pl) {
   if (pl->stream) cudaStreamSynchronize(pl->stream);
   if (pl->cg_exec) cudaGraphExecDestroy(pl->cg_exec);
   if (pl->var_exec) cudaGraphExecDestroy(pl->var_exec);
-  for (cufftHandle h : {pl->plan_var_c2r, pl->plan_var_r2c, pl->plan_het})
+  for (cufftHandle h : {pl->plan_var_c2r, pl->plan_var_r2c, pl->plan_het, pl->plan_het_r2c})
     if (h) cufftDestroy(h);
   for (void *b : {(void *)pl->var_x, (void *)pl->var_r, (void *)pl->var_p, (void *)pl->var_Ap, (void *)pl->var_X,
                   (void *)pl->var_Z, (void *)pl->var_Y, pl->var_st})
@@ -559,6 +569,7 @@ void efgp_destroy(efgp_handle pl) {
   if (pl->ev_in) cudaEventDestroy(pl->ev_in);
   if (pl->ev_out) cudaEventDestroy(pl->ev_out);
   if (pl->stream) cudaStreamDestroy(pl->stream);
+  if (pl->pool) cudaMemPoolDestroy(pl->pool);
   delete pl;
 }
 

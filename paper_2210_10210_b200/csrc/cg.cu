@@ -225,6 +225,10 @@ __global__ void k_cg_pad(const double2 *__restrict__ p, const double *__restrict
 
 static efgp_status ensure_hist(efgp_plan *pl, int64_t max_iter) {
   if (max_iter + 1 > pl->hist_cap) {
+    if (pl->cg_exec) {  // the captured CG graph holds the old history pointer
+      cudaGraphExecDestroy(pl->cg_exec);
+      pl->cg_exec = nullptr;
+    }
     if (pl->hist) cudaFree(pl->hist);
     pl->hist = nullptr;
     pl->hist_cap = 0;

@@ -170,6 +170,11 @@ struct efgp_plan {
   double2 *het_box = nullptr;
   double *het_grid = nullptr;
   cufftHandle plan_het = 0;
+  int het_path = 0;  // 1: last heteroskedastic fit used the sorted fused product
+  cufftHandle plan_het_r2c = 0;  // D2Z on n2 (sorted path), created lazily
+  // stream-ordered temporaries (hetero staging and sort, host-input chunks) come from this pool; it
+  // keeps freed memory for the next call (release threshold = max) and is destroyed with the handle
+  cudaMemPool_t pool = nullptr;
 
   // state of the last fit
   bool fitted = false;
@@ -229,6 +234,10 @@ efgp_status variance_targets(efgp_plan *pl, const double *xt, int64_t q, double 
       return r_ == CUFFT_ALLOC_FAILED ? EFGP_ERR_RESOURCE : EFGP_ERR_CUDA;               \
     }                                                                                    \
   } while (0)
+
+// stream-ordered allocation from the handle's pool
+#define EFGP_PALLOC(ptr, bytes, stream) \
+  EFGP_CUDA(cudaMallocFromPoolAsync((void **)(ptr), (bytes), pl->pool, (stream)))
 
 #define EFGP_TRY(call)                 \
   do {                                 \

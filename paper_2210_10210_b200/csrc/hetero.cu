@@ -11,8 +11,11 @@
 // data points and divides by sigma_n^2 (fused), K1 spreads those values (the same spreader as the
 // fit; its strength-y grid is the one used), cuFFT R2C + k_het_modes deconvolve, multiply by D and
 // add p.  The right-hand side is the same K1 -> R2C -> k_het_modes chain on y_n / sigma_n^2.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "efgp_internal.cuh"
 
@@ -67,6 +70,239 @@ __global__ void k_het_modes(const double2 *__restrict__ G, int64_t n, int m, con
   }
 }
 
+
+// ---- sorted NUFFT-pair product (d <= 2): the points never move between CG iterations, so they are
+// counting-sorted ONCE by their start cell on the type-2 grid n2 (structure of arrays: coordinates
+// and 1/sigma_n^2).  Each iteration is then one streaming pass: a warp takes a run of one cell's
+// points (lanes stride 32, coalesced), holds that cell's W^d grid window in registers, and per point
+// evaluates the kernel weights once and uses them twice: u = sum g w (type-2 at the point),
+// v = u / sigma_n^2, window += v w (type-1 of v).  The lanes' windows are reduced with shuffles and
+// added to the output grid with W^d atomics per run.  Both transforms use the same grid, kernel and
+// deconvolution, so the product is exactly Hermitian.
+#ifndef EFGP_HET_RUN
+#define EFGP_HET_RUN 2048
+#endif
+constexpr int kHetRun = EFGP_HET_RUN;  // points per warp work item (64 per lane)
+
+struct HetItem {
+  long long begin, end;
+  int cell, pad_;
+};
+
+template <int D, int W>
+__device__ __forceinline__ int het_cell_key(const double *__restrict__ x, int64_t i, double h, int n, int lo, int S) {
+  int key = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const double t = __dmul_rn(__dmul_rn(h, __ldg(x + i * D + k)), (double)n);  // = K9's h x n
+    int c = (int)ceil(__dsub_rn(t, 0.5 * W)) - lo;                             // es_weights' i0
+    c = c < 0 ? 0 : (c >= S ? S - 1 : c);  // never taken: S covers x in [0,1] (validated before)
+    key = key * S + c;
+  }
+  return key;
+}
+
+__device__ __forceinline__ void het_range(int64_t N, int64_t &a, int64_t &e) {
+  const int64_t per = (N + gridDim.x - 1) / gridDim.x;
+  a = (int64_t)blockIdx.x * per;
+  e = a + per < N ? a + per : N;
+}
+
+template <int D, int W>
+__global__ void k_het_count(const double *__restrict__ x, int64_t N, double h, int n, int lo, int S, int ncell,
+                            unsigned *__restrict__ hist) {
+  extern __shared__ unsigned hs[];
+  for (int i = threadIdx.x; i < ncell; i += blockDim.x) hs[i] = 0;
+  __syncthreads();
+  int64_t a, e;
+  het_range(N, a, e);
+  for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&hs[het_cell_key<D, W>(x, i, h, n, lo, S)], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < ncell; i += blockDim.x) hist[(size_t)blockIdx.x * ncell + i] = hs[i];
+}
+
+// per cell: exclusive scan over the CTAs (in place) and the cell total
+__global__ void k_het_colscan(unsigned *__restrict__ hist, int nblk, int ncell, long long *__restrict__ tot) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncell) return;
+  long long run = 0;
+  for (int b = 0; b < nblk; ++b) {
+    const unsigned v = hist[(size_t)b * ncell + c];
+    hist[(size_t)b * ncell + c] = (unsigned)run;  // < 2^32 points per cell
+    run += v;
+  }
+  tot[c] = run;
+}
+
+// off[c] = sum_{c' < c} tot[c'], off[ncell] = N (one CTA, sequential chunks of blockDim)
+__global__ void k_het_offsets(const long long *__restrict__ tot, int ncell, long long *__restrict__ off) {
+  __shared__ long long sh[1024];
+  __shared__ long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < ncell; c0 += blockDim.x) {
+    const int c = c0 + threadIdx.x;
+    sh[threadIdx.x] = c < ncell ? tot[c] : 0;
+    __syncthreads();
+    for (int o = 1; o < (int)blockDim.x; o <<= 1) {  // Hillis-Steele inclusive scan
+      const long long v = threadIdx.x >= (unsigned)o ? sh[threadIdx.x - o] : 0;
+      __syncthreads();
+      sh[threadIdx.x] += v;
+      __syncthreads();
+    }
+    if (c < ncell) off[c] = carry + sh[threadIdx.x] - (c < ncell ? tot[c] : 0);
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry += sh[threadIdx.x];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) off[ncell] = carry;
+}
+
+template <int D, int W>
+__global__ void k_het_scatter(const double *__restrict__ x, const double *__restrict__ sd, int64_t N, double h, int n,
+                              int lo, int S, int ncell, const unsigned *__restrict__ hist,
+                              const long long *__restrict__ off, double *__restrict__ xs, double *__restrict__ is2) {
+  extern __shared__ unsigned long long cur[];
+  for (int i = threadIdx.x; i < ncell; i += blockDim.x)
+    cur[i] = (unsigned long long)(off[i] + hist[(size_t)blockIdx.x * ncell + i]);
+  __syncthreads();
+  int64_t a, e;
+  het_range(N, a, e);
+  for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x) {
+    const int key = het_cell_key<D, W>(x, i, h, n, lo, S);
+    const long long pos = (long long)atomicAdd(&cur[key], 1ull);
+#pragma unroll
+    for (int k = 0; k < D; ++k) xs[(int64_t)k * N + pos] = __ldg(x + i * D + k);
+    const double sn = __ldg(sd + i);
+    is2[pos] = 1.0 / (sn * sn);
+  }
+}
+
+__device__ __forceinline__ int het_wrap(int i, int n) {
+  i %= n;
+  return i < 0 ? i + n : i;
+}
+
+#ifndef EFGP_HET_GSM
+#define EFGP_HET_GSM 1  // the warp's grid window in shared memory (broadcast reads) instead of registers
+#endif
+#ifndef EFGP_HET_UNROLL
+#define EFGP_HET_UNROLL 1  // points per lane in flight (2: more ILP, more registers; slower on B200)
+#endif
+#ifndef EFGP_HET_THREADS
+#define EFGP_HET_THREADS 128
+#endif
+// resident CTAs per SM the kernel is compiled for: 4 x 128 threads (<= 128 registers) for the 2D
+// W <= 5 windows (+21 % over the unconstrained 154 registers on c5), else no constraint
+template <int D, int W>
+constexpr int het_min_blocks() { return (D == 2 && W <= 5) ? 4 : 1; }
+constexpr int kHetThreads = EFGP_HET_THREADS;
+
+template <int D, int W>
+__device__ __forceinline__ void het_point(const double *__restrict__ xs, const double *__restrict__ is2, int64_t N,
+                                          long long r, double h, int n, const EsPoly &P,
+                                          const double *__restrict__ gw, double *__restrict__ acc) {
+  double w0[W], w1[W];
+  es_weights<W>(__dmul_rn(__dmul_rn(h, __ldg(xs + r)), (double)n), P, w0);
+  if constexpr (D == 2) es_weights<W>(__dmul_rn(__dmul_rn(h, __ldg(xs + N + r)), (double)n), P, w1);
+  const double is = __ldg(is2 + r);
+  double u = 0.0;
+  if constexpr (D == 1) {
+#pragma unroll
+    for (int a = 0; a < W; ++a) u = fma(gw[a], w0[a], u);
+    const double v = u * is;
+#pragma unroll
+    for (int a = 0; a < W; ++a) acc[a] = fma(v, w0[a], acc[a]);
+  } else {
+#pragma unroll
+    for (int a = 0; a < W; ++a) {
+      double ra = 0.0;
+#pragma unroll
+      for (int b = 0; b < W; ++b) ra = fma(gw[a * W + b], w1[b], ra);
+      u = fma(ra, w0[a], u);
+    }
+    const double v = u * is;
+#pragma unroll
+    for (int a = 0; a < W; ++a) {
+      const double va = v * w0[a];
+#pragma unroll
+      for (int b = 0; b < W; ++b) acc[a * W + b] = fma(va, w1[b], acc[a * W + b]);
+    }
+  }
+}
+
+template <int D, int W>
+__global__ void __launch_bounds__(kHetThreads, het_min_blocks<D, W>()) k_het_apply_sorted(const HetItem *__restrict__ items, int64_t nitems,
+                                                                  const double *__restrict__ xs,
+                                                                  const double *__restrict__ is2, int64_t N,
+                                                                  const double *__restrict__ g,
+                                                                  double *__restrict__ out, double h, int n, int lo,
+                                                                  int S, EsPoly P) {
+  constexpr int WD = D == 1 ? W : W * W;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+#if EFGP_HET_GSM
+  __shared__ double gsh[kHetThreads / 32][WD];
+  double *gw = gsh[threadIdx.x >> 5];
+#else
+  double gw[WD];
+#endif
+  for (int64_t it = warp; it < nitems; it += nwarps) {
+    const HetItem item = items[it];
+    int c0, c1 = 0;
+    if constexpr (D == 1) {
+      c0 = item.cell + lo;
+    } else {
+      c0 = item.cell / S + lo;
+      c1 = item.cell % S + lo;
+    }
+    double acc[WD];
+#if EFGP_HET_GSM
+    __syncwarp();
+    for (int q = lane; q < WD; q += 32) {
+      const int a = D == 1 ? q : q / W, b = D == 1 ? 0 : q % W;
+      const int64_t gi = D == 1 ? het_wrap(c0 + a, n) : (int64_t)het_wrap(c0 + a, n) * n + het_wrap(c1 + b, n);
+      gw[q] = __ldg(g + gi);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < WD; ++q) acc[q] = 0.0;
+#else
+#pragma unroll
+    for (int q = 0; q < WD; ++q) {
+      const int a = D == 1 ? q : q / W, b = D == 1 ? 0 : q % W;
+      const int64_t gi = D == 1 ? het_wrap(c0 + a, n) : (int64_t)het_wrap(c0 + a, n) * n + het_wrap(c1 + b, n);
+      gw[q] = __ldg(g + gi);
+      acc[q] = 0.0;
+    }
+#endif
+    long long r = item.begin + lane;
+#if EFGP_HET_UNROLL == 2
+    for (; r + 32 < item.end; r += 64) {
+      het_point<D, W>(xs, is2, N, r, h, n, P, gw, acc);
+      het_point<D, W>(xs, is2, N, r + 32, h, n, P, gw, acc);
+    }
+#endif
+    for (; r < item.end; r += 32) het_point<D, W>(xs, is2, N, r, h, n, P, gw, acc);
+#pragma unroll
+    for (int q = 0; q < WD; ++q) {
+      double v = acc[q];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      acc[q] = v;
+    }
+#pragma unroll
+    for (int q = 0; q < WD; ++q) {
+      if (lane == (q & 31) && acc[q] != 0.0) {
+        const int a = D == 1 ? q : q / W, b = D == 1 ? 0 : q % W;
+        const int64_t gi = D == 1 ? het_wrap(c0 + a, n) : (int64_t)het_wrap(c0 + a, n) * n + het_wrap(c1 + b, n);
+        atomicAdd(out + gi, acc[q]);
+      }
+    }
+  }
+}
+
 namespace {
 
 struct HetCtx {
@@ -117,6 +353,155 @@ efgp_status het_apply(efgp_plan *pl, const double2 *p, double2 *Ap, void *vctx) 
   return spread_to_modes(pl, c->x, c->w, c->N, p, Ap, s);
 }
 
+
+struct HetSorted {
+  int lo = 0, S = 0, ncell = 0;
+  double *xs = nullptr, *is2 = nullptr, *out = nullptr;
+  HetItem *items = nullptr;
+  int64_t nitems = 0;
+  cufftHandle r2c = 0;
+};
+
+// d <= 2, register windows up to 6 x 6 (d = 2) or 16 (d = 1), scatter cursors in shared memory
+bool het_sorted_geometry(const Params &P, HetSorted &H) {
+  const char *e = getenv("EFGP_HETERO_SORTED");
+  if (e && e[0] == '0') return false;
+  if (P.d > 2 || (P.d == 2 && P.w > 6)) return false;
+  H.lo = -(P.w / 2);  // ceil(-W/2)
+  const int hi = (int)std::ceil(P.h * (double)P.n2 - 0.5 * P.w);
+  H.S = hi - H.lo + 2;  // one spare row
+  H.ncell = P.d == 1 ? H.S : H.S * H.S;
+  return (size_t)H.ncell * 8 <= 200 * 1024;
+}
+
+template <int D, int W>
+efgp_status het_sort_t(efgp_plan *pl, HetSorted &H, const double *x, const double *sd, int64_t N, cudaStream_t s) {
+  const Params &P = pl->P;
+  const int B = pl->num_sms, T = 1024, n = (int)P.n2;
+  unsigned *hist = nullptr;
+  long long *tot = nullptr, *off = nullptr;
+  EFGP_PALLOC(&hist, sizeof(unsigned) * B * H.ncell, s);
+  EFGP_PALLOC(&tot, sizeof(long long) * H.ncell, s);
+  EFGP_PALLOC(&off, sizeof(long long) * (H.ncell + 1), s);
+  EFGP_PALLOC(&H.xs, sizeof(double) * N * D, s);
+  EFGP_PALLOC(&H.is2, sizeof(double) * N, s);
+  const size_t sm_count = sizeof(unsigned) * H.ncell, sm_scatter = sizeof(unsigned long long) * H.ncell;
+  EFGP_CUDA(cudaFuncSetAttribute(k_het_count<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_count));
+  EFGP_CUDA(cudaFuncSetAttribute(k_het_scatter<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_scatter));
+  k_het_count<D, W><<<B, T, sm_count, s>>>(x, N, P.h, n, H.lo, H.S, H.ncell, hist);
+  k_het_colscan<<<(H.ncell + 255) / 256, 256, 0, s>>>(hist, B, H.ncell, tot);
+  k_het_offsets<<<1, 1024, 0, s>>>(tot, H.ncell, off);
+  k_het_scatter<D, W><<<B, T, sm_scatter, s>>>(x, sd, N, P.h, n, H.lo, H.S, H.ncell, hist, off, H.xs, H.is2);
+  EFGP_CUDA(cudaGetLastError());
+  std::vector<long long> offh(H.ncell + 1);
+  EFGP_CUDA(cudaMemcpyAsync(offh.data(), off, sizeof(long long) * (H.ncell + 1), cudaMemcpyDeviceToHost, s));
+  EFGP_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(hist, s);
+  cudaFreeAsync(tot, s);
+  cudaFreeAsync(off, s);
+  if (offh[H.ncell] != N) {
+    pl->err = "internal: hetero counting sort lost points";
+    return EFGP_ERR_CUDA;
+  }
+  std::vector<HetItem> items;
+  for (int c = 0; c < H.ncell; ++c)
+    for (long long b = offh[c]; b < offh[c + 1]; b += kHetRun)
+      items.push_back(HetItem{b, std::min<long long>(b + kHetRun, offh[c + 1]), c, 0});
+  H.nitems = (int64_t)items.size();
+  EFGP_PALLOC(&H.items, sizeof(HetItem) * std::max<size_t>(items.size(), 1), s);
+  EFGP_CUDA(cudaMemcpyAsync(H.items, items.data(), sizeof(HetItem) * items.size(), cudaMemcpyHostToDevice, s));
+  int64_t cells = 1;
+  for (int k = 0; k < D; ++k) cells *= P.n2;
+  EFGP_PALLOC(&H.out, sizeof(double) * cells, s);
+  if (!pl->plan_het_r2c) {
+    int dims[3] = {(int)P.n2, (int)P.n2, (int)P.n2};
+    EFGP_CUFFT(cufftPlanMany(&pl->plan_het_r2c, D, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, 1));
+  }
+  H.r2c = pl->plan_het_r2c;
+  EFGP_CUDA(cudaStreamSynchronize(s));  // items (host vector) uploaded before it goes out of scope
+  return EFGP_OK;
+}
+
+void het_sorted_free(HetSorted &H, cudaStream_t s) {
+  for (void *p : {(void *)H.xs, (void *)H.is2, (void *)H.out, (void *)H.items})
+    if (p) cudaFreeAsync(p, s);
+  H = HetSorted{};  // (the r2c plan belongs to the handle)
+}
+
+template <int D, int W>
+efgp_status het_apply_sorted_t(efgp_plan *pl, const HetSorted &H, int64_t N, const double2 *p, double2 *Ap) {
+  const Params &P = pl->P;
+  cudaStream_t s = pl->stream;
+  const int n = (int)P.n2;
+  EFGP_TRY(type2_grid_on(pl, p, P.n2, pl->psi2, pl->plan_t2, pl->T2box, pl->t2grid, s));
+  int64_t cells = 1, box = P.n2 / 2 + 1;
+  for (int k = 0; k < D; ++k) cells *= P.n2;
+  for (int k = 0; k < D - 1; ++k) box *= P.n2;
+  EFGP_CUDA(cudaMemsetAsync(H.out, 0, sizeof(double) * cells, s));
+  int per_sm = 1;
+  EFGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_het_apply_sorted<D, W>, kHetThreads, 0));
+  int64_t blocks = std::min<int64_t>((int64_t)pl->num_sms * std::max(per_sm, 1),
+                                     (H.nitems * 32 + kHetThreads - 1) / kHetThreads);
+  if (blocks < 1) blocks = 1;
+  if (H.nitems > 0)
+    k_het_apply_sorted<D, W><<<(unsigned)blocks, kHetThreads, 0, s>>>(H.items, H.nitems, H.xs, H.is2, N, pl->t2grid, H.out,
+                                                               P.h, n, H.lo, H.S, P.poly);
+  EFGP_CUDA(cudaGetLastError());
+  EFGP_CUFFT(cufftSetStream(H.r2c, s));
+  EFGP_CUFFT(cufftExecD2Z(H.r2c, H.out, pl->T2box));  // the C2R input box is free again
+  const double sc = std::pow(2.0 * kPi / (double)n, D);
+  k_het_modes<D><<<grid_for(P.Mh, pl->num_sms), 256, 0, s>>>(pl->T2box, P.n2, (int)P.m, pl->psi2, sc, pl->D_half, p,
+                                                             Ap, P.Mh);
+  EFGP_CUDA(cudaGetLastError());
+  return EFGP_OK;
+}
+
+#define EFGP_HET_W1(M) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) M(16)
+#define EFGP_HET_W2(M) M(2) M(3) M(4) M(5) M(6)
+
+efgp_status het_sort(efgp_plan *pl, HetSorted &H, const double *x, const double *sd, int64_t N, cudaStream_t s) {
+  const int W = pl->P.w;
+  if (pl->P.d == 1) {
+    switch (W) {
+#define C1(WW) case WW: return het_sort_t<1, WW>(pl, H, x, sd, N, s);
+      EFGP_HET_W1(C1)
+#undef C1
+    }
+  } else {
+    switch (W) {
+#define C2(WW) case WW: return het_sort_t<2, WW>(pl, H, x, sd, N, s);
+      EFGP_HET_W2(C2)
+#undef C2
+    }
+  }
+  pl->err = "internal: no sorted hetero kernel for this width";
+  return EFGP_ERR_INVALID;
+}
+
+struct HetSortedCtx {
+  HetSorted *H;
+  int64_t N;
+};
+
+efgp_status het_apply_sorted(efgp_plan *pl, const double2 *p, double2 *Ap, void *vctx) {
+  const HetSortedCtx *c = static_cast<const HetSortedCtx *>(vctx);
+  const int W = pl->P.w;
+  if (pl->P.d == 1) {
+    switch (W) {
+#define C1(WW) case WW: return het_apply_sorted_t<1, WW>(pl, *c->H, c->N, p, Ap);
+      EFGP_HET_W1(C1)
+#undef C1
+    }
+  } else {
+    switch (W) {
+#define C2(WW) case WW: return het_apply_sorted_t<2, WW>(pl, *c->H, c->N, p, Ap);
+      EFGP_HET_W2(C2)
+#undef C2
+    }
+  }
+  return EFGP_ERR_INVALID;
+}
+
 float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0;
   if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
@@ -135,7 +520,7 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
   pl->op_valid = false;  // no Toeplitz operator: predict_var is refused after a heteroskedastic fit
   pl->t2_valid = false;  // the type-2 grid is rebuilt from beta by the next predict
   double *w = nullptr;
-  EFGP_CUDA(cudaMallocAsync((void **)&w, sizeof(double) * N, s));
+  EFGP_PALLOC(&w, sizeof(double) * N, s);
   unsigned long long *minbits = reinterpret_cast<unsigned long long *>(pl->scal + 24);
   EFGP_CUDA(cudaEventRecord(pl->ev[0], s));
   EFGP_CUDA(cudaMemsetAsync(minbits, 0xff, sizeof(unsigned long long), s));
@@ -174,39 +559,51 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
       max_iter = (int64_t)std::ceil(std::log(1.0 / P.cg_tol) * std::sqrt((double)N) / (2.0 * smin));
       if (max_iter < 10) max_iter = 10;
     }
-    // Both NUFFTs on the same fine grid n_rhs with the same kernel and deconvolution: the type-2 is
-    // then the exact adjoint of the type-1, so the applied operator is exactly Hermitian (CG's
-    // recurrences assume it; with the v grid n1 for the spread and n2 for the interpolation the
-    // mismatch ~nufft_tol slowed parity-mode CG by ~30 %).
-    HetCtx ctx{x, sd, w, N, P.n_rhs, nullptr, 0, nullptr, nullptr};
-    if (P.n_rhs == P.n2) {
-      ctx.psi = pl->psi2;
-      ctx.plan = pl->plan_t2;
-      ctx.box = pl->T2box;
-      ctx.grid = pl->t2grid;
+    HetSorted H;
+    if (het_sorted_geometry(P, H)) {
+      st = het_sort(pl, H, x, sd, N, s);
+      EFGP_CUDA(cudaEventRecord(pl->ev[2], s));
+      HetSortedCtx sctx{&H, N};
+      if (st == EFGP_OK) st = cg_solve_op(pl, max_iter, het_apply_sorted, &sctx);
+      pl->het_path = 1;
     } else {
-      if (!pl->het_grid) {
-        int64_t box = P.n_rhs / 2 + 1, cells = P.n_rhs;
-        for (int k = 0; k < P.d - 1; ++k) {
-          box *= P.n_rhs;
-          cells *= P.n_rhs;
+      EFGP_CUDA(cudaEventRecord(pl->ev[2], s));
+      // Both NUFFTs on the same fine grid n_rhs with the same kernel and deconvolution: the type-2 is
+      // then the exact adjoint of the type-1, so the applied operator is exactly Hermitian (CG's
+      // recurrences assume it; with the v grid n1 for the spread and n2 for the interpolation the
+      // mismatch ~nufft_tol slowed parity-mode CG by ~30 %).
+      HetCtx ctx{x, sd, w, N, P.n_rhs, nullptr, 0, nullptr, nullptr};
+      if (P.n_rhs == P.n2) {
+        ctx.psi = pl->psi2;
+        ctx.plan = pl->plan_t2;
+        ctx.box = pl->T2box;
+        ctx.grid = pl->t2grid;
+      } else {
+        if (!pl->het_grid) {
+          int64_t box = P.n_rhs / 2 + 1, cells = P.n_rhs;
+          for (int k = 0; k < P.d - 1; ++k) {
+            box *= P.n_rhs;
+            cells *= P.n_rhs;
+          }
+          EFGP_CUDA(cudaMalloc((void **)&pl->het_box, sizeof(double2) * box));
+          EFGP_CUDA(cudaMalloc((void **)&pl->het_grid, sizeof(double) * cells));
+          int dims[3] = {(int)P.n_rhs, (int)P.n_rhs, (int)P.n_rhs};
+          EFGP_CUFFT(cufftPlanMany(&pl->plan_het, P.d, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D, 1));
         }
-        EFGP_CUDA(cudaMalloc((void **)&pl->het_box, sizeof(double2) * box));
-        EFGP_CUDA(cudaMalloc((void **)&pl->het_grid, sizeof(double) * cells));
-        int dims[3] = {(int)P.n_rhs, (int)P.n_rhs, (int)P.n_rhs};
-        EFGP_CUFFT(cufftPlanMany(&pl->plan_het, P.d, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D, 1));
+        ctx.psi = pl->psi1;  // n_rhs == n1: psi1 covers k <= 2m
+        ctx.plan = pl->plan_het;
+        ctx.box = pl->het_box;
+        ctx.grid = pl->het_grid;
       }
-      ctx.psi = pl->psi1;  // n_rhs == n1: psi1 covers k <= 2m
-      ctx.plan = pl->plan_het;
-      ctx.box = pl->het_box;
-      ctx.grid = pl->het_grid;
+      st = cg_solve_op(pl, max_iter, het_apply, &ctx);
+      pl->het_path = 0;
     }
-    st = cg_solve_op(pl, max_iter, het_apply, &ctx);
+    het_sorted_free(H, s);
     EFGP_CUDA(cudaEventRecord(pl->ev[4], s));
     EFGP_CUDA(cudaEventSynchronize(pl->ev[4]));
-    pl->t_spread = elapsed_ms(pl->ev[0], pl->ev[1]);
-    pl->t_modes = 0;
-    pl->t_solve = elapsed_ms(pl->ev[1], pl->ev[4]);
+    pl->t_spread = elapsed_ms(pl->ev[0], pl->ev[1]);  // right-hand side (prep + type-1)
+    pl->t_modes = elapsed_ms(pl->ev[1], pl->ev[2]);   // sorted path: the one-time counting sort
+    pl->t_solve = elapsed_ms(pl->ev[2], pl->ev[4]);
     if (st == EFGP_OK || st == EFGP_ERR_NOCONVERGE) {
       pl->fitted = true;
       pl->N_last = N;

@@ -4,6 +4,7 @@
 // (cells reachable from x* in [0,1]^d) in shared memory once, then gathers from it; GLOBAL
 // variant gathers from L2.  Targets outside [0,1]^d or non-finite give mu = NaN and raise
 // dflags[1].
+#include <algorithm>
 #include <cmath>
 
 #include "efgp_internal.cuh"
@@ -27,8 +28,12 @@ __device__ __forceinline__ int wrapn(int i, int n) {
   return i < 0 ? i + n : i;
 }
 
+// threads per CTA the kernel is compiled for: 1024 where the weights fit in 64 registers
+template <int D, int W>
+constexpr int interp_max_threads() { return (D <= 2 && W <= 8) ? 1024 : 256; }
+
 template <int D, int W, bool SMEM>
-__global__ void __launch_bounds__(256) k_interp(const double *__restrict__ xt, int64_t q,
+__global__ void __launch_bounds__(interp_max_threads<D, W>()) k_interp(const double *__restrict__ xt, int64_t q,
                                                 const double *__restrict__ grid, int n, double h, EsPoly P,
                                                 int lo, int A, const double *__restrict__ sd,
                                                 double *__restrict__ mu, int *__restrict__ err) {
@@ -128,13 +133,17 @@ static efgp_status launch_interp(efgp_plan *pl, const double *grid, int n, const
   const size_t sb = cells * sizeof(double);
   int64_t blocks = (q + 255) / 256;
   if (sb <= 160 * 1024) {
-    // one wave of persistent CTAs so the staged grid is reused across many targets
-    const int64_t cap = (int64_t)pl->num_sms * (sb <= 48 * 1024 ? 4 : (sb <= 100 * 1024 ? 2 : 1));
+    // one wave of persistent CTAs so the staged grid is reused across many targets; 1024 resident
+    // threads per SM whatever the staged size (4 x 256, 2 x 512 or 1 x 1024)
+    const int per_sm = sb <= 48 * 1024 ? 4 : (sb <= 100 * 1024 ? 2 : 1);
+    const int threads = std::min(1024 / per_sm, interp_max_threads<D, W>());
+    blocks = (q + threads - 1) / threads;
+    const int64_t cap = (int64_t)pl->num_sms * per_sm;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     EFGP_CUDA(cudaFuncSetAttribute(k_interp<D, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-    k_interp<D, W, true><<<(unsigned)blocks, 256, sb, s>>>(xt, q, grid, n, P.h, P.poly, o.lo, o.A,
-                                                           sd, mu, pl->dflags);
+    k_interp<D, W, true><<<(unsigned)blocks, threads, sb, s>>>(xt, q, grid, n, P.h, P.poly, o.lo, o.A,
+                                                               sd, mu, pl->dflags);
   } else {
     const int64_t cap = (int64_t)pl->num_sms * 16;
     if (blocks > cap) blocks = cap;

@@ -19,9 +19,16 @@ def noise_sd(c, N, seed):
     return c.sigma * (0.5 + np.random.default_rng(seed).uniform(0, 1, N))
 
 
+@pytest.mark.parametrize("path", ["sorted", "unfused"])
 @pytest.mark.parametrize("name", list(CONFIGS))
-def test_hetero_parity(name):
+def test_hetero_parity(name, path, monkeypatch):
+    # "sorted": points counting-sorted once by cell, one fused type-2/type-1 pass per iteration (d <= 2);
+    # "unfused": K8 + C2R + K9 + K1 + R2C per iteration (the d = 3 path; forced here by the env switch)
+    if path == "unfused":
+        monkeypatch.setenv("EFGP_HETERO_SORTED", "0")
     c = CONFIGS[name]
+    if path == "sorted" and (c.d == 3 or c.name == "c3"):
+        pytest.skip("no sorted path: d = 3 (W^3 register windows) / c3 (W = 8 > 6 in 2D)")
     N, m_over = HET_SIZES[name]
     x, y, xt = generate(c, N=N, q=min(c.q, 1000))
     sd = noise_sd(c, N, 40 + c.id)
@@ -34,6 +41,7 @@ def test_hetero_parity(name):
     g.fit_hetero(dev(x), dev(y), dev(sd))
     mu = g.predict(dev(xt)).cpu().numpy()
     inf = g.info()
+    assert inf["hetero_sorted"] == (1 if path == "sorted" else 0)
     fit = O.efgp_fit_hetero(x, y, sd, c.kernel, c.ell, c.eps, nu=c.nu, h=kw.get("h"), m=kw.get("m"), cg_tol=cg_tol)
     ref = O.efgp_predict(fit, xt)
     assert rel(mu, ref) <= 10 * c.eps, (rel(mu, ref), 10 * c.eps)

@@ -497,3 +497,21 @@ def test_full_size_sampled(name):
     ref = O.posterior_mean(beta, D, h, xt)
     assert rel(mu, ref) <= 5 * tol
     g.close()
+
+
+def test_refit_with_larger_problem_on_same_handle():
+    # a second fit whose CG cap (~sqrt N) exceeds the first one's reallocates the residual
+    # history; the cached CG graph must not keep the freed buffer (regression: illegal address)
+    c = CONFIGS["c5"]
+    x1, y1, _ = generate(c, N=1000, q=1)
+    x2, y2, xt = generate(c, N=300_000, q=200)
+    g = model(c)
+    g.fit(dev(x1), dev(y1))
+    g.fit(dev(x2), dev(y2))
+    mu = g.predict(dev(xt)).cpu().numpy()
+    g2 = model(c)
+    g2.fit(dev(x2), dev(y2))
+    assert rel(mu, g2.predict(dev(xt)).cpu().numpy()) < 10 * c.eps
+    assert len(g.residual_history()) == g.info()["iters"] + 1
+    g.close()
+    g2.close()
