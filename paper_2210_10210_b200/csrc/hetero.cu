@@ -186,8 +186,8 @@ __device__ __forceinline__ int het_wrap(int i, int n) {
 #ifndef EFGP_HET_GSM
 #define EFGP_HET_GSM 1  // the warp's grid window in shared memory (broadcast reads) instead of registers
 #endif
-#ifndef EFGP_HET_UNROLL
-#define EFGP_HET_UNROLL 1  // points per lane in flight (2: more ILP, more registers; slower on B200)
+#ifndef EFGP_HET_PF
+#define EFGP_HET_PF 1  // prefetch distance in points per lane (1: +17 %; 2-4 cost occupancy)
 #endif
 #ifndef EFGP_HET_THREADS
 #define EFGP_HET_THREADS 128
@@ -195,17 +195,18 @@ __device__ __forceinline__ int het_wrap(int i, int n) {
 // resident CTAs per SM the kernel is compiled for: 4 x 128 threads (<= 128 registers) for the 2D
 // W <= 5 windows (+21 % over the unconstrained 154 registers on c5), else no constraint
 template <int D, int W>
-constexpr int het_min_blocks() { return (D == 2 && W <= 5) ? 4 : 1; }
+#ifndef EFGP_HET_MINB2
+#define EFGP_HET_MINB2 4
+#endif
+constexpr int het_min_blocks() { return (D == 2 && W <= 5) ? EFGP_HET_MINB2 : 1; }
 constexpr int kHetThreads = EFGP_HET_THREADS;
 
 template <int D, int W>
-__device__ __forceinline__ void het_point(const double *__restrict__ xs, const double *__restrict__ is2, int64_t N,
-                                          long long r, double h, int n, const EsPoly &P,
+__device__ __forceinline__ void het_point(double x0, double x1, double is, double h, int n, const EsPoly &P,
                                           const double *__restrict__ gw, double *__restrict__ acc) {
   double w0[W], w1[W];
-  es_weights<W>(__dmul_rn(__dmul_rn(h, __ldg(xs + r)), (double)n), P, w0);
-  if constexpr (D == 2) es_weights<W>(__dmul_rn(__dmul_rn(h, __ldg(xs + N + r)), (double)n), P, w1);
-  const double is = __ldg(is2 + r);
+  es_weights<W>(__dmul_rn(__dmul_rn(h, x0), (double)n), P, w0);
+  if constexpr (D == 2) es_weights<W>(__dmul_rn(__dmul_rn(h, x1), (double)n), P, w1);
   double u = 0.0;
   if constexpr (D == 1) {
 #pragma unroll
@@ -277,14 +278,34 @@ __global__ void __launch_bounds__(kHetThreads, het_min_blocks<D, W>()) k_het_app
       acc[q] = 0.0;
     }
 #endif
+    // the loads of the point PF positions ahead are in flight while this one is computed
+    // (long-scoreboard stalls dominated without it)
+    constexpr int PF = EFGP_HET_PF;
+    double px0[PF], px1[PF], pis[PF];
     long long r = item.begin + lane;
-#if EFGP_HET_UNROLL == 2
-    for (; r + 32 < item.end; r += 64) {
-      het_point<D, W>(xs, is2, N, r, h, n, P, gw, acc);
-      het_point<D, W>(xs, is2, N, r + 32, h, n, P, gw, acc);
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+      const long long rk = r + 32 * k;
+      const bool ok = rk < item.end;
+      px0[k] = ok ? __ldg(xs + rk) : 0.0;
+      px1[k] = (D == 2 && ok) ? __ldg(xs + N + rk) : 0.0;
+      pis[k] = ok ? __ldg(is2 + rk) : 0.0;
     }
-#endif
-    for (; r < item.end; r += 32) het_point<D, W>(xs, is2, N, r, h, n, P, gw, acc);
+    for (; r < item.end; r += 32) {
+      const double x0 = px0[0], x1 = px1[0], is = pis[0];
+#pragma unroll
+      for (int k = 0; k + 1 < PF; ++k) {
+        px0[k] = px0[k + 1];
+        px1[k] = px1[k + 1];
+        pis[k] = pis[k + 1];
+      }
+      const long long rn = r + 32 * PF;
+      const bool ok = rn < item.end;
+      px0[PF - 1] = ok ? __ldg(xs + rn) : 0.0;
+      px1[PF - 1] = (D == 2 && ok) ? __ldg(xs + N + rn) : 0.0;
+      pis[PF - 1] = ok ? __ldg(is2 + rn) : 0.0;
+      het_point<D, W>(x0, x1, is, h, n, P, gw, acc);
+    }
 #pragma unroll
     for (int q = 0; q < WD; ++q) {
       double v = acc[q];
