@@ -18,6 +18,8 @@ fast transform replaced by the sum that defines it:
   step 5/6 mu(x*) ............. :func:`posterior_mean`    direct sum, eq ``muws``
   NEXT-2  s(x*) ............... :func:`posterior_variance` one CG per target on eq ``eta``
                                  (P:571-575), then the direct sum of eq ``sws``
+  NEXT-4  preconditioner ...... :func:`kron_preconditioner` + :func:`pcg` (reading G12):
+                                 M = A_1 (x) ... (x) A_d + sigma^2 I from the axis lines of v and D
   NEXT-3  sigma_n ............. :func:`efgp_fit_hetero` CG on (Phi^* S^-1 Phi + I) beta = Phi^* S^-1 y,
                                  S = diag(sigma_n^2) (reading G11), Phi applied densely
 
@@ -28,6 +30,11 @@ Readings where the paper is silent, garbled or inconsistent (DESIGN.md "Readings
   G3  Matérn eps rescaling by the true ||k||_{L2(R^d)} (reading A); alternatives B (none), P (printed).
   G4  SE (h, m): Cor c:SEparams literally; h rounded down at the 12th significant digit.
   G6  CG: x0 = 0, unpreconditioned, recursive residual, Hermitian inner products.
+  G12 NEXT-4 preconditioner (P:2741-2745 names "Kronecker-structure Toeplitz preconditioners" only):
+      v^(i)_l = v_{l e_i}, T_i = T(v^(i)) ((2m+1)^2 Toeplitz), delta_i(j) = D_{j e_i} / D_0^((d-1)/d),
+      A_i = diag(delta_i) T_i diag(delta_i) / N^((d-1)/d), M = A_1 (x) ... (x) A_d + sigma^2 I, applied as
+      (Q_1 (x) ... ) (Lambda + sigma^2)^-1 (Q_1 (x) ...)^* from eigh(A_i).  Exact (M = A) when the points
+      form a tensor-product set and D is separable (SE); d = 1 gives M = A.  Standard PCG, same stop rule.
   G11 heteroskedastic noise (P:2759-2763 names it, gives no formula): the weight-space posterior mean
       for y = Phi beta + e, beta ~ N(0, I), e ~ N(0, S), S = diag(sigma_n^2): beta solves
       (Phi^* S^-1 Phi + I) beta = Phi^* S^-1 y, mu(x*) = phi(x*) beta.  With sigma_n = sigma it is
@@ -53,7 +60,8 @@ __all__ = [
     "mode_indices", "spectral_weights", "toeplitz_vector", "rhs_Fy", "rhs",
     "toeplitz_matrix", "toeplitz_apply", "system_apply", "cg", "default_max_iter",
     "posterior_mean", "posterior_variance", "design_matrix", "kernel_tilde_matrix", "dense_gp_mean",
-    "dense_gp_variance", "features", "hetero_system_apply", "efgp_fit_hetero", "dense_gp_mean_hetero",
+    "dense_gp_variance", "features", "hetero_system_apply", "KronPrecond", "kron_factors",
+    "kron_preconditioner", "kron_apply_inverse", "pcg", "efgp_fit_hetero", "dense_gp_mean_hetero",
     "OracleFit", "efgp_fit", "efgp_predict",
 ]
 
@@ -295,6 +303,92 @@ def cg(apply, b: np.ndarray, tol: float, max_iter: int):
 
 
 # ----------------------------------------------------------------------------------------------
+# NEXT-4: Kronecker preconditioner (reading G12) and preconditioned CG
+# ----------------------------------------------------------------------------------------------
+@dataclass
+class KronPrecond:
+    Q: list      # eigenvectors of A_i, (2m+1, 2m+1) each
+    lam: list    # eigenvalues of A_i
+    sigma2: float
+
+
+def kron_factors(v: np.ndarray, D: np.ndarray):
+    """The factors A_i = diag(delta_i) T(v^(i)) diag(delta_i) / N^((d-1)/d) of reading G12, where
+    v^(i)_l = v_{l e_i} (the line of v through j = 0 along axis i), delta_i(j) = D_{j e_i} / D_0^((d-1)/d)
+    and N = v_0 (eq ``88`` at j = 0)."""
+    d = D.ndim
+    m = (D.shape[0] - 1) // 2
+    N = float(v[(2 * m,) * d].real)
+    D0 = float(D[(m,) * d])
+    out = []
+    for i in range(d):
+        line_v = [2 * m] * d
+        line_v[i] = slice(None)
+        vi = v[tuple(line_v)]                                   # l = -2m..2m
+        line_d = [m] * d
+        line_d[i] = slice(None)
+        di = D[tuple(line_d)] / D0 ** ((d - 1) / d)
+        p = np.arange(2 * m + 1)
+        Ti = vi[p[:, None] - p[None, :] + 2 * m]                 # T_pq = v^(i)_{p-q}
+        out.append(di[:, None] * Ti * di[None, :] / N ** ((d - 1) / d))
+    return out
+
+
+def kron_preconditioner(v: np.ndarray, D: np.ndarray, sigma2: float) -> KronPrecond:
+    """M = A_1 (x) ... (x) A_d + sigma^2 I (reading G12), factored by numpy.linalg.eigh of each A_i."""
+    Q, lam = [], []
+    for A in kron_factors(v, D):
+        w, V = np.linalg.eigh(A)
+        Q.append(V)
+        lam.append(w)
+    return KronPrecond(Q, lam, sigma2)
+
+
+def kron_apply_inverse(P: KronPrecond, r: np.ndarray) -> np.ndarray:
+    """M^-1 r = (Q_1 (x) ... ) (Lambda_1 (x) ... + sigma^2)^-1 (Q_1 (x) ...)^* r, one axis at a time."""
+    z = np.asarray(r, dtype=np.complex128)
+    for i, Q in enumerate(P.Q):
+        z = np.moveaxis(np.tensordot(Q.conj().T, np.moveaxis(z, i, 0), axes=1), 0, i)
+    lam = P.lam[0]
+    for w in P.lam[1:]:
+        lam = np.multiply.outer(lam, w)
+    z = z / (lam + P.sigma2)
+    for i, Q in enumerate(P.Q):
+        z = np.moveaxis(np.tensordot(Q, np.moveaxis(z, i, 0), axes=1), 0, i)
+    return z
+
+
+def pcg(apply, precond, b: np.ndarray, tol: float, max_iter: int):
+    """Preconditioned CG (Golub & Van Loan Alg 11.5.1, the standard recurrences), x0 = 0, stopping
+    at the first k with ||r_k|| <= tol ||b|| (the same rule as :func:`cg`, reading G6).
+    Returns (x, iters, history of ||r_k|| / ||b||)."""
+    x = np.zeros_like(b, dtype=np.complex128)
+    r = b.astype(np.complex128).copy()
+    bnorm = math.sqrt(np.vdot(b, b).real)
+    if bnorm == 0.0:
+        return x, 0, [0.0]
+    z = precond(r)
+    p = z.copy()
+    rz = np.vdot(r, z).real
+    hist = [1.0]
+    k = 0
+    while hist[-1] > tol and k < max_iter:
+        Ap = apply(p)
+        alpha = rz / np.vdot(p, Ap).real
+        x = x + alpha * p
+        r = r - alpha * Ap
+        k += 1
+        hist.append(math.sqrt(np.vdot(r, r).real) / bnorm)
+        if hist[-1] <= tol:
+            break
+        z = precond(r)
+        rz_new = np.vdot(r, z).real
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return x, k, hist
+
+
+# ----------------------------------------------------------------------------------------------
 # Steps 5-6: posterior mean at targets
 # ----------------------------------------------------------------------------------------------
 def posterior_mean(beta, D, h, xt, chunk: int = 1 << 14, return_imag: bool = False):
@@ -478,9 +572,11 @@ class OracleFit:
 
 def efgp_fit(x, y, kernel: str, ell: float, sigma: float, eps: float, nu: float = 0.0,
              h: float | None = None, m: int | None = None, cg_tol: float | None = None,
-             max_iter: int | None = None, rescale: str = "A", dense_T_max: int = 4096) -> OracleFit:
+             max_iter: int | None = None, rescale: str = "A", dense_T_max: int = 4096,
+             precond: str | None = None) -> OracleFit:
     """Algorithm ``a1`` steps 1-4: (h, m); v (eq 88); rhs Phi^*y (eq rhs); CG to
-    relative residual cg_tol (default eps)."""
+    relative residual cg_tol (default eps).  precond="kron": PCG with the NEXT-4
+    preconditioner of reading G12 instead of plain CG."""
     x = np.asarray(x, dtype=np.float64)
     if x.ndim == 1:
         x = x[:, None]
@@ -495,7 +591,12 @@ def efgp_fit(x, y, kernel: str, ell: float, sigma: float, eps: float, nu: float 
     tol = eps if cg_tol is None else cg_tol
     cap = default_max_iter(N, sigma, tol) if max_iter is None else max_iter
     T = toeplitz_matrix(v, m) if (2 * m + 1) ** d <= dense_T_max else None
-    beta, iters, hist = cg(lambda p: system_apply(v, D, sigma ** 2, p, T), b, tol, cap)
+    A = lambda p: system_apply(v, D, sigma ** 2, p, T)
+    if precond == "kron":
+        Pk = kron_preconditioner(v, D, sigma ** 2)
+        beta, iters, hist = pcg(A, lambda r: kron_apply_inverse(Pk, r), b, tol, cap)
+    else:
+        beta, iters, hist = cg(A, b, tol, cap)
     return OracleFit(kernel, nu, ell, sigma, eps, d, h, m, D, v, b, beta, iters, hist)
 
 
