@@ -65,6 +65,15 @@ typedef enum { EFGP_SPREAD_AUTO = 0, EFGP_SPREAD_GLOBAL = 1, EFGP_SPREAD_SMEM = 
  * FP32 and MIXED are refused (EFGP_ERR_INVALID) for nufft_tol < 1e-6. */
 typedef enum { EFGP_WEIGHTS_FP64 = 0, EFGP_WEIGHTS_FP32 = 1, EFGP_WEIGHTS_MIXED = 2 } efgp_weights;
 
+/* NEXT-4 (reading G12): CG preconditioner of efgp_fit / efgp_fit_solve.
+ *   NONE: plain CG (Alg a1 step 4).
+ *   KRON: PCG with M = A_1 (x) ... (x) A_d + sigma^2 I, A_i = diag(delta_i) T(v^(i)) diag(delta_i) /
+ *         N^((d-1)/d) built from the axis lines of v and D (exact for tensor-product points with a
+ *         separable kernel, and in d = 1), factored by a (2m+1)^2 Hermitian eigen-decomposition per
+ *         axis (cuSOLVER) and applied by 2d small dense axis contractions per iteration.  Same answer
+ *         and stopping rule; fewer iterations.  efgp_predict_var is unaffected (plain CG). */
+typedef enum { EFGP_PRECOND_NONE = 0, EFGP_PRECOND_KRON = 1 } efgp_precond;
+
 typedef struct {
   double h;            /* grid spacing override when m > 0                        */
   int64_t m;           /* modes per dimension override (2m+1 per dim), 0 = rule (Alg a1 step 1) */
@@ -75,6 +84,7 @@ typedef struct {
   int spread_method;   /* efgp_spread_method                                                     */
   int graph_iters;     /* CG iterations per CUDA-graph launch, 0 = default                        */
   int spread_weights;  /* efgp_weights, default EFGP_WEIGHTS_FP64                                  */
+  int precond;         /* efgp_precond, default EFGP_PRECOND_NONE (Alg a1's plain CG)             */
   void *stream;        /* cudaStream_t for all device work (NULL = default stream)               */
 } efgp_options;
 
@@ -97,6 +107,7 @@ typedef struct {
   double t_var_ms;                                            /* device time of the last predict_var */
   int64_t var_iters_max, var_batch;                           /* its largest CG count, targets/batch */
   int64_t hetero_sorted; /* last efgp_fit_hetero: 1 = points sorted once by cell, fused NUFFT-pair pass */
+  int64_t precond;       /* efgp_precond of the fit */
 } efgp_info;
 
 /* Fill *opt with defaults (all zero / automatic). */

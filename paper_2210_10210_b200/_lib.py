@@ -19,7 +19,7 @@ STATUS_NAMES = {0: "EFGP_OK", 1: "EFGP_ERR_NOCONVERGE", 2: "EFGP_ERR_INVALID", 3
 class Options(C.Structure):
     _fields_ = [("h", C.c_double), ("m", C.c_int64), ("cg_tol", C.c_double), ("max_iter", C.c_int64),
                 ("nufft_tol", C.c_double), ("matern_rescale", C.c_int), ("spread_method", C.c_int),
-                ("graph_iters", C.c_int), ("spread_weights", C.c_int), ("stream", C.c_void_p)]
+                ("graph_iters", C.c_int), ("spread_weights", C.c_int), ("precond", C.c_int), ("stream", C.c_void_p)]
 
 
 class Info(C.Structure):
@@ -31,7 +31,8 @@ class Info(C.Structure):
                 ("t_solve_ms", C.c_double), ("t_predict_ms", C.c_double), ("sorted_t1", C.c_int64),
                 ("sorted_t2", C.c_int64), ("sorted_chunk", C.c_int64), ("sorted_round", C.c_int64),
                 ("spread_precision", C.c_int64), ("t_var_ms", C.c_double), ("var_iters_max", C.c_int64),
-                ("var_batch", C.c_int64), ("hetero_sorted", C.c_int64)]
+                ("var_batch", C.c_int64), ("hetero_sorted", C.c_int64),
+                ("precond", C.c_int64)]
 
 
 # every symbol include/efgp.h declares, with (restype, argtypes)

@@ -4,6 +4,8 @@
 #include <cstring>
 #include <new>
 
+#include <cusolverDn.h>
+
 #include "efgp_internal.cuh"
 
 using namespace efgp;
@@ -91,7 +93,7 @@ efgp_status build(efgp_plan *pl) {
     EFGP_CUDA(cudaMemset(*v, 0, sizeof(double2) * P.Mh));
   }
   pl->cg_blocks = pl->num_sms * 4;
-  EFGP_TRY(dalloc(pl, &pl->partials, 2 * pl->cg_blocks));
+  EFGP_TRY(dalloc(pl, &pl->partials, 3 * pl->cg_blocks));  // (p,Ap) | (r,r) | PCG (r,z)
   EFGP_TRY(dalloc(pl, &pl->scal, 32));
   EFGP_TRY(dalloc(pl, &pl->dflags, 4));
   EFGP_CUDA(cudaMallocHost((void **)&pl->h_pinned, 256));
@@ -223,7 +225,13 @@ efgp_status fit_solve_impl(efgp_plan *pl, const double *modes, int64_t N_total) 
   EFGP_CUDA(cudaMemcpyAsync(pl->modes_sum, modes, sizeof(double) * 2 * (P.Kvh + P.Mh), cudaMemcpyDefault, s));
   EFGP_TRY(toeplitz_setup(pl, pl->modes_sum, s));
   pl->op_valid = true;
-  const efgp_status st = cg_solve(pl, N_total);
+  efgp_status st;
+  if (P.precond) {  // NEXT-4: Kronecker-preconditioned CG (reading G12)
+    EFGP_TRY(precond_setup(pl, pl->modes_sum));
+    st = pcg_solve(pl, N_total);
+  } else {
+    st = cg_solve(pl, N_total);
+  }
   EFGP_CUDA(cudaEventRecord(pl->ev[4], s));
   EFGP_CUDA(cudaEventSynchronize(pl->ev[4]));
   pl->t_solve = elapsed(pl->ev[3], pl->ev[4]);
@@ -521,6 +529,7 @@ efgp_status efgp_get_info(efgp_handle pl, efgp_info *o) {
     o->var_batch = pl->var_B;
   }
   o->hetero_sorted = pl->het_path;
+  o->precond = P.precond;
   return EFGP_OK;
 }
 
@@ -548,6 +557,8 @@ void efgp_destroy(efgp_handle pl) {
   if (pl->stream) cudaStreamSynchronize(pl->stream);
   if (pl->cg_exec) cudaGraphExecDestroy(pl->cg_exec);
   if (pl->var_exec) cudaGraphExecDestroy(pl->var_exec);
+  if (pl->pcg_exec) cudaGraphExecDestroy(pl->pcg_exec);
+  if (pl->pc_solver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(pl->pc_solver));
   for (cufftHandle h : {pl->plan_var_c2r, pl->plan_var_r2c, pl->plan_het, pl->plan_het_r2c})
     if (h) cufftDestroy(h);
   for (void *b : {(void *)pl->var_x, (void *)pl->var_r, (void *)pl->var_p, (void *)pl->var_Ap, (void *)pl->var_X,
@@ -559,7 +570,8 @@ void efgp_destroy(efgp_handle pl) {
                   pl->Xbox, pl->Yr, pl->vhat, pl->Zbox, pl->b, pl->x, pl->r, pl->p, pl->Ap, pl->partials,
                   pl->scal, pl->hist, pl->dflags, pl->T2box, pl->t2grid, pl->stage[0], pl->stage[1],
                   pl->rec[0], pl->rec[1], pl->rec[2], pl->trace,
-                  pl->sync_buf, pl->het_box, pl->het_grid};
+                  pl->sync_buf, pl->het_box, pl->het_grid, pl->pc_Q, pl->pc_F0, pl->pc_F1, pl->pc_work, pl->z,
+                  pl->pc_lam, pl->pc_info};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (pl->h_pinned) cudaFreeHost(pl->h_pinned);

@@ -27,6 +27,7 @@ struct CGState {
   long long max_iter;
   int done;         // 1: converged, 2: hit max_iter
   int pad_;
+  double rz;        // PCG: (r, z) of the current residual (NEXT-4)
 };
 
 constexpr int kCGThreads = 256;
@@ -165,11 +166,14 @@ __global__ void k_cg_apply(const double2 *__restrict__ Z, const double2 *__restr
 // alpha = rr / <p,Ap>; x += alpha p; r -= alpha Ap; partial ||r||^2
 __global__ void k_cg_xr(double2 *__restrict__ x, double2 *__restrict__ r, const double2 *__restrict__ p,
                         const double2 *__restrict__ Ap, int64_t Mh, int m, CGState *st,
-                        const double *__restrict__ part_pAp, double *__restrict__ part_rr, int nblk) {
+                        const double *__restrict__ part_pAp, double *__restrict__ part_rr, int nblk,
+                        const double *__restrict__ part_rz = nullptr) {
   __shared__ double sh[40];
   if (st->done) return;
   const double pAp = reduce_partials(part_pAp, nblk, sh);
-  const double rr = st->rr;
+  // CG: alpha = (r,r)/(p,Ap); PCG: alpha = (r,z)/(p,Ap), (r,z) reduced from its partials
+  const double rr = part_rz ? reduce_partials(part_rz, nblk, sh) : st->rr;
+  if (part_rz && blockIdx.x == 0 && threadIdx.x == 0) st->rz = rr;
   const double alpha = rr / pAp;
   double acc = 0.0;
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
@@ -187,7 +191,7 @@ __global__ void k_cg_xr(double2 *__restrict__ x, double2 *__restrict__ r, const 
   acc = block_sum(acc, sh);
   if (threadIdx.x == 0) {
     part_rr[blockIdx.x] = acc;
-    if (blockIdx.x == 0) st->rr_old = rr;
+    if (blockIdx.x == 0 && !part_rz) st->rr_old = rr;
   }
 }
 
@@ -225,10 +229,11 @@ __global__ void k_cg_pad(const double2 *__restrict__ p, const double *__restrict
 
 static efgp_status ensure_hist(efgp_plan *pl, int64_t max_iter) {
   if (max_iter + 1 > pl->hist_cap) {
-    if (pl->cg_exec) {  // the captured CG graph holds the old history pointer
-      cudaGraphExecDestroy(pl->cg_exec);
-      pl->cg_exec = nullptr;
-    }
+    for (cudaGraphExec_t *e : {&pl->cg_exec, &pl->pcg_exec})  // captured graphs hold the old pointer
+      if (*e) {
+        cudaGraphExecDestroy(*e);
+        *e = nullptr;
+      }
     if (pl->hist) cudaFree(pl->hist);
     pl->hist = nullptr;
     pl->hist_cap = 0;
@@ -384,6 +389,144 @@ efgp_status cg_solve_op(efgp_plan *pl, int64_t max_iter, CGOp op, void *ctx) {
     case 1: return cg_solve_op_d<1>(pl, max_iter, op, ctx);
     case 2: return cg_solve_op_d<2>(pl, max_iter, op, ctx);
     case 3: return cg_solve_op_d<3>(pl, max_iter, op, ctx);
+  }
+  return EFGP_ERR_INVALID;
+}
+
+// ---- NEXT-4: preconditioned CG with the Kronecker preconditioner of precond.cu (reading G12).
+// Standard PCG recurrences; the stopping rule and history are those of CG (||r_k|| / ||b||, G6).
+__global__ void k_pcg_check(CGState *st, const double *__restrict__ part_rr, int nblk, double *__restrict__ hist) {
+  __shared__ double sh[40];
+  if (st->done) return;
+  const double rr = reduce_partials(part_rr, nblk, sh);
+  if (threadIdx.x == 0) {
+    st->rr = rr;
+    const long long it = st->iter + 1;
+    st->iter = it;
+    const double rel = sqrt(rr) / st->bnorm;
+    hist[it] = rel;
+    if (rel <= st->tol) st->done = 1;
+    else if (it >= st->max_iter) st->done = 2;
+  }
+}
+
+__global__ void k_pcg_dot(const double2 *__restrict__ r, const double2 *__restrict__ z, int64_t Mh, int m,
+                          const CGState *st, double *__restrict__ part) {
+  __shared__ double sh[40];
+  if (st->done) return;
+  double acc = 0.0;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 a = r[q], b = z[q];
+    const double wq = (q % (m + 1)) ? 2.0 : 1.0;
+    acc += wq * (a.x * b.x + a.y * b.y);
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+// p = z + (rz_new / rz) p   (first == true: p = z)
+__global__ void k_pcg_p(const double2 *__restrict__ z, double2 *__restrict__ p, int64_t Mh, const CGState *st,
+                        const double *__restrict__ part_rz, int nblk, int first) {
+  __shared__ double sh[40];
+  if (st->done) return;
+  const double bcg = first ? 0.0 : reduce_partials(part_rz, nblk, sh) / st->rz;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 zq = z[q], pp = p[q];
+    p[q] = make_double2(zq.x + bcg * pp.x, zq.y + bcg * pp.y);
+  }
+}
+
+template <int D>
+static efgp_status enqueue_pcg_iteration(efgp_plan *pl, cudaStream_t s, CGState *st, int64_t box, int64_t Ld,
+                                         unsigned nb, unsigned nbox) {
+  const Params &P = pl->P;
+  double *part_pAp = pl->partials, *part_rr = pl->partials + pl->cg_blocks, *part_rz = pl->partials + 2 * pl->cg_blocks;
+  EFGP_CUFFT(cufftExecZ2D(pl->plan_c2r_L, pl->Xbox, pl->Yr));
+  k_mul<<<nblocks(Ld, pl->num_sms), kCGThreads, 0, s>>>(pl->Yr, pl->vhat, Ld, st);
+  EFGP_CUFFT(cufftExecD2Z(pl->plan_r2c_L, pl->Yr, pl->Zbox));
+  k_cg_apply<D><<<nb, kCGThreads, 0, s>>>(pl->Zbox, pl->p, pl->D_half, pl->Ap, P.Mh, (int)P.m, P.L, st, part_pAp);
+  k_cg_xr<<<nb, kCGThreads, 0, s>>>(pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp, part_rr, (int)nb,
+                                    part_rz);
+  k_pcg_check<<<1, kCGThreads, 0, s>>>(st, part_rr, (int)nb, pl->hist);
+  EFGP_TRY(precond_apply(pl, pl->r, pl->z, &st->done, s));
+  k_pcg_dot<<<nb, kCGThreads, 0, s>>>(pl->r, pl->z, P.Mh, (int)P.m, st, part_rz);
+  k_pcg_p<<<nb, kCGThreads, 0, s>>>(pl->z, pl->p, P.Mh, st, part_rz, (int)nb, 0);
+  k_cg_pad<D><<<nbox, kCGThreads, 0, s>>>(pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box, st);
+  EFGP_CUDA(cudaGetLastError());
+  return EFGP_OK;
+}
+
+template <int D>
+static efgp_status pcg_solve_d(efgp_plan *pl, int64_t N_total) {
+  const Params &P = pl->P;
+  cudaStream_t s = pl->stream;
+  int64_t box = P.L / 2 + 1, Ld = P.L;
+  for (int k = 0; k < D - 1; ++k) {
+    box *= P.L;
+    Ld *= P.L;
+  }
+  const unsigned nb = nblocks(P.Mh, pl->num_sms);
+  const unsigned nbox = nblocks(box, pl->num_sms);
+  int64_t max_iter = P.max_iter_opt;
+  if (max_iter <= 0) {
+    const double Nd = (double)(N_total > 0 ? N_total : 1);
+    max_iter = (int64_t)std::ceil(std::log(1.0 / P.cg_tol) * std::sqrt(Nd) / (2.0 * P.sigma));
+    if (max_iter < 10) max_iter = 10;
+  }
+  pl->max_iter_used = max_iter;
+  EFGP_TRY(ensure_hist(pl, max_iter));
+  CGState *st = reinterpret_cast<CGState *>(pl->scal);
+  CGState init{};
+  init.tol = P.cg_tol;
+  init.sigma2 = P.sigma * P.sigma;
+  init.max_iter = max_iter;
+  double *part_rz = pl->partials + 2 * pl->cg_blocks;
+  EFGP_CUDA(cudaMemcpyAsync(st, &init, sizeof(CGState), cudaMemcpyHostToDevice, s));
+  k_cg_init<<<nb, kCGThreads, 0, s>>>(pl->b, pl->x, pl->r, pl->p, P.Mh, (int)P.m, pl->partials);
+  k_cg_init2<<<1, kCGThreads, 0, s>>>(st, pl->partials, (int)nb, pl->hist);
+  EFGP_TRY(precond_apply(pl, pl->r, pl->z, &st->done, s));          // z0 = M^-1 b
+  k_pcg_dot<<<nb, kCGThreads, 0, s>>>(pl->r, pl->z, P.Mh, (int)P.m, st, part_rz);
+  k_pcg_p<<<nb, kCGThreads, 0, s>>>(pl->z, pl->p, P.Mh, st, part_rz, (int)nb, 1);  // p0 = z0
+  k_cg_pad0<D><<<nbox, kCGThreads, 0, s>>>(pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box);
+  EFGP_CUDA(cudaGetLastError());
+  EFGP_CUFFT(cufftSetStream(pl->plan_c2r_L, s));
+  EFGP_CUFFT(cufftSetStream(pl->plan_r2c_L, s));
+  const int G = P.graph_iters;
+  if (!pl->pcg_exec || pl->pcg_exec_iters != G) {
+    if (pl->pcg_exec) cudaGraphExecDestroy(pl->pcg_exec);
+    pl->pcg_exec = nullptr;
+    cudaGraph_t graph;
+    EFGP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    for (int it = 0; it < G; ++it) {
+      efgp_status e = enqueue_pcg_iteration<D>(pl, s, st, box, Ld, nb, nbox);
+      if (e != EFGP_OK) {
+        cudaStreamEndCapture(s, &graph);
+        return e;
+      }
+    }
+    EFGP_CUDA(cudaStreamEndCapture(s, &graph));
+    EFGP_CUDA(cudaGraphInstantiate(&pl->pcg_exec, graph, 0));
+    cudaGraphDestroy(graph);
+    pl->pcg_exec_iters = G;
+  }
+  CGState host{};
+  for (;;) {
+    EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned, st, sizeof(CGState), cudaMemcpyDeviceToHost, s));
+    EFGP_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(&host, pl->h_pinned, sizeof(CGState));
+    if (host.done) break;
+    EFGP_CUDA(cudaGraphLaunch(pl->pcg_exec, s));
+  }
+  pl->iters = host.iter;
+  pl->rel_resid = host.bnorm > 0 ? std::sqrt(host.rr) / host.bnorm : 0.0;
+  return host.done == 2 ? EFGP_ERR_NOCONVERGE : EFGP_OK;
+}
+
+efgp_status pcg_solve(efgp_plan *pl, int64_t N_total) {
+  switch (pl->P.d) {
+    case 1: return pcg_solve_d<1>(pl, N_total);
+    case 2: return pcg_solve_d<2>(pl, N_total);
+    case 3: return pcg_solve_d<3>(pl, N_total);
   }
   return EFGP_ERR_INVALID;
 }

@@ -58,6 +58,7 @@ struct Params {
   EsPoly poly{};
   EsPolyF polyf{};
   EsPolyP polyp{};
+  int precond = 0;             // NEXT-4: 0 none (Alg a1's plain CG), 1 Kronecker (reading G12)
   int spread_mode = 0;         // SORTED precision: 0 fp64, 1 fp32 weights, 2 fp32 weights + round sums
   // SORTED spreading geometry (2D)
   int s_lo = 0, s_count = 0;   // start cells i0 in [s_lo, s_lo + s_count) per dim
@@ -170,6 +171,13 @@ struct efgp_plan {
   double2 *het_box = nullptr;
   double *het_grid = nullptr;
   cufftHandle plan_het = 0;
+  // NEXT-4 Kronecker preconditioner (precond.cu): eigenvectors/values of the d factors, work grids
+  double2 *pc_Q = nullptr, *pc_F0 = nullptr, *pc_F1 = nullptr, *pc_work = nullptr, *z = nullptr;
+  double *pc_lam = nullptr;
+  int *pc_info = nullptr;
+  void *pc_solver = nullptr;  // cusolverDnHandle_t
+  cudaGraphExec_t pcg_exec = nullptr;
+  int pcg_exec_iters = 0;
   int het_path = 0;  // 1: last heteroskedastic fit used the sorted fused product
   cufftHandle plan_het_r2c = 0;  // D2Z on n2 (sorted path), created lazily
   // stream-ordered temporaries (hetero staging and sort, host-input chunks) come from this pool; it
@@ -202,6 +210,10 @@ efgp_status type2_grid_on(efgp_plan *pl, const double2 *beta, int64_t n, const d
                           double2 *boxbuf, double *grid, cudaStream_t s);
 // cg.cu
 efgp_status cg_solve(efgp_plan *pl, int64_t N_total);
+efgp_status pcg_solve(efgp_plan *pl, int64_t N_total);  // NEXT-4
+// precond.cu (NEXT-4): build the Kronecker preconditioner from the fit's v; z = M^-1 r
+efgp_status precond_setup(efgp_plan *pl, const double *modes);
+efgp_status precond_apply(efgp_plan *pl, const double2 *r, double2 *z, const int *done, cudaStream_t s);
 typedef efgp_status (*CGOp)(efgp_plan *pl, const double2 *p, double2 *Ap, void *ctx);  // Ap = A p
 efgp_status cg_solve_op(efgp_plan *pl, int64_t max_iter, CGOp op, void *ctx);
 // interp.cu

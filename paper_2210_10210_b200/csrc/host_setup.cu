@@ -237,6 +237,8 @@ std::string validate_and_choose(Params &p, const efgp_options &opt) {
   if (opt.spread_weights != EFGP_WEIGHTS_FP64 && p.nufft_tol < 1e-6)
     return "fp32 spreading weights need nufft_tol >= 1e-6";
   p.spread_mode = opt.spread_weights;
+  if (opt.precond < 0 || opt.precond > 1) return "unknown precond";
+  p.precond = opt.precond;
   resolve_spread_method(p);
   return "";
 }

@@ -75,7 +75,8 @@ class EFGP:
     def __init__(self, kernel: str, ell: float, sigma: float, eps: float, d: int, nu: float = 0.0, *,
                  h: float | None = None, m: int | None = None, cg_tol: float | None = None,
                  max_iter: int | None = None, nufft_tol: float | None = None, matern_rescale: str = "A",
-                 spread: str = "auto", weights: str = "fp64", graph_iters: int | None = None, stream=None, device=None):
+                 spread: str = "auto", weights: str = "fp64", graph_iters: int | None = None, stream=None, device=None,
+                 precond: str | None = None):
         import torch
         self._lib = L.load()
         self._torch = torch
@@ -98,6 +99,7 @@ class EFGP:
         opt.matern_rescale = _RESCALE[matern_rescale]
         opt.spread_method = _SPREAD[spread]
         opt.spread_weights = {"fp64": 0, "fp32": 1, "mixed": 2}[weights]
+        opt.precond = {None: 0, "none": 0, "kron": 1}[precond]  # NEXT-4 (reading G12)
         if graph_iters is not None:
             opt.graph_iters = int(graph_iters)
         opt.stream = C.c_void_p(stream.cuda_stream)
