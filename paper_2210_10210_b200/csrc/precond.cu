@@ -11,9 +11,10 @@
 // on the full (2m+1)^d grid: expand the Hermitian half, d axis passes with Q^*, a diagonal scale, d
 // axis passes with Q, extract the half (M maps Hermitian-symmetric vectors to Hermitian-symmetric
 // vectors: T(v)_{-p,-q} = conj T(v)_{p,q}, D even).  Each axis pass is a small dense contraction
-// ((2m+1) terms per output, <= 0.1 GFLOP for c4) done by a thread per output element.
+// ((2m+1) terms per output, <= 0.1 GFLOP for c4) done by a warp per output element.
 #include <cusolverDn.h>
 
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstring>
@@ -80,30 +81,34 @@ __global__ void k_pc_extract(const double2 *__restrict__ full, int m, double2 *_
   }
 }
 
-// out[.., j, ..] = sum_k Op[j, k] in[.., k, ..] along one axis (stride = n^(d-1-axis)).
+// out[.., j, ..] = sum_k Op[j, k] in[.., k, ..] along one axis (stride = n^(d-1-axis)), one warp per
+// output element (lanes split the k sum, shuffle reduction): the sums are short ((2m+1) terms) and a
+// thread-per-output loop is a chain of dependent L2 loads (20 us per pass on c3).
 // V holds the eigenvectors column-major (V[k n + p] = Q_{p k}).  ADJ: Op = Q^* (Op[j,k] = conj Q_{k j});
 // otherwise Op = Q.
 template <bool ADJ>
 __global__ void k_pc_axis(const double2 *__restrict__ in, double2 *__restrict__ out, const double2 *__restrict__ V,
                           int n, int64_t stride, int64_t total, const int *__restrict__ done) {
   if (done && *done) return;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t idx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; idx < total;
+       idx += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int j = (int)((idx / stride) % n);
     const int64_t base = idx - (int64_t)j * stride;
     double re = 0.0, im = 0.0;
-    for (int k = 0; k < n; ++k) {
+    for (int k = lane; k < n; k += 32) {
       const double2 q = ADJ ? V[(int64_t)j * n + k] : V[(int64_t)k * n + j];
       const double2 z = in[base + (int64_t)k * stride];
-      if (ADJ) {  // conj(q) z
-        re = fma(q.x, z.x, fma(q.y, z.y, re));
-        im = fma(q.x, z.y, fma(-q.y, z.x, im));
-      } else {
-        re = fma(q.x, z.x, fma(-q.y, z.y, re));
-        im = fma(q.x, z.y, fma(q.y, z.x, im));
-      }
+      const double qy = ADJ ? -q.y : q.y;  // conj(q) z or q z
+      re = fma(q.x, z.x, fma(-qy, z.y, re));
+      im = fma(q.x, z.y, fma(qy, z.x, im));
     }
-    out[idx] = make_double2(re, im);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      re += __shfl_xor_sync(0xffffffffu, re, o);
+      im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    if (lane == 0) out[idx] = make_double2(re, im);
   }
 }
 
@@ -126,6 +131,7 @@ __global__ void k_pc_scale(double2 *__restrict__ z, const double *__restrict__ l
     z[idx] = make_double2(v.x * s, v.y * s);
   }
 }
+
 
 static unsigned pc_grid(int64_t n, int sms) {
   int64_t b = (n + 255) / 256;
@@ -225,19 +231,20 @@ static efgp_status precond_apply_d(efgp_plan *pl, const double2 *r, double2 *z, 
   const int m = (int)P.m, n = 2 * m + 1;
   const int64_t total = ipow_(n, D);
   const unsigned g = pc_grid(total, pl->num_sms);
+  const unsigned gw = (unsigned)std::min<int64_t>((total * 32 + 255) / 256, (int64_t)pl->num_sms * 8);
   double2 *a = pl->pc_F0, *b = pl->pc_F1;
   k_pc_expand<D><<<g, 256, 0, s>>>(r, m, a, total, done);
   int64_t stride = total;
   for (int i = 0; i < D; ++i) {
     stride /= n;
-    k_pc_axis<true><<<g, 256, 0, s>>>(a, b, pl->pc_Q + (size_t)i * n * n, n, stride, total, done);
+    k_pc_axis<true><<<gw, 256, 0, s>>>(a, b, pl->pc_Q + (size_t)i * n * n, n, stride, total, done);
     std::swap(a, b);
   }
   k_pc_scale<D><<<g, 256, 0, s>>>(a, pl->pc_lam, n, P.sigma * P.sigma, total, done);
   stride = total;
   for (int i = 0; i < D; ++i) {
     stride /= n;
-    k_pc_axis<false><<<g, 256, 0, s>>>(a, b, pl->pc_Q + (size_t)i * n * n, n, stride, total, done);
+    k_pc_axis<false><<<gw, 256, 0, s>>>(a, b, pl->pc_Q + (size_t)i * n * n, n, stride, total, done);
     std::swap(a, b);
   }
   k_pc_extract<D><<<pc_grid(P.Mh, pl->num_sms), 256, 0, s>>>(a, m, z, P.Mh, done);
