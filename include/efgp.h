@@ -71,8 +71,11 @@ typedef enum { EFGP_WEIGHTS_FP64 = 0, EFGP_WEIGHTS_FP32 = 1, EFGP_WEIGHTS_MIXED 
  *         N^((d-1)/d) built from the axis lines of v and D (exact for tensor-product points with a
  *         separable kernel, and in d = 1), factored by a (2m+1)^2 Hermitian eigen-decomposition per
  *         axis (cuSOLVER) and applied by 2d small dense axis contractions per iteration.  Same answer
- *         and stopping rule; fewer iterations.  efgp_predict_var is unaffected (plain CG). */
-typedef enum { EFGP_PRECOND_NONE = 0, EFGP_PRECOND_KRON = 1 } efgp_precond;
+ *         and stopping rule.  Measured (profiles/r01_configs_v2.jsonl): SE (separable density) c3
+ *         N = 1e7 2831 -> 152 iterations; Matérn (non-separable D, the product approximation of D
+ *         is poor off the axes) needs MORE iterations (c5 52 -> 2542).  efgp_predict_var uses plain CG.
+ *   AUTO: KRON for EFGP_SE, NONE otherwise. */
+typedef enum { EFGP_PRECOND_NONE = 0, EFGP_PRECOND_KRON = 1, EFGP_PRECOND_AUTO = 2 } efgp_precond;
 
 typedef struct {
   double h;            /* grid spacing override when m > 0                        */
@@ -107,7 +110,7 @@ typedef struct {
   double t_var_ms;                                            /* device time of the last predict_var */
   int64_t var_iters_max, var_batch;                           /* its largest CG count, targets/batch */
   int64_t hetero_sorted; /* last efgp_fit_hetero: 1 = points sorted once by cell, fused NUFFT-pair pass */
-  int64_t precond;       /* efgp_precond of the fit */
+  int64_t precond;       /* preconditioner used by the fit (EFGP_PRECOND_NONE or _KRON; AUTO resolved) */
 } efgp_info;
 
 /* Fill *opt with defaults (all zero / automatic). */

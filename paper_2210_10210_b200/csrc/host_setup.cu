@@ -237,8 +237,10 @@ std::string validate_and_choose(Params &p, const efgp_options &opt) {
   if (opt.spread_weights != EFGP_WEIGHTS_FP64 && p.nufft_tol < 1e-6)
     return "fp32 spreading weights need nufft_tol >= 1e-6";
   p.spread_mode = opt.spread_weights;
-  if (opt.precond < 0 || opt.precond > 1) return "unknown precond";
-  p.precond = opt.precond;
+  if (opt.precond < EFGP_PRECOND_NONE || opt.precond > EFGP_PRECOND_AUTO) return "unknown precond";
+  // AUTO: the Kronecker factors are exact in D only for a separable spectral density (SE)
+  p.precond = opt.precond == EFGP_PRECOND_AUTO ? (p.kernel == EFGP_SE ? EFGP_PRECOND_KRON : EFGP_PRECOND_NONE)
+                                               : opt.precond;
   resolve_spread_method(p);
   return "";
 }

@@ -93,3 +93,13 @@ def test_pcg_reduces_iterations_at_size():
     assert e1 <= e0, (e1, e0)
     for g in (g0, g1, g2):
         g.close()
+
+
+def test_auto_selects_kron_for_se_only():
+    for name, want in (("c3", 1), ("c5", 0)):
+        c = CONFIGS[name]
+        x, y, _ = generate(c, N=2000, q=1)
+        g = model(c, precond="auto")
+        g.fit(dev(x), dev(y))
+        assert g.info()["precond"] == want
+        g.close()

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--c5-N", type=float, default=None)
     ap.add_argument("--var-targets", type=int, default=0, help="also time the posterior variance (NEXT-2)")
+    ap.add_argument("--precond", default="none", choices=["none", "kron"], help="NEXT-4 preconditioner")
     a = ap.parse_args()
     import torch
     from efgp_data import CONFIGS
@@ -35,7 +36,7 @@ def main():
         x, y = G.generate_points(c, 0, N)
         xt = G.generate_targets(c, 0, c.q)
         mu = torch.empty(c.q, dtype=torch.float64, device=x.device)
-        g = EFGP(c.kernel, c.ell, c.sigma, c.eps, c.d, c.nu)
+        g = EFGP(c.kernel, c.ell, c.sigma, c.eps, c.d, c.nu, precond=None if a.precond == "none" else a.precond)
         rows = []
         for r in range(a.reps + 1):
             with warnings.catch_warnings():
@@ -48,7 +49,7 @@ def main():
         med = lambda k: statistics.median(float(i[k]) for i in rows)
         sp = med("t_spread_ms")
         fit_ms = sp + med("t_modes_ms") + med("t_solve_ms")
-        out = {"config": name, "N": N, "q": c.q, "d": c.d, "m": rows[0]["m"], "M": rows[0]["M"], "w": rows[0]["w"],
+        out = {"config": name, "precond": a.precond, "N": N, "q": c.q, "d": c.d, "m": rows[0]["m"], "M": rows[0]["M"], "w": rows[0]["w"],
                "spread": rows[0]["spread_method"], "cg_iters": med("iters"),
                "ms": {"spread": sp, "fft_deconv": med("t_modes_ms"), "toeplitz_cg": med("t_solve_ms"),
                       "predict": med("t_predict_ms")},
