@@ -53,7 +53,10 @@ typedef enum {
 typedef enum { EFGP_RESCALE_NONE = 0, EFGP_RESCALE_L2 = 1, EFGP_RESCALE_PRINTED = 2 } efgp_rescale;
 
 /* Spreading strategy for the type-1 step. AUTO picks the fastest valid one. */
-typedef enum { EFGP_SPREAD_AUTO = 0, EFGP_SPREAD_GLOBAL = 1, EFGP_SPREAD_SMEM = 2, EFGP_SPREAD_SORTED = 3 } efgp_spread_method;
+typedef enum {
+  EFGP_SPREAD_AUTO = 0, EFGP_SPREAD_GLOBAL = 1, EFGP_SPREAD_SMEM = 2, EFGP_SPREAD_SORTED = 3,
+  EFGP_SPREAD_CELLSORT = 4 /* counting sort by (super-)cell + warp-per-run accumulation (2D W >= 7, 3D) */
+} efgp_spread_method;
 
 /* Arithmetic of the SORTED spreader (DESIGN.md §7 "K1 precision").  FFTs, CG, deconvolution, the
  * fine grids and all outputs are fp64 in every mode.

@@ -201,6 +201,12 @@ efgp_status spread_points(efgp_plan *pl, const double *x, const double *y, int64
 efgp_status spread_begin(efgp_plan *pl, cudaStream_t s);
 efgp_status spread_end(efgp_plan *pl, cudaStream_t s);
 efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s);
+// spread_cellsort.cu: K1 CELLSORT (2D any W, 3D W <= 6); EFGP_ERR_RESOURCE if not applicable
+efgp_status spread_cellsort(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s);
+bool cellsort_geometry(const Params &p, int &lo, int &S, int &ncell);
+// hetero.cu: counting-sort offset kernels (shared with CELLSORT)
+__global__ void k_het_colscan(unsigned *__restrict__ hist, int nblk, int ncell, long long *__restrict__ tot);
+__global__ void k_het_offsets(const long long *__restrict__ tot, int ncell, long long *__restrict__ off);
 // modes.cu
 efgp_status type1_modes(efgp_plan *pl, double *modes_out, cudaStream_t s);
 efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s);

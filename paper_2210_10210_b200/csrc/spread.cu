@@ -12,6 +12,8 @@
 //   SMEM  : one CTA per SM keeps a private copy of the *occupied* part of both grids (cells reachable
 //           from x in [0,1]^d) in shared memory, CAS-accumulates, flushes once with RED.
 //   SORTED: d = 2, W <= 6, bin-sorted register accumulation (spread_sorted.cu).
+//   CELLSORT: d = 2 (any W) or 3 (W <= 6): counting sort by (super-)cell, warp-per-run accumulation
+//           with shared-memory weight rows (spread_cellsort.cu).
 // Every thread also validates its point (x in [0,1]^d, finite y) and raises dflags[0] otherwise.
 #include <cstdio>
 
@@ -208,11 +210,16 @@ void resolve_spread_method(Params &p) {
   // SORTED: 2D, register windows up to 6 x 6, start-cell lookup tables up to 2048 per dimension
   const bool sorted_ok = p.d == 2 && p.w <= 6 && p.h * p.n1 + p.w < 2048 && !p.sorted_disabled;
   const bool smem_ok = smem_bytes(p) <= 200 * 1024;
-  if (m == EFGP_SPREAD_AUTO) m = sorted_ok ? EFGP_SPREAD_SORTED : (smem_ok ? EFGP_SPREAD_SMEM : EFGP_SPREAD_GLOBAL);
-  if (m == EFGP_SPREAD_SORTED && !sorted_ok) m = smem_ok ? EFGP_SPREAD_SMEM : EFGP_SPREAD_GLOBAL;
+  int lo, S, ncell;
+  const bool cellsort_ok = cellsort_geometry(p, lo, S, ncell);
+  const int fallback = cellsort_ok ? EFGP_SPREAD_CELLSORT : (smem_ok ? EFGP_SPREAD_SMEM : EFGP_SPREAD_GLOBAL);
+  if (m == EFGP_SPREAD_AUTO) m = sorted_ok ? EFGP_SPREAD_SORTED : fallback;
+  if (m == EFGP_SPREAD_SORTED && !sorted_ok) m = fallback;
+  if (m == EFGP_SPREAD_CELLSORT && !cellsort_ok) m = smem_ok ? EFGP_SPREAD_SMEM : EFGP_SPREAD_GLOBAL;
   if (m == EFGP_SPREAD_SMEM && !smem_ok) m = EFGP_SPREAD_GLOBAL;
   p.spread_method = m;
-  p.n_rhs = (m == EFGP_SPREAD_SORTED) ? p.n1 : p.n2;
+  // SORTED and CELLSORT spread both strengths onto the n1 grid (psi1 covers |j| <= 2m >= m)
+  p.n_rhs = (m == EFGP_SPREAD_SORTED || m == EFGP_SPREAD_CELLSORT) ? p.n1 : p.n2;
 }
 
 template <int D, int W>
@@ -275,6 +282,11 @@ efgp_status spread_points(efgp_plan *pl, const double *x, const double *y, int64
       if (st != EFGP_ERR_RESOURCE) return st;
       pl->err.clear();  // co-residency not available now: same grids, direct spreading below
     }
+    method = EFGP_SPREAD_GLOBAL;
+  } else if (method == EFGP_SPREAD_CELLSORT) {
+    const efgp_status st = spread_cellsort(pl, x, y, N, s);
+    if (st != EFGP_ERR_RESOURCE) return st;
+    pl->err.clear();  // (N >= 2^32 in one call): same grids, direct spreading below
     method = EFGP_SPREAD_GLOBAL;
   }
   switch (pl->P.d) {

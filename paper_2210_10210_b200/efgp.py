@@ -16,7 +16,7 @@ from . import _lib as L
 
 _KERNELS = {"se": 0, "matern": 1}
 _RESCALE = {"B": 0, "none": 0, "A": 1, "l2": 1, "P": 2, "printed": 2}
-_SPREAD = {"auto": 0, "global": 1, "smem": 2, "sorted": 3}
+_SPREAD = {"auto": 0, "global": 1, "smem": 2, "sorted": 3, "cellsort": 4}
 SPREAD_NAMES = {v: k for k, v in _SPREAD.items()}
 
 

@@ -75,6 +75,47 @@ def test_spread_strategies_agree():
     assert rel(out["sorted"][1], out["global"][1]) < 2 * c.eps / 10
 
 
+@pytest.mark.parametrize("name,N", [("c3", 100_003), ("c4", 60_001), ("c5", 77_777), ("c2", 50_000)])
+def test_cellsort_matches_global(name, N):
+    # CELLSORT (counting sort by (super-)cell, warp-per-run accumulation) against GLOBAL: same kernel
+    # weights and grid for v (roundoff only); y on the n1 grid (as SORTED) vs n2: NUFFT tolerance.
+    # Ragged N (not a multiple of any run or CTA size); 3D uses 4^3 super-cells.
+    c = CONFIGS[name]
+    x, y, _ = generate(c, N=N, q=1)
+    kw = {}
+    if name in ("c2", "c4"):
+        h0, _ = O.choose_params(c.kernel, c.ell, c.d, c.eps, c.nu)
+        kw = dict(h=h0, m={"c2": 20, "c4": 8}[name])
+    out = {}
+    for method in ("global", "cellsort"):
+        g = model(c, max_iter=1, spread=method, **kw)
+        with pytest.warns(RuntimeWarning):
+            g.fit(dev(x), dev(y))
+        assert g.info()["spread_method"] == method
+        out[method] = (g.vector("v"), g.vector("rhs"), g.info()["nufft_tol"])
+        g.close()
+    assert rel(out["cellsort"][0], out["global"][0]) < 1e-12
+    assert rel(out["cellsort"][1], out["global"][1]) < 2 * out["global"][2]
+
+
+def test_cellsort_auto_and_invalid_input():
+    from paper_2210_10210_b200 import EFGPError
+    c = CONFIGS["c3"]                                # 2D, W = 8: beyond the SORTED register windows
+    x, y, _ = generate(c, N=5000, q=1)
+    g = model(c)
+    g.fit(dev(x), dev(y))
+    assert g.info()["spread_method"] == "cellsort"
+    xb = x.copy()
+    xb[4321, 0] = -0.25
+    with pytest.raises(EFGPError, match="INVALID"):
+        g.fit(dev(xb), dev(y))
+    yb = y.copy()
+    yb[17] = np.nan
+    with pytest.raises(EFGPError, match="INVALID"):
+        g.fit(dev(x), dev(yb))
+    g.close()
+
+
 @pytest.mark.parametrize("weights", ["fp32", "mixed"])
 @pytest.mark.parametrize("name", ["c2", "c5"])
 def test_type1_fp32_weights(name, weights):
