@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <cufft.h>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -204,6 +205,14 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
 // spread_cellsort.cu: K1 CELLSORT (2D any W, 3D W <= 6); EFGP_ERR_RESOURCE if not applicable
 efgp_status spread_cellsort(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s);
 bool cellsort_geometry(const Params &p, int &lo, int &S, int &ncell);
+// CTAs of the counting-sort kernels (count and scatter share the partition): one per SM.  Fewer CTAs
+// keep fewer partially written 32-byte sectors open in L2 (the c3 scatter reads 4x and writes 3.5x
+// its algorithmic bytes), but measured: 148 -> 17 CTAs made c3 slower (2.1 -> 2.8 ms) and the hetero
+// sort 132 -> 119 ms only (profiles/r01_SUMMARY.md).  EFGP_SORT_CTAS overrides.
+inline int sort_ctas(int num_sms) {
+  const char *e = getenv("EFGP_SORT_CTAS");
+  return (e && atoi(e) > 0) ? atoi(e) : num_sms;
+}
 // hetero.cu: counting-sort offset kernels (shared with CELLSORT)
 __global__ void k_het_colscan(unsigned *__restrict__ hist, int nblk, int ncell, long long *__restrict__ tot);
 __global__ void k_het_offsets(const long long *__restrict__ tot, int ncell, long long *__restrict__ off);

@@ -398,7 +398,7 @@ bool het_sorted_geometry(const Params &P, HetSorted &H) {
 template <int D, int W>
 efgp_status het_sort_t(efgp_plan *pl, HetSorted &H, const double *x, const double *sd, int64_t N, cudaStream_t s) {
   const Params &P = pl->P;
-  const int B = pl->num_sms, T = 1024, n = (int)P.n2;
+  const int B = sort_ctas(pl->num_sms), T = 1024, n = (int)P.n2;
   unsigned *hist = nullptr;
   long long *tot = nullptr, *off = nullptr;
   EFGP_PALLOC(&hist, sizeof(unsigned) * B * H.ncell, s);

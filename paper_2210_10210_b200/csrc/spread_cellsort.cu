@@ -203,7 +203,7 @@ static efgp_status cellsort_t(efgp_plan *pl, const double *x, const double *y, i
   const Params &P = pl->P;
   int lo, S, ncell;
   if (!cellsort_geometry(P, lo, S, ncell)) return EFGP_ERR_RESOURCE;
-  const int B = pl->num_sms, T = 1024, n = (int)P.n1;
+  const int B = sort_ctas(pl->num_sms), T = 1024, n = (int)P.n1;
   unsigned *hist = nullptr;
   long long *tot = nullptr, *off = nullptr;
   double *xs = nullptr, *ys = nullptr;
