@@ -162,6 +162,8 @@ struct efgp_plan {
   cufftHandle plan_var_c2r = 0, plan_var_r2c = 0;
   cudaGraphExec_t var_exec = nullptr;
   int var_exec_max_iter = 0;
+  int var_exec_pc = 0;  // the captured variance graph uses the preconditioned step
+  bool var_pc = false;  // last predict_var used the Kronecker preconditioner
   int var_iters_max = 0;
   bool op_valid = false;  // the Toeplitz operator (vhat) of a fit is in place
   double t_var = 0;

@@ -25,6 +25,7 @@ constexpr int kVarMaxM = 256;  // per-dimension phasor tables in shared memory (
 struct VarTarget {
   double rr, bnorm;
   int iters, done;
+  double rz;  // PCG (NEXT-4 preconditioner): (r, z)
 };
 
 __device__ __forceinline__ double vblock_sum(double v, double *sh) {
@@ -109,14 +110,111 @@ __device__ void pad_target(const double2 *__restrict__ p, const double *__restri
   }
 }
 
-// rhs = sigma^2 conj(phi(x*)) = sigma^2 D_j e^{-2 pi i h j.x*}; x = 0; r = p = rhs; first C2R input
+
+// NEXT-4 inside one CTA (the CTA of one target): z = M^-1 r with the Kronecker factors of the fit
+// (precond.cu, reading G12) staged in shared memory: expand the half, d passes with Q^*, scale, d
+// passes with Q, extract; every thread carries up to 4 outputs per pass (independent FMA chains).
+// smem: Q (d n^2) | A | B (n^d each), double2.
 template <int D>
+__device__ void pc_apply_cta(const double2 *__restrict__ r, double2 *__restrict__ z, int m, double2 *Q, double2 *A,
+                             double2 *Bf, const double *__restrict__ lam, double sigma2, int64_t Mh) {
+  const int n = 2 * m + 1;
+  const int total = D == 1 ? n : n * n;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    int j[D];
+    int rem = idx;
+#pragma unroll
+    for (int k = D - 1; k >= 0; --k) {
+      j[k] = rem % n - m;
+      rem /= n;
+    }
+    const bool neg = j[D - 1] < 0;
+    if (neg) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) j[k] = -j[k];
+    }
+    int64_t q = j[D - 1];
+    if (D == 2) q += (int64_t)(j[0] + m) * (m + 1);
+    const double2 v = r[q];
+    A[idx] = neg ? make_double2(v.x, -v.y) : v;
+  }
+  __syncthreads();
+  double2 *a = A, *b = Bf;
+  for (int phase = 0; phase < 2; ++phase) {
+    int stride = total;
+    for (int ax = 0; ax < D; ++ax) {
+      stride /= n;
+      const double2 *V = Q + ax * n * n;
+      const bool adj = phase == 0;
+      for (int base0 = 0; base0 < total; base0 += 4 * blockDim.x) {
+        int jj[4], bb[4];
+        double re[4], im[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int idx = base0 + threadIdx.x + t * blockDim.x;
+          const int ic = idx < total ? idx : 0;
+          jj[t] = (ic / stride) % n;
+          bb[t] = ic - jj[t] * stride;
+          re[t] = im[t] = 0.0;
+        }
+        for (int k = 0; k < n; ++k) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const double2 qv = adj ? V[jj[t] * n + k] : V[k * n + jj[t]];
+            const double2 av = a[bb[t] + k * stride];
+            const double qy = adj ? -qv.y : qv.y;
+            re[t] = fma(qv.x, av.x, fma(-qy, av.y, re[t]));
+            im[t] = fma(qv.x, av.y, fma(qy, av.x, im[t]));
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int idx = base0 + threadIdx.x + t * blockDim.x;
+          if (idx < total) b[idx] = make_double2(re[t], im[t]);
+        }
+      }
+      __syncthreads();
+      double2 *tmp = a;
+      a = b;
+      b = tmp;
+    }
+    if (phase == 0) {
+      for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+        double pr = lam[(D - 1) * n + idx % n];
+        if (D == 2) pr *= lam[idx / n];
+        const double sc = 1.0 / (pr + sigma2);
+        a[idx] = make_double2(a[idx].x * sc, a[idx].y * sc);
+      }
+      __syncthreads();
+    }
+  }
+  for (int64_t q = threadIdx.x; q < Mh; q += blockDim.x) {
+    int j[D];
+    half_modes<D>(q, m, j);
+    int idx = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) idx = idx * n + (j[k] + m);
+    z[q] = a[idx];
+  }
+  __syncthreads();
+}
+
+// stage the d factors into shared memory
+template <int D>
+__device__ __forceinline__ void pc_load_q(const double2 *__restrict__ Qg, int m, double2 *Q) {
+  const int n = 2 * m + 1;
+  for (int i = threadIdx.x; i < D * n * n; i += blockDim.x) Q[i] = Qg[i];
+}
+
+// rhs = sigma^2 conj(phi(x*)) = sigma^2 D_j e^{-2 pi i h j.x*}; x = 0; r = p = rhs; first C2R input
+template <int D, bool PC>
 __global__ void __launch_bounds__(kVarThreads) k_var_init(const double *__restrict__ xt, int nt, double h, int m,
                                                           double sigma2, const double *__restrict__ Dh, int64_t Mh,
                                                           int64_t L, int64_t box, double2 *__restrict__ vx,
                                                           double2 *__restrict__ vr, double2 *__restrict__ vp,
                                                           double2 *__restrict__ X, VarTarget *__restrict__ st,
-                                                          unsigned *__restrict__ ndone, int *__restrict__ err) {
+                                                          unsigned *__restrict__ ndone, int *__restrict__ err,
+                                                          const double2 *__restrict__ pcQ, const double *__restrict__ pcl) {
   extern __shared__ double2 E[];
   __shared__ double sh[40];
   const int t = blockIdx.x;
@@ -150,8 +248,24 @@ __global__ void __launch_bounds__(kVarThreads) k_var_init(const double *__restri
   }
   const double rr = vblock_sum(acc, sh);
   __syncthreads();
+  double rz = rr;
+  if constexpr (PC) {  // p0 = z0 = M^-1 r0
+    const int n = 2 * m + 1, total = D == 1 ? n : n * n;
+    double2 *Q = E + D * n, *A = Q + D * n * n, *Bf = A + total;
+    pc_load_q<D>(pcQ, m, Q);
+    __syncthreads();
+    pc_apply_cta<D>(r, p, m, Q, A, Bf, pcl, sigma2, Mh);
+    acc = 0.0;
+    for (int64_t q = threadIdx.x; q < Mh; q += blockDim.x) {
+      const double2 a = r[q], z = p[q];
+      acc += ((q % (m + 1)) ? 2.0 : 1.0) * (a.x * z.x + a.y * z.y);
+    }
+    rz = vblock_sum(acc, sh);
+    __syncthreads();
+  }
   pad_target<D>(p, Dh, m, L, X + (int64_t)t * box, box);
   if (threadIdx.x == 0) {
+    st[t].rz = rz;
     st[t].rr = rr;
     st[t].bnorm = sqrt(rr);
     st[t].iters = 0;
@@ -167,19 +281,22 @@ __global__ void k_var_mul(double *__restrict__ Y, const double *__restrict__ vha
 }
 
 // one CG iteration of one target (CTA = target)
-template <int D>
+template <int D, bool PC>
 __global__ void __launch_bounds__(kVarThreads) k_var_step(const double2 *__restrict__ Zall, const double *__restrict__ Dh,
                                                           int64_t Mh, int m, int64_t L, int64_t box, double sigma2,
                                                           double tol, int max_iter, double2 *__restrict__ vx,
                                                           double2 *__restrict__ vr, double2 *__restrict__ vp,
                                                           double2 *__restrict__ vAp, double2 *__restrict__ X,
-                                                          VarTarget *__restrict__ st, unsigned *__restrict__ ndone) {
+                                                          VarTarget *__restrict__ st, unsigned *__restrict__ ndone,
+                                                          const double2 *__restrict__ pcQ, const double *__restrict__ pcl) {
+  extern __shared__ double2 pcsm[];  // PC: Q | A | B
   __shared__ double sh[40];
   const int t = blockIdx.x;
   if (st[t].done) return;
   const double2 *Z = Zall + (int64_t)t * box;
   double2 *x = vx + (int64_t)t * Mh, *r = vr + (int64_t)t * Mh, *p = vp + (int64_t)t * Mh, *Ap = vAp + (int64_t)t * Mh;
   const double rr = st[t].rr;
+  const double num = PC ? st[t].rz : rr;  // alpha = (r, z) / (p, Ap); plain CG: z = r
   double acc = 0.0;
   for (int64_t q = threadIdx.x; q < Mh; q += blockDim.x) {
     int j[D];
@@ -196,7 +313,7 @@ __global__ void __launch_bounds__(kVarThreads) k_var_step(const double2 *__restr
     Ap[q] = a;
     acc += (j[D - 1] ? 2.0 : 1.0) * (pp.x * a.x + pp.y * a.y);
   }
-  const double alpha = rr / vblock_sum(acc, sh);
+  const double alpha = num / vblock_sum(acc, sh);
   acc = 0.0;
   for (int64_t q = threadIdx.x; q < Mh; q += blockDim.x) {
     const double2 pp = p[q], a = Ap[q];
@@ -210,18 +327,42 @@ __global__ void __launch_bounds__(kVarThreads) k_var_step(const double2 *__restr
     acc += ((q % (m + 1)) ? 2.0 : 1.0) * (rq.x * rq.x + rq.y * rq.y);
   }
   const double rr_new = vblock_sum(acc, sh);
-  const double bcg = rr_new / rr;
-  for (int64_t q = threadIdx.x; q < Mh; q += blockDim.x) {
-    const double2 rq = r[q], pp = p[q];
-    p[q] = make_double2(rq.x + bcg * pp.x, rq.y + bcg * pp.y);
+  const int it = st[t].iters + 1;
+  const bool fin = sqrt(rr_new) <= tol * st[t].bnorm || it >= max_iter;
+  if constexpr (PC) {
+    if (!fin) {  // z = M^-1 r into the (now free) Ap buffer; p = z + ((r,z)_new / (r,z)) p
+      const int n = 2 * m + 1, total = D == 1 ? n : n * n;
+      double2 *Q = pcsm, *A = Q + D * n * n, *Bf = A + total;
+      __syncthreads();
+      pc_load_q<D>(pcQ, m, Q);
+      __syncthreads();
+      pc_apply_cta<D>(r, Ap, m, Q, A, Bf, pcl, sigma2, Mh);
+      acc = 0.0;
+      for (int64_t q = threadIdx.x; q < Mh; q += blockDim.x) {
+        const double2 a = r[q], z = Ap[q];
+        acc += ((q % (m + 1)) ? 2.0 : 1.0) * (a.x * z.x + a.y * z.y);
+      }
+      const double rz_new = vblock_sum(acc, sh);
+      const double bcg = rz_new / num;
+      for (int64_t q = threadIdx.x; q < Mh; q += blockDim.x) {
+        const double2 zq = Ap[q], pp = p[q];
+        p[q] = make_double2(zq.x + bcg * pp.x, zq.y + bcg * pp.y);
+      }
+      if (threadIdx.x == 0) st[t].rz = rz_new;
+    }
+  } else {
+    const double bcg = rr_new / rr;
+    for (int64_t q = threadIdx.x; q < Mh; q += blockDim.x) {
+      const double2 rq = r[q], pp = p[q];
+      p[q] = make_double2(rq.x + bcg * pp.x, rq.y + bcg * pp.y);
+    }
   }
   __syncthreads();
-  pad_target<D>(p, Dh, m, L, X + (int64_t)t * box, box);
+  if (!fin) pad_target<D>(p, Dh, m, L, X + (int64_t)t * box, box);
   if (threadIdx.x == 0) {
     st[t].rr = rr_new;
-    const int it = st[t].iters + 1;
     st[t].iters = it;
-    if (sqrt(rr_new) <= tol * st[t].bnorm || it >= max_iter) {
+    if (fin) {
       st[t].done = 1;
       atomicAdd(ndone, 1u);
     }
@@ -303,23 +444,47 @@ static efgp_status var_batch(efgp_plan *pl, const double *xt, int nt, double *ou
   unsigned *ndone = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(pl->var_st) + B * sizeof(VarTarget));
   const size_t esm = sizeof(double2) * D * (2 * P.m + 1);
   const double sigma2 = P.sigma * P.sigma;
+  // NEXT-4 in the variance CGs: the fit's Kronecker factors, applied per target inside its CTA
+  const int64_t n = 2 * P.m + 1, total = D == 1 ? n : n * n;
+  const size_t pcsm = sizeof(double2) * (D * n * n + 2 * total);
+  const bool pc = D <= 2 && P.precond == EFGP_PRECOND_KRON && pl->pc_Q && esm + pcsm <= 200 * 1024;
+  pl->var_pc = pc;
   EFGP_CUDA(cudaMemsetAsync(ndone, 0, sizeof(unsigned), s));
-  k_var_init<D><<<B, kVarThreads, esm, s>>>(xt, nt, P.h, (int)P.m, sigma2, pl->D_half, P.Mh, P.L, box, pl->var_x,
-                                            pl->var_r, pl->var_p, pl->var_X, st, ndone, pl->dflags);
+  if (pc) {
+    EFGP_CUDA(cudaFuncSetAttribute(k_var_init<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(esm + pcsm)));
+    EFGP_CUDA(cudaFuncSetAttribute(k_var_step<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcsm));
+    k_var_init<D, true><<<B, kVarThreads, esm + pcsm, s>>>(xt, nt, P.h, (int)P.m, sigma2, pl->D_half, P.Mh, P.L, box,
+                                                           pl->var_x, pl->var_r, pl->var_p, pl->var_X, st, ndone,
+                                                           pl->dflags, pl->pc_Q, pl->pc_lam);
+  } else {
+    k_var_init<D, false><<<B, kVarThreads, esm, s>>>(xt, nt, P.h, (int)P.m, sigma2, pl->D_half, P.Mh, P.L, box,
+                                                     pl->var_x, pl->var_r, pl->var_p, pl->var_X, st, ndone, pl->dflags,
+                                                     nullptr, nullptr);
+  }
   EFGP_CUDA(cudaGetLastError());
   EFGP_CUFFT(cufftSetStream(pl->plan_var_c2r, s));
   EFGP_CUFFT(cufftSetStream(pl->plan_var_r2c, s));
   const int max_iter = (int)std::min<int64_t>(pl->max_iter_used > 0 ? pl->max_iter_used : 1000, 1 << 30);
+  if (pl->var_exec && pl->var_exec_pc != (int)pc) {
+    cudaGraphExecDestroy(pl->var_exec);
+    pl->var_exec = nullptr;
+  }
   if (!pl->var_exec) {
+    pl->var_exec_pc = (int)pc;
     cudaGraph_t graph;
     EFGP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     for (int it = 0; it < P.graph_iters; ++it) {
       cufftExecZ2D(pl->plan_var_c2r, pl->var_X, pl->var_Y);
       k_var_mul<<<pl->num_sms * 4, 256, 0, s>>>(pl->var_Y, pl->vhat, Ld, Ld * B);
       cufftExecD2Z(pl->plan_var_r2c, pl->var_Y, pl->var_Z);
-      k_var_step<D><<<B, kVarThreads, 0, s>>>(pl->var_Z, pl->D_half, P.Mh, (int)P.m, P.L, box, sigma2, P.cg_tol,
-                                              max_iter, pl->var_x, pl->var_r, pl->var_p, pl->var_Ap, pl->var_X, st,
-                                              ndone);
+      if (pc)
+        k_var_step<D, true><<<B, kVarThreads, pcsm, s>>>(pl->var_Z, pl->D_half, P.Mh, (int)P.m, P.L, box, sigma2,
+                                                         P.cg_tol, max_iter, pl->var_x, pl->var_r, pl->var_p,
+                                                         pl->var_Ap, pl->var_X, st, ndone, pl->pc_Q, pl->pc_lam);
+      else
+        k_var_step<D, false><<<B, kVarThreads, 0, s>>>(pl->var_Z, pl->D_half, P.Mh, (int)P.m, P.L, box, sigma2,
+                                                       P.cg_tol, max_iter, pl->var_x, pl->var_r, pl->var_p,
+                                                       pl->var_Ap, pl->var_X, st, ndone, nullptr, nullptr);
     }
     const cudaError_t ce = cudaStreamEndCapture(s, &graph);
     if (ce != cudaSuccess) {

@@ -103,3 +103,40 @@ def test_auto_selects_kron_for_se_only():
         g.fit(dev(x), dev(y))
         assert g.info()["precond"] == want
         g.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_variance_with_kron_preconditioner(name, monkeypatch):
+    # NEXT-2 with NEXT-4: the per-target CGs preconditioned by the fit's Kronecker factors (inside each
+    # target's CTA).  Same variances as the oracle's plain per-target CG (parity mode).
+    c = CONFIGS[name]
+    x, y, _ = generate(c, N=3000, q=1)
+    xt = np.random.default_rng(40 + c.id).uniform(0, 1, (37, c.d))
+    xt[0] = x[0]
+    cg_tol = c.eps / 1000
+    monkeypatch.setenv("EFGP_VAR_BATCH", "16")
+    g = model(c, cg_tol=cg_tol, precond="kron")
+    g.fit(dev(x), dev(y))
+    var = g.predict_var(dev(xt)).cpu().numpy()
+    fit = O.efgp_fit(x, y, c.kernel, c.ell, c.sigma, c.eps, nu=c.nu, cg_tol=cg_tol)
+    ref = O.posterior_variance(fit, xt, cg_tol=cg_tol)
+    assert rel(var, ref) <= 10 * c.eps, (rel(var, ref), 10 * c.eps)
+    if name == "c1":
+        assert g.info()["var_iters_max"] <= 2                      # d = 1: M is the system matrix
+    g.close()
+
+
+def test_variance_kron_reduces_iterations_at_size():
+    # c3 at N = 1e5 (device generator): preconditioned vs plain batched CG, both to eps/100
+    from efgp_data import gpu as G
+    c = CONFIGS["c3"]
+    x, y = G.generate_points(c, 0, 100_000)
+    xt = G.generate_targets(c, 0, 48)
+    out = {}
+    for pc in (None, "kron"):
+        g = model(c, cg_tol=c.eps / 100, precond=pc)
+        g.fit(x, y)
+        out[pc] = (g.predict_var(xt).cpu().numpy(), g.info()["var_iters_max"])
+        g.close()
+    assert rel(out["kron"][0], out[None][0]) <= 10 * c.eps
+    assert out["kron"][1] < out[None][1] / 2, (out["kron"][1], out[None][1])
