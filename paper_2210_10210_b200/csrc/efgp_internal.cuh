@@ -290,11 +290,18 @@ __device__ __forceinline__ double es_kernel(double z, double beta) {
 // is even, so piece W-1-a is piece a mirrored, p_{W-1-a}(s) = p_a(-s) (es_poly_fit builds them so):
 // with p_a = E_a(s^2) + s O_a(s^2), one even and one odd Horner in s^2 give both weights, half the
 // FMAs of W separate Horner evaluations.
+// Reduced coordinate of es_weights: i0 = ceil(t - W/2) (returned) and s = 2 (i0 - (t - W/2)) - 1.
 template <int W>
-__device__ __forceinline__ int es_weights(double t, const EsPoly &P, double (&w)[W]) {
+__device__ __forceinline__ int es_reduce(double t, double &s) {
   const double tm = __dsub_rn(t, 0.5 * W);  // no FMA contraction: the SORTED binning must agree
   const double i0 = ceil(tm);
-  const double s = 2.0 * (i0 - tm) - 1.0;
+  s = 2.0 * (i0 - tm) - 1.0;
+  return (int)i0;
+}
+
+// The W weights from the reduced coordinate s (es_weights = es_reduce + es_weights_s).
+template <int W>
+__device__ __forceinline__ void es_weights_s(double s, const EsPoly &P, double (&w)[W]) {
   const double s2 = s * s;
   constexpr int D = es_degree(W);
   constexpr int DE = D & ~1, DO = (D & 1) ? D : D - 1;  // highest even / odd power
@@ -314,7 +321,14 @@ __device__ __forceinline__ int es_weights(double t, const EsPoly &P, double (&w)
     for (int k = DE - 2; k >= 0; k -= 2) e = fma(e, s2, P.c[W / 2][k]);
     w[W / 2] = e;
   }
-  return (int)i0;
+}
+
+template <int W>
+__device__ __forceinline__ int es_weights(double t, const EsPoly &P, double (&w)[W]) {
+  double s;
+  const int i0 = es_reduce<W>(t, s);
+  es_weights_s<W>(s, P, w);
+  return i0;
 }
 
 // Signed mode index of FFT bin k in a length-n transform whose modes satisfy |j| <= jmax

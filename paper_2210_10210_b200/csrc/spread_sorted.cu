@@ -672,9 +672,14 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
           const double4 rv = raw[j];
           unsigned char *st = stage + (size_t)(coff[__double2loint(rv.w)] + __double2hiint(rv.w)) * SB;
           if constexpr (MODE == kModeF64) {
+            // the reduced coordinates s1, s2 (es_reduce) are computed here, in the load-balanced
+            // thread-per-record pass, instead of in phase C (thread per cell, Poisson-imbalanced)
             double *d = reinterpret_cast<double *>(st);
-            d[0] = rv.x;
-            d[1] = rv.y;
+            double s1, s2;
+            es_reduce<W>(grid_t(h, rv.x, n1), s1);
+            es_reduce<W>(grid_t(h, rv.y, n1), s2);
+            d[0] = s1;
+            d[1] = s2;
             d[2] = rv.z;
           } else {
             constexpr int WP = (W + 1) / 2, WE = 2 * WP, NF = SB / 4;
@@ -714,8 +719,8 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
               const double *d = reinterpret_cast<const double *>(sp);
               const double yv = d[2];
               double w1[W], w2[W];
-              es_weights<W>(grid_t(h, d[0], n1), P, w1);
-              es_weights<W>(grid_t(h, d[1], n1), P, w2);
+              es_weights_s<W>(d[0], P, w1);
+              es_weights_s<W>(d[1], P, w2);
 #pragma unroll
               for (int a = 0; a < W; ++a) {
                 const double ca = w1[a], cy = yv * w1[a];
