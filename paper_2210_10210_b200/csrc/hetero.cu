@@ -383,11 +383,11 @@ struct HetSorted {
   cufftHandle r2c = 0;
 };
 
-// d <= 2, register windows up to 6 x 6 (d = 2) or 16 (d = 1), scatter cursors in shared memory
+// d <= 2, register windows up to 8 x 8 (d = 2) or 16 (d = 1), scatter cursors in shared memory
 bool het_sorted_geometry(const Params &P, HetSorted &H) {
   const char *e = getenv("EFGP_HETERO_SORTED");
   if (e && e[0] == '0') return false;
-  if (P.d > 2 || (P.d == 2 && P.w > 6)) return false;
+  if (P.d > 2 || (P.d == 2 && P.w > 8)) return false;
   H.lo = -(P.w / 2);  // ceil(-W/2)
   const int hi = (int)std::ceil(P.h * (double)P.n2 - 0.5 * P.w);
   H.S = hi - H.lo + 2;  // one spare row
@@ -478,7 +478,7 @@ efgp_status het_apply_sorted_t(efgp_plan *pl, const HetSorted &H, int64_t N, con
 }
 
 #define EFGP_HET_W1(M) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) M(16)
-#define EFGP_HET_W2(M) M(2) M(3) M(4) M(5) M(6)
+#define EFGP_HET_W2(M) M(2) M(3) M(4) M(5) M(6) M(7) M(8)
 
 efgp_status het_sort(efgp_plan *pl, HetSorted &H, const double *x, const double *sd, int64_t N, cudaStream_t s) {
   const int W = pl->P.w;

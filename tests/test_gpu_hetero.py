@@ -27,8 +27,8 @@ def test_hetero_parity(name, path, monkeypatch):
     if path == "unfused":
         monkeypatch.setenv("EFGP_HETERO_SORTED", "0")
     c = CONFIGS[name]
-    if path == "sorted" and (c.d == 3 or c.name == "c3"):
-        pytest.skip("no sorted path: d = 3 (W^3 register windows) / c3 (W = 8 > 6 in 2D)")
+    if path == "sorted" and c.d == 3:
+        pytest.skip("no sorted path in 3D (W^3 register windows)")
     N, m_over = HET_SIZES[name]
     x, y, xt = generate(c, N=N, q=min(c.q, 1000))
     sd = noise_sd(c, N, 40 + c.id)
