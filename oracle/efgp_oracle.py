@@ -57,7 +57,7 @@ import scipy.special
 __all__ = [
     "khat", "kernel_value", "kernel_l2_norm", "matern_l2_norm_printed",
     "round_down_sig", "choose_params_se", "choose_params_matern", "choose_params",
-    "mode_indices", "spectral_weights", "toeplitz_vector", "rhs_Fy", "rhs",
+    "mode_indices", "spectral_weights", "toeplitz_vector", "toeplitz_vector_weighted", "rhs_Fy", "rhs",
     "toeplitz_matrix", "toeplitz_apply", "system_apply", "cg", "default_max_iter",
     "posterior_mean", "posterior_variance", "design_matrix", "kernel_tilde_matrix", "dense_gp_mean",
     "dense_gp_variance", "features", "hetero_system_apply", "KronPrecond", "kron_factors",
@@ -222,6 +222,12 @@ def toeplitz_vector(x: np.ndarray, h: float, m: int) -> np.ndarray:
     """v_j = sum_n exp(-2 pi i h j.x_n), j in J_{2m}  (eq ``88``; sign reading G1).
     Returned as a (4m+1,)*d array indexed by j + 2m."""
     return _signed_sum(x, None, h, 2 * m)
+
+
+def toeplitz_vector_weighted(x: np.ndarray, w: np.ndarray, h: float, m: int) -> np.ndarray:
+    """v^w_j = sum_n w_n exp(-2 pi i h j.x_n), j in J_{2m}: eq ``88`` with per-point weights (reading
+    G11b: with w_n = sigma_n^-2, Phi^* S^-1 Phi = D T(v^w) D).  Returned indexed by j + 2m."""
+    return _signed_sum(x, w, h, 2 * m)
 
 
 def rhs_Fy(x: np.ndarray, y: np.ndarray, h: float, m: int) -> np.ndarray:

@@ -85,3 +85,22 @@ def test_dense_and_chunked_products_agree():
     dense = p.reshape(-1) + Phi.conj().T @ np.diag(1 / sd ** 2) @ Phi @ p.reshape(-1)
     np.testing.assert_allclose(O.hetero_system_apply(x, sd, D, 0.5, 6, p, chunk=77).reshape(-1), dense,
                                rtol=1e-12, atol=1e-12 * np.max(np.abs(dense)))
+
+
+@pytest.mark.parametrize("d", [1, 2])
+def test_weighted_toeplitz_identity(d):
+    # Phi^* S^-1 Phi = D T(v^w) D with v^w_j = sum_n sigma_n^-2 exp(-2 pi i h j.x_n) (eq "88" with
+    # weights): the per-point noise keeps the Toeplitz structure (reading G11b).  Checked against the
+    # dense product of the design matrix.
+    rng = np.random.default_rng(16)
+    N = 150
+    x = rng.uniform(0, 1, (N, d))
+    sd = rng.uniform(0.05, 1.0, N)
+    h, m = 0.37, 4
+    D = O.spectral_weights("matern", 0.3, d, h, m, 1.5)
+    Phi = O.design_matrix(x, h, m, D)
+    dense = Phi.conj().T @ (Phi / sd[:, None] ** 2)
+    vw = O.toeplitz_vector_weighted(x, 1.0 / sd ** 2, h, m)
+    T = O.toeplitz_matrix(vw, m)
+    Dv = D.reshape(-1)
+    np.testing.assert_allclose(Dv[:, None] * T * Dv[None, :], dense, rtol=0, atol=1e-12 * np.max(np.abs(dense)))
