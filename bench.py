@@ -292,23 +292,30 @@ def main():
             gen = torch.Generator(device=dev)
             gen.manual_seed(1234 + rank)
             sd = cfg.sigma * (0.5 + torch.rand(b - a, dtype=torch.float64, device=dev, generator=gen))
-            torch.cuda.synchronize()
-            model.fit_hetero(x, y, sd)  # warm-up: grows the handle's memory pool, builds the r2c plan
-            torch.cuda.synchronize()
-            th0 = time.perf_counter()
-            model.fit_hetero(x, y, sd)
-            torch.cuda.synchronize()
-            wall = (time.perf_counter() - th0) * 1e3
-            ih = model.info()
-            per_it = ih["t_solve_ms"] / max(ih["iters"], 1)
-            hetero = {"N": b - a, "iters": ih["iters"], "sorted_path": bool(ih["hetero_sorted"]),
-                      "fit_ms": ih["t_spread_ms"] + ih["t_modes_ms"] + ih["t_solve_ms"], "wall_ms": wall,
-                      "rhs_ms": ih["t_spread_ms"], "sort_ms": ih["t_modes_ms"], "solve_ms": ih["t_solve_ms"],
-                      "ms_per_iteration": per_it, "points_per_s_per_iteration": (b - a) / (per_it / 1e3),
-                      "points_per_s": (b - a) / (wall / 1e3),
-                      "note": "per CG iteration one fused pass over the cell-sorted points: type-2 at each "
-                              "point, / sigma_n^2, type-1 of the result (k_het_apply_sorted), plus two small FFTs"}
-            model.fit(x, y)  # restore the homoskedastic fit for anything after this
+            hetero = {}
+            # TOEPLITZ: the weighted Toeplitz system (reading G11b: v^w from strengths 1/sigma_n^2, one
+            # extra type-1 pass, then the FFT Toeplitz CG); NUFFT: the BBMM-style CG of P:2762-2763 with
+            # one fused type-2/type-1 pass over the cell-sorted points per iteration
+            for meth in ("toeplitz", "nufft"):
+                mh = EFGP(cfg.kernel, cfg.ell, cfg.sigma, cfg.eps, cfg.d, cfg.nu, spread=args.spread,
+                          weights=args.weights, hetero=meth)
+                torch.cuda.synchronize()
+                mh.fit_hetero(x, y, sd)  # warm-up: grows the handle's memory pool, builds plans
+                torch.cuda.synchronize()
+                th0 = time.perf_counter()
+                mh.fit_hetero(x, y, sd)
+                torch.cuda.synchronize()
+                wall = (time.perf_counter() - th0) * 1e3
+                ih = mh.info()
+                per_it = ih["t_solve_ms"] / max(ih["iters"], 1)
+                hetero[meth] = {"N": b - a, "iters": ih["iters"], "solver": {0: "nufft-unfused", 1: "nufft-sorted",
+                                                                             2: "toeplitz"}[ih["hetero_sorted"]],
+                                "fit_ms": ih["t_spread_ms"] + ih["t_modes_ms"] + ih["t_solve_ms"], "wall_ms": wall,
+                                "type1_ms": ih["t_spread_ms"], "setup_ms": ih["t_modes_ms"], "solve_ms": ih["t_solve_ms"],
+                                "ms_per_iteration": per_it, "points_per_s": (b - a) / (wall / 1e3)}
+                if meth == "nufft":
+                    hetero[meth]["points_per_s_per_iteration"] = (b - a) / (per_it / 1e3)
+                mh.close()
             del sd
         except Exception as exc:
             hetero = {"error": f"{type(exc).__name__}: {exc}"[:200]}

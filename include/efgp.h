@@ -80,6 +80,15 @@ typedef enum { EFGP_WEIGHTS_FP64 = 0, EFGP_WEIGHTS_FP32 = 1, EFGP_WEIGHTS_MIXED 
  *   AUTO: KRON for EFGP_SE, NONE otherwise. */
 typedef enum { EFGP_PRECOND_NONE = 0, EFGP_PRECOND_KRON = 1, EFGP_PRECOND_AUTO = 2 } efgp_precond;
 
+/* NEXT-3 solver of efgp_fit_hetero (readings G11, G11b).
+ *   TOEPLITZ: Phi^* S^-1 Phi = D T(v^w) D with v^w = eq "88" with strengths sigma_n^-2: one extra
+ *             type-1 pass, then the FFT Toeplitz CG of efgp_fit with sigma^2 -> 1 (needs the SORTED or
+ *             CELLSORT spreading, whose y grid is the v grid; otherwise NUFFT is used).
+ *   NUFFT   : the BBMM-style CG the paper suggests: a type-2 + type-1 NUFFT pair over the
+ *             N points per iteration (sorted fused pass for d <= 2).
+ *   AUTO    : TOEPLITZ where available. */
+typedef enum { EFGP_HETERO_AUTO = 0, EFGP_HETERO_TOEPLITZ = 1, EFGP_HETERO_NUFFT = 2 } efgp_hetero_method;
+
 typedef struct {
   double h;            /* grid spacing override when m > 0                        */
   int64_t m;           /* modes per dimension override (2m+1 per dim), 0 = rule (Alg a1 step 1) */
@@ -91,6 +100,7 @@ typedef struct {
   int graph_iters;     /* CG iterations per CUDA-graph launch, 0 = default                        */
   int spread_weights;  /* efgp_weights, default EFGP_WEIGHTS_FP64                                  */
   int precond;         /* efgp_precond, default EFGP_PRECOND_NONE (Alg a1's plain CG)             */
+  int hetero_method;   /* efgp_hetero_method, default EFGP_HETERO_AUTO                            */
   void *stream;        /* cudaStream_t for all device work (NULL = default stream)               */
 } efgp_options;
 
@@ -112,7 +122,8 @@ typedef struct {
   int64_t spread_precision;                                   /* efgp_weights of the SORTED path */
   double t_var_ms;                                            /* device time of the last predict_var */
   int64_t var_iters_max, var_batch;                           /* its largest CG count, targets/batch */
-  int64_t hetero_sorted; /* last efgp_fit_hetero: 1 = points sorted once by cell, fused NUFFT-pair pass */
+  int64_t hetero_sorted; /* last efgp_fit_hetero: 0 unfused NUFFT pair, 1 sorted fused NUFFT pair,
+                            2 weighted Toeplitz (G11b) */
   int64_t precond;       /* preconditioner used by the fit (EFGP_PRECOND_NONE or _KRON; AUTO resolved) */
 } efgp_info;
 
@@ -134,16 +145,16 @@ efgp_status efgp_setup(efgp_handle *out, efgp_kernel kernel, double nu, double e
  * max_iter (beta is still usable). */
 efgp_status efgp_fit(efgp_handle, const double *x, const double *y, int64_t N);
 
-/* NEXT-3: fit with heteroskedastic noise (per-point sigma_n, reading G11).
- * Solves (Phi^* S^-1 Phi + I) beta = Phi^* S^-1 y, S = diag(noise_sd^2), by CG (reading G6) whose
- * product is applied with one type-2 and one type-1 NUFFT over the N points per iteration (the
- * Toeplitz structure is gone); mu(x*) = phi(x*) beta as in efgp_predict.  For
- * noise_sd_n = sigma it gives efgp_fit's beta (the same system divided by sigma^2).  The sigma given
- * at setup is not used; the CG cap default is P:1766 with sigma = min noise_sd.
- * x: (N, d), y: (N), noise_sd: (N); all device or all host (host inputs are copied to the device
- * for the whole solve: N (d + 2) doubles).  Returns EFGP_ERR_INVALID for N < 1, a non-positive or
- * non-finite noise_sd, points outside [0,1]^d, non-finite y; EFGP_ERR_NOCONVERGE as efgp_fit.
- * After it, efgp_predict works; efgp_predict_var is refused (no Toeplitz operator). */
+/* NEXT-3: fit with heteroskedastic noise (per-point sigma_n, readings G11,
+ * G11b).  Solves (Phi^* S^-1 Phi + I) beta = Phi^* S^-1 y, S = diag(noise_sd^2), with the solver of
+ * options.hetero_method (weighted-Toeplitz CG, or the NUFFT-pair CG); mu(x*) = phi(x*) beta as in
+ * efgp_predict.  For noise_sd_n = sigma it gives efgp_fit's beta (the same system divided by sigma^2).
+ * The sigma given at setup is not used; the CG cap default is P:1766 with sigma = min noise_sd.
+ * options.precond applies to the TOEPLITZ solver.  x: (N, d), y: (N), noise_sd: (N); all device or
+ * all host (host inputs are copied to the device for the whole solve: N (d + 2) doubles).  Returns
+ * EFGP_ERR_INVALID for N < 1, a non-positive or non-finite noise_sd, points outside [0,1]^d,
+ * non-finite y; EFGP_ERR_NOCONVERGE as efgp_fit.  After it, efgp_predict works, and
+ * efgp_predict_var after a TOEPLITZ solve (sigma^2 -> 1 in eq "eta"; refused after NUFFT). */
 efgp_status efgp_fit_hetero(efgp_handle, const double *x, const double *y, const double *noise_sd, int64_t N);
 
 /* Multi-process split of efgp_fit.  efgp_fit_local spreads this rank's

@@ -61,7 +61,7 @@ __all__ = [
     "toeplitz_matrix", "toeplitz_apply", "system_apply", "cg", "default_max_iter",
     "posterior_mean", "posterior_variance", "design_matrix", "kernel_tilde_matrix", "dense_gp_mean",
     "dense_gp_variance", "features", "hetero_system_apply", "KronPrecond", "kron_factors",
-    "kron_preconditioner", "kron_apply_inverse", "pcg", "efgp_fit_hetero", "dense_gp_mean_hetero",
+    "kron_preconditioner", "kron_apply_inverse", "pcg", "posterior_variance_hetero", "efgp_fit_hetero", "dense_gp_mean_hetero",
     "OracleFit", "efgp_fit", "efgp_predict",
 ]
 
@@ -505,6 +505,20 @@ def efgp_fit_hetero(x, y, noise_sd, kernel: str, ell: float, eps: float, nu: flo
         apply = lambda p: hetero_system_apply(x, sd, D, h, m, p)
     beta, iters, hist = cg(apply, b, tol, cap)
     return OracleFit(kernel, nu, ell, smin, eps, d, h, m, D, None, b, beta, iters, hist)
+
+
+def posterior_variance_hetero(fit: OracleFit, x, noise_sd, xt) -> np.ndarray:
+    """Heteroskedastic posterior variance (reading G11 with eq ``eta`` / ``sws``, sigma^2 -> 1):
+    s(x*) = phi(x*) (Phi^* S^-1 Phi + I)^-1 phi(x*)^*, by a dense LAPACK solve of the weight-space
+    matrix (small problems only)."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.ndim == 1:
+        x = x[:, None]
+    Phi = design_matrix(x, fit.h, fit.m, fit.D)
+    A = Phi.conj().T @ (Phi / np.asarray(noise_sd, dtype=np.float64)[:, None] ** 2) + np.eye(Phi.shape[1])
+    F = features(fit.D, fit.h, np.asarray(xt, dtype=np.float64)).reshape(len(xt), -1)
+    eta = np.linalg.solve(A, F.conj().T)
+    return np.einsum("tj,jt->t", F, eta).real
 
 
 # ----------------------------------------------------------------------------------------------

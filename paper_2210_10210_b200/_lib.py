@@ -19,7 +19,8 @@ STATUS_NAMES = {0: "EFGP_OK", 1: "EFGP_ERR_NOCONVERGE", 2: "EFGP_ERR_INVALID", 3
 class Options(C.Structure):
     _fields_ = [("h", C.c_double), ("m", C.c_int64), ("cg_tol", C.c_double), ("max_iter", C.c_int64),
                 ("nufft_tol", C.c_double), ("matern_rescale", C.c_int), ("spread_method", C.c_int),
-                ("graph_iters", C.c_int), ("spread_weights", C.c_int), ("precond", C.c_int), ("stream", C.c_void_p)]
+                ("graph_iters", C.c_int), ("spread_weights", C.c_int), ("precond", C.c_int),
+                ("hetero_method", C.c_int), ("stream", C.c_void_p)]
 
 
 class Info(C.Structure):

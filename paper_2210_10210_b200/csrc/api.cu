@@ -225,6 +225,8 @@ efgp_status fit_solve_impl(efgp_plan *pl, const double *modes, int64_t N_total) 
   EFGP_CUDA(cudaMemcpyAsync(pl->modes_sum, modes, sizeof(double) * 2 * (P.Kvh + P.Mh), cudaMemcpyDefault, s));
   EFGP_TRY(toeplitz_setup(pl, pl->modes_sum, s));
   pl->op_valid = true;
+  pl->sigma2_sys = P.sigma * P.sigma;  // (Phi^*Phi + sigma^2 I)
+  pl->cap_sigma = P.sigma;
   efgp_status st;
   if (P.precond) {  // NEXT-4: Kronecker-preconditioned CG (reading G12)
     EFGP_TRY(precond_setup(pl, pl->modes_sum));

@@ -285,7 +285,7 @@ static efgp_status cg_solve_d(efgp_plan *pl, int64_t N_total) {
   int64_t max_iter = P.max_iter_opt;
   if (max_iter <= 0) {
     const double Nd = (double)(N_total > 0 ? N_total : 1);
-    max_iter = (int64_t)std::ceil(std::log(1.0 / P.cg_tol) * std::sqrt(Nd) / (2.0 * P.sigma));
+    max_iter = (int64_t)std::ceil(std::log(1.0 / P.cg_tol) * std::sqrt(Nd) / (2.0 * pl->cap_sigma));
     if (max_iter < 10) max_iter = 10;
   }
   pl->max_iter_used = max_iter;
@@ -293,7 +293,7 @@ static efgp_status cg_solve_d(efgp_plan *pl, int64_t N_total) {
   CGState *st = reinterpret_cast<CGState *>(pl->scal);
   CGState init{};
   init.tol = P.cg_tol;
-  init.sigma2 = P.sigma * P.sigma;
+  init.sigma2 = pl->sigma2_sys;
   init.max_iter = max_iter;
   EFGP_CUDA(cudaMemcpyAsync(st, &init, sizeof(CGState), cudaMemcpyHostToDevice, s));
   k_cg_init<<<nb, kCGThreads, 0, s>>>(pl->b, pl->x, pl->r, pl->p, P.Mh, (int)P.m, pl->partials);
@@ -470,7 +470,7 @@ static efgp_status pcg_solve_d(efgp_plan *pl, int64_t N_total) {
   int64_t max_iter = P.max_iter_opt;
   if (max_iter <= 0) {
     const double Nd = (double)(N_total > 0 ? N_total : 1);
-    max_iter = (int64_t)std::ceil(std::log(1.0 / P.cg_tol) * std::sqrt(Nd) / (2.0 * P.sigma));
+    max_iter = (int64_t)std::ceil(std::log(1.0 / P.cg_tol) * std::sqrt(Nd) / (2.0 * pl->cap_sigma));
     if (max_iter < 10) max_iter = 10;
   }
   pl->max_iter_used = max_iter;
@@ -478,7 +478,7 @@ static efgp_status pcg_solve_d(efgp_plan *pl, int64_t N_total) {
   CGState *st = reinterpret_cast<CGState *>(pl->scal);
   CGState init{};
   init.tol = P.cg_tol;
-  init.sigma2 = P.sigma * P.sigma;
+  init.sigma2 = pl->sigma2_sys;
   init.max_iter = max_iter;
   double *part_rz = pl->partials + 2 * pl->cg_blocks;
   EFGP_CUDA(cudaMemcpyAsync(st, &init, sizeof(CGState), cudaMemcpyHostToDevice, s));
@@ -492,7 +492,8 @@ static efgp_status pcg_solve_d(efgp_plan *pl, int64_t N_total) {
   EFGP_CUFFT(cufftSetStream(pl->plan_c2r_L, s));
   EFGP_CUFFT(cufftSetStream(pl->plan_r2c_L, s));
   const int G = P.graph_iters;
-  if (!pl->pcg_exec || pl->pcg_exec_iters != G) {
+  if (!pl->pcg_exec || pl->pcg_exec_iters != G || pl->pcg_exec_sigma2 != pl->sigma2_sys) {
+    pl->pcg_exec_sigma2 = pl->sigma2_sys;
     if (pl->pcg_exec) cudaGraphExecDestroy(pl->pcg_exec);
     pl->pcg_exec = nullptr;
     cudaGraph_t graph;

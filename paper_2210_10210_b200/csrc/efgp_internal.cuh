@@ -59,6 +59,7 @@ struct Params {
   EsPoly poly{};
   EsPolyF polyf{};
   EsPolyP polyp{};
+  int hetero_method = 0;       // NEXT-3: 0 auto, 1 weighted Toeplitz (G11b), 2 NUFFT pair per iteration
   int precond = 0;             // NEXT-4: 0 none (Alg a1's plain CG), 1 Kronecker (reading G12)
   int spread_mode = 0;         // SORTED precision: 0 fp64, 1 fp32 weights, 2 fp32 weights + round sums
   // SORTED spreading geometry (2D)
@@ -163,9 +164,12 @@ struct efgp_plan {
   cudaGraphExec_t var_exec = nullptr;
   int var_exec_max_iter = 0;
   int var_exec_pc = 0;  // the captured variance graph uses the preconditioned step
+  double var_exec_sigma2 = -1;  // sigma2_sys baked into the captured variance graph
   bool var_pc = false;  // last predict_var used the Kronecker preconditioner
   int var_iters_max = 0;
   bool op_valid = false;  // the Toeplitz operator (vhat) of a fit is in place
+  double sigma2_sys = 0;  // diagonal shift of the solved system: sigma^2, or 1 for (D T(v^w) D + I) (G11b)
+  double cap_sigma = 0;   // sigma of the default CG cap: sigma, or min sigma_n
   double t_var = 0;
   int cg_exec_iters = 0;
 
@@ -181,6 +185,7 @@ struct efgp_plan {
   void *pc_solver = nullptr;  // cusolverDnHandle_t
   cudaGraphExec_t pcg_exec = nullptr;
   int pcg_exec_iters = 0;
+  double pcg_exec_sigma2 = -1;  // sigma2_sys baked into the captured PCG graph (preconditioner scale)
   int het_path = 0;  // 1: last heteroskedastic fit used the sorted fused product
   cufftHandle plan_het_r2c = 0;  // D2Z on n2 (sorted path), created lazily
   // stream-ordered temporaries (hetero staging and sort, host-input chunks) come from this pool; it
@@ -223,6 +228,9 @@ efgp_status type1_modes(efgp_plan *pl, double *modes_out, cudaStream_t s);
 efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s);
 efgp_status type2_grid(efgp_plan *pl, cudaStream_t s);
 efgp_status type2_grid_from(efgp_plan *pl, const double2 *beta, cudaStream_t s);
+// deconvolved Hermitian-half modes over J_K of a half-spectrum box G of an n^d grid (K2 for one grid)
+efgp_status type1_half(efgp_plan *pl, const double2 *G, int64_t n, int K, const double *psi, double2 *out,
+                       cudaStream_t s);
 efgp_status type2_grid_on(efgp_plan *pl, const double2 *beta, int64_t n, const double *psi, cufftHandle plan,
                           double2 *boxbuf, double *grid, cudaStream_t s);
 // cg.cu

@@ -24,7 +24,8 @@ namespace efgp {
 // w_n = y_n / sigma_n^2; raise dflags[2] for sigma_n <= 0 or non-finite; min sigma_n into *minbits
 // (for positive doubles the IEEE bit pattern is ordered like the value)
 __global__ void k_het_prep(const double *__restrict__ y, const double *__restrict__ sd, int64_t N,
-                           double *__restrict__ w, unsigned long long *__restrict__ minbits, int *__restrict__ err) {
+                           double *__restrict__ w, unsigned long long *__restrict__ minbits, int *__restrict__ err,
+                           double *__restrict__ iv = nullptr) {
   unsigned long long lmin = ~0ull;
   bool bad = false;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
@@ -32,6 +33,7 @@ __global__ void k_het_prep(const double *__restrict__ y, const double *__restric
     const bool ok = s > 0.0 && isfinite(s);
     bad |= !ok;
     w[i] = ok ? y[i] / (s * s) : 0.0;
+    if (iv) iv[i] = ok ? 1.0 / (s * s) : 0.0;
     if (ok) {
       const unsigned long long b = (unsigned long long)__double_as_longlong(s);
       lmin = b < lmin ? b : lmin;
@@ -540,13 +542,16 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
   pl->fitted = false;
   pl->op_valid = false;  // no Toeplitz operator: predict_var is refused after a heteroskedastic fit
   pl->t2_valid = false;  // the type-2 grid is rebuilt from beta by the next predict
-  double *w = nullptr;
+  // G11b route: the weighted Toeplitz system, where the y spreading grid is the v grid (n_rhs = n1)
+  const bool tz = P.hetero_method != EFGP_HETERO_NUFFT && P.n_rhs == P.n1;
+  double *w = nullptr, *iv = nullptr;
   EFGP_PALLOC(&w, sizeof(double) * N, s);
+  if (tz) EFGP_PALLOC(&iv, sizeof(double) * N, s);
   unsigned long long *minbits = reinterpret_cast<unsigned long long *>(pl->scal + 24);
   EFGP_CUDA(cudaEventRecord(pl->ev[0], s));
   EFGP_CUDA(cudaMemsetAsync(minbits, 0xff, sizeof(unsigned long long), s));
   EFGP_CUDA(cudaMemsetAsync(pl->dflags + 2, 0, sizeof(int), s));
-  k_het_prep<<<grid_for(N, pl->num_sms), 256, 0, s>>>(y, sd, N, w, minbits, pl->dflags);
+  k_het_prep<<<grid_for(N, pl->num_sms), 256, 0, s>>>(y, sd, N, w, minbits, pl->dflags, iv);
   EFGP_CUDA(cudaGetLastError());
   int flags[4];
   unsigned long long mb = 0;
@@ -559,6 +564,61 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
   if (flags[2]) {
     pl->err = "fit_hetero: every noise standard deviation must be finite and > 0";
     st = EFGP_ERR_INVALID;
+  }
+  if (st == EFGP_OK && tz) {
+    // v^w (J_2m) from strengths 1/sigma_n^2 and F^*(y/sigma^2) (J_m), both spread as the "y" strength
+    // onto the v grid, then the homoskedastic Toeplitz machinery with sigma^2 -> 1 (reading G11b)
+    double2 *vh = reinterpret_cast<double2 *>(pl->modes_sum), *fyh = vh + P.Kvh;
+    for (int pass = 0; pass < 2 && st == EFGP_OK; ++pass) {
+      st = spread_begin(pl, s);
+      if (st == EFGP_OK) st = spread_points(pl, x, pass == 0 ? iv : w, N, s);
+      if (st == EFGP_OK) st = spread_end(pl, s);
+      if (st != EFGP_OK) break;
+      EFGP_CUFFT(cufftSetStream(pl->plan_g2, s));
+      EFGP_CUFFT(cufftExecD2Z(pl->plan_g2, pl->g2, pl->G2h));
+      if (pass == 0) st = type1_half(pl, pl->G2h, P.n1, (int)(2 * P.m), pl->psi1, vh, s);
+      else st = type1_half(pl, pl->G2h, P.n1, (int)P.m, pl->psi1, fyh, s);
+      EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned, pl->dflags, sizeof(int) * 4, cudaMemcpyDeviceToHost, s));
+      EFGP_CUDA(cudaStreamSynchronize(s));
+      std::memcpy(flags, pl->h_pinned, sizeof(flags));
+      if (st == EFGP_OK && flags[0]) {
+        pl->err = "fit_hetero: a coordinate is outside [0,1] or non-finite, or an observation is non-finite";
+        st = EFGP_ERR_INVALID;
+      }
+    }
+    EFGP_CUDA(cudaEventRecord(pl->ev[1], s));
+    if (st == EFGP_OK) {
+      double smin = 0;
+      std::memcpy(&smin, &mb, sizeof(smin));
+      pl->sigma2_sys = 1.0;
+      pl->cap_sigma = smin;
+      st = toeplitz_setup(pl, pl->modes_sum, s);
+      EFGP_CUDA(cudaEventRecord(pl->ev[2], s));
+      if (st == EFGP_OK) {
+        pl->op_valid = true;
+        if (P.precond) {
+          st = precond_setup(pl, pl->modes_sum);
+          if (st == EFGP_OK) st = pcg_solve(pl, N);
+        } else {
+          st = cg_solve(pl, N);
+        }
+      }
+      pl->het_path = 2;
+      EFGP_CUDA(cudaEventRecord(pl->ev[4], s));
+      EFGP_CUDA(cudaEventSynchronize(pl->ev[4]));
+      pl->t_spread = elapsed_ms(pl->ev[0], pl->ev[1]);
+      pl->t_modes = elapsed_ms(pl->ev[1], pl->ev[2]);
+      pl->t_solve = elapsed_ms(pl->ev[2], pl->ev[4]);
+      if (st == EFGP_OK || st == EFGP_ERR_NOCONVERGE) {
+        pl->fitted = true;
+        pl->N_last = N;
+      }
+      if (st == EFGP_ERR_NOCONVERGE) pl->err = "CG reached max_iter before the relative residual reached cg_tol";
+    }
+    cudaFreeAsync(w, s);
+    if (iv) cudaFreeAsync(iv, s);
+    EFGP_CUDA(cudaStreamSynchronize(s));
+    return st;
   }
   // b = D F^*(y / sigma^2); spread_begin clears the input flags, spread_points raises dflags[0]
   if (st == EFGP_OK) st = spread_to_modes(pl, x, w, N, nullptr, pl->b, s);
@@ -632,6 +692,7 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
     if (st == EFGP_ERR_NOCONVERGE) pl->err = "CG reached max_iter before the relative residual reached cg_tol";
   }
   cudaFreeAsync(w, s);
+  if (iv) cudaFreeAsync(iv, s);
   EFGP_CUDA(cudaStreamSynchronize(s));
   return st;
 }

@@ -112,6 +112,24 @@ efgp_status type1_modes(efgp_plan *pl, double *modes_out, cudaStream_t s) {
   return EFGP_OK;
 }
 
+efgp_status type1_half(efgp_plan *pl, const double2 *G, int64_t n, int K, const double *psi, double2 *out,
+                       cudaStream_t s) {
+  const Params &P = pl->P;
+  const double sc = std::pow(2.0 * kPi / (double)n, P.d);
+  // k_deconv's first part (idx < Kvh) handles J_{2m}, its second (J_m) the rest: use one or the other
+  const bool vgrid = K == 2 * P.m;
+  const int64_t cnt = vgrid ? P.Kvh : P.Mh;
+  const unsigned g = grid_for(cnt, 256, pl->num_sms);
+  const int64_t kv = vgrid ? P.Kvh : 0, mh = vgrid ? 0 : P.Mh;
+  switch (P.d) {
+    case 1: k_deconv<1><<<g, 256, 0, s>>>(G, n, G, n, (int)P.m, psi, psi, sc, sc, out, out, kv, mh); break;
+    case 2: k_deconv<2><<<g, 256, 0, s>>>(G, n, G, n, (int)P.m, psi, psi, sc, sc, out, out, kv, mh); break;
+    case 3: k_deconv<3><<<g, 256, 0, s>>>(G, n, G, n, (int)P.m, psi, psi, sc, sc, out, out, kv, mh); break;
+  }
+  EFGP_CUDA(cudaGetLastError());
+  return EFGP_OK;
+}
+
 efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s) {
   const Params &P = pl->P;
   const double2 *vh = reinterpret_cast<const double2 *>(modes);

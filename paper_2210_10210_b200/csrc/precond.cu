@@ -240,7 +240,7 @@ static efgp_status precond_apply_d(efgp_plan *pl, const double2 *r, double2 *z, 
     k_pc_axis<true><<<gw, 256, 0, s>>>(a, b, pl->pc_Q + (size_t)i * n * n, n, stride, total, done);
     std::swap(a, b);
   }
-  k_pc_scale<D><<<g, 256, 0, s>>>(a, pl->pc_lam, n, P.sigma * P.sigma, total, done);
+  k_pc_scale<D><<<g, 256, 0, s>>>(a, pl->pc_lam, n, pl->sigma2_sys, total, done);
   stride = total;
   for (int i = 0; i < D; ++i) {
     stride /= n;

@@ -443,7 +443,7 @@ static efgp_status var_batch(efgp_plan *pl, const double *xt, int nt, double *ou
   VarTarget *st = reinterpret_cast<VarTarget *>(pl->var_st);
   unsigned *ndone = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(pl->var_st) + B * sizeof(VarTarget));
   const size_t esm = sizeof(double2) * D * (2 * P.m + 1);
-  const double sigma2 = P.sigma * P.sigma;
+  const double sigma2 = pl->sigma2_sys;  // sigma^2, or 1 after a heteroskedastic Toeplitz fit (G11b)
   // NEXT-4 in the variance CGs: the fit's Kronecker factors, applied per target inside its CTA
   const int64_t n = 2 * P.m + 1, total = D == 1 ? n : n * n;
   const size_t pcsm = sizeof(double2) * (D * n * n + 2 * total);
@@ -465,12 +465,13 @@ static efgp_status var_batch(efgp_plan *pl, const double *xt, int nt, double *ou
   EFGP_CUFFT(cufftSetStream(pl->plan_var_c2r, s));
   EFGP_CUFFT(cufftSetStream(pl->plan_var_r2c, s));
   const int max_iter = (int)std::min<int64_t>(pl->max_iter_used > 0 ? pl->max_iter_used : 1000, 1 << 30);
-  if (pl->var_exec && pl->var_exec_pc != (int)pc) {
+  if (pl->var_exec && (pl->var_exec_pc != (int)pc || pl->var_exec_sigma2 != sigma2)) {
     cudaGraphExecDestroy(pl->var_exec);
     pl->var_exec = nullptr;
   }
   if (!pl->var_exec) {
     pl->var_exec_pc = (int)pc;
+    pl->var_exec_sigma2 = sigma2;
     cudaGraph_t graph;
     EFGP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     for (int it = 0; it < P.graph_iters; ++it) {

@@ -76,7 +76,7 @@ class EFGP:
                  h: float | None = None, m: int | None = None, cg_tol: float | None = None,
                  max_iter: int | None = None, nufft_tol: float | None = None, matern_rescale: str = "A",
                  spread: str = "auto", weights: str = "fp64", graph_iters: int | None = None, stream=None, device=None,
-                 precond: str | None = None):
+                 precond: str | None = None, hetero: str = "auto"):
         import torch
         self._lib = L.load()
         self._torch = torch
@@ -100,6 +100,7 @@ class EFGP:
         opt.spread_method = _SPREAD[spread]
         opt.spread_weights = {"fp64": 0, "fp32": 1, "mixed": 2}[weights]
         opt.precond = {None: 0, "none": 0, "kron": 1, "auto": 2}[precond]  # NEXT-4 (reading G12)
+        opt.hetero_method = {"auto": 0, "toeplitz": 1, "nufft": 2}[hetero]  # NEXT-3 (G11, G11b)
         if graph_iters is not None:
             opt.graph_iters = int(graph_iters)
         opt.stream = C.c_void_p(stream.cuda_stream)

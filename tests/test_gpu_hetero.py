@@ -19,16 +19,20 @@ def noise_sd(c, N, seed):
     return c.sigma * (0.5 + np.random.default_rng(seed).uniform(0, 1, N))
 
 
-@pytest.mark.parametrize("path", ["sorted", "unfused"])
+@pytest.mark.parametrize("path", ["toeplitz", "sorted", "unfused"])
 @pytest.mark.parametrize("name", list(CONFIGS))
 def test_hetero_parity(name, path, monkeypatch):
-    # "sorted": points counting-sorted once by cell, one fused type-2/type-1 pass per iteration (d <= 2);
-    # "unfused": K8 + C2R + K9 + K1 + R2C per iteration (the d = 3 path; forced here by the env switch)
+    # "toeplitz": the weighted Toeplitz system of reading G11b (SORTED / CELLSORT spreading: c2-c5);
+    # "sorted": NUFFT pair per iteration, points counting-sorted once by cell, one fused pass (d <= 2);
+    # "unfused": K8 + C2R + K9 + K1 + R2C per iteration (the d = 3 path; forced by the env switch)
+    kw_h = {"hetero": "toeplitz" if path == "toeplitz" else "nufft"}
     if path == "unfused":
         monkeypatch.setenv("EFGP_HETERO_SORTED", "0")
     c = CONFIGS[name]
     if path == "sorted" and c.d == 3:
         pytest.skip("no sorted path in 3D (W^3 register windows)")
+    if path == "toeplitz" and name == "c1":
+        pytest.skip("c1 spreads y on n2 (SMEM): the TOEPLITZ solver needs the v grid (falls back to NUFFT)")
     N, m_over = HET_SIZES[name]
     x, y, xt = generate(c, N=N, q=min(c.q, 1000))
     sd = noise_sd(c, N, 40 + c.id)
@@ -37,11 +41,11 @@ def test_hetero_parity(name, path, monkeypatch):
     if m_over is not None:
         h0, _ = O.choose_params(c.kernel, c.ell, c.d, c.eps, c.nu)
         kw = dict(h=h0, m=m_over)
-    g = model(c, cg_tol=cg_tol, **kw)
+    g = model(c, cg_tol=cg_tol, **kw, **kw_h)
     g.fit_hetero(dev(x), dev(y), dev(sd))
     mu = g.predict(dev(xt)).cpu().numpy()
     inf = g.info()
-    assert inf["hetero_sorted"] == (1 if path == "sorted" else 0)
+    assert inf["hetero_sorted"] == {"toeplitz": 2, "sorted": 1, "unfused": 0}[path]
     fit = O.efgp_fit_hetero(x, y, sd, c.kernel, c.ell, c.eps, nu=c.nu, h=kw.get("h"), m=kw.get("m"), cg_tol=cg_tol)
     ref = O.efgp_predict(fit, xt)
     assert rel(mu, ref) <= 10 * c.eps, (rel(mu, ref), 10 * c.eps)
@@ -58,6 +62,16 @@ def test_hetero_parity(name, path, monkeypatch):
     from paper_2210_10210_b200 import half_to_full
     b = half_to_full(g.vector("rhs"), inf["m"], c.d)
     assert rel(b, fit.b) <= 5 * inf["nufft_tol"]
+    if path == "toeplitz":
+        # v^w = eq 88 with strengths sigma_n^-2 (reading G11b), and the variance with sigma^2 -> 1
+        vw = half_to_full(g.vector("v"), inf["m"], c.d, K=2 * inf["m"])
+        vw_ref = O.toeplitz_vector_weighted(x, 1.0 / sd ** 2, fit.h, fit.m)
+        assert rel(vw, vw_ref) <= 5 * inf["nufft_tol"]
+        if c.d <= 2:
+            xv = xt[:8]
+            var = g.predict_var(dev(xv)).cpu().numpy()
+            ref_v = O.posterior_variance_hetero(fit, x, sd, xv)
+            assert rel(var, ref_v) <= 10 * c.eps, (rel(var, ref_v), 10 * c.eps)
     g.close()
 
 
@@ -69,7 +83,7 @@ def test_hetero_constant_noise_matches_toeplitz_fit(spread):
     x, y, xt = generate(c, N=200_000, q=500)
     g1 = model(c, cg_tol=c.eps / 1000, spread=spread)
     g1.fit(dev(x), dev(y))
-    g2 = model(c, cg_tol=c.eps / 1000, spread=spread)
+    g2 = model(c, cg_tol=c.eps / 1000, spread=spread, hetero="nufft")
     g2.fit_hetero(dev(x), dev(y), dev(np.full(len(x), c.sigma)))
     i1, i2 = g1.info(), g2.info()
     assert abs(i1["iters"] - i2["iters"]) <= 0.1 * i1["iters"] + 2
@@ -102,8 +116,12 @@ def test_hetero_edge_cases():
     # spreading atomics make runs agree to roundoff; CG amplifies it (as test_host_inputs_match_device_inputs)
     assert rel(g.vector("rhs"), b_d) < 1e-13
     assert rel(g.predict(dev(xt)).cpu().numpy(), mu_d) < 10 * c.eps
+    g.predict_var(dev(xt))                                         # TOEPLITZ solve: variance available
+    gn = model(c, hetero="nufft")
+    gn.fit_hetero(dev(x), dev(y), dev(sd))
     with pytest.raises(EFGPError, match="INVALID"):
-        g.predict_var(dev(xt))                                     # no Toeplitz operator
+        gn.predict_var(dev(xt))                                    # NUFFT solve: no Toeplitz operator
+    gn.close()
     # a single point: closed form mu(x0) = k~(0) y / (k~(0) + sd^2), to the NUFFT tolerance
     x0 = np.array([[0.3, 0.6]])
     g.fit_hetero(dev(x0), dev(np.array([2.0])), dev(np.array([0.5])))

@@ -104,3 +104,25 @@ def test_weighted_toeplitz_identity(d):
     T = O.toeplitz_matrix(vw, m)
     Dv = D.reshape(-1)
     np.testing.assert_allclose(Dv[:, None] * T * Dv[None, :], dense, rtol=0, atol=1e-12 * np.max(np.abs(dense)))
+
+
+def test_hetero_variance_woodbury():
+    # phi (Phi^* S^-1 Phi + I)^-1 phi^* = k~(x*,x*) - k~(x*,X) (K~ + S)^-1 k~(X,x*)  (Woodbury, exact)
+    rng = np.random.default_rng(17)
+    x = rng.uniform(0, 1, (120, 2))
+    sd = rng.uniform(0.05, 0.5, 120)
+    xt = rng.uniform(0, 1, (9, 2))
+    fit = O.efgp_fit_hetero(x, np.zeros(120), sd, "matern", 0.2, 1e-2, nu=1.5, cg_tol=1e-12)
+    s = O.posterior_variance_hetero(fit, x, sd, xt)
+    kt = lambda a, b: O.kernel_tilde_matrix(a, b, fit.h, fit.m, fit.D)
+    K = kt(x, x) + np.diag(sd ** 2)
+    Kt = kt(xt, x)
+    ref = np.array([kt(xt[i:i + 1], xt[i:i + 1])[0, 0] for i in range(9)]) - np.einsum(
+        "ij,ji->i", Kt, np.linalg.solve(K, Kt.T))
+    np.testing.assert_allclose(s, ref, rtol=1e-9, atol=1e-12)
+    # sigma_n = sigma reduces to the homoskedastic variance
+    sig = 0.1
+    fit2 = O.efgp_fit_hetero(x, np.zeros(120), np.full(120, sig), "se", 0.2, 1e-6, cg_tol=1e-12)
+    hom = O.efgp_fit(x, np.zeros(120), "se", 0.2, sig, 1e-6, cg_tol=1e-12)
+    np.testing.assert_allclose(O.posterior_variance_hetero(fit2, x, np.full(120, sig), xt),
+                               O.posterior_variance(hom, xt, cg_tol=1e-13, max_iter=50000), rtol=1e-7)
