@@ -125,6 +125,7 @@ typedef struct {
   int64_t hetero_sorted; /* last efgp_fit_hetero: 0 unfused NUFFT pair, 1 sorted fused NUFFT pair,
                             2 weighted Toeplitz (G11b) */
   int64_t precond;       /* preconditioner used by the fit (EFGP_PRECOND_NONE or _KRON; AUTO resolved) */
+  int64_t comm_size;     /* ranks of the handle's NCCL communicator (0: none) */
 } efgp_info;
 
 /* Fill *opt with defaults (all zero / automatic). */
@@ -156,6 +157,16 @@ efgp_status efgp_fit(efgp_handle, const double *x, const double *y, int64_t N);
  * non-finite y; EFGP_ERR_NOCONVERGE as efgp_fit.  After it, efgp_predict works, and
  * efgp_predict_var after a TOEPLITZ solve (sigma^2 -> 1 in eq "eta"; refused after NUFFT). */
 efgp_status efgp_fit_hetero(efgp_handle, const double *x, const double *y, const double *noise_sd, int64_t N);
+
+/* Multi-GPU with a library-owned NCCL communicator.
+ * efgp_comm_unique_id writes NCCL_UNIQUE_ID_BYTES (128) bytes on one rank; the caller broadcasts
+ * them; every rank then calls efgp_comm_init(handle, id, nranks, rank) on its own device.  From then
+ * on efgp_fit(x, y, N) takes THIS rank's shard: it spreads it, sums the partial modes (and N) over
+ * ranks with one ncclAllReduce on the library stream, and runs the CG replicated; efgp_fit_hetero
+ * (TOEPLITZ solver) does the same with its weighted modes (and min sigma_n).  NCCL is loaded at run
+ * time (libnccl.so.2); EFGP_ERR_NCCL if it is missing or a call fails.  nranks = 1 is allowed. */
+efgp_status efgp_comm_unique_id(void *id_out);
+efgp_status efgp_comm_init(efgp_handle, const void *id, int nranks, int rank);
 
 /* Multi-process split of efgp_fit.  efgp_fit_local spreads this rank's
  * shard and writes its partial modes (the Hermitian halves of v and F^*y, efgp_modes_count doubles)

@@ -33,7 +33,7 @@ class Info(C.Structure):
                 ("sorted_t2", C.c_int64), ("sorted_chunk", C.c_int64), ("sorted_round", C.c_int64),
                 ("spread_precision", C.c_int64), ("t_var_ms", C.c_double), ("var_iters_max", C.c_int64),
                 ("var_batch", C.c_int64), ("hetero_sorted", C.c_int64),
-                ("precond", C.c_int64)]
+                ("precond", C.c_int64), ("comm_size", C.c_int64)]
 
 
 # every symbol include/efgp.h declares, with (restype, argtypes)
@@ -45,6 +45,8 @@ SIGNATURES = {
     "efgp_fit": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
     "efgp_fit_hetero": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
     "efgp_modes_count": (C.c_int64, [C.c_void_p]),
+    "efgp_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "efgp_comm_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     "efgp_fit_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "efgp_fit_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
     "efgp_predict": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),

@@ -46,7 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in srcs]
     if force or jobs or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs +
-             ["-L/usr/local/cuda/lib64", "-lcufft", "-lcusolver", "-Xlinker", "-rpath=/usr/local/cuda/lib64"])
+             ["-L/usr/local/cuda/lib64", "-lcufft", "-lcusolver", "-ldl", "-Xlinker", "-rpath=/usr/local/cuda/lib64"])
     return LIB
 
 

@@ -305,7 +305,21 @@ efgp_status efgp_setup(efgp_handle *out, efgp_kernel kernel, double nu, double e
 efgp_status efgp_fit(efgp_handle pl, const double *x, const double *y, int64_t N) {
   if (!pl) return EFGP_ERR_INVALID;
   EFGP_TRY(fit_local_impl(pl, x, y, N, pl->modes));
+  if (pl->comm) {  // the one collective of a multi-GPU fit: partial modes and counts summed over ranks
+    EFGP_TRY(comm_sum(pl, pl->modes, (size_t)2 * (pl->P.Kvh + pl->P.Mh)));
+    EFGP_TRY(comm_count_min(pl, &N, nullptr));
+  }
   return fit_solve_impl(pl, pl->modes, N);
+}
+
+efgp_status efgp_comm_unique_id(void *id_out) {
+  if (!id_out) return EFGP_ERR_INVALID;
+  return comm_unique_id(id_out);
+}
+
+efgp_status efgp_comm_init(efgp_handle pl, const void *id, int nranks, int rank) {
+  if (!pl || !id) return EFGP_ERR_INVALID;
+  return comm_init(pl, id, nranks, rank);
 }
 
 efgp_status efgp_fit_hetero(efgp_handle pl, const double *x, const double *y, const double *noise_sd, int64_t N) {
@@ -532,6 +546,7 @@ efgp_status efgp_get_info(efgp_handle pl, efgp_info *o) {
   }
   o->hetero_sorted = pl->het_path;
   o->precond = P.precond;
+  o->comm_size = pl->comm_size;
   return EFGP_OK;
 }
 
@@ -557,6 +572,7 @@ const char *efgp_last_error(efgp_handle pl) { return pl ? pl->err.c_str() : "nul
 void efgp_destroy(efgp_handle pl) {
   if (!pl) return;
   if (pl->stream) cudaStreamSynchronize(pl->stream);
+  comm_destroy(pl);
   if (pl->cg_exec) cudaGraphExecDestroy(pl->cg_exec);
   if (pl->var_exec) cudaGraphExecDestroy(pl->var_exec);
   if (pl->pcg_exec) cudaGraphExecDestroy(pl->pcg_exec);
@@ -573,7 +589,7 @@ void efgp_destroy(efgp_handle pl) {
                   pl->scal, pl->hist, pl->dflags, pl->T2box, pl->t2grid, pl->stage[0], pl->stage[1],
                   pl->rec[0], pl->rec[1], pl->rec[2], pl->trace,
                   pl->sync_buf, pl->het_box, pl->het_grid, pl->pc_Q, pl->pc_F0, pl->pc_F1, pl->pc_work, pl->z,
-                  pl->pc_lam, pl->pc_info};
+                  pl->pc_lam, pl->pc_info, pl->comm_buf};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (pl->h_pinned) cudaFreeHost(pl->h_pinned);

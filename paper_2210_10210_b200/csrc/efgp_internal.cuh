@@ -186,6 +186,10 @@ struct efgp_plan {
   cudaGraphExec_t pcg_exec = nullptr;
   int pcg_exec_iters = 0;
   double pcg_exec_sigma2 = -1;  // sigma2_sys baked into the captured PCG graph (preconditioner scale)
+  // NCCL communicator owned by the handle (comm.cu): efgp_fit sums the partial modes over ranks
+  void *comm = nullptr;  // ncclComm_t
+  int comm_size = 0, comm_rank = 0;
+  double *comm_buf = nullptr;
   int het_path = 0;  // 1: last heteroskedastic fit used the sorted fused product
   cufftHandle plan_het_r2c = 0;  // D2Z on n2 (sorted path), created lazily
   // stream-ordered temporaries (hetero staging and sort, host-input chunks) come from this pool; it
@@ -248,6 +252,12 @@ efgp_status interp_weighted(efgp_plan *pl, const double *grid, int64_t n, const 
                             const double *sd, double *out, cudaStream_t s);
 // hetero.cu (NEXT-3): fit with per-point noise; x, y, sd device-resident
 efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, const double *sd, int64_t N);
+// comm.cu (multi-GPU plumbing; NCCL resolved at run time)
+efgp_status comm_unique_id(void *id_out);
+efgp_status comm_init(efgp_plan *pl, const void *id, int nranks, int rank);
+void comm_destroy(efgp_plan *pl);
+efgp_status comm_sum(efgp_plan *pl, double *buf, size_t n);
+efgp_status comm_count_min(efgp_plan *pl, int64_t *count, double *minval);
 // variance.cu
 efgp_status variance_targets(efgp_plan *pl, const double *xt, int64_t q, double *out, cudaStream_t s);
 }  // namespace efgp

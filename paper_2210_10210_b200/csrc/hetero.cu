@@ -587,9 +587,14 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
       }
     }
     EFGP_CUDA(cudaEventRecord(pl->ev[1], s));
+    double smin = 0;
+    std::memcpy(&smin, &mb, sizeof(smin));
+    int64_t Ntot = N;
+    if (st == EFGP_OK && pl->comm) {  // multi-GPU: v^w and F^*(y/sigma^2) are sums over the points
+      st = comm_sum(pl, pl->modes_sum, (size_t)2 * (P.Kvh + P.Mh));
+      if (st == EFGP_OK) st = comm_count_min(pl, &Ntot, &smin);
+    }
     if (st == EFGP_OK) {
-      double smin = 0;
-      std::memcpy(&smin, &mb, sizeof(smin));
       pl->sigma2_sys = 1.0;
       pl->cap_sigma = smin;
       st = toeplitz_setup(pl, pl->modes_sum, s);
@@ -598,9 +603,9 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
         pl->op_valid = true;
         if (P.precond) {
           st = precond_setup(pl, pl->modes_sum);
-          if (st == EFGP_OK) st = pcg_solve(pl, N);
+          if (st == EFGP_OK) st = pcg_solve(pl, Ntot);
         } else {
-          st = cg_solve(pl, N);
+          st = cg_solve(pl, Ntot);
         }
       }
       pl->het_path = 2;
@@ -611,7 +616,7 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
       pl->t_solve = elapsed_ms(pl->ev[2], pl->ev[4]);
       if (st == EFGP_OK || st == EFGP_ERR_NOCONVERGE) {
         pl->fitted = true;
-        pl->N_last = N;
+        pl->N_last = Ntot;
       }
       if (st == EFGP_ERR_NOCONVERGE) pl->err = "CG reached max_iter before the relative residual reached cg_tol";
     }
@@ -619,6 +624,10 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
     if (iv) cudaFreeAsync(iv, s);
     EFGP_CUDA(cudaStreamSynchronize(s));
     return st;
+  }
+  if (st == EFGP_OK && pl->comm && pl->comm_size > 1) {
+    pl->err = "fit_hetero: the NUFFT-pair solver is single-process (use hetero_method TOEPLITZ with a communicator)";
+    st = EFGP_ERR_INVALID;
   }
   // b = D F^*(y / sigma^2); spread_begin clears the input flags, spread_points raises dflags[0]
   if (st == EFGP_OK) st = spread_to_modes(pl, x, w, N, nullptr, pl->b, s);

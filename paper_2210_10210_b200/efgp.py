@@ -183,6 +183,26 @@ class EFGP:
             self._check(self._lib.efgp_fit_solve(self._h, C.c_void_p(modes.data_ptr()), int(N_total)))
         return self
 
+    def comm_init(self, group=None):
+        """Give the library its own NCCL communicator over the torch.distributed group (a 1-rank
+        communicator without torch.distributed).  Afterwards fit()/fit_hetero() take this rank's
+        shard and sum the partial modes over ranks inside the library (include/efgp.h)."""
+        import torch.distributed as dist
+        on = dist.is_available() and dist.is_initialized()
+        world = dist.get_world_size(group) if on else 1
+        rank = dist.get_rank(group) if on else 0
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            self._check(self._lib.efgp_comm_unique_id(uid), allow_noconverge=False)
+        if world > 1:
+            obj = [bytes(uid)]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(obj, src=src, group=group)
+            C.memmove(uid, obj[0], 128)
+        with self._torch.cuda.device(self.device):
+            self._check(self._lib.efgp_comm_init(self._h, uid, world, rank), allow_noconverge=False)
+        return self
+
     def fit_distributed(self, x, y, group=None):
         """Multi-GPU fit: local spreading, ONE allreduce of the partial modes
         over the process group, replicated CG.  x, y: this rank's shard."""

@@ -556,3 +556,25 @@ def test_refit_with_larger_problem_on_same_handle():
     assert len(g.residual_history()) == g.info()["iters"] + 1
     g.close()
     g2.close()
+
+
+def test_library_nccl_communicator_single_rank():
+    # efgp_comm_unique_id / efgp_comm_init with one rank: efgp_fit runs the in-library ncclAllReduce of
+    # the partial modes and of N (identity for one rank) and must give the plain fit's answer
+    c = CONFIGS["c5"]
+    x, y, xt = generate(c, N=50_000, q=300)
+    g0 = model(c, cg_tol=1e-10)
+    g0.fit(dev(x), dev(y))
+    g1 = model(c, cg_tol=1e-10)
+    g1.comm_init()
+    assert g1.info()["comm_size"] == 1
+    g1.fit(dev(x), dev(y))
+    assert g1.info()["N"] == 50_000
+    assert rel(g1.vector("v"), g0.vector("v")) < 1e-13
+    assert rel(g1.predict(dev(xt)).cpu().numpy(), g0.predict(dev(xt)).cpu().numpy()) < 10 * c.eps
+    sd = np.full(len(x), c.sigma)
+    g1.fit_hetero(dev(x), dev(y), dev(sd))                         # TOEPLITZ solver with the communicator
+    assert g1.info()["hetero_sorted"] == 2
+    assert rel(g1.predict(dev(xt)).cpu().numpy(), g0.predict(dev(xt)).cpu().numpy()) < 10 * c.eps
+    g0.close()
+    g1.close()
