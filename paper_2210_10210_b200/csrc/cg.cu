@@ -32,6 +32,28 @@ struct CGState {
 
 constexpr int kCGThreads = 256;
 
+// Programmatic dependent launch between the CG's own kernels (launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel lets its successor be scheduled at
+// once (launch_dependents) and waits for its predecessor's completion and memory (wait) before
+// touching any data, so consecutive launches overlap their latency instead of serialising it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ double block_sum(double v, double *sh) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -137,6 +159,7 @@ __global__ void k_cg_apply(const double2 *__restrict__ Z, const double2 *__restr
                            double2 *__restrict__ Ap, int64_t Mh, int m, int64_t L, const CGState *st,
                            double *__restrict__ part) {
   __shared__ double sh[40];
+  pdl_trigger();
   if (st->done) return;
   const double s2 = st->sigma2;
   double acc = 0.0;
@@ -169,6 +192,8 @@ __global__ void k_cg_xr(double2 *__restrict__ x, double2 *__restrict__ r, const 
                         const double *__restrict__ part_pAp, double *__restrict__ part_rr, int nblk,
                         const double *__restrict__ part_rz = nullptr) {
   __shared__ double sh[40];
+  pdl_wait();
+  pdl_trigger();
   if (st->done) return;
   const double pAp = reduce_partials(part_pAp, nblk, sh);
   // CG: alpha = (r,r)/(p,Ap); PCG: alpha = (r,z)/(p,Ap), (r,z) reduced from its partials
@@ -201,6 +226,8 @@ __global__ void k_cg_p(const double2 *__restrict__ r, double2 *__restrict__ p, c
                        int64_t Mh, int m, int64_t L, double2 *__restrict__ X, int64_t box, CGState *st,
                        const double *__restrict__ part_rr, int nblk, double *__restrict__ hist) {
   __shared__ double sh[40];
+  pdl_wait();
+  pdl_trigger();
   if (st->done) return;
   const double rr_new = reduce_partials(part_rr, nblk, sh);
   const double bcg = rr_new / st->rr_old;
@@ -224,6 +251,7 @@ template <int D>
 __global__ void k_cg_pad(const double2 *__restrict__ p, const double *__restrict__ Dh, int m, int64_t L,
                          double2 *__restrict__ X, int64_t box, const CGState *st) {
   // runs even when done was just set: harmless (the next C2R input is never used)
+  pdl_wait();
   pad_box<D>(p, Dh, m, L, X, box);
 }
 
@@ -259,10 +287,12 @@ static efgp_status enqueue_iteration(efgp_plan *pl, cudaStream_t s, CGState *st,
   k_mul<<<nblocks(Ld, pl->num_sms), kCGThreads, 0, s>>>(pl->Yr, pl->vhat, Ld, st);
   EFGP_CUFFT(cufftExecD2Z(pl->plan_r2c_L, pl->Yr, pl->Zbox));
   k_cg_apply<D><<<nb, kCGThreads, 0, s>>>(pl->Zbox, pl->p, pl->D_half, pl->Ap, P.Mh, (int)P.m, P.L, st, part_pAp);
-  k_cg_xr<<<nb, kCGThreads, 0, s>>>(pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp, part_rr, (int)nb);
-  k_cg_p<D><<<nb, kCGThreads, 0, s>>>(pl->r, pl->p, pl->D_half, P.Mh, (int)P.m, P.L, pl->Xbox, box, st, part_rr,
-                                      (int)nb, pl->hist);
-  k_cg_pad<D><<<nbox, kCGThreads, 0, s>>>(pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box, st);
+  EFGP_CUDA(launch_pdl(k_cg_xr, nb, kCGThreads, s, pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp,
+                       part_rr, (int)nb, (const double *)nullptr));
+  EFGP_CUDA(launch_pdl(k_cg_p<D>, nb, kCGThreads, s, pl->r, pl->p, pl->D_half, P.Mh, (int)P.m, P.L, pl->Xbox, box,
+                       st, part_rr, (int)nb, pl->hist));
+  EFGP_CUDA(launch_pdl(k_cg_pad<D>, nbox, kCGThreads, s, pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box,
+                       (const CGState *)st));
   EFGP_CUDA(cudaGetLastError());
   return EFGP_OK;
 }
