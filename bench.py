@@ -72,25 +72,39 @@ class ClockSampler:
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
-        self.lines = []
+        self.lines = []  # (arrival time, csv line)
         self.proc = None
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
+        """Start nvidia-smi sampling (every 20 ms) before the timed region, so that it is already
+        producing samples when the region starts (its start-up takes ~0.1-0.3 s)."""
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "100", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                                          "-lms", "20", "-i", str(self.idx)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.time() + 5.0
+            while not self.lines and time.time() < deadline:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
 
+    def __enter__(self):
+        if self.proc is None:
+            self.start()
+        self.t0 = time.time()
+        return self
+
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *a):
+        self.t1 = time.time()
+        time.sleep(0.05)  # the sample that covers the end of the region
         if self.proc:
             self.proc.terminate()
             try:
@@ -102,7 +116,10 @@ class ClockSampler:
     def summary(self):
         sm, smax, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0 = self.t0 if self.t0 is not None else 0.0
+        t1 = (self.t1 if self.t1 is not None else time.time()) + 0.045
+        inside = [ln for (ta, ln) in self.lines if t0 <= ta <= t1]
+        for ln in inside:
             f = [s.strip() for s in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -216,13 +233,14 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    clk = ClockSampler(local).start()  # sampling is running before the timed region starts
     for _ in range(max(args.warmup, 0)):
         step(x, y, xt, mu)
     barrier()
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     spread_ms, solve_ms, modes_ms, pred_ms, iters, launches = [], [], [], [], [], 0
-    with ClockSampler(local) as clk:
+    with clk:
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
