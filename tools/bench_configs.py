@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--c5-N", type=float, default=None)
     ap.add_argument("--var-targets", type=int, default=0, help="also time the posterior variance (NEXT-2)")
     ap.add_argument("--precond", default="none", choices=["none", "kron", "auto"], help="NEXT-4 preconditioner")
+    ap.add_argument("--hetero", action="store_true", help="also time NEXT-3 (fit_hetero, sigma_n = sigma (0.5 + U))")
     a = ap.parse_args()
     import torch
     from efgp_data import CONFIGS
@@ -65,6 +66,19 @@ def main():
             iv = g.info()
             out["variance"] = {"q": qv, "ms": iv["t_var_ms"], "targets_per_s": qv / (iv["t_var_ms"] / 1e3),
                                "cg_iters_max": iv["var_iters_max"]}
+        if a.hetero:
+            gen = torch.Generator(device=x.device)
+            gen.manual_seed(99)
+            sd = c.sigma * (0.5 + torch.rand(N, dtype=torch.float64, device=x.device, generator=gen))
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                g.fit_hetero(x, y, sd)
+                g.fit_hetero(x, y, sd)
+            ih = g.info()
+            out["hetero"] = {"solver": {0: "nufft-unfused", 1: "nufft-sorted", 2: "toeplitz"}[ih["hetero_sorted"]],
+                             "iters": ih["iters"], "ms": ih["t_spread_ms"] + ih["t_modes_ms"] + ih["t_solve_ms"],
+                             "type1_ms": ih["t_spread_ms"], "solve_ms": ih["t_solve_ms"]}
+            del sd
         print(json.dumps(out), flush=True)
         g.close()
         del x, y, xt, mu
