@@ -404,18 +404,55 @@ __global__ void __launch_bounds__(kVarThreads) k_var_eval(const double *__restri
   if (threadIdx.x == 0) out[t] = s;
 }
 
+static void free_var(efgp_plan *pl) {
+  if (pl->var_exec) cudaGraphExecDestroy(pl->var_exec);
+  pl->var_exec = nullptr;
+  for (cufftHandle *h : {&pl->plan_var_c2r, &pl->plan_var_r2c})
+    if (*h) {
+      cufftDestroy(*h);
+      *h = 0;
+    }
+  for (void **b : {(void **)&pl->var_x, (void **)&pl->var_r, (void **)&pl->var_p, (void **)&pl->var_Ap,
+                   (void **)&pl->var_X, (void **)&pl->var_Z, (void **)&pl->var_Y, &pl->var_st})
+    if (*b) {
+      cudaFree(*b);
+      *b = nullptr;
+    }
+  pl->var_B = 0;
+}
+
+// batch of targets per CG: the call's q (rounded up to 16), within min(8 GB, free / 4) of buffers
+// (c4's 3D boxes are ~95 MB per target: a fixed 768 MB budget allowed 8 targets per batch); every
+// batched FFT runs B wide, so B is not larger than the work (q) either
 template <int D>
-static efgp_status setup_var(efgp_plan *pl) {
+static int64_t var_batch_size(const efgp_plan *pl, int64_t q) {
   const Params &P = pl->P;
   int64_t box = P.L / 2 + 1, Ld = P.L;
   for (int k = 0; k < D - 1; ++k) {
     box *= P.L;
     Ld *= P.L;
   }
-  // batch size: ~768 MB of per-target buffers
-  const int64_t per = 4 * P.Mh * 16 + 2 * box * 16 + Ld * 8 + (int64_t)sizeof(VarTarget);
-  int64_t B = std::max<int64_t>(1, std::min<int64_t>(2048, (int64_t(768) << 20) / per));
+  const int64_t per = 4 * P.Mh * 16 + 2 * box * 16 + Ld * 8 + 64;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    cudaGetLastError();
+    free_b = size_t(4) << 30;
+  }
+  const int64_t budget = std::min<int64_t>(int64_t(8) << 30, (int64_t)(free_b / 4) + (int64_t)pl->var_B * per);
+  int64_t B = std::max<int64_t>(1, std::min<int64_t>({int64_t(2048), budget / per, (q + 15) / 16 * 16}));
   if (const char *e = std::getenv("EFGP_VAR_BATCH")) B = std::max<int64_t>(1, std::min<int64_t>(B, std::atoll(e)));
+  return B;
+}
+
+template <int D>
+static efgp_status setup_var(efgp_plan *pl, int64_t Bwant) {
+  const Params &P = pl->P;
+  int64_t box = P.L / 2 + 1, Ld = P.L;
+  for (int k = 0; k < D - 1; ++k) {
+    box *= P.L;
+    Ld *= P.L;
+  }
+  const int64_t B = Bwant;
   pl->var_B = (int)B;
   EFGP_CUDA(cudaMalloc((void **)&pl->var_x, B * P.Mh * 16));
   EFGP_CUDA(cudaMalloc((void **)&pl->var_r, B * P.Mh * 16));
@@ -519,7 +556,9 @@ static efgp_status var_targets_d(efgp_plan *pl, const double *xt, int64_t q, dou
     pl->err = "posterior variance: m too large for the per-target phasor tables";
     return EFGP_ERR_INVALID;
   }
-  if (!pl->var_x) EFGP_TRY(setup_var<D>(pl));
+  const int64_t Bw = var_batch_size<D>(pl, q);
+  if (pl->var_x && (Bw > pl->var_B || 4 * Bw < pl->var_B)) free_var(pl);  // resize to the work
+  if (!pl->var_x) EFGP_TRY(setup_var<D>(pl, Bw));
   if (pl->var_exec && pl->var_exec_max_iter != (int)std::min<int64_t>(pl->max_iter_used > 0 ? pl->max_iter_used : 1000, 1 << 30)) {
     cudaGraphExecDestroy(pl->var_exec);  // the cap is baked into the graph
     pl->var_exec = nullptr;
