@@ -41,11 +41,12 @@ def parse():
     ap.add_argument("--q", type=float, default=None, help="override the number of targets")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-interp-n", action="store_true", help="skip the NEXT-1 measurement (mu at the N points)")
-    ap.add_argument("--variance", action="store_true",
-                    help="also time NEXT-2 (posterior variance; at N=1e9 its CG needs ~5e4 iterations: minutes)")
-    ap.add_argument("--var-targets", type=float, default=256, help="targets of the NEXT-2 measurement")
-    ap.add_argument("--hetero", action="store_true",
-                    help="also time NEXT-3 (heteroskedastic fit: a type-2 + type-1 NUFFT pair per CG iteration)")
+    ap.add_argument("--no-variance", action="store_true",
+                    help="skip NEXT-2 (posterior variance at --var-targets targets; ~4.3e4 CG iterations at N=1e9)")
+    ap.add_argument("--variance", action="store_true", help=argparse.SUPPRESS)  # (default on; kept for old scripts)
+    ap.add_argument("--var-targets", type=float, default=64, help="targets of the NEXT-2 measurement")
+    ap.add_argument("--no-hetero", action="store_true", help="skip NEXT-3 (heteroskedastic fit, both solvers)")
+    ap.add_argument("--hetero", action="store_true", help=argparse.SUPPRESS)  # (default on)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-points", type=float, default=1e6, help="cpu_baseline sample size")
     ap.add_argument("--spread", default="auto")
@@ -285,13 +286,13 @@ def main():
 
     # NEXT-2: posterior variance at a sample of the targets (eqs eta/sws, batched CG)
     variance = None
-    if args.variance:
+    if not args.no_variance:
         try:
             qv = min(int(args.var_targets), xt.shape[0])
             var = torch.empty(qv, dtype=torch.float64, device=dev)
             model.predict_var(xt[:qv], out=var)  # warm-up (allocates the batched buffers, captures the graph)
             tv = []
-            for _ in range(2):
+            for _ in range(1):
                 model.predict_var(xt[:qv], out=var)
                 tv.append(model.info()["t_var_ms"])
             iv = model.info()
@@ -305,7 +306,7 @@ def main():
     # NEXT-3: heteroskedastic fit, sigma_n = sigma (0.5 + u), u ~ U[0,1) (seeded); every
     # CG iteration is K8 + C2R + K9 (q = N, fused / sigma_n^2) + K1 (N points) + R2C + deconvolution
     hetero = None
-    if args.hetero:
+    if not args.no_hetero:
         try:
             gen = torch.Generator(device=dev)
             gen.manual_seed(1234 + rank)
