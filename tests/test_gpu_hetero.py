@@ -152,3 +152,27 @@ def test_hetero_large_n_two_noise_levels():
     assert rel(mu_h, mu_ref) <= 10 * c.eps, rel(mu_h, mu_ref)
     g.close()
     g2.close()
+
+
+def test_hetero_toeplitz_with_kron_preconditioner():
+    # the TOEPLITZ solver accepts the NEXT-4 preconditioner (factors from the weighted v^w, sigma^2 -> 1):
+    # same answer as the plain CG, fewer iterations (c3: SE, separable density)
+    from efgp_data import gpu as G
+    import torch
+    c = CONFIGS["c3"]
+    N = 200_000
+    x, y = G.generate_points(c, 0, N)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7)
+    sd = c.sigma * (0.5 + torch.rand(N, dtype=torch.float64, device="cuda", generator=gen))
+    xt = dev(np.random.default_rng(8).uniform(0, 1, (300, 2)))
+    out = {}
+    for pc in (None, "kron"):
+        g = model(c, cg_tol=c.eps / 1000, precond=pc)               # parity mode (reading G9)
+        g.fit_hetero(x, y, sd)
+        inf = g.info()
+        assert inf["hetero_sorted"] == 2 and inf["precond"] == (1 if pc else 0)
+        out[pc] = (g.predict(xt).cpu().numpy(), inf["iters"])
+        g.close()
+    assert rel(out["kron"][0], out[None][0]) <= 10 * c.eps
+    assert out["kron"][1] < out[None][1] / 2, (out["kron"][1], out[None][1])
