@@ -14,6 +14,7 @@ by index, partial modes are summed with one NCCL allreduce, CG replicated, targe
 from __future__ import annotations
 
 import argparse
+import warnings
 import json
 import math
 import os
@@ -46,6 +47,7 @@ def parse():
     ap.add_argument("--variance", action="store_true", help=argparse.SUPPRESS)  # (default on; kept for old scripts)
     ap.add_argument("--var-targets", type=float, default=64, help="targets of the NEXT-2 measurement")
     ap.add_argument("--no-hetero", action="store_true", help="skip NEXT-3 (heteroskedastic fit, both solvers)")
+    ap.add_argument("--no-spread-variants", action="store_true", help="skip the fp32 / mixed K1 arithmetic variants")
     ap.add_argument("--hetero", action="store_true", help=argparse.SUPPRESS)  # (default on)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-points", type=float, default=1e6, help="cpu_baseline sample size")
@@ -305,6 +307,26 @@ def main():
 
     # NEXT-3: heteroskedastic fit, sigma_n = sigma (0.5 + u), u ~ U[0,1) (seeded); every
     # CG iteration is K8 + C2R + K9 (q = N, fused / sigma_n^2) + K1 (N points) + R2C + deconvolution
+    # K1 arithmetic variants ("report both variants"): the spreading time of one fit with
+    # fp32 kernel weights (FP32) and fp32 weights + fp32 round sums (MIXED) beside the fp64 headline
+    spread_variants = None
+    if not args.no_spread_variants and args.spread in ("auto", "sorted") and cfg.eps / 10 >= 1e-6:
+        try:
+            spread_variants = {"fp64": {"ms": statistics.median(spread_ms), "points_per_s": (b - a) / (statistics.median(spread_ms) / 1e3)}}
+            for wv in ("fp32", "mixed"):
+                mv = EFGP(cfg.kernel, cfg.ell, cfg.sigma, cfg.eps, cfg.d, cfg.nu, spread=args.spread, weights=wv,
+                          max_iter=1)
+                ts = []
+                for _ in range(2):
+                    with warnings.catch_warnings():
+                        warnings.simplefilter("ignore")
+                        mv.fit(x, y)
+                    ts.append(mv.info()["t_spread_ms"])
+                spread_variants[wv] = {"ms": ts[-1], "points_per_s": (b - a) / (ts[-1] / 1e3)}
+                mv.close()
+        except Exception as exc:
+            spread_variants = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
     hetero = None
     if not args.no_hetero:
         try:
@@ -407,7 +429,7 @@ def main():
                             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                             "alg_bytes_per_launch": alg_bytes},
                "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "mu_at_training_points": interp_n,
-               "posterior_variance": variance, "hetero_fit": hetero}
+               "posterior_variance": variance, "hetero_fit": hetero, "spread_variants": spread_variants}
         if not args.no_cpu_baseline:
             try:
                 ns = int(args.oracle_points)
