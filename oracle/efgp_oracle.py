@@ -21,7 +21,9 @@ fast transform replaced by the sum that defines it:
   NEXT-4  preconditioner ...... :func:`kron_preconditioner` + :func:`pcg` (reading G12):
                                  M = A_1 (x) ... (x) A_d + sigma^2 I from the axis lines of v and D
   NEXT-3  sigma_n ............. :func:`efgp_fit_hetero` CG on (Phi^* S^-1 Phi + I) beta = Phi^* S^-1 y,
-                                 S = diag(sigma_n^2) (reading G11), Phi applied densely
+                                 S = diag(sigma_n^2) (P:2759-2763, reading G11), Phi applied densely;
+                                 :func:`toeplitz_vector_weighted` (reading G11b: Phi^* S^-1 Phi =
+                                 D T(v^w) D); :func:`posterior_variance_hetero` (dense solve)
 
 Readings where the paper is silent, garbled or inconsistent:
   G1  exponent signs: v_j = sum_n exp(-2 pi i h j.x_n), (F^*y)_j = sum_n exp(-2 pi i h j.x_n) y_n,
@@ -35,6 +37,7 @@ Readings where the paper is silent, garbled or inconsistent (DESIGN.md "Readings
       A_i = diag(delta_i) T_i diag(delta_i) / N^((d-1)/d), M = A_1 (x) ... (x) A_d + sigma^2 I, applied as
       (Q_1 (x) ... ) (Lambda + sigma^2)^-1 (Q_1 (x) ...)^* from eigh(A_i).  Exact (M = A) when the points
       form a tensor-product set and D is separable (SE); d = 1 gives M = A.  Standard PCG, same stop rule.
+  G11b Phi^* S^-1 Phi = D T(v^w) D with v^w = eq 88 with strengths sigma_n^-2 (pinned densely).
   G11 heteroskedastic noise (P:2759-2763 names it, gives no formula): the weight-space posterior mean
       for y = Phi beta + e, beta ~ N(0, I), e ~ N(0, S), S = diag(sigma_n^2): beta solves
       (Phi^* S^-1 Phi + I) beta = Phi^* S^-1 y, mu(x*) = phi(x*) beta.  With sigma_n = sigma it is
