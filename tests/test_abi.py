@@ -52,3 +52,28 @@ def test_missing_library_fails_loudly(tmp_path):
             _lib.load(str(tmp_path / "nope.so"))
     finally:
         _lib._lib = saved
+
+
+def _struct_fields(name):
+    """Field names of `typedef struct { ... } name;` in include/efgp.h, in declaration order."""
+    src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    m = re.search(r"typedef struct \{([^{}]*)\}\s*" + name + r";", src)
+    assert m, name
+    out = []
+    for decl in m.group(1).split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        # "double t_spread_ms, t_modes_ms" / "void *stream" / "int64_t nf1, nf2, L"
+        first, *rest = [d.strip() for d in decl.split(",")]
+        out.append(re.split(r"[\s*]+", first)[-1])
+        out.extend(r.lstrip("*").strip() for r in rest)
+    return out
+
+
+@pytest.mark.parametrize("cname,pyname", [("efgp_options", "Options"), ("efgp_info", "Info")])
+def test_binding_structs_match_header(cname, pyname):
+    # the ctypes mirrors must list the header's fields in the same order (ABI: layout by position)
+    from paper_2210_10210_b200 import _lib
+    py = [f for f, _ in getattr(_lib, pyname)._fields_]
+    assert py == _struct_fields(cname)
