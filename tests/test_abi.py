@@ -77,3 +77,25 @@ def test_binding_structs_match_header(cname, pyname):
     from paper_2210_10210_b200 import _lib
     py = [f for f, _ in getattr(_lib, pyname)._fields_]
     assert py == _struct_fields(cname)
+
+
+@pytest.mark.parametrize("cname,pyname", [("efgp_options", "Options"), ("efgp_info", "Info")])
+def test_binding_struct_offsets_match_c(cname, pyname, tmp_path):
+    # byte offsets and size of each field as the C compiler lays them out (gcc on the header) equal
+    # the ctypes mirror's (catches a type mismatch, not only a name or order mismatch)
+    import shutil
+    import subprocess
+    from paper_2210_10210_b200 import _lib
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    names = _struct_fields(cname)
+    src = tmp_path / "off.c"
+    body = "".join(f'  printf("%zu\\n", offsetof({cname}, {n}));\n' for n in names)
+    src.write_text(f'#include <stdio.h>\n#include <stddef.h>\n#include "{HEADER}"\nint main(void) {{\n{body}'
+                   f'  printf("%zu\\n", sizeof({cname}));\n  return 0;\n}}\n')
+    exe = tmp_path / "off"
+    subprocess.run(["gcc", str(src), "-o", str(exe)], check=True)
+    c_vals = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    cls = getattr(_lib, pyname)
+    py_vals = [getattr(cls, n).offset for n in names] + [ctypes.sizeof(cls)]
+    assert py_vals == c_vals
