@@ -176,3 +176,26 @@ def test_hetero_toeplitz_with_kron_preconditioner():
         g.close()
     assert rel(out["kron"][0], out[None][0]) <= 10 * c.eps
     assert out["kron"][1] < out[None][1] / 2, (out["kron"][1], out[None][1])
+
+
+@pytest.mark.parametrize("eps", [1e-1, 1e-2, 1e-5])
+def test_hetero_solvers_agree_every_width(eps):
+    # the NUFFT-pair solver (sorted fused pass, widths W = 3, 4, 7 here) and the TOEPLITZ solver solve
+    # the same system: their means agree to the NUFFT tolerance (both CGs in parity mode)
+    from paper_2210_10210_b200 import EFGP
+    rng = np.random.default_rng(int(1 / eps))
+    N = 30_000
+    x = rng.uniform(0, 1, (N, 2))
+    y = np.sin(5 * x[:, 0]) * np.cos(3 * x[:, 1]) + 0.1 * rng.standard_normal(N)
+    sd = 0.1 * (0.5 + rng.uniform(0, 1, N))
+    xt = rng.uniform(0, 1, (200, 2))
+    mus, ws = {}, {}
+    for meth in ("nufft", "toeplitz"):
+        g = EFGP("matern", 0.2, 0.1, eps, 2, 1.5, cg_tol=eps / 1000, hetero=meth)
+        g.fit_hetero(dev(x), dev(y), dev(sd))
+        inf = g.info()
+        assert inf["hetero_sorted"] == (1 if meth == "nufft" else 2)
+        mus[meth] = g.predict(dev(xt)).cpu().numpy()
+        ws[meth] = inf["w"]
+        g.close()
+    assert rel(mus["nufft"], mus["toeplitz"]) <= 10 * eps, rel(mus["nufft"], mus["toeplitz"])

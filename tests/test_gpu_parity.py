@@ -578,3 +578,27 @@ def test_library_nccl_communicator_single_rank():
     assert rel(g1.predict(dev(xt)).cpu().numpy(), g0.predict(dev(xt)).cpu().numpy()) < 10 * c.eps
     g0.close()
     g1.close()
+
+
+@pytest.mark.parametrize("d,eps", [(2, 1e-1), (2, 1e-2), (2, 1e-3), (2, 1e-4), (2, 1e-5), (2, 1e-6),
+                                   (3, 1e-1), (3, 1e-2), (3, 1e-3), (3, 1e-4)])
+def test_every_kernel_width_matches_global(d, eps):
+    # every ES width W = 3..8 (eps 1e-1 .. 1e-6) through the strategy AUTO picks (SORTED in 2D up to
+    # W = 6, CELLSORT beyond and in 3D) against GLOBAL on the same grids: v to roundoff, F^*y to the
+    # NUFFT tolerance (y goes to the n1 grid in SORTED / CELLSORT, to n2 in GLOBAL)
+    from paper_2210_10210_b200 import EFGP
+    rng = np.random.default_rng(int(1 / eps) + d)
+    N = 40_000 if d == 2 else 20_000
+    x = rng.uniform(0, 1, (N, d))
+    y = np.sin(5 * x[:, 0]) + 0.1 * rng.standard_normal(N)
+    out = {}
+    for spread in ("auto", "global"):
+        g = EFGP("matern", 0.2, 0.1, eps, d, 1.5, max_iter=1, m=6 if d == 3 else 10, h=0.4, spread=spread)
+        with pytest.warns(RuntimeWarning):
+            g.fit(dev(x), dev(y))
+        out[spread] = (g.vector("v"), g.vector("rhs"), g.info())
+        g.close()
+    inf = out["auto"][2]
+    assert inf["spread_method"] == ("sorted" if d == 2 and inf["w"] <= 6 else "cellsort"), inf["spread_method"]
+    assert rel(out["auto"][0], out["global"][0]) < 1e-12
+    assert rel(out["auto"][1], out["global"][1]) < 2 * inf["nufft_tol"]
