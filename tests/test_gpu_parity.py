@@ -602,3 +602,23 @@ def test_every_kernel_width_matches_global(d, eps):
     assert inf["spread_method"] == ("sorted" if d == 2 and inf["w"] <= 6 else "cellsort"), inf["spread_method"]
     assert rel(out["auto"][0], out["global"][0]) < 1e-12
     assert rel(out["auto"][1], out["global"][1]) < 2 * inf["nufft_tol"]
+
+
+@pytest.mark.parametrize("d,eps", [(1, 1e-1), (1, 1e-9), (2, 1e-1), (2, 1e-2), (2, 1e-5), (3, 1e-2), (3, 1e-5)])
+def test_type2_every_kernel_width(d, eps):
+    # K9 at widths the configs do not use (W = 3 .. 11), shared-memory and L2 gather variants, against
+    # the oracle's direct sum, from random Hermitian weights
+    from paper_2210_10210_b200 import EFGP, full_to_half
+    m = {1: 20, 2: 10, 3: 5}[d]
+    g = EFGP("matern", 0.2, 0.1, eps, d, 1.5, m=m, h=0.45)
+    inf = g.info()
+    rng = np.random.default_rng(7 + d)
+    full = rng.normal(size=(2 * m + 1,) * d) + 1j * rng.normal(size=(2 * m + 1,) * d)
+    full = 0.5 * (full + np.conj(full[(slice(None, None, -1),) * d]))
+    g.load_weights(full_to_half(full))
+    xt = np.concatenate([rng.uniform(0, 1, (700, d)), np.zeros((1, d)), np.ones((1, d))])
+    mu = g.predict(dev(xt)).cpu().numpy()
+    D = O.spectral_weights("matern", 0.2, d, 0.45, m, 1.5)
+    ref = O.posterior_mean(full, D, 0.45, xt)
+    assert rel(mu, ref) <= 5 * inf["nufft_tol"], (inf["w"], rel(mu, ref))
+    g.close()
