@@ -622,3 +622,4 @@ def test_type2_every_kernel_width(d, eps):
     ref = O.posterior_mean(full, D, 0.45, xt)
     assert rel(mu, ref) <= 5 * inf["nufft_tol"], (inf["w"], rel(mu, ref))
     g.close()
+
