@@ -255,6 +255,106 @@ __global__ void k_cg_pad(const double2 *__restrict__ p, const double *__restrict
   pad_box<D>(p, Dh, m, L, X, box);
 }
 
+
+// Toeplitz product by direct convolution (2D, small m; toeplitz_direct): CTA = output row j1.
+//   out_j = sum_{k in J_m} v_{j-k} u_k,  u = D p (Hermitian completion of the half),  j = (j1, 0..m)
+//   Ap_j = D_j out_j + sigma^2 p_j,  partial <p, Ap>
+// Replaces pad + C2R + multiply + R2C + apply of the FFT path; the same operator (the FFT path's
+// circulant embedding is exact for |j - k| <= 2m), summed directly.  c3 / c5: 25-28 -> 20-21 us per
+// CG iteration (1024 threads; 256 threads gave 23-24 us, a thread per output 27 us).
+constexpr int kToepThreads = 1024;
+__global__ void __launch_bounds__(kToepThreads) k_cg_toep2(const double2 *__restrict__ vfull,
+                                                           const double2 *__restrict__ p,
+                                                           const double *__restrict__ Dh, double2 *__restrict__ Ap,
+                                                           int m, const CGState *st, double *__restrict__ part) {
+  extern __shared__ double2 tsm[];
+  __shared__ double sh[40];
+  pdl_trigger();
+  if (st->done) return;
+  const int n = 2 * m + 1, nv = 4 * m + 1, j1 = (int)blockIdx.x - m;
+  double2 *u = tsm;                // n x n: u[(k1+m) n + (k2+m)]
+  double2 *vr = tsm + n * n;       // n rows x nv: vr[(k1+m) nv + (s+2m)] = v_{j1-k1, s}
+  double2 *red = vr + n * nv;      // partial sums [slices][m+1]
+  // u from the canonical half (k2 > 0, or k2 = 0 and k1 >= 0): the redundant (k1 < 0, 0) entries of the
+  // stored half are not read, so the product is exactly Hermitian (the FFT path's C2R projects the
+  // same way); without this the CG stalls on the c3 systems (roundoff in the j2 = 0 plane)
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    int k1 = idx / n - m, k2 = idx % n - m;
+    const bool neg = k2 < 0 || (k2 == 0 && k1 < 0);
+    if (neg) {
+      k1 = -k1;
+      k2 = -k2;
+    }
+    const int64_t q = (int64_t)(k1 + m) * (m + 1) + k2;
+    const double2 pp = p[q];
+    const double dq = Dh[q];
+    u[idx] = make_double2(dq * pp.x, neg ? -dq * pp.y : dq * pp.y);
+  }
+  for (int idx = threadIdx.x; idx < n * nv; idx += blockDim.x) {
+    const int k1 = idx / nv - m, sc = idx % nv;
+    vr[idx] = vfull[(int64_t)(j1 - k1 + 2 * m) * nv + sc];
+  }
+  __syncthreads();
+  // each thread: 4 consecutive outputs j2 .. j2+3 over a slice of the k1 rows; along k2 the four
+  // v_{j1-k1, j2+o-k2} form a sliding window (one new shared load per step): 2 loads per 4 MACs
+  const int nout = m + 1, ngrp = (nout + 3) / 4, slices = blockDim.x / ngrp;
+  const int t = threadIdx.x, g4 = t % ngrp, sl = t / ngrp, j2b = 4 * g4;
+  if (sl < slices) {
+    double re[4] = {0.0, 0.0, 0.0, 0.0}, im[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k1 = sl; k1 < n; k1 += slices) {  // k1 + m
+      const double2 *ur = u + k1 * n;
+      // v index of (j2b + o) - k2 at k2 = -m: j2b + o + m + 2m
+      const double2 *vrow = vr + k1 * nv + (j2b + 3 * m);
+      double2 w[4];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) w[o] = (j2b + o <= m) ? vrow[o] : make_double2(0.0, 0.0);
+      for (int k2 = 0; k2 < n; ++k2) {  // k2 + m; the window moves down by one cell per step
+        const double2 b = ur[k2];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+          re[o] = fma(w[o].x, b.x, fma(-w[o].y, b.y, re[o]));
+          im[o] = fma(w[o].x, b.y, fma(w[o].y, b.x, im[o]));
+        }
+#pragma unroll
+        for (int o = 3; o > 0; --o) w[o] = w[o - 1];
+        const int nxt = j2b + 3 * m - (k2 + 1);  // v index of output j2b at the next k2
+        w[0] = (k2 + 1 < n) ? vr[k1 * nv + nxt] : make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < 4; ++o)
+      if (j2b + o <= m) red[sl * nout + j2b + o] = make_double2(re[o], im[o]);
+  }
+  __syncthreads();
+  double acc = 0.0;
+  if (t < nout && !(t == 0 && j1 < 0)) {  // (j1 < 0, 0) is written by row -j1 as the conjugate
+    double2 o = make_double2(0.0, 0.0);
+    for (int k = 0; k < slices; ++k) {
+      o.x += red[k * nout + t].x;
+      o.y += red[k * nout + t].y;
+    }
+    const int64_t q = (int64_t)(j1 + m) * (m + 1) + t;
+    const double2 pp = p[q];
+    const double dq = Dh[q], s2 = st->sigma2;
+    double2 a = make_double2(dq * o.x + s2 * pp.x, dq * o.y + s2 * pp.y);
+    if (t == 0 && j1 == 0) a.y = s2 * pp.y;  // j = 0: (T u)_0 is real
+    Ap[q] = a;
+    acc = (t ? 2.0 : 1.0) * (pp.x * a.x + pp.y * a.y);
+    if (t == 0 && j1 > 0) {  // the mirrored entry (-j1, 0) = conj, with the canonical p
+      Ap[(int64_t)(m - j1) * (m + 1)] = make_double2(a.x, -a.y);
+      acc *= 2.0;
+    }
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+static size_t toep2_smem(int m) {
+  const int n = 2 * m + 1, nv = 4 * m + 1;
+  const int nout = m + 1, slices = kToepThreads / ((nout + 3) / 4);
+  return sizeof(double2) * ((size_t)n * n + (size_t)n * nv + (size_t)slices * nout);
+}
+
 static efgp_status ensure_hist(efgp_plan *pl, int64_t max_iter) {
   if (max_iter + 1 > pl->hist_cap) {
     for (cudaGraphExec_t *e : {&pl->cg_exec, &pl->pcg_exec})  // captured graphs hold the old pointer
@@ -283,16 +383,26 @@ static efgp_status enqueue_iteration(efgp_plan *pl, cudaStream_t s, CGState *st,
                                      unsigned nb, unsigned nbox) {
   const Params &P = pl->P;
   double *part_pAp = pl->partials, *part_rr = pl->partials + pl->cg_blocks;
+  const bool direct = D == 2 && toeplitz_direct(P);
+  if (direct) {  // the partials come from 2m+1 CTAs
+    const int nrow = (int)(2 * P.m + 1);
+    k_cg_toep2<<<nrow, kToepThreads, toep2_smem((int)P.m), s>>>(pl->vfull, pl->p, pl->D_half, pl->Ap, (int)P.m, st,
+                                                                part_pAp);
+    EFGP_CUDA(launch_pdl(k_cg_xr, nb, kCGThreads, s, pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp,
+                         part_rr, nrow, (const double *)nullptr));
+  } else {
   EFGP_CUFFT(cufftExecZ2D(pl->plan_c2r_L, pl->Xbox, pl->Yr));
   k_mul<<<nblocks(Ld, pl->num_sms), kCGThreads, 0, s>>>(pl->Yr, pl->vhat, Ld, st);
   EFGP_CUFFT(cufftExecD2Z(pl->plan_r2c_L, pl->Yr, pl->Zbox));
   k_cg_apply<D><<<nb, kCGThreads, 0, s>>>(pl->Zbox, pl->p, pl->D_half, pl->Ap, P.Mh, (int)P.m, P.L, st, part_pAp);
   EFGP_CUDA(launch_pdl(k_cg_xr, nb, kCGThreads, s, pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp,
                        part_rr, (int)nb, (const double *)nullptr));
+  }
   EFGP_CUDA(launch_pdl(k_cg_p<D>, nb, kCGThreads, s, pl->r, pl->p, pl->D_half, P.Mh, (int)P.m, P.L, pl->Xbox, box,
                        st, part_rr, (int)nb, pl->hist));
-  EFGP_CUDA(launch_pdl(k_cg_pad<D>, nbox, kCGThreads, s, pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box,
-                       (const CGState *)st));
+  if (!direct)
+    EFGP_CUDA(launch_pdl(k_cg_pad<D>, nbox, kCGThreads, s, pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box,
+                         (const CGState *)st));
   EFGP_CUDA(cudaGetLastError());
   return EFGP_OK;
 }
@@ -332,6 +442,8 @@ static efgp_status cg_solve_d(efgp_plan *pl, int64_t N_total) {
   EFGP_CUDA(cudaGetLastError());
   EFGP_CUFFT(cufftSetStream(pl->plan_c2r_L, s));
   EFGP_CUFFT(cufftSetStream(pl->plan_r2c_L, s));
+  if (D == 2 && toeplitz_direct(P))
+    EFGP_CUDA(cudaFuncSetAttribute(k_cg_toep2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)toep2_smem((int)P.m)));
 
   const int G = P.graph_iters;
   if (!pl->cg_exec || pl->cg_exec_iters != G) {
@@ -423,6 +535,34 @@ efgp_status cg_solve_op(efgp_plan *pl, int64_t max_iter, CGOp op, void *ctx) {
   return EFGP_ERR_INVALID;
 }
 
+// PCG x/r update after the direct Toeplitz product: (p, Ap) partials come from its nrow CTAs, (r, z)
+// partials from the previous dot over nb CTAs
+__global__ void k_cg_xr_pc_direct(double2 *__restrict__ x, double2 *__restrict__ r, const double2 *__restrict__ p,
+                                  const double2 *__restrict__ Ap, int64_t Mh, int m, CGState *st,
+                                  const double *__restrict__ part_pAp, int npAp, double *__restrict__ part_rr,
+                                  const double *__restrict__ part_rz, int nblk) {
+  __shared__ double sh[40];
+  if (st->done) return;
+  const double pAp = reduce_partials(part_pAp, npAp, sh);
+  const double rz = reduce_partials(part_rz, nblk, sh);
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->rz = rz;
+  const double alpha = rz / pAp;
+  double acc = 0.0;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 pp = p[q], a = Ap[q];
+    double2 xx = x[q], rq = r[q];
+    xx.x += alpha * pp.x;
+    xx.y += alpha * pp.y;
+    rq.x -= alpha * a.x;
+    rq.y -= alpha * a.y;
+    x[q] = xx;
+    r[q] = rq;
+    acc += ((q % (m + 1)) ? 2.0 : 1.0) * (rq.x * rq.x + rq.y * rq.y);
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) part_rr[blockIdx.x] = acc;
+}
+
 // ---- NEXT-4: preconditioned CG with the Kronecker preconditioner of precond.cu (reading G12).
 // Standard PCG recurrences; the stopping rule and history are those of CG (||r_k|| / ||b||, G6).
 __global__ void k_pcg_check(CGState *st, const double *__restrict__ part_rr, int nblk, double *__restrict__ hist) {
@@ -471,17 +611,27 @@ static efgp_status enqueue_pcg_iteration(efgp_plan *pl, cudaStream_t s, CGState 
                                          unsigned nb, unsigned nbox) {
   const Params &P = pl->P;
   double *part_pAp = pl->partials, *part_rr = pl->partials + pl->cg_blocks, *part_rz = pl->partials + 2 * pl->cg_blocks;
+  const bool direct = D == 2 && toeplitz_direct(P);
+  if (direct) {
+    const int nrow = (int)(2 * P.m + 1);
+    k_cg_toep2<<<nrow, kToepThreads, toep2_smem((int)P.m), s>>>(pl->vfull, pl->p, pl->D_half, pl->Ap, (int)P.m, st,
+                                                                part_pAp);
+    // (x, r update: alpha from the toep2 partials, (r, z) from the previous dot's partials)
+    k_cg_xr_pc_direct<<<nb, kCGThreads, 0, s>>>(pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp, nrow,
+                                                 part_rr, part_rz, (int)nb);
+  } else {
   EFGP_CUFFT(cufftExecZ2D(pl->plan_c2r_L, pl->Xbox, pl->Yr));
   k_mul<<<nblocks(Ld, pl->num_sms), kCGThreads, 0, s>>>(pl->Yr, pl->vhat, Ld, st);
   EFGP_CUFFT(cufftExecD2Z(pl->plan_r2c_L, pl->Yr, pl->Zbox));
   k_cg_apply<D><<<nb, kCGThreads, 0, s>>>(pl->Zbox, pl->p, pl->D_half, pl->Ap, P.Mh, (int)P.m, P.L, st, part_pAp);
   k_cg_xr<<<nb, kCGThreads, 0, s>>>(pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp, part_rr, (int)nb,
                                     part_rz);
+  }
   k_pcg_check<<<1, kCGThreads, 0, s>>>(st, part_rr, (int)nb, pl->hist);
   EFGP_TRY(precond_apply(pl, pl->r, pl->z, &st->done, s));
   k_pcg_dot<<<nb, kCGThreads, 0, s>>>(pl->r, pl->z, P.Mh, (int)P.m, st, part_rz);
   k_pcg_p<<<nb, kCGThreads, 0, s>>>(pl->z, pl->p, P.Mh, st, part_rz, (int)nb, 0);
-  k_cg_pad<D><<<nbox, kCGThreads, 0, s>>>(pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box, st);
+  if (!direct) k_cg_pad<D><<<nbox, kCGThreads, 0, s>>>(pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box, st);
   EFGP_CUDA(cudaGetLastError());
   return EFGP_OK;
 }
@@ -521,6 +671,8 @@ static efgp_status pcg_solve_d(efgp_plan *pl, int64_t N_total) {
   EFGP_CUDA(cudaGetLastError());
   EFGP_CUFFT(cufftSetStream(pl->plan_c2r_L, s));
   EFGP_CUFFT(cufftSetStream(pl->plan_r2c_L, s));
+  if (D == 2 && toeplitz_direct(P))
+    EFGP_CUDA(cudaFuncSetAttribute(k_cg_toep2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)toep2_smem((int)P.m)));
   const int G = P.graph_iters;
   if (!pl->pcg_exec || pl->pcg_exec_iters != G || pl->pcg_exec_sigma2 != pl->sigma2_sys) {
     pl->pcg_exec_sigma2 = pl->sigma2_sys;

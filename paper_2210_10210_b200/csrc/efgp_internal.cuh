@@ -123,6 +123,7 @@ struct efgp_plan {
   double2 *Xbox = nullptr;    // L^(d-1) (L/2+1) complex, C2R input
   double *Yr = nullptr;       // L^d real
   double *vhat = nullptr;     // L^d real, C2R(v)/L^d
+  double2 *vfull = nullptr;   // (4m+1)^2 complex, full v (direct Toeplitz product, small m, 2D)
   double2 *Zbox = nullptr;    // R2C output
   double2 *b = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *Ap = nullptr;  // Mh each
   double *partials = nullptr; // 2 * cg_blocks
@@ -228,6 +229,16 @@ inline int sort_ctas(int num_sms) {
 __global__ void k_het_colscan(unsigned *__restrict__ hist, int nblk, int ncell, long long *__restrict__ tot);
 __global__ void k_het_offsets(const long long *__restrict__ tot, int ncell, long long *__restrict__ off);
 // modes.cu
+// the CG's Toeplitz product by direct 2D convolution (one CTA per output row) instead of the padded
+// real FFTs: (2m+1)^4 complex MACs per product, cheaper than four cuFFT launches for small m
+inline bool toeplitz_direct(const Params &P) {
+  const char *e = getenv("EFGP_TOEP_DIRECT");
+  if (e && e[0] == '0') return false;
+  if (P.d != 2 || P.m > 32) return false;
+  // shared memory of k_cg_toep2 (1024 threads): u (n^2) + v rows (n (4m+1)) + partial sums
+  const int64_t n = 2 * P.m + 1, nv = 4 * P.m + 1, nout = P.m + 1, slices = 1024 / ((nout + 3) / 4);
+  return 16 * (n * n + n * nv + slices * nout) <= 220 * 1024;
+}
 efgp_status type1_modes(efgp_plan *pl, double *modes_out, cudaStream_t s);
 efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s);
 efgp_status type2_grid(efgp_plan *pl, cudaStream_t s);

@@ -130,6 +130,23 @@ efgp_status type1_half(efgp_plan *pl, const double2 *G, int64_t n, int K, const 
   return EFGP_OK;
 }
 
+
+// full v over J_2m ((4m+1)^2, row-major over (j1+2m, j2+2m)) from its Hermitian half (2D; the direct
+// Toeplitz product of small-m CGs reads it)
+__global__ void k_expand_v2(const double2 *__restrict__ vh, int m, double2 *__restrict__ vf) {
+  const int K = 2 * m, n = 2 * K + 1;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * n; idx += gridDim.x * blockDim.x) {
+    int j[2] = {idx / n - K, idx % n - K};
+    const bool neg = j[1] < 0;
+    if (neg) {
+      j[0] = -j[0];
+      j[1] = -j[1];
+    }
+    const double2 v = vh[encode_half<2>(j, K)];
+    vf[idx] = neg ? make_double2(v.x, -v.y) : v;
+  }
+}
+
 efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s) {
   const Params &P = pl->P;
   const double2 *vh = reinterpret_cast<const double2 *>(modes);
@@ -151,6 +168,12 @@ efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s) {
   EFGP_CUFFT(cufftExecZ2D(pl->plan_c2r_L, pl->Xbox, pl->vhat));  // real: v is Hermitian (A.10)
   k_make_b<<<grid_for(P.Mh, 256, pl->num_sms), 256, 0, s>>>(fyh, pl->D_half, pl->b, P.Mh);
   EFGP_CUDA(cudaGetLastError());
+  if (toeplitz_direct(P)) {  // small m: the CG applies T by direct convolution with the full v
+    const int n = (int)(4 * P.m + 1);
+    if (!pl->vfull) EFGP_CUDA(cudaMalloc((void **)&pl->vfull, sizeof(double2) * n * n));
+    k_expand_v2<<<grid_for((int64_t)n * n, 256, pl->num_sms), 256, 0, s>>>(vh, (int)P.m, pl->vfull);
+    EFGP_CUDA(cudaGetLastError());
+  }
   return EFGP_OK;
 }
 
