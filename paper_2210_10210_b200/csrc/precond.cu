@@ -133,6 +133,82 @@ __global__ void k_pc_scale(double2 *__restrict__ z, const double *__restrict__ l
 }
 
 
+
+// One axis pass with the neighbouring steps fused (fewer launches per PCG iteration): IN_HALF reads the
+// input from the Hermitian half (conjugate completion) instead of an expanded grid, SCALE divides the
+// output by prod lambda + sigma^2, OUT_HALF writes only the Hermitian-half entries (the extract).
+template <int D, bool ADJ, bool IN_HALF, bool SCALE, bool OUT_HALF>
+__global__ void k_pc_axis_f(const double2 *__restrict__ in, double2 *__restrict__ out, const double2 *__restrict__ V,
+                            int m, int64_t stride, int64_t total, const double *__restrict__ lam, double sigma2,
+                            const int *__restrict__ done) {
+  if (done && *done) return;
+  const int n = 2 * m + 1;
+  const int lane = threadIdx.x & 31;
+  for (int64_t idx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; idx < total;
+       idx += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int j = (int)((idx / stride) % n);
+    const int64_t base = idx - (int64_t)j * stride;
+    double re = 0.0, im = 0.0;
+    for (int k = lane; k < n; k += 32) {
+      const double2 q = ADJ ? V[(int64_t)j * n + k] : V[(int64_t)k * n + j];
+      double2 zv;
+      const int64_t fi = base + (int64_t)k * stride;
+      if constexpr (IN_HALF) {
+        int jj[D];
+        int64_t rem = fi;
+#pragma unroll
+        for (int c = D - 1; c >= 0; --c) {
+          jj[c] = (int)(rem % n) - m;
+          rem /= n;
+        }
+        const bool neg = jj[D - 1] < 0;
+        if (neg) {
+#pragma unroll
+          for (int c = 0; c < D; ++c) jj[c] = -jj[c];
+        }
+        const double2 h = in[encode_half<D>(jj, m)];
+        zv = neg ? make_double2(h.x, -h.y) : h;
+      } else {
+        zv = in[fi];
+      }
+      const double qy = ADJ ? -q.y : q.y;  // conj(q) z or q z
+      re = fma(q.x, zv.x, fma(-qy, zv.y, re));
+      im = fma(q.x, zv.y, fma(qy, zv.x, im));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      re += __shfl_xor_sync(0xffffffffu, re, o);
+      im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    if (lane == 0) {
+      int jj[D];
+      int64_t rem = idx;
+#pragma unroll
+      for (int c = D - 1; c >= 0; --c) {
+        jj[c] = (int)(rem % n);
+        rem /= n;
+      }
+      if constexpr (SCALE) {
+        double pr = 1.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) pr *= lam[c * n + jj[c]];
+        const double sc = 1.0 / (pr + sigma2);
+        re *= sc;
+        im *= sc;
+      }
+      if constexpr (OUT_HALF) {
+        if (jj[D - 1] >= m) {  // j_d >= 0
+#pragma unroll
+          for (int c = 0; c < D; ++c) jj[c] -= m;
+          out[encode_half<D>(jj, m)] = make_double2(re, im);
+        }
+      } else {
+        out[idx] = make_double2(re, im);
+      }
+    }
+  }
+}
+
 static unsigned pc_grid(int64_t n, int sms) {
   int64_t b = (n + 255) / 256;
   const int64_t cap = (int64_t)sms * 8;
@@ -233,6 +309,23 @@ static efgp_status precond_apply_d(efgp_plan *pl, const double2 *r, double2 *z, 
   const unsigned g = pc_grid(total, pl->num_sms);
   const unsigned gw = (unsigned)std::min<int64_t>((total * 32 + 255) / 256, (int64_t)pl->num_sms * 8);
   double2 *a = pl->pc_F0, *b = pl->pc_F1;
+  const double2 *Q = pl->pc_Q;
+  const double s2 = pl->sigma2_sys;
+  const int64_t st0 = total / n;  // axis-0 stride
+  if constexpr (D == 2) {  // 4 fused passes: (half -> Q0^*) (Q1^*, scale) (Q0) (Q1 -> half)
+    k_pc_axis_f<2, true, true, false, false><<<gw, 256, 0, s>>>(r, a, Q, m, st0, total, pl->pc_lam, s2, done);
+    k_pc_axis_f<2, true, false, true, false><<<gw, 256, 0, s>>>(a, b, Q + (size_t)n * n, m, 1, total, pl->pc_lam, s2, done);
+    k_pc_axis_f<2, false, false, false, false><<<gw, 256, 0, s>>>(b, a, Q, m, st0, total, pl->pc_lam, s2, done);
+    k_pc_axis_f<2, false, false, false, true><<<gw, 256, 0, s>>>(a, z, Q + (size_t)n * n, m, 1, total, pl->pc_lam, s2, done);
+    EFGP_CUDA(cudaGetLastError());
+    return EFGP_OK;
+  } else if constexpr (D == 1) {  // (half -> Q^*, scale) (Q -> half)
+    k_pc_axis_f<1, true, true, true, false><<<gw, 256, 0, s>>>(r, a, Q, m, 1, total, pl->pc_lam, s2, done);
+    k_pc_axis_f<1, false, false, false, true><<<gw, 256, 0, s>>>(a, z, Q, m, 1, total, pl->pc_lam, s2, done);
+    EFGP_CUDA(cudaGetLastError());
+    return EFGP_OK;
+  }
+  // D = 3: expand, three Q^* passes, scale, three Q passes, extract
   k_pc_expand<D><<<g, 256, 0, s>>>(r, m, a, total, done);
   int64_t stride = total;
   for (int i = 0; i < D; ++i) {
