@@ -32,27 +32,7 @@ struct CGState {
 
 constexpr int kCGThreads = 256;
 
-// Programmatic dependent launch between the CG's own kernels (launched with
-// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel lets its successor be scheduled at
-// once (launch_dependents) and waits for its predecessor's completion and memory (wait) before
-// touching any data, so consecutive launches overlap their latency instead of serialising it.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-template <typename... KArgs, typename... Args>
-static cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
-}
 
 __device__ __forceinline__ double block_sum(double v, double *sh) {
 #pragma unroll
@@ -542,6 +522,8 @@ __global__ void k_cg_xr_pc_direct(double2 *__restrict__ x, double2 *__restrict__
                                   const double *__restrict__ part_pAp, int npAp, double *__restrict__ part_rr,
                                   const double *__restrict__ part_rz, int nblk) {
   __shared__ double sh[40];
+  pdl_wait();
+  pdl_trigger();
   if (st->done) return;
   const double pAp = reduce_partials(part_pAp, npAp, sh);
   const double rz = reduce_partials(part_rz, nblk, sh);
@@ -567,6 +549,8 @@ __global__ void k_cg_xr_pc_direct(double2 *__restrict__ x, double2 *__restrict__
 // Standard PCG recurrences; the stopping rule and history are those of CG (||r_k|| / ||b||, G6).
 __global__ void k_pcg_check(CGState *st, const double *__restrict__ part_rr, int nblk, double *__restrict__ hist) {
   __shared__ double sh[40];
+  pdl_wait();
+  pdl_trigger();
   if (st->done) return;
   const double rr = reduce_partials(part_rr, nblk, sh);
   if (threadIdx.x == 0) {
@@ -583,6 +567,8 @@ __global__ void k_pcg_check(CGState *st, const double *__restrict__ part_rr, int
 __global__ void k_pcg_dot(const double2 *__restrict__ r, const double2 *__restrict__ z, int64_t Mh, int m,
                           const CGState *st, double *__restrict__ part) {
   __shared__ double sh[40];
+  pdl_wait();
+  pdl_trigger();
   if (st->done) return;
   double acc = 0.0;
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
@@ -598,6 +584,8 @@ __global__ void k_pcg_dot(const double2 *__restrict__ r, const double2 *__restri
 __global__ void k_pcg_p(const double2 *__restrict__ z, double2 *__restrict__ p, int64_t Mh, const CGState *st,
                         const double *__restrict__ part_rz, int nblk, int first) {
   __shared__ double sh[40];
+  pdl_wait();
+  pdl_trigger();
   if (st->done) return;
   const double bcg = first ? 0.0 : reduce_partials(part_rz, nblk, sh) / st->rz;
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
@@ -617,8 +605,8 @@ static efgp_status enqueue_pcg_iteration(efgp_plan *pl, cudaStream_t s, CGState 
     k_cg_toep2<<<nrow, kToepThreads, toep2_smem((int)P.m), s>>>(pl->vfull, pl->p, pl->D_half, pl->Ap, (int)P.m, st,
                                                                 part_pAp);
     // (x, r update: alpha from the toep2 partials, (r, z) from the previous dot's partials)
-    k_cg_xr_pc_direct<<<nb, kCGThreads, 0, s>>>(pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp, nrow,
-                                                 part_rr, part_rz, (int)nb);
+    EFGP_CUDA(launch_pdl(k_cg_xr_pc_direct, nb, kCGThreads, s, pl->x, pl->r, pl->p, (const double2 *)pl->Ap, P.Mh,
+                         (int)P.m, st, (const double *)part_pAp, nrow, part_rr, (const double *)part_rz, (int)nb));
   } else {
   EFGP_CUFFT(cufftExecZ2D(pl->plan_c2r_L, pl->Xbox, pl->Yr));
   k_mul<<<nblocks(Ld, pl->num_sms), kCGThreads, 0, s>>>(pl->Yr, pl->vhat, Ld, st);
@@ -627,10 +615,12 @@ static efgp_status enqueue_pcg_iteration(efgp_plan *pl, cudaStream_t s, CGState 
   k_cg_xr<<<nb, kCGThreads, 0, s>>>(pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp, part_rr, (int)nb,
                                     part_rz);
   }
-  k_pcg_check<<<1, kCGThreads, 0, s>>>(st, part_rr, (int)nb, pl->hist);
-  EFGP_TRY(precond_apply(pl, pl->r, pl->z, &st->done, s));
-  k_pcg_dot<<<nb, kCGThreads, 0, s>>>(pl->r, pl->z, P.Mh, (int)P.m, st, part_rz);
-  k_pcg_p<<<nb, kCGThreads, 0, s>>>(pl->z, pl->p, P.Mh, st, part_rz, (int)nb, 0);
+  EFGP_CUDA(launch_pdl(k_pcg_check, 1, kCGThreads, s, st, (const double *)part_rr, (int)nb, pl->hist));
+  EFGP_TRY(precond_apply(pl, pl->r, pl->z, &st->done, s, true));
+  EFGP_CUDA(launch_pdl(k_pcg_dot, nb, kCGThreads, s, (const double2 *)pl->r, (const double2 *)pl->z, P.Mh, (int)P.m,
+                       (const CGState *)st, part_rz));
+  EFGP_CUDA(launch_pdl(k_pcg_p, nb, kCGThreads, s, (const double2 *)pl->z, pl->p, P.Mh, (const CGState *)st,
+                       (const double *)part_rz, (int)nb, 0));
   if (!direct) k_cg_pad<D><<<nbox, kCGThreads, 0, s>>>(pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box, st);
   EFGP_CUDA(cudaGetLastError());
   return EFGP_OK;

@@ -253,7 +253,8 @@ efgp_status cg_solve(efgp_plan *pl, int64_t N_total);
 efgp_status pcg_solve(efgp_plan *pl, int64_t N_total);  // NEXT-4
 // precond.cu (NEXT-4): build the Kronecker preconditioner from the fit's v; z = M^-1 r
 efgp_status precond_setup(efgp_plan *pl, const double *modes);
-efgp_status precond_apply(efgp_plan *pl, const double2 *r, double2 *z, const int *done, cudaStream_t s);
+efgp_status precond_apply(efgp_plan *pl, const double2 *r, double2 *z, const int *done, cudaStream_t s,
+                          bool pdl = false);
 typedef efgp_status (*CGOp)(efgp_plan *pl, const double2 *p, double2 *Ap, void *ctx);  // Ap = A p
 efgp_status cg_solve_op(efgp_plan *pl, int64_t max_iter, CGOp op, void *ctx);
 // interp.cu
@@ -414,6 +415,28 @@ __device__ __forceinline__ bool box_to_mode(int64_t idx, int64_t n, int K, int (
     j[k] = (int)jj;
   }
   return true;
+}
+
+// Programmatic dependent launch between the CG's own kernels (launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel lets its successor be scheduled at
+// once (launch_dependents) and waits for its predecessor's completion and memory (wait) before
+// touching any data, so consecutive launches overlap their latency instead of serialising it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
 }  // namespace efgp

@@ -141,6 +141,8 @@ template <int D, bool ADJ, bool IN_HALF, bool SCALE, bool OUT_HALF>
 __global__ void k_pc_axis_f(const double2 *__restrict__ in, double2 *__restrict__ out, const double2 *__restrict__ V,
                             int m, int64_t stride, int64_t total, const double *__restrict__ lam, double sigma2,
                             const int *__restrict__ done) {
+  pdl_wait();
+  pdl_trigger();
   if (done && *done) return;
   const int n = 2 * m + 1;
   const int lane = threadIdx.x & 31;
@@ -302,7 +304,8 @@ efgp_status precond_setup(efgp_plan *pl, const double *modes) {
 
 // z = M^-1 r on Hermitian halves; kernels return at entry when *done (captured in the CG graph)
 template <int D>
-static efgp_status precond_apply_d(efgp_plan *pl, const double2 *r, double2 *z, const int *done, cudaStream_t s) {
+static efgp_status precond_apply_d(efgp_plan *pl, const double2 *r, double2 *z, const int *done, cudaStream_t s,
+                                   bool pdl) {
   const Params &P = pl->P;
   const int m = (int)P.m, n = 2 * m + 1;
   const int64_t total = ipow_(n, D);
@@ -312,17 +315,22 @@ static efgp_status precond_apply_d(efgp_plan *pl, const double2 *r, double2 *z, 
   const double2 *Q = pl->pc_Q;
   const double s2 = pl->sigma2_sys;
   const int64_t st0 = total / n;  // axis-0 stride
+  // (pdl: the passes are launched as programmatic dependents of their predecessors; they wait before
+  // reading anything)
+  auto L = [&](auto kern, const double2 *in, double2 *out, const double2 *V, int64_t stride) {
+    if (pdl) return launch_pdl(kern, gw, 256, s, in, out, V, m, stride, total, (const double *)pl->pc_lam, s2, done);
+    kern<<<gw, 256, 0, s>>>(in, out, V, m, stride, total, pl->pc_lam, s2, done);
+    return cudaGetLastError();
+  };
   if constexpr (D == 2) {  // 4 fused passes: (half -> Q0^*) (Q1^*, scale) (Q0) (Q1 -> half)
-    k_pc_axis_f<2, true, true, false, false><<<gw, 256, 0, s>>>(r, a, Q, m, st0, total, pl->pc_lam, s2, done);
-    k_pc_axis_f<2, true, false, true, false><<<gw, 256, 0, s>>>(a, b, Q + (size_t)n * n, m, 1, total, pl->pc_lam, s2, done);
-    k_pc_axis_f<2, false, false, false, false><<<gw, 256, 0, s>>>(b, a, Q, m, st0, total, pl->pc_lam, s2, done);
-    k_pc_axis_f<2, false, false, false, true><<<gw, 256, 0, s>>>(a, z, Q + (size_t)n * n, m, 1, total, pl->pc_lam, s2, done);
-    EFGP_CUDA(cudaGetLastError());
+    EFGP_CUDA(L(k_pc_axis_f<2, true, true, false, false>, r, a, Q, st0));
+    EFGP_CUDA(L(k_pc_axis_f<2, true, false, true, false>, a, b, Q + (size_t)n * n, 1));
+    EFGP_CUDA(L(k_pc_axis_f<2, false, false, false, false>, b, a, Q, st0));
+    EFGP_CUDA(L(k_pc_axis_f<2, false, false, false, true>, a, z, Q + (size_t)n * n, 1));
     return EFGP_OK;
   } else if constexpr (D == 1) {  // (half -> Q^*, scale) (Q -> half)
-    k_pc_axis_f<1, true, true, true, false><<<gw, 256, 0, s>>>(r, a, Q, m, 1, total, pl->pc_lam, s2, done);
-    k_pc_axis_f<1, false, false, false, true><<<gw, 256, 0, s>>>(a, z, Q, m, 1, total, pl->pc_lam, s2, done);
-    EFGP_CUDA(cudaGetLastError());
+    EFGP_CUDA(L(k_pc_axis_f<1, true, true, true, false>, r, a, Q, 1));
+    EFGP_CUDA(L(k_pc_axis_f<1, false, false, false, true>, a, z, Q, 1));
     return EFGP_OK;
   }
   // D = 3: expand, three Q^* passes, scale, three Q passes, extract
@@ -345,11 +353,11 @@ static efgp_status precond_apply_d(efgp_plan *pl, const double2 *r, double2 *z, 
   return EFGP_OK;
 }
 
-efgp_status precond_apply(efgp_plan *pl, const double2 *r, double2 *z, const int *done, cudaStream_t s) {
+efgp_status precond_apply(efgp_plan *pl, const double2 *r, double2 *z, const int *done, cudaStream_t s, bool pdl) {
   switch (pl->P.d) {
-    case 1: return precond_apply_d<1>(pl, r, z, done, s);
-    case 2: return precond_apply_d<2>(pl, r, z, done, s);
-    case 3: return precond_apply_d<3>(pl, r, z, done, s);
+    case 1: return precond_apply_d<1>(pl, r, z, done, s, pdl);
+    case 2: return precond_apply_d<2>(pl, r, z, done, s, pdl);
+    case 3: return precond_apply_d<3>(pl, r, z, done, s, pdl);
   }
   return EFGP_ERR_INVALID;
 }
