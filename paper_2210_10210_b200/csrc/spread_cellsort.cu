@@ -4,7 +4,7 @@
 //
 // Both strengths (1 and y) go to the n1 grid (n_rhs = n1, like SORTED).  Per call:
 //   1. k_cs_count   : per-CTA shared-memory histogram of the points' super-cells (G^d start cells;
-//                     G = 1 in 2D, 4 in 3D so the key space fits shared memory); validates the input.
+//                     G = 1 in 2D (2 for large grids), 4 in 3D so the key space fits shared memory).
 //   2. k_het_colscan / k_het_offsets (hetero.cu): bucket offsets per CTA.
 //   3. k_cs_scatter : counting-sort scatter into structure-of-arrays buffers (coordinates, y).
 //   4. k_cs_spread  : a warp per run of <= kCsRun points of one super-cell.  Batches of 32 points: lane
@@ -30,13 +30,11 @@ struct CsItem {
   int cell, pad_;
 };
 
-template <int D> constexpr int cs_group() { return D == 3 ? 4 : 1; }
 
 // super-cell key of point i; validates x in [0,1]^d and finite y (raises *err)
-template <int D, int W>
+template <int D, int W, int G>
 __device__ __forceinline__ int cs_key(const double *__restrict__ x, const double *__restrict__ y, int64_t i, double h,
                                       int n, int lo, int S, int *__restrict__ err) {
-  constexpr int G = cs_group<D>();
   int key = 0;
   bool ok = isfinite(__ldg(y + i));
 #pragma unroll
@@ -58,7 +56,7 @@ __device__ __forceinline__ void cs_range(int64_t N, int64_t &a, int64_t &e) {
   e = a + per < N ? a + per : N;
 }
 
-template <int D, int W>
+template <int D, int W, int G>
 __global__ void k_cs_count(const double *__restrict__ x, const double *__restrict__ y, int64_t N, double h, int n,
                            int lo, int S, int ncell, unsigned *__restrict__ hist, int *__restrict__ err) {
   extern __shared__ unsigned cs_h[];
@@ -66,12 +64,12 @@ __global__ void k_cs_count(const double *__restrict__ x, const double *__restric
   __syncthreads();
   int64_t a, e;
   cs_range(N, a, e);
-  for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&cs_h[cs_key<D, W>(x, y, i, h, n, lo, S, err)], 1u);
+  for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&cs_h[cs_key<D, W, G>(x, y, i, h, n, lo, S, err)], 1u);
   __syncthreads();
   for (int i = threadIdx.x; i < ncell; i += blockDim.x) hist[(size_t)blockIdx.x * ncell + i] = cs_h[i];
 }
 
-template <int D, int W>
+template <int D, int W, int G>
 __global__ void k_cs_scatter(const double *__restrict__ x, const double *__restrict__ y, int64_t N, double h, int n,
                              int lo, int S, int ncell, const unsigned *__restrict__ hist,
                              const long long *__restrict__ off, double *__restrict__ xs, double *__restrict__ ys,
@@ -82,7 +80,7 @@ __global__ void k_cs_scatter(const double *__restrict__ x, const double *__restr
   int64_t a, e;
   cs_range(N, a, e);
   for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x) {
-    const int key = cs_key<D, W>(x, y, i, h, n, lo, S, err);
+    const int key = cs_key<D, W, G>(x, y, i, h, n, lo, S, err);
     const long long pos = off[key] + (long long)atomicAdd(&cs_c[key], 1u);
 #pragma unroll
     for (int k = 0; k < D; ++k) xs[(int64_t)k * N + pos] = __ldg(x + i * D + k);
@@ -95,12 +93,11 @@ __device__ __forceinline__ int cs_wrap(int i, int n) {
   return i < 0 ? i + n : i;
 }
 
-template <int D, int W>
+template <int D, int W, int G>
 __global__ void __launch_bounds__(kCsThreads) k_cs_spread(const CsItem *__restrict__ items, int64_t nitems,
                                                           const double *__restrict__ xs, const double *__restrict__ ys,
                                                           int64_t N, double *__restrict__ g1, double *__restrict__ g2,
                                                           double h, int n, int lo, int S, EsPoly P) {
-  constexpr int G = cs_group<D>();
   constexpr int U = W + G - 1;                   // union window per dimension of a super-cell
   constexpr int UD = D == 2 ? U * U : U * U * U;
   constexpr int E = (UD + 31) / 32;              // window elements per lane
@@ -187,22 +184,30 @@ __global__ void __launch_bounds__(kCsThreads) k_cs_spread(const CsItem *__restri
   }
 }
 
-bool cellsort_geometry(const Params &p, int &lo, int &S, int &ncell) {
+// super-cell size: 1 in 2D (2 when the start-cell count does not fit the shared-memory histogram,
+// e.g. m = 94), 4 in 3D
+bool cellsort_geometry(const Params &p, int &lo, int &S, int &ncell, int &G) {
   if (p.d < 2 || p.d > 3 || (p.d == 3 && p.w > 6)) return false;
-  const int G = p.d == 3 ? 4 : 1;
   lo = -(p.w / 2);
   const int hi = (int)std::ceil(p.h * (double)p.n1 - 0.5 * p.w);
   const int cells = hi - lo + 2;  // start cells per dimension (+1 spare)
-  S = (cells + G - 1) / G;
-  ncell = p.d == 2 ? S * S : S * S * S;
-  return (size_t)ncell * 4 <= 200 * 1024;
+  for (G = (p.d == 3 ? 4 : 1); G <= (p.d == 3 ? 4 : 2); ++G) {
+    S = (cells + G - 1) / G;
+    ncell = p.d == 2 ? S * S : S * S * S;
+    if ((size_t)ncell * 4 <= 200 * 1024) return true;
+  }
+  return false;
+}
+bool cellsort_geometry(const Params &p, int &lo, int &S, int &ncell) {
+  int G;
+  return cellsort_geometry(p, lo, S, ncell, G);
 }
 
-template <int D, int W>
+template <int D, int W, int G>
 static efgp_status cellsort_t(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s) {
   const Params &P = pl->P;
-  int lo, S, ncell;
-  if (!cellsort_geometry(P, lo, S, ncell)) return EFGP_ERR_RESOURCE;
+  int lo, S, ncell, Gs;
+  if (!cellsort_geometry(P, lo, S, ncell, Gs) || Gs != G) return EFGP_ERR_RESOURCE;
   const int B = sort_ctas(pl->num_sms), T = 1024, n = (int)P.n1;
   unsigned *hist = nullptr;
   long long *tot = nullptr, *off = nullptr;
@@ -214,12 +219,12 @@ static efgp_status cellsort_t(efgp_plan *pl, const double *x, const double *y, i
   EFGP_PALLOC(&xs, sizeof(double) * N * D, s);
   EFGP_PALLOC(&ys, sizeof(double) * N, s);
   const size_t sm = sizeof(unsigned) * ncell;
-  EFGP_CUDA(cudaFuncSetAttribute(k_cs_count<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  EFGP_CUDA(cudaFuncSetAttribute(k_cs_scatter<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_cs_count<D, W><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, pl->dflags);
+  EFGP_CUDA(cudaFuncSetAttribute(k_cs_count<D, W, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  EFGP_CUDA(cudaFuncSetAttribute(k_cs_scatter<D, W, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_cs_count<D, W, G><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, pl->dflags);
   k_het_colscan<<<(ncell + 255) / 256, 256, 0, s>>>(hist, B, ncell, tot);
   k_het_offsets<<<1, 1024, 0, s>>>(tot, ncell, off);
-  k_cs_scatter<D, W><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, off, xs, ys, pl->dflags);
+  k_cs_scatter<D, W, G><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, off, xs, ys, pl->dflags);
   EFGP_CUDA(cudaGetLastError());
   std::vector<long long> offh(ncell + 1);
   EFGP_CUDA(cudaMemcpyAsync(offh.data(), off, sizeof(long long) * (ncell + 1), cudaMemcpyDeviceToHost, s));
@@ -232,10 +237,10 @@ static efgp_status cellsort_t(efgp_plan *pl, const double *x, const double *y, i
   EFGP_PALLOC(&items, sizeof(CsItem) * std::max<size_t>(it.size(), 1), s);
   EFGP_CUDA(cudaMemcpyAsync(items, it.data(), sizeof(CsItem) * it.size(), cudaMemcpyHostToDevice, s));
   int per_sm = 1;
-  EFGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cs_spread<D, W>, kCsThreads, 0));
+  EFGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cs_spread<D, W, G>, kCsThreads, 0));
   int64_t blocks = std::min<int64_t>((int64_t)pl->num_sms * std::max(per_sm, 1), (nitems * 32 + kCsThreads - 1) / kCsThreads);
   if (nitems > 0)
-    k_cs_spread<D, W><<<(unsigned)std::max<int64_t>(blocks, 1), kCsThreads, 0, s>>>(items, nitems, xs, ys, N, pl->g1,
+    k_cs_spread<D, W, G><<<(unsigned)std::max<int64_t>(blocks, 1), kCsThreads, 0, s>>>(items, nitems, xs, ys, N, pl->g1,
                                                                                      pl->g2, P.h, n, lo, S, P.poly);
   EFGP_CUDA(cudaGetLastError());
   EFGP_CUDA(cudaStreamSynchronize(s));  // the host item vector is consumed by the copy above
@@ -246,15 +251,23 @@ static efgp_status cellsort_t(efgp_plan *pl, const double *x, const double *y, i
 efgp_status spread_cellsort(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s) {
   if (N >= (1ll << 32)) return EFGP_ERR_RESOURCE;  // 32-bit bucket cursors
   const int W = pl->P.w;
-  if (pl->P.d == 2) {
+  int lo, S, ncell, G;
+  if (!cellsort_geometry(pl->P, lo, S, ncell, G)) return EFGP_ERR_RESOURCE;
+  if (pl->P.d == 2 && G == 1) {
     switch (W) {
-#define C2(WW) case WW: return cellsort_t<2, WW>(pl, x, y, N, s);
+#define C2(WW) case WW: return cellsort_t<2, WW, 1>(pl, x, y, N, s);
+      C2(2) C2(3) C2(4) C2(5) C2(6) C2(7) C2(8) C2(9) C2(10) C2(11) C2(12) C2(13) C2(14) C2(15) C2(16)
+#undef C2
+    }
+  } else if (pl->P.d == 2 && G == 2) {
+    switch (W) {
+#define C2(WW) case WW: return cellsort_t<2, WW, 2>(pl, x, y, N, s);
       C2(2) C2(3) C2(4) C2(5) C2(6) C2(7) C2(8) C2(9) C2(10) C2(11) C2(12) C2(13) C2(14) C2(15) C2(16)
 #undef C2
     }
   } else if (pl->P.d == 3) {
     switch (W) {
-#define C3(WW) case WW: return cellsort_t<3, WW>(pl, x, y, N, s);
+#define C3(WW) case WW: return cellsort_t<3, WW, 4>(pl, x, y, N, s);
       C3(2) C3(3) C3(4) C3(5) C3(6)
 #undef C3
     }

@@ -623,3 +623,23 @@ def test_type2_every_kernel_width(d, eps):
     assert rel(mu, ref) <= 5 * inf["nufft_tol"], (inf["w"], rel(mu, ref))
     g.close()
 
+
+
+def test_cellsort_supercells_for_large_grids():
+    # m = 94 (the paper's headline eps = 1e-5 grid): the start cells exceed the shared-memory
+    # histogram, so CELLSORT bins 2 x 2 super-cells (union windows of W + 1) — against GLOBAL
+    from paper_2210_10210_b200 import EFGP
+    rng = np.random.default_rng(94)
+    N = 60_000
+    x = rng.uniform(0, 1, (N, 2))
+    y = np.cos(2 * np.pi * (3 * x[:, 0] + 4 * x[:, 1]) + 1.3) + 0.1 * rng.standard_normal(N)
+    out = {}
+    for spread in ("auto", "global"):
+        g = EFGP("matern", 0.1, 0.1, 1e-5, 2, 1.5, max_iter=1, spread=spread)
+        with pytest.warns(RuntimeWarning):
+            g.fit(dev(x), dev(y))
+        out[spread] = (g.vector("v"), g.vector("rhs"), g.info())
+        g.close()
+    assert out["auto"][2]["m"] == 94 and out["auto"][2]["spread_method"] == "cellsort"
+    assert rel(out["auto"][0], out["global"][0]) < 1e-12
+    assert rel(out["auto"][1], out["global"][1]) < 2 * out["auto"][2]["nufft_tol"]

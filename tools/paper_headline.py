@@ -1,0 +1,52 @@
+"""The paper's own headline workload (Table tbig1; abstract P:38-40) on one B200, for context:
+2D Matérn-3/2, l = 0.1, sigma = 0.1, eps = 1e-5 (m = 94), N = 1e9 iid uniform points,
+y = cos(2 pi <x, (3, 4)> + 1.3) + 0.1 N(0, 1), mu on a 1000^2 target grid.
+The paper reports 103 s total on 12 Xeon cores (MATLAB + FINUFFT).  Points come from the c5 device
+generator (iid uniform); y is formed on the device with torch.
+
+    python tools/paper_headline.py [--N 1e9]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--N", default="1e9")
+    a = ap.parse_args()
+    import math
+    import torch
+    from efgp_data import CONFIGS
+    from efgp_data import gpu as G
+    from paper_2210_10210_b200 import EFGP
+    N = int(float(a.N))
+    x, _ = G.generate_points(CONFIGS["c5"], 0, N)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(2591)
+    y = torch.cos(2 * math.pi * (3 * x[:, 0] + 4 * x[:, 1]) + 1.3)
+    y += 0.1 * torch.randn(N, dtype=torch.float64, device="cuda", generator=gen)
+    t = torch.linspace(0, 1, 1000, dtype=torch.float64, device="cuda")
+    xt = torch.stack(torch.meshgrid(t, t, indexing="ij"), -1).reshape(-1, 2).contiguous()
+    g = EFGP("matern", 0.1, 0.1, 1e-5, 2, 1.5)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g.fit(x, y)
+    mu = g.predict(xt)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    inf = g.info()
+    print(json.dumps({"workload": "paper Table tbig1 headline (P:2591): 2D Matern-3/2 l=0.1 sigma=0.1 eps=1e-5",
+                      "N": N, "m": inf["m"], "w": inf["w"], "spread": inf["spread_method"], "cg_iters": inf["iters"],
+                      "ms": {"spread": inf["t_spread_ms"], "fft_deconv": inf["t_modes_ms"], "solve": inf["t_solve_ms"],
+                             "predict_1000x1000": inf["t_predict_ms"]},
+                      "wall_s": wall, "points_per_s": N / wall,
+                      "paper": {"total_s": 103, "cores": 12, "iters": 1027, "source": "P:2591"}}))
+
+
+if __name__ == "__main__":
+    main()
