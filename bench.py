@@ -160,6 +160,12 @@ def cpu_baseline(cfg, n_points: int, q_targets: int):
                       f"{dt:.1f} s"}
 
 
+def workload_name(cfg, N, q):
+    kern = f"Matern-{cfg.nu:g}" if cfg.kernel == "matern" else "SE"
+    return (f"{cfg.name}: {cfg.d}D {kern} l={cfg.ell} sigma={cfg.sigma} eps={cfg.eps}, "
+            f"N={N:.0e} {cfg.points} points, q={q:.0e} {cfg.targets} targets, seed {cfg.seed}")
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -179,7 +185,10 @@ def run_reference(args, cfg):
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": 1e3 * ns / v, "higher_is_better": True,
            "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic", "config": {"workload": f"{cfg.name} oracle sample", "N": ns, "q": qs},
+           "data": "synthetic",
+           # the same workload as the GPU arm (metric per point of it); each step times a bounded sample
+           "config": {"workload": workload_name(cfg, N, q), "N": N, "q": q,
+                      "sample": {"N": ns, "q": qs, "note": "oracle steps run on this prefix of the workload"}},
            "cpu_baseline": {**last, "value": v},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -416,8 +425,7 @@ def main():
                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (device Philox generator, efgp_data)",
-               "config": {"workload": f"{cfg.name}: 2D Matern-3/2 l={cfg.ell} sigma={cfg.sigma} eps={cfg.eps}, "
-                                      f"N={N:.0e} uniform points, q={q:.0e} uniform targets, seed {cfg.seed}",
+               "config": {"workload": workload_name(cfg, N, q),
                           "N": N, "q": q, "spread": inf["spread_method"], "spread_arithmetic": args.weights,
                           "m": inf["m"], "M": inf["M"], "cg_iters": statistics.median(iters),
                           "l2": "inputs (24 GB/N_gpus) larger than the 126 MB L2; no explicit flush",
