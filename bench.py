@@ -438,7 +438,7 @@ def main():
                             "alg_bytes_per_launch": alg_bytes},
                "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "mu_at_training_points": interp_n,
                "posterior_variance": variance, "hetero_fit": hetero, "spread_variants": spread_variants}
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # the oracle baseline: rank 0 at N = 1 only
             try:
                 ns = int(args.oracle_points)
                 out["cpu_baseline"] = cpu_baseline(cfg, ns, max(1, int(round(ns * q / N))))
