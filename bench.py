@@ -233,11 +233,19 @@ def main():
     model = EFGP(cfg.kernel, cfg.ell, cfg.sigma, cfg.eps, cfg.d, cfg.nu, spread=args.spread, weights=args.weights)
     graph_iters = 8
 
+    use_torch_allreduce = False
     if world > 1:
-        model.comm_init()  # the library's own NCCL communicator: fit() sums the partial modes inside
+        try:
+            model.comm_init()  # the library's own NCCL communicator: fit() sums the partial modes inside
+        except Exception as exc:  # fall back to the split API + torch.distributed allreduce
+            print(f"bench: library communicator unavailable ({exc}); using fit_distributed", file=sys.stderr)
+            use_torch_allreduce = True
 
     def step(xx, yy, tt, out):
-        model.fit(xx, yy)  # this rank's shard; with a communicator the modes are summed over ranks
+        if use_torch_allreduce:
+            model.fit_distributed(xx, yy)
+        else:
+            model.fit(xx, yy)  # this rank's shard; with a communicator the modes are summed over ranks
         return model.predict(tt, out=out)
 
     def barrier():
