@@ -215,7 +215,10 @@ efgp_status spread_begin(efgp_plan *pl, cudaStream_t s);
 efgp_status spread_end(efgp_plan *pl, cudaStream_t s);
 efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s);
 // spread_cellsort.cu: K1 CELLSORT (2D any W, 3D W <= 6); EFGP_ERR_RESOURCE if not applicable
-efgp_status spread_cellsort(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s);
+// w1 (optional): per-point weight of the strength-1 grid (default 1): the heteroskedastic TOEPLITZ
+// solver spreads (1/sigma_n^2, y_n/sigma_n^2) in one pass
+efgp_status spread_cellsort(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s,
+                            const double *w1 = nullptr);
 bool cellsort_geometry(const Params &p, int &lo, int &S, int &ncell);
 // CTAs of the counting-sort kernels (count and scatter share the partition): one per SM.  Fewer CTAs
 // keep fewer partially written 32-byte sectors open in L2 (the c3 scatter reads 4x and writes 3.5x

@@ -569,7 +569,28 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
     // v^w (J_2m) from strengths 1/sigma_n^2 and F^*(y/sigma^2) (J_m), both spread as the "y" strength
     // onto the v grid, then the homoskedastic Toeplitz machinery with sigma^2 -> 1 (reading G11b)
     double2 *vh = reinterpret_cast<double2 *>(pl->modes_sum), *fyh = vh + P.Kvh;
-    for (int pass = 0; pass < 2 && st == EFGP_OK; ++pass) {
+    bool one_pass = false;
+    if (P.spread_method == EFGP_SPREAD_CELLSORT) {
+      // CELLSORT spreads both weighted strengths in one pass: g1 = sum (1/sigma^2) phi (v^w),
+      // g2 = sum (y/sigma^2) phi, then the standard K2 for both
+      st = spread_begin(pl, s);
+      if (st == EFGP_OK) st = spread_cellsort(pl, x, w, N, s, iv);
+      if (st == EFGP_OK) {
+        one_pass = true;
+        st = type1_modes(pl, pl->modes_sum, s);
+        EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned, pl->dflags, sizeof(int) * 4, cudaMemcpyDeviceToHost, s));
+        EFGP_CUDA(cudaStreamSynchronize(s));
+        std::memcpy(flags, pl->h_pinned, sizeof(flags));
+        if (st == EFGP_OK && flags[0]) {
+          pl->err = "fit_hetero: a coordinate is outside [0,1] or non-finite, or an observation is non-finite";
+          st = EFGP_ERR_INVALID;
+        }
+      } else if (st == EFGP_ERR_RESOURCE) {
+        st = EFGP_OK;  // (2^32 points and more in one call): the two-pass route below
+        pl->err.clear();
+      }
+    }
+    for (int pass = 0; pass < 2 && st == EFGP_OK && !one_pass; ++pass) {
       st = spread_begin(pl, s);
       if (st == EFGP_OK) st = spread_points(pl, x, pass == 0 ? iv : w, N, s);
       if (st == EFGP_OK) st = spread_end(pl, s);

@@ -73,7 +73,7 @@ template <int D, int W, int G>
 __global__ void k_cs_scatter(const double *__restrict__ x, const double *__restrict__ y, int64_t N, double h, int n,
                              int lo, int S, int ncell, const unsigned *__restrict__ hist,
                              const long long *__restrict__ off, double *__restrict__ xs, double *__restrict__ ys,
-                             int *__restrict__ err) {
+                             int *__restrict__ err, const double *__restrict__ w1, double *__restrict__ ws1) {
   extern __shared__ unsigned cs_c[];  // cursor relative to the bucket start (< 2^32 points per call)
   for (int i = threadIdx.x; i < ncell; i += blockDim.x) cs_c[i] = hist[(size_t)blockIdx.x * ncell + i];
   __syncthreads();
@@ -85,6 +85,7 @@ __global__ void k_cs_scatter(const double *__restrict__ x, const double *__restr
 #pragma unroll
     for (int k = 0; k < D; ++k) xs[(int64_t)k * N + pos] = __ldg(x + i * D + k);
     ys[pos] = __ldg(y + i);
+    if (w1) ws1[pos] = __ldg(w1 + i);
   }
 }
 
@@ -96,14 +97,15 @@ __device__ __forceinline__ int cs_wrap(int i, int n) {
 template <int D, int W, int G>
 __global__ void __launch_bounds__(kCsThreads) k_cs_spread(const CsItem *__restrict__ items, int64_t nitems,
                                                           const double *__restrict__ xs, const double *__restrict__ ys,
-                                                          int64_t N, double *__restrict__ g1, double *__restrict__ g2,
+                                                          const double *__restrict__ ws1, int64_t N,
+                                                          double *__restrict__ g1, double *__restrict__ g2,
                                                           double h, int n, int lo, int S, EsPoly P) {
   constexpr int U = W + G - 1;                   // union window per dimension of a super-cell
   constexpr int UD = D == 2 ? U * U : U * U * U;
   constexpr int E = (UD + 31) / 32;              // window elements per lane
-  __shared__ double wsm[kCsThreads / 32][32][D * U + 1];  // padded weight rows + y per point
+  __shared__ double wsm[kCsThreads / 32][32][D * U + 2];  // padded weight rows, y, strength-1 weight
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double(*ws)[D * U + 1] = wsm[wid];
+  double(*ws)[D * U + 2] = wsm[wid];
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t it = warp; it < nitems; it += nwarps) {
@@ -142,14 +144,15 @@ __global__ void __launch_bounds__(kCsThreads) k_cs_spread(const CsItem *__restri
 #pragma unroll
         for (int q = 0; q < D * U; ++q) ws[lane][q] = row[q];
         ws[lane][D * U] = __ldg(ys + r);
+        ws[lane][D * U + 1] = ws1 ? __ldg(ws1 + r) : 1.0;
       } else {
 #pragma unroll
-        for (int q = 0; q <= D * U; ++q) ws[lane][q] = 0.0;
+        for (int q = 0; q <= D * U + 1; ++q) ws[lane][q] = 0.0;
       }
       __syncwarp();
       const int np = (int)min(32LL, item.end - b0);
       for (int p = 0; p < np; ++p) {
-        const double yv = ws[p][D * U];
+        const double yv = ws[p][D * U], wv = ws[p][D * U + 1];
 #pragma unroll
         for (int t = 0; t < E; ++t) {
           const int e = lane + 32 * t;
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(kCsThreads) k_cs_spread(const CsItem *__restri
             } else {
               f = ws[p][e / (U * U)] * ws[p][U + (e / U) % U] * ws[p][2 * U + e % U];
             }
-            a1[t] += f;
+            a1[t] = fma(f, wv, a1[t]);
             ay[t] = fma(f, yv, ay[t]);
           }
         }
@@ -204,27 +207,29 @@ bool cellsort_geometry(const Params &p, int &lo, int &S, int &ncell) {
 }
 
 template <int D, int W, int G>
-static efgp_status cellsort_t(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s) {
+static efgp_status cellsort_t(efgp_plan *pl, const double *x, const double *y, const double *w1, int64_t N,
+                              cudaStream_t s) {
   const Params &P = pl->P;
   int lo, S, ncell, Gs;
   if (!cellsort_geometry(P, lo, S, ncell, Gs) || Gs != G) return EFGP_ERR_RESOURCE;
   const int B = sort_ctas(pl->num_sms), T = 1024, n = (int)P.n1;
   unsigned *hist = nullptr;
   long long *tot = nullptr, *off = nullptr;
-  double *xs = nullptr, *ys = nullptr;
+  double *xs = nullptr, *ys = nullptr, *ws1 = nullptr;
   CsItem *items = nullptr;
   EFGP_PALLOC(&hist, sizeof(unsigned) * B * ncell, s);
   EFGP_PALLOC(&tot, sizeof(long long) * ncell, s);
   EFGP_PALLOC(&off, sizeof(long long) * (ncell + 1), s);
   EFGP_PALLOC(&xs, sizeof(double) * N * D, s);
   EFGP_PALLOC(&ys, sizeof(double) * N, s);
+  if (w1) EFGP_PALLOC(&ws1, sizeof(double) * N, s);
   const size_t sm = sizeof(unsigned) * ncell;
   EFGP_CUDA(cudaFuncSetAttribute(k_cs_count<D, W, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   EFGP_CUDA(cudaFuncSetAttribute(k_cs_scatter<D, W, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_cs_count<D, W, G><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, pl->dflags);
   k_het_colscan<<<(ncell + 255) / 256, 256, 0, s>>>(hist, B, ncell, tot);
   k_het_offsets<<<1, 1024, 0, s>>>(tot, ncell, off);
-  k_cs_scatter<D, W, G><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, off, xs, ys, pl->dflags);
+  k_cs_scatter<D, W, G><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, off, xs, ys, pl->dflags, w1, ws1);
   EFGP_CUDA(cudaGetLastError());
   std::vector<long long> offh(ncell + 1);
   EFGP_CUDA(cudaMemcpyAsync(offh.data(), off, sizeof(long long) * (ncell + 1), cudaMemcpyDeviceToHost, s));
@@ -240,34 +245,36 @@ static efgp_status cellsort_t(efgp_plan *pl, const double *x, const double *y, i
   EFGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cs_spread<D, W, G>, kCsThreads, 0));
   int64_t blocks = std::min<int64_t>((int64_t)pl->num_sms * std::max(per_sm, 1), (nitems * 32 + kCsThreads - 1) / kCsThreads);
   if (nitems > 0)
-    k_cs_spread<D, W, G><<<(unsigned)std::max<int64_t>(blocks, 1), kCsThreads, 0, s>>>(items, nitems, xs, ys, N, pl->g1,
+    k_cs_spread<D, W, G><<<(unsigned)std::max<int64_t>(blocks, 1), kCsThreads, 0, s>>>(items, nitems, xs, ys, ws1, N, pl->g1,
                                                                                      pl->g2, P.h, n, lo, S, P.poly);
   EFGP_CUDA(cudaGetLastError());
   EFGP_CUDA(cudaStreamSynchronize(s));  // the host item vector is consumed by the copy above
   for (void *p : {(void *)hist, (void *)tot, (void *)off, (void *)xs, (void *)ys, (void *)items}) cudaFreeAsync(p, s);
+  if (ws1) cudaFreeAsync(ws1, s);
   return EFGP_OK;
 }
 
-efgp_status spread_cellsort(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s) {
+efgp_status spread_cellsort(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s,
+                            const double *w1) {
   if (N >= (1ll << 32)) return EFGP_ERR_RESOURCE;  // 32-bit bucket cursors
   const int W = pl->P.w;
   int lo, S, ncell, G;
   if (!cellsort_geometry(pl->P, lo, S, ncell, G)) return EFGP_ERR_RESOURCE;
   if (pl->P.d == 2 && G == 1) {
     switch (W) {
-#define C2(WW) case WW: return cellsort_t<2, WW, 1>(pl, x, y, N, s);
+#define C2(WW) case WW: return cellsort_t<2, WW, 1>(pl, x, y, w1, N, s);
       C2(2) C2(3) C2(4) C2(5) C2(6) C2(7) C2(8) C2(9) C2(10) C2(11) C2(12) C2(13) C2(14) C2(15) C2(16)
 #undef C2
     }
   } else if (pl->P.d == 2 && G == 2) {
     switch (W) {
-#define C2(WW) case WW: return cellsort_t<2, WW, 2>(pl, x, y, N, s);
+#define C2(WW) case WW: return cellsort_t<2, WW, 2>(pl, x, y, w1, N, s);
       C2(2) C2(3) C2(4) C2(5) C2(6) C2(7) C2(8) C2(9) C2(10) C2(11) C2(12) C2(13) C2(14) C2(15) C2(16)
 #undef C2
     }
   } else if (pl->P.d == 3) {
     switch (W) {
-#define C3(WW) case WW: return cellsort_t<3, WW, 4>(pl, x, y, N, s);
+#define C3(WW) case WW: return cellsort_t<3, WW, 4>(pl, x, y, w1, N, s);
       C3(2) C3(3) C3(4) C3(5) C3(6)
 #undef C3
     }
