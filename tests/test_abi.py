@@ -99,3 +99,18 @@ def test_binding_struct_offsets_match_c(cname, pyname, tmp_path):
     cls = getattr(_lib, pyname)
     py_vals = [getattr(cls, n).offset for n in names] + [ctypes.sizeof(cls)]
     assert py_vals == c_vals
+
+
+def test_product_path_never_touches_the_oracle():
+    # only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference legs may use oracle/;
+    # the package and the library sources must not import or mention it as code
+    pkg = os.path.join(ROOT, "paper_2210_10210_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f), encoding="utf-8", errors="replace").read()
+                assert not re.search(r"^\s*(import oracle|from oracle)", src, flags=re.M), f
+    for f in os.listdir(os.path.join(ROOT, "tools")):
+        if f.endswith(".py"):
+            src = open(os.path.join(ROOT, "tools", f), encoding="utf-8").read()
+            assert "import oracle" not in src and "from oracle" not in src and "_util" not in src, f
