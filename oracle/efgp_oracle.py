@@ -37,6 +37,7 @@ Readings where the paper is silent, garbled or inconsistent (DESIGN.md "Readings
       A_i = diag(delta_i) T_i diag(delta_i) / N^((d-1)/d), M = A_1 (x) ... (x) A_d + sigma^2 I, applied as
       (Q_1 (x) ... ) (Lambda + sigma^2)^-1 (Q_1 (x) ...)^* from eigh(A_i).  Exact (M = A) when the points
       form a tensor-product set and D is separable (SE); d = 1 gives M = A.  Standard PCG, same stop rule.
+  G12b Jacobi preconditioner: diag(D T D + sigma^2 I) = D^2 v_0 + sigma^2 (pinned against the dense diagonal).
   G11b Phi^* S^-1 Phi = D T(v^w) D with v^w = eq 88 with strengths sigma_n^-2 (pinned densely).
   G11 heteroskedastic noise (P:2759-2763 names it, gives no formula): the weight-space posterior mean
       for y = Phi beta + e, beta ~ N(0, I), e ~ N(0, S), S = diag(sigma_n^2): beta solves
@@ -64,7 +65,7 @@ __all__ = [
     "toeplitz_matrix", "toeplitz_apply", "system_apply", "cg", "default_max_iter",
     "posterior_mean", "posterior_variance", "design_matrix", "kernel_tilde_matrix", "dense_gp_mean",
     "dense_gp_variance", "features", "hetero_system_apply", "KronPrecond", "kron_factors",
-    "kron_preconditioner", "kron_apply_inverse", "pcg", "posterior_variance_hetero", "efgp_fit_hetero", "dense_gp_mean_hetero",
+    "kron_preconditioner", "kron_apply_inverse", "pcg", "posterior_variance_hetero", "jacobi_diagonal", "efgp_fit_hetero", "dense_gp_mean_hetero",
     "OracleFit", "efgp_fit", "efgp_predict",
 ]
 
@@ -367,6 +368,14 @@ def kron_apply_inverse(P: KronPrecond, r: np.ndarray) -> np.ndarray:
     return z
 
 
+def jacobi_diagonal(v: np.ndarray, D: np.ndarray, sigma2: float) -> np.ndarray:
+    """diag(D T D + sigma^2 I) = D_j^2 v_0 + sigma^2 (T_jj = v_0 = N, eq ``88`` at j = 0): the Jacobi
+    preconditioner of reading G12b."""
+    d = D.ndim
+    m = (D.shape[0] - 1) // 2
+    return D ** 2 * float(v[(2 * m,) * d].real) + sigma2
+
+
 def pcg(apply, precond, b: np.ndarray, tol: float, max_iter: int):
     """Preconditioned CG (Golub & Van Loan Alg 11.5.1, the standard recurrences), x0 = 0, stopping
     at the first k with ||r_k|| <= tol ||b|| (the same rule as :func:`cg`, reading G6).
@@ -442,7 +451,7 @@ def features(D, h, xt) -> np.ndarray:
 
 
 def posterior_variance(fit, xt, cg_tol: float | None = None, max_iter: int | None = None,
-                       return_iters: bool = False):
+                       return_iters: bool = False, precond: str | None = None):
     """s(x*) = sum_j eta_j phi_j(x*)  (eq ``sws``) where, per target,
     (Phi^*Phi + sigma^2 I) eta = sigma^2 conj(phi(x*))  (eq ``eta``), solved by the same
     plain CG and system_apply as the mean ("a new right-hand side ... per target").
@@ -459,7 +468,12 @@ def posterior_variance(fit, xt, cg_tol: float | None = None, max_iter: int | Non
     out = np.empty(len(xt))
     iters = []
     for t in range(len(xt)):
-        eta, k, _ = cg(lambda p: system_apply(fit.v, fit.D, s2, p, T), s2 * np.conj(Phi[t]), tol, cap)
+        A = lambda p: system_apply(fit.v, fit.D, s2, p, T)
+        if precond == "jacobi":
+            dg = jacobi_diagonal(fit.v, fit.D, s2)
+            eta, k, _ = pcg(A, lambda r: r / dg, s2 * np.conj(Phi[t]), tol, cap)
+        else:
+            eta, k, _ = cg(A, s2 * np.conj(Phi[t]), tol, cap)
         out[t] = np.sum(eta * Phi[t]).real
         iters.append(k)
     return (out, iters) if return_iters else out
@@ -618,6 +632,9 @@ def efgp_fit(x, y, kernel: str, ell: float, sigma: float, eps: float, nu: float 
     if precond == "kron":
         Pk = kron_preconditioner(v, D, sigma ** 2)
         beta, iters, hist = pcg(A, lambda r: kron_apply_inverse(Pk, r), b, tol, cap)
+    elif precond == "jacobi":
+        dg = jacobi_diagonal(v, D, sigma ** 2)
+        beta, iters, hist = pcg(A, lambda r: r / dg, b, tol, cap)
     else:
         beta, iters, hist = cg(A, b, tol, cap)
     return OracleFit(kernel, nu, ell, sigma, eps, d, h, m, D, v, b, beta, iters, hist)
