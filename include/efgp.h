@@ -77,8 +77,11 @@ typedef enum { EFGP_WEIGHTS_FP64 = 0, EFGP_WEIGHTS_FP32 = 1, EFGP_WEIGHTS_MIXED 
  *         and stopping rule.  Measured (profiles/r01_configs_v2.jsonl): SE (separable density) c3
  *         N = 1e7 2831 -> 152 iterations; Matérn (non-separable D, the product approximation of D
  *         is poor off the axes) needs MORE iterations (c5 52 -> 2542).  efgp_predict_var uses plain CG.
- *   AUTO: KRON for EFGP_SE, NONE otherwise. */
-typedef enum { EFGP_PRECOND_NONE = 0, EFGP_PRECOND_KRON = 1, EFGP_PRECOND_AUTO = 2 } efgp_precond;
+ *   JACOBI: PCG with M = diag(D_j^2 v_0 + sigma^2) (reading G12b), the diagonal of the system; for the
+ *         Matérn configs 3-8x fewer iterations at the production tolerance (oracle: c5 22 -> 7,
+ *         c2 199 -> 36), variance systems more (c5 718 -> 29).
+ *   AUTO: KRON for EFGP_SE, JACOBI otherwise. */
+typedef enum { EFGP_PRECOND_NONE = 0, EFGP_PRECOND_KRON = 1, EFGP_PRECOND_AUTO = 2, EFGP_PRECOND_JACOBI = 3 } efgp_precond;
 
 /* NEXT-3 solver of efgp_fit_hetero (readings G11, G11b).
  *   TOEPLITZ: Phi^* S^-1 Phi = D T(v^w) D with v^w = eq "88" with strengths sigma_n^-2: one extra

@@ -589,7 +589,7 @@ void efgp_destroy(efgp_handle pl) {
                   pl->scal, pl->hist, pl->dflags, pl->T2box, pl->t2grid, pl->stage[0], pl->stage[1],
                   pl->rec[0], pl->rec[1], pl->rec[2], pl->trace,
                   pl->sync_buf, pl->het_box, pl->het_grid, pl->pc_Q, pl->pc_F0, pl->pc_F1, pl->pc_work, pl->z,
-                  pl->pc_lam, pl->pc_info, pl->comm_buf, pl->vfull};
+                  pl->pc_lam, pl->pc_info, pl->comm_buf, pl->vfull, pl->pc_diag};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (pl->h_pinned) cudaFreeHost(pl->h_pinned);

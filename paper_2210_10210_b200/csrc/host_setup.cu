@@ -237,11 +237,11 @@ std::string validate_and_choose(Params &p, const efgp_options &opt) {
   if (opt.spread_weights != EFGP_WEIGHTS_FP64 && p.nufft_tol < 1e-6)
     return "fp32 spreading weights need nufft_tol >= 1e-6";
   p.spread_mode = opt.spread_weights;
-  if (opt.precond < EFGP_PRECOND_NONE || opt.precond > EFGP_PRECOND_AUTO) return "unknown precond";
+  if (opt.precond < EFGP_PRECOND_NONE || opt.precond > EFGP_PRECOND_JACOBI) return "unknown precond";
   // AUTO: the Kronecker factors are exact in D only for a separable spectral density (SE)
   if (opt.hetero_method < EFGP_HETERO_AUTO || opt.hetero_method > EFGP_HETERO_NUFFT) return "unknown hetero_method";
   p.hetero_method = opt.hetero_method;
-  p.precond = opt.precond == EFGP_PRECOND_AUTO ? (p.kernel == EFGP_SE ? EFGP_PRECOND_KRON : EFGP_PRECOND_NONE)
+  p.precond = opt.precond == EFGP_PRECOND_AUTO ? (p.kernel == EFGP_SE ? EFGP_PRECOND_KRON : EFGP_PRECOND_JACOBI)
                                                : opt.precond;
   resolve_spread_method(p);
   return "";

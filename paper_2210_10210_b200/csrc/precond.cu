@@ -211,6 +211,31 @@ __global__ void k_pc_axis_f(const double2 *__restrict__ in, double2 *__restrict_
   }
 }
 
+
+// Jacobi (reading G12b): diag_q = D_q^2 v_0 + sigma^2 on the Hermitian half; z = r / diag
+template <int D>
+__global__ void k_jacobi_diag(const double2 *__restrict__ vh, const double *__restrict__ Dh, int64_t Mh, int m,
+                              double sigma2, double *__restrict__ diag) {
+  int j0[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) j0[k] = 0;
+  const double v0 = vh[encode_half<D>(j0, 2 * m)].x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x)
+    diag[q] = Dh[q] * Dh[q] * v0 + sigma2;
+}
+
+__global__ void k_pc_jacobi(const double2 *__restrict__ r, double2 *__restrict__ z, const double *__restrict__ diag,
+                            int64_t Mh, const int *__restrict__ done) {
+  pdl_wait();
+  pdl_trigger();
+  if (done && *done) return;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 a = r[q];
+    const double w = 1.0 / diag[q];
+    z[q] = make_double2(a.x * w, a.y * w);
+  }
+}
+
 static unsigned pc_grid(int64_t n, int sms) {
   int64_t b = (n + 255) / 256;
   const int64_t cap = (int64_t)sms * 8;
@@ -219,6 +244,19 @@ static unsigned pc_grid(int64_t n, int sms) {
 
 efgp_status precond_setup(efgp_plan *pl, const double *modes) {
   const Params &P = pl->P;
+  if (P.precond == EFGP_PRECOND_JACOBI) {
+    if (!pl->pc_diag) EFGP_CUDA(cudaMalloc((void **)&pl->pc_diag, sizeof(double) * P.Mh));
+    if (!pl->z) EFGP_CUDA(cudaMalloc((void **)&pl->z, sizeof(double2) * P.Mh));
+    const double2 *vh = reinterpret_cast<const double2 *>(modes);
+    const unsigned g = pc_grid(P.Mh, pl->num_sms);
+    switch (P.d) {
+      case 1: k_jacobi_diag<1><<<g, 256, 0, pl->stream>>>(vh, pl->D_half, P.Mh, (int)P.m, pl->sigma2_sys, pl->pc_diag); break;
+      case 2: k_jacobi_diag<2><<<g, 256, 0, pl->stream>>>(vh, pl->D_half, P.Mh, (int)P.m, pl->sigma2_sys, pl->pc_diag); break;
+      case 3: k_jacobi_diag<3><<<g, 256, 0, pl->stream>>>(vh, pl->D_half, P.Mh, (int)P.m, pl->sigma2_sys, pl->pc_diag); break;
+    }
+    EFGP_CUDA(cudaGetLastError());
+    return EFGP_OK;
+  }
   const int d = P.d;
   const int64_t m = P.m, n = 2 * m + 1, K = 2 * m;
   cudaStream_t s = pl->stream;
@@ -354,6 +392,13 @@ static efgp_status precond_apply_d(efgp_plan *pl, const double2 *r, double2 *z, 
 }
 
 efgp_status precond_apply(efgp_plan *pl, const double2 *r, double2 *z, const int *done, cudaStream_t s, bool pdl) {
+  if (pl->P.precond == EFGP_PRECOND_JACOBI) {
+    const unsigned g = pc_grid(pl->P.Mh, pl->num_sms);
+    if (pdl) EFGP_CUDA(launch_pdl(k_pc_jacobi, g, 256, s, r, z, (const double *)pl->pc_diag, pl->P.Mh, done));
+    else k_pc_jacobi<<<g, 256, 0, s>>>(r, z, pl->pc_diag, pl->P.Mh, done);
+    EFGP_CUDA(cudaGetLastError());
+    return EFGP_OK;
+  }
   switch (pl->P.d) {
     case 1: return precond_apply_d<1>(pl, r, z, done, s, pdl);
     case 2: return precond_apply_d<2>(pl, r, z, done, s, pdl);

@@ -207,7 +207,7 @@ __device__ __forceinline__ void pc_load_q(const double2 *__restrict__ Qg, int m,
 }
 
 // rhs = sigma^2 conj(phi(x*)) = sigma^2 D_j e^{-2 pi i h j.x*}; x = 0; r = p = rhs; first C2R input
-template <int D, bool PC>
+template <int D, int PC>  // PC: 0 plain CG, 1 Kronecker (G12), 2 Jacobi (G12b)
 __global__ void __launch_bounds__(kVarThreads) k_var_init(const double *__restrict__ xt, int nt, double h, int m,
                                                           double sigma2, const double *__restrict__ Dh, int64_t Mh,
                                                           int64_t L, int64_t box, double2 *__restrict__ vx,
@@ -250,11 +250,19 @@ __global__ void __launch_bounds__(kVarThreads) k_var_init(const double *__restri
   __syncthreads();
   double rz = rr;
   if constexpr (PC) {  // p0 = z0 = M^-1 r0
-    const int n = 2 * m + 1, total = D == 1 ? n : n * n;
-    double2 *Q = E + D * n, *A = Q + D * n * n, *Bf = A + total;
-    pc_load_q<D>(pcQ, m, Q);
-    __syncthreads();
-    pc_apply_cta<D>(r, p, m, Q, A, Bf, pcl, sigma2, Mh);
+    if constexpr (PC == 2) {
+      for (int64_t q = threadIdx.x; q < Mh; q += blockDim.x) {
+        const double2 a = r[q];
+        const double w = 1.0 / pcl[q];
+        p[q] = make_double2(a.x * w, a.y * w);
+      }
+    } else {
+      const int n = 2 * m + 1, total = D == 1 ? n : n * n;
+      double2 *Q = E + D * n, *A = Q + D * n * n, *Bf = A + total;
+      pc_load_q<D>(pcQ, m, Q);
+      __syncthreads();
+      pc_apply_cta<D>(r, p, m, Q, A, Bf, pcl, sigma2, Mh);
+    }
     acc = 0.0;
     for (int64_t q = threadIdx.x; q < Mh; q += blockDim.x) {
       const double2 a = r[q], z = p[q];
@@ -281,7 +289,7 @@ __global__ void k_var_mul(double *__restrict__ Y, const double *__restrict__ vha
 }
 
 // one CG iteration of one target (CTA = target)
-template <int D, bool PC>
+template <int D, int PC>  // PC: 0 plain CG, 1 Kronecker (G12), 2 Jacobi (G12b)
 __global__ void __launch_bounds__(kVarThreads) k_var_step(const double2 *__restrict__ Zall, const double *__restrict__ Dh,
                                                           int64_t Mh, int m, int64_t L, int64_t box, double sigma2,
                                                           double tol, int max_iter, double2 *__restrict__ vx,
@@ -331,12 +339,20 @@ __global__ void __launch_bounds__(kVarThreads) k_var_step(const double2 *__restr
   const bool fin = sqrt(rr_new) <= tol * st[t].bnorm || it >= max_iter;
   if constexpr (PC) {
     if (!fin) {  // z = M^-1 r into the (now free) Ap buffer; p = z + ((r,z)_new / (r,z)) p
-      const int n = 2 * m + 1, total = D == 1 ? n : n * n;
-      double2 *Q = pcsm, *A = Q + D * n * n, *Bf = A + total;
-      __syncthreads();
-      pc_load_q<D>(pcQ, m, Q);
-      __syncthreads();
-      pc_apply_cta<D>(r, Ap, m, Q, A, Bf, pcl, sigma2, Mh);
+      if constexpr (PC == 2) {
+        for (int64_t q = threadIdx.x; q < Mh; q += blockDim.x) {
+          const double2 a = r[q];
+          const double w = 1.0 / pcl[q];
+          Ap[q] = make_double2(a.x * w, a.y * w);
+        }
+      } else {
+        const int n = 2 * m + 1, total = D == 1 ? n : n * n;
+        double2 *Q = pcsm, *A = Q + D * n * n, *Bf = A + total;
+        __syncthreads();
+        pc_load_q<D>(pcQ, m, Q);
+        __syncthreads();
+        pc_apply_cta<D>(r, Ap, m, Q, A, Bf, pcl, sigma2, Mh);
+      }
       acc = 0.0;
       for (int64_t q = threadIdx.x; q < Mh; q += blockDim.x) {
         const double2 a = r[q], z = Ap[q];
@@ -484,17 +500,23 @@ static efgp_status var_batch(efgp_plan *pl, const double *xt, int nt, double *ou
   // NEXT-4 in the variance CGs: the fit's Kronecker factors, applied per target inside its CTA
   const int64_t n = 2 * P.m + 1, total = D == 1 ? n : n * n;
   const size_t pcsm = sizeof(double2) * (D * n * n + 2 * total);
-  const bool pc = D <= 2 && P.precond == EFGP_PRECOND_KRON && pl->pc_Q && esm + pcsm <= 200 * 1024;
+  const int pc = P.precond == EFGP_PRECOND_JACOBI && pl->pc_diag
+                     ? 2
+                     : (D <= 2 && P.precond == EFGP_PRECOND_KRON && pl->pc_Q && esm + pcsm <= 200 * 1024 ? 1 : 0);
   pl->var_pc = pc;
   EFGP_CUDA(cudaMemsetAsync(ndone, 0, sizeof(unsigned), s));
-  if (pc) {
-    EFGP_CUDA(cudaFuncSetAttribute(k_var_init<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(esm + pcsm)));
-    EFGP_CUDA(cudaFuncSetAttribute(k_var_step<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcsm));
-    k_var_init<D, true><<<B, kVarThreads, esm + pcsm, s>>>(xt, nt, P.h, (int)P.m, sigma2, pl->D_half, P.Mh, P.L, box,
+  if (pc == 2) {
+    k_var_init<D, 2><<<B, kVarThreads, esm, s>>>(xt, nt, P.h, (int)P.m, sigma2, pl->D_half, P.Mh, P.L, box, pl->var_x,
+                                                 pl->var_r, pl->var_p, pl->var_X, st, ndone, pl->dflags, nullptr,
+                                                 pl->pc_diag);
+  } else if (pc) {
+    EFGP_CUDA(cudaFuncSetAttribute(k_var_init<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(esm + pcsm)));
+    EFGP_CUDA(cudaFuncSetAttribute(k_var_step<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcsm));
+    k_var_init<D, 1><<<B, kVarThreads, esm + pcsm, s>>>(xt, nt, P.h, (int)P.m, sigma2, pl->D_half, P.Mh, P.L, box,
                                                            pl->var_x, pl->var_r, pl->var_p, pl->var_X, st, ndone,
                                                            pl->dflags, pl->pc_Q, pl->pc_lam);
   } else {
-    k_var_init<D, false><<<B, kVarThreads, esm, s>>>(xt, nt, P.h, (int)P.m, sigma2, pl->D_half, P.Mh, P.L, box,
+    k_var_init<D, 0><<<B, kVarThreads, esm, s>>>(xt, nt, P.h, (int)P.m, sigma2, pl->D_half, P.Mh, P.L, box,
                                                      pl->var_x, pl->var_r, pl->var_p, pl->var_X, st, ndone, pl->dflags,
                                                      nullptr, nullptr);
   }
@@ -515,12 +537,16 @@ static efgp_status var_batch(efgp_plan *pl, const double *xt, int nt, double *ou
       cufftExecZ2D(pl->plan_var_c2r, pl->var_X, pl->var_Y);
       k_var_mul<<<pl->num_sms * 4, 256, 0, s>>>(pl->var_Y, pl->vhat, Ld, Ld * B);
       cufftExecD2Z(pl->plan_var_r2c, pl->var_Y, pl->var_Z);
-      if (pc)
-        k_var_step<D, true><<<B, kVarThreads, pcsm, s>>>(pl->var_Z, pl->D_half, P.Mh, (int)P.m, P.L, box, sigma2,
+      if (pc == 2)
+        k_var_step<D, 2><<<B, kVarThreads, 0, s>>>(pl->var_Z, pl->D_half, P.Mh, (int)P.m, P.L, box, sigma2, P.cg_tol,
+                                                   max_iter, pl->var_x, pl->var_r, pl->var_p, pl->var_Ap, pl->var_X,
+                                                   st, ndone, nullptr, pl->pc_diag);
+      else if (pc)
+        k_var_step<D, 1><<<B, kVarThreads, pcsm, s>>>(pl->var_Z, pl->D_half, P.Mh, (int)P.m, P.L, box, sigma2,
                                                          P.cg_tol, max_iter, pl->var_x, pl->var_r, pl->var_p,
                                                          pl->var_Ap, pl->var_X, st, ndone, pl->pc_Q, pl->pc_lam);
       else
-        k_var_step<D, false><<<B, kVarThreads, 0, s>>>(pl->var_Z, pl->D_half, P.Mh, (int)P.m, P.L, box, sigma2,
+        k_var_step<D, 0><<<B, kVarThreads, 0, s>>>(pl->var_Z, pl->D_half, P.Mh, (int)P.m, P.L, box, sigma2,
                                                        P.cg_tol, max_iter, pl->var_x, pl->var_r, pl->var_p,
                                                        pl->var_Ap, pl->var_X, st, ndone, nullptr, nullptr);
     }

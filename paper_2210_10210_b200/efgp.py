@@ -99,7 +99,7 @@ class EFGP:
         opt.matern_rescale = _RESCALE[matern_rescale]
         opt.spread_method = _SPREAD[spread]
         opt.spread_weights = {"fp64": 0, "fp32": 1, "mixed": 2}[weights]
-        opt.precond = {None: 0, "none": 0, "kron": 1, "auto": 2}[precond]  # NEXT-4 (reading G12)
+        opt.precond = {None: 0, "none": 0, "kron": 1, "auto": 2, "jacobi": 3}[precond]  # NEXT-4 (G12, G12b)
         opt.hetero_method = {"auto": 0, "toeplitz": 1, "nufft": 2}[hetero]  # NEXT-3 (G11, G11b)
         if graph_iters is not None:
             opt.graph_iters = int(graph_iters)

@@ -178,6 +178,27 @@ def test_hetero_toeplitz_with_kron_preconditioner():
     assert out["kron"][1] < out[None][1] / 2, (out["kron"][1], out[None][1])
 
 
+def test_hetero_toeplitz_with_jacobi_preconditioner():
+    # Jacobi (reading G12b) on the weighted system D T(v^w) D + I of reading G11b: the same mean as the
+    # oracle's dense heteroskedastic solve path (efgp_fit_hetero), c5 (Matern, 1D)
+    c = CONFIGS["c5"]
+    rng = np.random.default_rng(17)
+    x, y, xt = generate(c, N=3_000, q=300)                         # oracle: ~16 s
+    sd = c.sigma * (0.5 + rng.uniform(0, 1, len(x)))
+    out = {}
+    for pc in (None, "jacobi"):
+        g = model(c, cg_tol=c.eps / 1000, precond=pc)
+        g.fit_hetero(dev(x), dev(y), dev(sd))
+        inf = g.info()
+        assert inf["hetero_sorted"] == 2 and inf["precond"] == (3 if pc else 0)
+        out[pc] = (g.predict(dev(xt)).cpu().numpy(), inf["iters"])
+        g.close()
+    fit = O.efgp_fit_hetero(x, y, sd, c.kernel, c.ell, c.eps, nu=c.nu, cg_tol=c.eps / 1000)
+    ref = O.efgp_predict(fit, xt)
+    assert rel(out["jacobi"][0], ref) <= 10 * c.eps
+    assert rel(out[None][0], ref) <= 10 * c.eps
+
+
 @pytest.mark.parametrize("eps", [1e-1, 1e-2, 1e-5])
 def test_hetero_solvers_agree_every_width(eps):
     # the NUFFT-pair solver (sorted fused pass, widths W = 3, 4, 7 here) and the TOEPLITZ solver solve

@@ -95,8 +95,8 @@ def test_pcg_reduces_iterations_at_size():
         g.close()
 
 
-def test_auto_selects_kron_for_se_only():
-    for name, want in (("c3", 1), ("c5", 0)):
+def test_auto_selects_kron_for_se_jacobi_otherwise():
+    for name, want in (("c3", 1), ("c5", 3)):
         c = CONFIGS[name]
         x, y, _ = generate(c, N=2000, q=1)
         g = model(c, precond="auto")
@@ -140,3 +140,67 @@ def test_variance_kron_reduces_iterations_at_size():
         g.close()
     assert rel(out["kron"][0], out[None][0]) <= 10 * c.eps
     assert out["kron"][1] < out[None][1] / 2, (out["kron"][1], out[None][1])
+
+
+# ---- NEXT-4, Jacobi preconditioner M = diag(D_j^2 v_0 + sigma^2) (reading G12b)
+
+@pytest.mark.parametrize("name", ["c2", "c5", "c4"])
+def test_pcg_jacobi_parity(name):
+    c = CONFIGS[name]
+    N, m_over = PC_SIZES[name]
+    x, y, xt = generate(c, N=N, q=min(c.q, 2000))
+    cg_tol = c.eps / 1000                                          # parity mode (reading G9)
+    kw = {}
+    if m_over is not None:
+        h0, _ = O.choose_params(c.kernel, c.ell, c.d, c.eps, c.nu)
+        kw = dict(h=h0, m=m_over)
+    g = model(c, cg_tol=cg_tol, precond="jacobi", **kw)
+    g.fit(dev(x), dev(y))
+    mu = g.predict(dev(xt)).cpu().numpy()
+    inf = g.info()
+    assert inf["precond"] == 3
+    fit = O.efgp_fit(x, y, c.kernel, c.ell, c.sigma, c.eps, nu=c.nu, cg_tol=cg_tol, h=kw.get("h"), m=kw.get("m"),
+                     precond="jacobi")
+    ref = O.efgp_predict(fit, xt)
+    assert rel(mu, ref) <= 10 * c.eps, (rel(mu, ref), 10 * c.eps)
+    hist = g.residual_history()
+    assert len(hist) == inf["iters"] + 1 and hist[-1] <= cg_tol
+    assert abs(inf["iters"] - fit.iters) <= max(3, 0.1 * fit.iters), (inf["iters"], fit.iters)
+    k = min(5, fit.iters, inf["iters"])
+    big = [i for i in range(k + 1) if fit.history[i] > 1e3 * cg_tol]
+    np.testing.assert_allclose(np.asarray(hist)[big], np.asarray(fit.history)[big], rtol=1e-2)
+    g.close()
+
+
+def test_pcg_jacobi_reduces_iterations_matern():
+    # c5 (Matern-3/2, 1D heavy-tailed spectral density: D_j^2 v_0 spans many decades) at N = 1e6
+    from efgp_data import gpu as G
+    c = CONFIGS["c5"]
+    x, y = G.generate_points(c, 0, 1_000_000)
+    out = {}
+    for pc in (None, "jacobi"):
+        g = model(c, precond=pc)
+        g.fit(x, y)
+        out[pc] = g.info()["iters"]
+        g.close()
+    assert out["jacobi"] < out[None] / 2, out
+
+
+@pytest.mark.parametrize("name", ["c2", "c5"])
+def test_variance_with_jacobi_preconditioner(name, monkeypatch):
+    c = CONFIGS[name]
+    x, y, _ = generate(c, N=3000, q=1)
+    xt = np.random.default_rng(50 + c.id).uniform(0, 1, (8, c.d))   # oracle: ~1e3 iterations per target
+    xt[0] = x[0]
+    cg_tol = c.eps / 1000
+    kw = {}
+    if name == "c2":                                               # m = 12 keeps the oracle in seconds
+        kw = dict(h=O.choose_params(c.kernel, c.ell, c.d, c.eps, c.nu)[0], m=12)
+    monkeypatch.setenv("EFGP_VAR_BATCH", "16")
+    g = model(c, cg_tol=cg_tol, precond="jacobi", **kw)
+    g.fit(dev(x), dev(y))
+    var = g.predict_var(dev(xt)).cpu().numpy()
+    fit = O.efgp_fit(x, y, c.kernel, c.ell, c.sigma, c.eps, nu=c.nu, cg_tol=cg_tol, **kw)
+    ref = O.posterior_variance(fit, xt, cg_tol=cg_tol, precond="jacobi")
+    assert rel(var, ref) <= 10 * c.eps, (rel(var, ref), 10 * c.eps)
+    g.close()

@@ -22,7 +22,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--c5-N", type=float, default=None)
     ap.add_argument("--var-targets", type=int, default=0, help="also time the posterior variance (NEXT-2)")
-    ap.add_argument("--precond", default="none", choices=["none", "kron", "auto"], help="NEXT-4 preconditioner")
+    ap.add_argument("--precond", default="none", choices=["none", "kron", "auto", "jacobi"], help="NEXT-4 preconditioner")
     ap.add_argument("--hetero", action="store_true", help="also time NEXT-3 (fit_hetero, sigma_n = sigma (0.5 + U))")
     a = ap.parse_args()
     import torch
