@@ -127,7 +127,7 @@ typedef struct {
   int64_t var_iters_max, var_batch;                           /* its largest CG count, targets/batch */
   int64_t hetero_sorted; /* last efgp_fit_hetero: 0 unfused NUFFT pair, 1 sorted fused NUFFT pair,
                             2 weighted Toeplitz (G11b) */
-  int64_t precond;       /* preconditioner used by the fit (EFGP_PRECOND_NONE or _KRON; AUTO resolved) */
+  int64_t precond;       /* preconditioner the last fit used (NONE, KRON or JACOBI; AUTO resolved; NONE after a NUFFT-pair hetero fit) */
   int64_t comm_size;     /* ranks of the handle's NCCL communicator (0: none) */
 } efgp_info;
 

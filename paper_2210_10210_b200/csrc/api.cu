@@ -228,7 +228,8 @@ efgp_status fit_solve_impl(efgp_plan *pl, const double *modes, int64_t N_total) 
   pl->sigma2_sys = P.sigma * P.sigma;  // (Phi^*Phi + sigma^2 I)
   pl->cap_sigma = P.sigma;
   efgp_status st;
-  if (P.precond) {  // NEXT-4: Kronecker-preconditioned CG (reading G12)
+  pl->pc_used = P.precond;
+  if (P.precond) {  // NEXT-4: Kronecker (G12) or Jacobi (G12b) preconditioned CG
     EFGP_TRY(precond_setup(pl, pl->modes_sum));
     st = pcg_solve(pl, N_total);
   } else {
@@ -545,7 +546,7 @@ efgp_status efgp_get_info(efgp_handle pl, efgp_info *o) {
     o->var_batch = pl->var_B;
   }
   o->hetero_sorted = pl->het_path;
-  o->precond = P.precond;
+  o->precond = pl->pc_used;
   o->comm_size = pl->comm_size;
   return EFGP_OK;
 }

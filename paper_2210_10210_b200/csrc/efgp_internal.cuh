@@ -182,7 +182,8 @@ struct efgp_plan {
   // NEXT-4 Kronecker preconditioner (precond.cu): eigenvectors/values of the d factors, work grids
   double2 *pc_Q = nullptr, *pc_F0 = nullptr, *pc_F1 = nullptr, *pc_work = nullptr, *z = nullptr;
   double *pc_lam = nullptr;
-  double *pc_diag = nullptr;  // Jacobi: D_q^2 v_0 + sigma^2 on the half (reading G12b)
+  double *pc_diag = nullptr;
+  int pc_used = 0;  // preconditioner of the last fit's solve (0 after a NUFFT-pair hetero fit)  // Jacobi: D_q^2 v_0 + sigma^2 on the half (reading G12b)
   int *pc_info = nullptr;
   void *pc_solver = nullptr;  // cusolverDnHandle_t
   cudaGraphExec_t pcg_exec = nullptr;

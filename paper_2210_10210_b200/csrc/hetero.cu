@@ -622,6 +622,7 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
       EFGP_CUDA(cudaEventRecord(pl->ev[2], s));
       if (st == EFGP_OK) {
         pl->op_valid = true;
+        pl->pc_used = P.precond;
         if (P.precond) {
           st = precond_setup(pl, pl->modes_sum);
           if (st == EFGP_OK) st = pcg_solve(pl, Ntot);
@@ -677,6 +678,7 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
       HetSortedCtx sctx{&H, N};
       if (st == EFGP_OK) st = cg_solve_op(pl, max_iter, het_apply_sorted, &sctx);
       pl->het_path = 1;
+      pl->pc_used = 0;
     } else {
       EFGP_CUDA(cudaEventRecord(pl->ev[2], s));
       // Both NUFFTs on the same fine grid n_rhs with the same kernel and deconvolution: the type-2 is
@@ -708,6 +710,7 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
       }
       st = cg_solve_op(pl, max_iter, het_apply, &ctx);
       pl->het_path = 0;
+      pl->pc_used = 0;
     }
     het_sorted_free(H, s);
     EFGP_CUDA(cudaEventRecord(pl->ev[4], s));

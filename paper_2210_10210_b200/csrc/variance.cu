@@ -500,9 +500,9 @@ static efgp_status var_batch(efgp_plan *pl, const double *xt, int nt, double *ou
   // NEXT-4 in the variance CGs: the fit's Kronecker factors, applied per target inside its CTA
   const int64_t n = 2 * P.m + 1, total = D == 1 ? n : n * n;
   const size_t pcsm = sizeof(double2) * (D * n * n + 2 * total);
-  const int pc = P.precond == EFGP_PRECOND_JACOBI && pl->pc_diag
+  const int pc = pl->pc_used == EFGP_PRECOND_JACOBI && pl->pc_diag
                      ? 2
-                     : (D <= 2 && P.precond == EFGP_PRECOND_KRON && pl->pc_Q && esm + pcsm <= 200 * 1024 ? 1 : 0);
+                     : (D <= 2 && pl->pc_used == EFGP_PRECOND_KRON && pl->pc_Q && esm + pcsm <= 200 * 1024 ? 1 : 0);
   pl->var_pc = pc;
   EFGP_CUDA(cudaMemsetAsync(ndone, 0, sizeof(unsigned), s));
   if (pc == 2) {

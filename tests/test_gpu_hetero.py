@@ -238,3 +238,22 @@ def test_hetero_solvers_agree_every_width(eps):
         ws[meth] = inf["w"]
         g.close()
     assert rel(mus["nufft"], mus["toeplitz"]) <= 10 * eps, rel(mus["nufft"], mus["toeplitz"])
+
+
+def test_nufft_solver_reports_no_preconditioner():
+    # options.precond applies to the TOEPLITZ solver only: a NUFFT-pair fit after a preconditioned
+    # homoskedastic fit reports NONE
+    c = CONFIGS["c5"]
+    x, y, xt = generate(c, N=5_000, q=20)
+    sd = noise_sd(c, len(x), 77)
+    g = model(c, precond="jacobi", hetero="toeplitz")
+    g.fit_hetero(dev(x), dev(y), dev(sd))
+    assert g.info()["precond"] == 3
+    g.close()
+    g = model(c, precond="jacobi", hetero="nufft")
+    g.fit(dev(x), dev(y))
+    assert g.info()["precond"] == 3
+    g.fit_hetero(dev(x), dev(y), dev(sd))
+    assert g.info()["precond"] == 0 and g.info()["hetero_sorted"] in (0, 1)
+    assert np.all(np.isfinite(g.predict(dev(xt)).cpu().numpy()))
+    g.close()
