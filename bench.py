@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--variance", action="store_true", help=argparse.SUPPRESS)  # (default on; kept for old scripts)
     ap.add_argument("--var-targets", type=float, default=64, help="targets of the NEXT-2 measurement")
     ap.add_argument("--no-hetero", action="store_true", help="skip NEXT-3 (heteroskedastic fit, both solvers)")
+    ap.add_argument("--no-precond", action="store_true", help="skip NEXT-4 (fit with precond=auto)")
     ap.add_argument("--no-spread-variants", action="store_true", help="skip the fp32 / mixed K1 arithmetic variants")
     ap.add_argument("--hetero", action="store_true", help=argparse.SUPPRESS)  # (default on)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -324,6 +325,28 @@ def main():
 
     # NEXT-3: heteroskedastic fit, sigma_n = sigma (0.5 + u), u ~ U[0,1) (seeded); every
     # CG iteration is K8 + C2R + K9 (q = N, fused / sigma_n^2) + K1 (N points) + R2C + deconvolution
+    # NEXT-4: the same fit with precond = AUTO (Kronecker for SE, Jacobi otherwise,
+    # readings G12 / G12b) beside the headline's plain CG (Alg a1); one rank only
+    precond = None
+    if not args.no_precond and world == 1:
+        try:
+            mp = EFGP(cfg.kernel, cfg.ell, cfg.sigma, cfg.eps, cfg.d, cfg.nu, spread=args.spread,
+                      weights=args.weights, precond="auto")
+            mp.fit(x, y)  # warm-up
+            torch.cuda.synchronize()
+            tp0 = time.perf_counter()
+            mp.fit(x, y)
+            torch.cuda.synchronize()
+            wall = (time.perf_counter() - tp0) * 1e3
+            ip = mp.info()
+            precond = {"precond": {0: "none", 1: "kron", 3: "jacobi"}[ip["precond"]], "iters": ip["iters"],
+                       "iters_plain_cg": statistics.median(iters), "solve_ms": ip["t_solve_ms"],
+                       "solve_ms_plain_cg": statistics.median(solve_ms),
+                       "fit_ms": ip["t_spread_ms"] + ip["t_modes_ms"] + ip["t_solve_ms"], "wall_ms": wall}
+            mp.close()
+        except Exception as exc:
+            precond = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
     # K1 arithmetic variants ("report both variants"): the spreading time of one fit with
     # fp32 kernel weights (FP32) and fp32 weights + fp32 round sums (MIXED) beside the fp64 headline
     spread_variants = None
@@ -445,7 +468,8 @@ def main():
                             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                             "alg_bytes_per_launch": alg_bytes},
                "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "mu_at_training_points": interp_n,
-               "posterior_variance": variance, "hetero_fit": hetero, "spread_variants": spread_variants}
+               "posterior_variance": variance, "hetero_fit": hetero, "preconditioned_fit": precond,
+               "spread_variants": spread_variants}
         if not args.no_cpu_baseline and world == 1:  # the oracle baseline: rank 0 at N = 1 only
             try:
                 ns = int(args.oracle_points)
