@@ -114,3 +114,19 @@ def test_product_path_never_touches_the_oracle():
         if f.endswith(".py"):
             src = open(os.path.join(ROOT, "tools", f), encoding="utf-8").read()
             assert "import oracle" not in src and "from oracle" not in src and "_util" not in src, f
+
+
+def test_binding_enums_match_header():
+    # the binding's string -> enum maps use the header's values (NEXT-4 preconditioner: G12, G12b)
+    import re
+    import inspect
+    from paper_2210_10210_b200 import efgp as E
+    hdr = open(HEADER).read()
+    vals = {k: int(v) for k, v in re.findall(r"EFGP_PRECOND_(\w+)\s*=\s*(\d+)", hdr)}
+    assert vals == {"NONE": 0, "KRON": 1, "AUTO": 2, "JACOBI": 3}
+    src = inspect.getsource(E)
+    m = re.search(r"opt\.precond = (\{[^}]*\})", src)
+    assert m, "precond map not found in the binding"
+    mp = eval(m.group(1))
+    for name, v in (("none", "NONE"), ("kron", "KRON"), ("auto", "AUTO"), ("jacobi", "JACOBI")):
+        assert mp[name] == vals[v]
