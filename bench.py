@@ -8,8 +8,9 @@ efgp_predict (type-2) over the whole data set, inputs resident in HBM (24 GB, la
 explicit flush is needed).  value = N_total / (device time per step), max over ranks.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--N 1e9] [--no-e2e]
-Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N (strong scaling: the 1e9 points are sharded
-by index, partial modes are summed with one NCCL allreduce, CG replicated, targets sharded).
+Multi-GPU: `bench.py --gpus N` re-launches itself under torch.distributed.run with N ranks (or run it
+under torchrun directly); strong scaling: the 1e9 points are sharded by index, the partial modes are
+summed with one NCCL allreduce inside the library, the CG runs replicated, targets are sharded.
 """
 from __future__ import annotations
 
@@ -55,7 +56,53 @@ def parse():
     ap.add_argument("--spread", default="auto")
     ap.add_argument("--weights", default="fp64", choices=["fp64", "fp32", "mixed"],
                     help="SORTED spreading arithmetic (include/efgp.h efgp_weights); fp64 is the strict default")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check without a GPU: every rank reports its shard over gloo, rank 0 prints them")
     return ap.parse_args()
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` started as ONE process (no WORLD_SIZE in the environment): re-launch this
+    script under torch.distributed.run with N ranks on 127.0.0.1 (the driver's own form) and return
+    its exit code.  Returns None when this process already is a rank (or N = 1)."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None:
+        if int(world_env) != args.gpus and args.gpus != 1:
+            raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world_env}")
+        return None
+    if args.gpus <= 1:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def dry_run(args, cfg):
+    """Launcher check (CPU, gloo): each rank derives its point and target shards exactly as the GPU
+    arm does; rank 0 prints them all."""
+    import torch.distributed as dist
+    from efgp_data.configs import shard_range
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    N = int(args.N or cfg.N)
+    q = int(args.q or cfg.q)
+    mine = [rank, *shard_range(N, rank, world), *shard_range(q, rank, world)]
+    allv = [None] * world
+    if world > 1:
+        dist.all_gather_object(allv, mine)
+        dist.destroy_process_group()
+    else:
+        allv = [mine]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "N": N, "q": q,
+                          "shards": [{"rank": r, "points": [a, b], "targets": [c, d]} for r, a, b, c, d in allv]}),
+              flush=True)
 
 
 def peaks():
@@ -209,6 +256,11 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    rc = spawn_ranks(args)  # --gpus N from a single process: N ranks, one per GPU
+    if rc is not None:
+        sys.exit(rc)
+    if args.dry_run:
+        return dry_run(args, cfg)
 
     import torch
     import torch.distributed as dist
@@ -219,6 +271,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench: {world} ranks but only {torch.cuda.device_count()} visible GPUs")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -276,6 +330,12 @@ def main():
         e1.record(stream)
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
+    inf0 = model.info()
+    # no silent fallback on the headline: the planned spreader must be the one that ran
+    if inf0["spread_fallback"] != "none" or (args.spread == "auto" and cfg.name in ("c2", "c5")
+                                              and inf0["spread_method"] != "sorted"):
+        raise SystemExit(f"bench: the headline spreading ran {inf0['spread_method']} "
+                         f"(fallback: {inf0['spread_fallback']}), not the planned SORTED kernel")
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

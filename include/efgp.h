@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define EFGP_ABI_VERSION 4
+#define EFGP_ABI_VERSION 5
 
 typedef struct efgp_plan *efgp_handle;
 
@@ -46,7 +46,7 @@ typedef enum {
   EFGP_ERR_INVALID = 2,    /* bad argument or input data                                 */
   EFGP_ERR_RESOURCE = 3,   /* a grid or buffer does not fit in device memory                       */
   EFGP_ERR_CUDA = 4,       /* CUDA runtime / cuFFT failure                                          */
-  EFGP_ERR_NCCL = 5        /* reserved for the collective path                                      */
+  EFGP_ERR_NCCL = 5        /* NCCL missing or a collective failed (multi-GPU path)                  */
 } efgp_status;
 
 /* Matérn eps rescaling (§7.1; reading G3). */
@@ -57,6 +57,15 @@ typedef enum {
   EFGP_SPREAD_AUTO = 0, EFGP_SPREAD_GLOBAL = 1, EFGP_SPREAD_SMEM = 2, EFGP_SPREAD_SORTED = 3,
   EFGP_SPREAD_CELLSORT = 4 /* counting sort by (super-)cell + warp-per-run accumulation (2D W >= 7, 3D) */
 } efgp_spread_method;
+
+/* Why the last fit's spreading did not run the planned method (efgp_info.spread_fallback).  The
+ * fallback (GLOBAL: one fp64 RED per touch) gives the same grids to roundoff, ~10x slower.
+ *   UNALIGNED       : SORTED bulk-copies x and y, which needs 16-byte aligned pointers.
+ *   CORESIDENCY     : SORTED's cooperative launch could not place one CTA on every SM right now.
+ *   TOO_MANY_POINTS : CELLSORT's 32-bit per-call point indices (N >= 2^32 in one call). */
+typedef enum {
+  EFGP_FALLBACK_NONE = 0, EFGP_FALLBACK_UNALIGNED = 1, EFGP_FALLBACK_CORESIDENCY = 2, EFGP_FALLBACK_TOO_MANY_POINTS = 3
+} efgp_spread_fallback;
 
 /* Arithmetic of the SORTED spreader (DESIGN.md §7 "K1 precision").  FFTs, CG, deconvolution, the
  * fine grids and all outputs are fp64 in every mode.
@@ -76,7 +85,8 @@ typedef enum { EFGP_WEIGHTS_FP64 = 0, EFGP_WEIGHTS_FP32 = 1, EFGP_WEIGHTS_MIXED 
  *         axis (cuSOLVER) and applied by 2d small dense axis contractions per iteration.  Same answer
  *         and stopping rule.  Measured (profiles/r01_configs_v2.jsonl): SE (separable density) c3
  *         N = 1e7 2831 -> 152 iterations; Matérn (non-separable D, the product approximation of D
- *         is poor off the axes) needs MORE iterations (c5 52 -> 2542).  efgp_predict_var uses plain CG.
+ *         is poor off the axes) needs MORE iterations (c5 52 -> 2542).  efgp_predict_var uses the same
+ *         preconditioner (per target).
  *   JACOBI: PCG with M = diag(D_j^2 v_0 + sigma^2) (reading G12b), the diagonal of the system; for the
  *         Matérn configs 3-8x fewer iterations at the production tolerance (oracle: c5 22 -> 7,
  *         c2 199 -> 36), variance systems more (c5 718 -> 29).
@@ -119,9 +129,9 @@ typedef struct {
   int64_t w;            /* ES kernel width (cells per dimension)                   */
   double beta_es;       /* ES kernel shape parameter                               */
   double nufft_tol;
-  int spread_method;    /* method actually used by the last fit                   */
+  int spread_method;    /* method that actually spread the last fit's points      */
   double t_spread_ms, t_modes_ms, t_solve_ms, t_predict_ms; /* device time of the last calls */
-  int64_t sorted_t1, sorted_t2, sorted_chunk, sorted_round;   /* SORTED geometry (0 otherwise)  */
+  int64_t sorted_t1, sorted_t2, sorted_chunk, sorted_round;   /* SORTED geometry (0 unless SORTED ran) */
   int64_t spread_precision;                                   /* efgp_weights of the SORTED path */
   double t_var_ms;                                            /* device time of the last predict_var */
   int64_t var_iters_max, var_batch;                           /* its largest CG count, targets/batch */
@@ -129,6 +139,7 @@ typedef struct {
                             2 weighted Toeplitz (G11b) */
   int64_t precond;       /* preconditioner the last fit used (NONE, KRON or JACOBI; AUTO resolved; NONE after a NUFFT-pair hetero fit) */
   int64_t comm_size;     /* ranks of the handle's NCCL communicator (0: none) */
+  int64_t spread_fallback; /* efgp_spread_fallback of the last fit (NONE: the planned method ran) */
 } efgp_info;
 
 /* Fill *opt with defaults (all zero / automatic). */
@@ -166,8 +177,12 @@ efgp_status efgp_fit_hetero(efgp_handle, const double *x, const double *y, const
  * them; every rank then calls efgp_comm_init(handle, id, nranks, rank) on its own device.  From then
  * on efgp_fit(x, y, N) takes THIS rank's shard: it spreads it, sums the partial modes (and N) over
  * ranks with one ncclAllReduce on the library stream, and runs the CG replicated; efgp_fit_hetero
- * (TOEPLITZ solver) does the same with its weighted modes (and min sigma_n).  NCCL is loaded at run
- * time (libnccl.so.2); EFGP_ERR_NCCL if it is missing or a call fails.  nranks = 1 is allowed. */
+ * (TOEPLITZ solver) does the same with its weighted modes (and min sigma_n).  Every rank takes part
+ * in the collectives even when its own spreading failed (e.g. an invalid coordinate): a failure
+ * flag is reduced with the point counts, and then EVERY rank returns an error (the failing rank its
+ * own status, the others EFGP_ERR_INVALID "failed on another rank"), so no rank waits forever.  NCCL
+ * is loaded at run time (libnccl.so.2); EFGP_ERR_NCCL if it is missing or a call fails.  nranks = 1
+ * is allowed. */
 efgp_status efgp_comm_unique_id(void *id_out);
 efgp_status efgp_comm_init(efgp_handle, const void *id, int nranks, int rank);
 
@@ -189,12 +204,16 @@ efgp_status efgp_predict(efgp_handle, const double *xt, int64_t q, double *mu_ou
  * over targets with the Toeplitz operator of the last fit, each CG stopped at cg_tol (reading G6).
  * xt: (q, d) row-major; var_out: q doubles (host or device).  Needs a previous successful efgp_fit
  * or efgp_fit_solve (EFGP_ERR_INVALID otherwise); targets outside [0,1]^d give NaN and
- * EFGP_ERR_INVALID.  q = 0 is a no-op. */
+ * EFGP_ERR_INVALID.  The CGs use the fit's preconditioner (efgp_info.precond: plain CG, KRON or
+ * JACOBI) and its cap max_iter; if any target's CG reaches the cap before cg_tol the variances are
+ * still written (the unconverged ones are CG iterates) and EFGP_ERR_NOCONVERGE is returned.
+ * q = 0 is a no-op. */
 efgp_status efgp_predict_var(efgp_handle, const double *xt, int64_t q, double *var_out);
 
 /* Model state (SPEC S:369 serialisation).  beta is the Hermitian-half weight vector: for j in J_m
  * with j_d >= 0, row-major over (j_1+m, ..., j_{d-1}+m, j_d), interleaved (re, im) doubles;
- * efgp_weights_count() doubles.  Pointers may be host or device. */
+ * efgp_weights_count() doubles.  Pointers may be host or device; the copies are ordered after the
+ * work already enqueued on options.stream and complete before the call returns. */
 int64_t efgp_weights_count(efgp_handle);
 efgp_status efgp_get_weights(efgp_handle, double *beta_out);
 efgp_status efgp_load_weights(efgp_handle, const double *beta_in);

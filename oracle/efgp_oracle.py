@@ -14,7 +14,8 @@ fast transform replaced by the sum that defines it:
   step 2  v_j ................. :func:`toeplitz_vector`   direct sum, eq ``88``, sign G1
   step 3  Phi^* y ............. :func:`rhs`               direct sum, eqs ``rhs``/``97``
   step 4  CG .................. :func:`cg` on :func:`system_apply`; Toeplitz product by direct
-                                 convolution (P:796-825, P:846-848), CG as P:895-901, P:1973-1974
+                                 convolution (P:796-825, P:846-848), CG as P:895-901, P:1973-1974;
+                                 c4 only: :func:`toeplitz_apply_fft` (host pocketfft, reading G11)
   step 5/6 mu(x*) ............. :func:`posterior_mean`    direct sum, eq ``muws``
   NEXT-2  s(x*) ............... :func:`posterior_variance` one CG per target on eq ``eta``
                                  (P:571-575), then the direct sum of eq ``sws``
@@ -32,6 +33,8 @@ Readings where the paper is silent, garbled or inconsistent (DESIGN.md "Readings
   G3  Matérn eps rescaling by the true ||k||_{L2(R^d)} (reading A); alternatives B (none), P (printed).
   G4  SE (h, m): Cor c:SEparams literally; h rounded down at the 12th significant digit.
   G6  CG: x0 = 0, unpreconditioned, recursive residual, Hermitian inner products.
+  G11 (c4 Toeplitz product): the direct O(M^2) product is too slow at M = 4.2e5, so the oracle may use
+      an independent host FFT (numpy/pocketfft, never cuFFT), validated against the direct product.
   G12 NEXT-4 preconditioner (P:2741-2745 names "Kronecker-structure Toeplitz preconditioners" only):
       v^(i)_l = v_{l e_i}, T_i = T(v^(i)) ((2m+1)^2 Toeplitz), delta_i(j) = D_{j e_i} / D_0^((d-1)/d),
       A_i = diag(delta_i) T_i diag(delta_i) / N^((d-1)/d), M = A_1 (x) ... (x) A_d + sigma^2 I, applied as
@@ -62,7 +65,7 @@ __all__ = [
     "khat", "kernel_value", "kernel_l2_norm", "matern_l2_norm_printed",
     "round_down_sig", "choose_params_se", "choose_params_matern", "choose_params",
     "mode_indices", "spectral_weights", "toeplitz_vector", "toeplitz_vector_weighted", "rhs_Fy", "rhs",
-    "toeplitz_matrix", "toeplitz_apply", "system_apply", "cg", "default_max_iter",
+    "toeplitz_matrix", "toeplitz_apply", "toeplitz_apply_fft", "system_apply", "cg", "default_max_iter",
     "posterior_mean", "posterior_variance", "design_matrix", "kernel_tilde_matrix", "dense_gp_mean",
     "dense_gp_variance", "features", "hetero_system_apply", "KronPrecond", "kron_factors",
     "kron_preconditioner", "kron_apply_inverse", "pcg", "posterior_variance_hetero", "jacobi_diagonal", "efgp_fit_hetero", "dense_gp_mean_hetero",
@@ -272,9 +275,31 @@ def toeplitz_apply(v: np.ndarray, beta: np.ndarray, T: np.ndarray | None = None)
     return out
 
 
-def system_apply(v, D, sigma2, beta, T=None):
+def toeplitz_apply_fft(v: np.ndarray, beta: np.ndarray) -> np.ndarray:
+    """(T beta)_p = sum_{q in J_m} v_{p-q} beta_q by a host FFT (numpy's pocketfft), reading G11: the
+    one allowed exception to the direct product, for c4 only (M = 4.2e5 makes the direct O(M^2)
+    product ~1.8e11 MACs).  It is Alg ``a:FF`` written with complex FFTs of length
+    L = 4m+1 per axis: v_j is placed at index j mod L, beta_q at q + m (zero-padded); the circular
+    convolution at index p + m equals the linear one because |p - q| <= 2m < L (no wrap-around).
+    Pinned against :func:`toeplitz_apply` (full at small m, sampled outputs at c4's m)."""
+    d = beta.ndim
+    m = (beta.shape[0] - 1) // 2
+    L = 4 * m + 1
+    vb = np.zeros((L,) * d, dtype=np.complex128)
+    idx = np.arange(-2 * m, 2 * m + 1) % L
+    vb[np.ix_(*([idx] * d))] = v
+    bb = np.zeros((L,) * d, dtype=np.complex128)
+    bb[(slice(0, 2 * m + 1),) * d] = beta
+    c = np.fft.ifftn(np.fft.fftn(vb) * np.fft.fftn(bb))
+    return c[(slice(0, 2 * m + 1),) * d]       # index p + m, p in J_m
+
+
+def system_apply(v, D, sigma2, beta, T=None, fft=False):
     """(Phi^*Phi + sigma^2 I) beta = D (F^*F) (D beta) + sigma^2 beta   (eq ``97``, P:766-768,
-    the three steps of P:846-848)."""
+    the three steps of P:846-848).  fft=True: the Toeplitz product by :func:`toeplitz_apply_fft`
+    (reading G11, c4 only)."""
+    if fft:
+        return D * toeplitz_apply_fft(v, D * beta) + sigma2 * beta
     return D * toeplitz_apply(v, D * beta, T) + sigma2 * beta
 
 
@@ -610,10 +635,11 @@ class OracleFit:
 def efgp_fit(x, y, kernel: str, ell: float, sigma: float, eps: float, nu: float = 0.0,
              h: float | None = None, m: int | None = None, cg_tol: float | None = None,
              max_iter: int | None = None, rescale: str = "A", dense_T_max: int = 4096,
-             precond: str | None = None) -> OracleFit:
+             precond: str | None = None, toeplitz_fft: bool = False) -> OracleFit:
     """Algorithm ``a1`` steps 1-4: (h, m); v (eq 88); rhs Phi^*y (eq rhs); CG to
     relative residual cg_tol (default eps).  precond="kron": PCG with the NEXT-4
-    preconditioner of reading G12 instead of plain CG."""
+    preconditioner of reading G12 instead of plain CG.  toeplitz_fft=True: the Toeplitz product by
+    the host FFT of reading G11 (c4 only; otherwise the direct product, dense when M <= dense_T_max)."""
     x = np.asarray(x, dtype=np.float64)
     if x.ndim == 1:
         x = x[:, None]
@@ -627,8 +653,8 @@ def efgp_fit(x, y, kernel: str, ell: float, sigma: float, eps: float, nu: float 
     b = rhs(x, y, h, m, D)
     tol = eps if cg_tol is None else cg_tol
     cap = default_max_iter(N, sigma, tol) if max_iter is None else max_iter
-    T = toeplitz_matrix(v, m) if (2 * m + 1) ** d <= dense_T_max else None
-    A = lambda p: system_apply(v, D, sigma ** 2, p, T)
+    T = toeplitz_matrix(v, m) if (2 * m + 1) ** d <= dense_T_max and not toeplitz_fft else None
+    A = lambda p: system_apply(v, D, sigma ** 2, p, T, fft=toeplitz_fft)
     if precond == "kron":
         Pk = kron_preconditioner(v, D, sigma ** 2)
         beta, iters, hist = pcg(A, lambda r: kron_apply_inverse(Pk, r), b, tol, cap)

@@ -11,6 +11,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("EFGP_LIB", os.path.join(HERE, "libefgp.so"))  # override: A/B builds
 
+FALLBACK_NAMES = {0: "none", 1: "unaligned", 2: "coresidency", 3: "too_many_points"}
 EFGP_OK, EFGP_ERR_NOCONVERGE, EFGP_ERR_INVALID, EFGP_ERR_RESOURCE, EFGP_ERR_CUDA, EFGP_ERR_NCCL = range(6)
 STATUS_NAMES = {0: "EFGP_OK", 1: "EFGP_ERR_NOCONVERGE", 2: "EFGP_ERR_INVALID", 3: "EFGP_ERR_RESOURCE",
                 4: "EFGP_ERR_CUDA", 5: "EFGP_ERR_NCCL"}
@@ -33,7 +34,7 @@ class Info(C.Structure):
                 ("sorted_t2", C.c_int64), ("sorted_chunk", C.c_int64), ("sorted_round", C.c_int64),
                 ("spread_precision", C.c_int64), ("t_var_ms", C.c_double), ("var_iters_max", C.c_int64),
                 ("var_batch", C.c_int64), ("hetero_sorted", C.c_int64),
-                ("precond", C.c_int64), ("comm_size", C.c_int64)]
+                ("precond", C.c_int64), ("comm_size", C.c_int64), ("spread_fallback", C.c_int64)]
 
 
 # every symbol include/efgp.h declares, with (restype, argtypes)

@@ -305,10 +305,27 @@ efgp_status efgp_setup(efgp_handle *out, efgp_kernel kernel, double nu, double e
 
 efgp_status efgp_fit(efgp_handle pl, const double *x, const double *y, int64_t N) {
   if (!pl) return EFGP_ERR_INVALID;
-  EFGP_TRY(fit_local_impl(pl, x, y, N, pl->modes));
-  if (pl->comm) {  // the one collective of a multi-GPU fit: partial modes and counts summed over ranks
+  const efgp_status st = fit_local_impl(pl, x, y, N, pl->modes);
+  if (pl->comm) {
+    // the one collective of a multi-GPU fit: partial modes and counts summed over ranks.  Every rank
+    // takes part even when its own spreading failed (its modes are then meaningless, and so is the
+    // sum): the failure flag travels with the counts and all ranks return an error together.
+    const std::string local_err = pl->err;
+    int fail = st != EFGP_OK;
+    int64_t n = st == EFGP_OK ? N : 0;
     EFGP_TRY(comm_sum(pl, pl->modes, (size_t)2 * (pl->P.Kvh + pl->P.Mh)));
-    EFGP_TRY(comm_count_min(pl, &N, nullptr));
+    EFGP_TRY(comm_count_min(pl, &n, nullptr, &fail));
+    if (st != EFGP_OK) {
+      pl->err = local_err;
+      return st;
+    }
+    if (fail) {
+      pl->err = "fit: the spreading failed on another rank (invalid input there); no rank solved";
+      return EFGP_ERR_INVALID;
+    }
+    N = n;
+  } else if (st != EFGP_OK) {
+    return st;
   }
   return fit_solve_impl(pl, pl->modes, N);
 }
@@ -435,8 +452,17 @@ efgp_status efgp_predict_var(efgp_handle pl, const double *xt, int64_t q, double
   EFGP_CUDA(cudaEventRecord(pl->ev[5], s));
   EFGP_CUDA(cudaMemsetAsync(pl->dflags + 1, 0, sizeof(int), s));
   const bool dx = is_device_ptr(xt), dm = is_device_ptr(var_out);
+  efgp_status vst = EFGP_OK;  // NOCONVERGE (a target CG hit the cap) is reported after the outputs
+  auto var_call = [&](const double *a, int64_t n, double *o) -> efgp_status {
+    const efgp_status r = variance_targets(pl, a, n, o, s);
+    if (r == EFGP_ERR_NOCONVERGE) {
+      vst = r;
+      return EFGP_OK;
+    }
+    return r;
+  };
   if (dx && dm) {
-    EFGP_TRY(variance_targets(pl, xt, q, var_out, s));
+    EFGP_TRY(var_call(xt, q, var_out));
   } else {
     const int64_t chunk = std::min<int64_t>(q, 1ll << 20);
     double *dxt = nullptr, *dv = nullptr;
@@ -445,7 +471,7 @@ efgp_status efgp_predict_var(efgp_handle pl, const double *xt, int64_t q, double
     for (int64_t s0 = 0; s0 < q; s0 += chunk) {
       const int64_t n = std::min(chunk, q - s0);
       EFGP_CUDA(cudaMemcpyAsync(dxt, xt + s0 * d, sizeof(double) * n * d, cudaMemcpyDefault, s));
-      EFGP_TRY(variance_targets(pl, dxt, n, dv, s));
+      EFGP_TRY(var_call(dxt, n, dv));
       EFGP_CUDA(cudaMemcpyAsync(var_out + s0, dv, sizeof(double) * n, cudaMemcpyDefault, s));
     }
     EFGP_CUDA(cudaFreeAsync(dxt, s));
@@ -462,25 +488,27 @@ efgp_status efgp_predict_var(efgp_handle pl, const double *xt, int64_t q, double
     pl->err = "predict_var: a target is outside [0,1]^d or non-finite (its variance is NaN)";
     return EFGP_ERR_INVALID;
   }
-  return EFGP_OK;
+  return vst;
 }
 
 int64_t efgp_weights_count(efgp_handle pl) { return pl ? 2 * pl->P.Mh : -1; }
 
 efgp_status efgp_get_weights(efgp_handle pl, double *beta_out) {
   if (!pl || !beta_out) return EFGP_ERR_INVALID;
+  EFGP_TRY(enter(pl));  // after the caller's pending work (a device beta_out may still be in use)
   EFGP_CUDA(cudaMemcpyAsync(beta_out, pl->x, sizeof(double2) * pl->P.Mh, cudaMemcpyDefault, pl->stream));
   EFGP_CUDA(cudaStreamSynchronize(pl->stream));
-  return EFGP_OK;
+  return leave(pl);
 }
 
 efgp_status efgp_load_weights(efgp_handle pl, const double *beta_in) {
   if (!pl || !beta_in) return EFGP_ERR_INVALID;
+  EFGP_TRY(enter(pl));  // a device beta_in just written on the caller's stream is complete first
   EFGP_CUDA(cudaMemcpyAsync(pl->x, beta_in, sizeof(double2) * pl->P.Mh, cudaMemcpyDefault, pl->stream));
   EFGP_CUDA(cudaStreamSynchronize(pl->stream));
   pl->fitted = true;
   pl->t2_valid = false;
-  return EFGP_OK;
+  return leave(pl);
 }
 
 int64_t efgp_copy_vector(efgp_handle pl, int which, double *out, int64_t cap) {
@@ -501,8 +529,8 @@ int64_t efgp_copy_vector(efgp_handle pl, int which, double *out, int64_t cap) {
     return -1;
   }
   if (cap < n) return -1;
-  if (cudaMemcpyAsync(out, src, sizeof(double) * n, cudaMemcpyDefault, pl->stream) != cudaSuccess ||
-      cudaStreamSynchronize(pl->stream) != cudaSuccess) {
+  if (enter(pl) != EFGP_OK || cudaMemcpyAsync(out, src, sizeof(double) * n, cudaMemcpyDefault, pl->stream) != cudaSuccess ||
+      cudaStreamSynchronize(pl->stream) != cudaSuccess || leave(pl) != EFGP_OK) {
     cudaGetLastError();
     return -1;
   }
@@ -533,7 +561,8 @@ efgp_status efgp_get_info(efgp_handle pl, efgp_info *o) {
   o->t_modes_ms = pl->t_modes;
   o->t_solve_ms = pl->t_solve;
   o->t_predict_ms = pl->t_predict;
-  if (P.spread_method == EFGP_SPREAD_SORTED) {
+  o->spread_fallback = pl->spread_fallback;
+  if (pl->spread_used == EFGP_SPREAD_SORTED) {
     o->sorted_t1 = P.T1;  // (the SORTED kernel is one cooperative launch per fit)
     o->sorted_t2 = P.T2;
     o->sorted_chunk = P.chunk;

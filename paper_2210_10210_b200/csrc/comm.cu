@@ -82,7 +82,7 @@ efgp_status comm_init(efgp_plan *pl, const void *id, int nranks, int rank) {
   pl->comm = c;
   pl->comm_size = nranks;
   pl->comm_rank = rank;
-  if (!pl->comm_buf) EFGP_CUDA(cudaMalloc((void **)&pl->comm_buf, 4 * sizeof(double)));
+  if (!pl->comm_buf) EFGP_CUDA(cudaMalloc((void **)&pl->comm_buf, 4 * sizeof(double)));  // count | min | fail
   return EFGP_OK;
 }
 
@@ -99,19 +99,24 @@ efgp_status comm_sum(efgp_plan *pl, double *buf, size_t n) {
                     "allReduce");
 }
 
-// sum of an int64 count and min of a double over ranks (host values in, host values out)
-efgp_status comm_count_min(efgp_plan *pl, int64_t *count, double *minval) {
-  double h[2] = {(double)*count, minval ? *minval : 0.0};
+// sum of an int64 count, min of a double and max of a failure flag over ranks (host values in,
+// host values out).  Every rank calls it after its local step, whether that step failed or not, so
+// the collectives always match up; *fail then says whether ANY rank failed.
+efgp_status comm_count_min(efgp_plan *pl, int64_t *count, double *minval, int *fail) {
+  double h[3] = {(double)*count, minval ? *minval : 0.0, fail ? (double)*fail : 0.0};
   EFGP_CUDA(cudaMemcpyAsync(pl->comm_buf, h, sizeof(h), cudaMemcpyHostToDevice, pl->stream));
   const NcclApi &a = nccl();
   ncclComm_t c = static_cast<ncclComm_t>(pl->comm);
   EFGP_TRY(nccl_check(pl, a.allReduce(pl->comm_buf, pl->comm_buf, 1, ncclFloat64, ncclSum, c, pl->stream), "allReduce"));
   EFGP_TRY(nccl_check(pl, a.allReduce(pl->comm_buf + 1, pl->comm_buf + 1, 1, ncclFloat64, ncclMin, c, pl->stream),
                       "allReduce"));
+  EFGP_TRY(nccl_check(pl, a.allReduce(pl->comm_buf + 2, pl->comm_buf + 2, 1, ncclFloat64, ncclMax, c, pl->stream),
+                      "allReduce"));
   EFGP_CUDA(cudaMemcpyAsync(h, pl->comm_buf, sizeof(h), cudaMemcpyDeviceToHost, pl->stream));
   EFGP_CUDA(cudaStreamSynchronize(pl->stream));
   *count = (int64_t)(h[0] + 0.5);  // exact below 2^53 points
   if (minval) *minval = h[1];
+  if (fail) *fail = h[2] > 0.0;
   return EFGP_OK;
 }
 

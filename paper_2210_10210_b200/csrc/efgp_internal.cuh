@@ -182,8 +182,8 @@ struct efgp_plan {
   // NEXT-4 Kronecker preconditioner (precond.cu): eigenvectors/values of the d factors, work grids
   double2 *pc_Q = nullptr, *pc_F0 = nullptr, *pc_F1 = nullptr, *pc_work = nullptr, *z = nullptr;
   double *pc_lam = nullptr;
-  double *pc_diag = nullptr;
-  int pc_used = 0;  // preconditioner of the last fit's solve (0 after a NUFFT-pair hetero fit)  // Jacobi: D_q^2 v_0 + sigma^2 on the half (reading G12b)
+  double *pc_diag = nullptr;  // Jacobi: D_q^2 v_0 + sigma^2 on the half (reading G12b)
+  int pc_used = 0;  // preconditioner of the last fit's solve (0 after a NUFFT-pair hetero fit)
   int *pc_info = nullptr;
   void *pc_solver = nullptr;  // cusolverDnHandle_t
   cudaGraphExec_t pcg_exec = nullptr;
@@ -205,7 +205,8 @@ struct efgp_plan {
   int64_t iters = 0;
   double rel_resid = 0;
   int64_t max_iter_used = 0;
-  int spread_used = 0;
+  int spread_used = 0;      // method that actually spread the last fit's points
+  int spread_fallback = 0;  // efgp_spread_fallback: why it is not the planned method
   double t_spread = 0, t_modes = 0, t_solve = 0, t_predict = 0;
   cudaEvent_t ev[8] = {};
 };
@@ -214,7 +215,6 @@ namespace efgp {
 // spread.cu
 efgp_status spread_points(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s);
 efgp_status spread_begin(efgp_plan *pl, cudaStream_t s);
-efgp_status spread_end(efgp_plan *pl, cudaStream_t s);
 efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s);
 // spread_cellsort.cu: K1 CELLSORT (2D any W, 3D W <= 6); EFGP_ERR_RESOURCE if not applicable
 // w1 (optional): per-point weight of the strength-1 grid (default 1): the heteroskedastic TOEPLITZ
@@ -274,7 +274,7 @@ efgp_status comm_unique_id(void *id_out);
 efgp_status comm_init(efgp_plan *pl, const void *id, int nranks, int rank);
 void comm_destroy(efgp_plan *pl);
 efgp_status comm_sum(efgp_plan *pl, double *buf, size_t n);
-efgp_status comm_count_min(efgp_plan *pl, int64_t *count, double *minval);
+efgp_status comm_count_min(efgp_plan *pl, int64_t *count, double *minval, int *fail);
 // variance.cu
 efgp_status variance_targets(efgp_plan *pl, const double *xt, int64_t q, double *out, cudaStream_t s);
 }  // namespace efgp

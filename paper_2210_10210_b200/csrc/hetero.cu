@@ -351,7 +351,6 @@ efgp_status spread_to_modes(efgp_plan *pl, const double *x, const double *w, int
   const Params &P = pl->P;
   EFGP_TRY(spread_begin(pl, s));
   EFGP_TRY(spread_points(pl, x, w, N, s));
-  EFGP_TRY(spread_end(pl, s));
   EFGP_CUFFT(cufftSetStream(pl->plan_g2, s));
   EFGP_CUFFT(cufftExecD2Z(pl->plan_g2, pl->g2, pl->G2h));
   const int64_t nr = P.n_rhs;
@@ -593,7 +592,6 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
     for (int pass = 0; pass < 2 && st == EFGP_OK && !one_pass; ++pass) {
       st = spread_begin(pl, s);
       if (st == EFGP_OK) st = spread_points(pl, x, pass == 0 ? iv : w, N, s);
-      if (st == EFGP_OK) st = spread_end(pl, s);
       if (st != EFGP_OK) break;
       EFGP_CUFFT(cufftSetStream(pl->plan_g2, s));
       EFGP_CUFFT(cufftExecD2Z(pl->plan_g2, pl->g2, pl->G2h));
@@ -611,9 +609,21 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
     double smin = 0;
     std::memcpy(&smin, &mb, sizeof(smin));
     int64_t Ntot = N;
-    if (st == EFGP_OK && pl->comm) {  // multi-GPU: v^w and F^*(y/sigma^2) are sums over the points
-      st = comm_sum(pl, pl->modes_sum, (size_t)2 * (P.Kvh + P.Mh));
-      if (st == EFGP_OK) st = comm_count_min(pl, &Ntot, &smin);
+    if (pl->comm) {  // multi-GPU: v^w and F^*(y/sigma^2) are sums over the points
+      // every rank takes part even after a local failure (failure flag reduced with the counts), so
+      // no rank is left waiting in the collective; all ranks then return an error together
+      const std::string local_err = pl->err;
+      int fail = st != EFGP_OK;
+      efgp_status cs = comm_sum(pl, pl->modes_sum, (size_t)2 * (P.Kvh + P.Mh));
+      if (cs == EFGP_OK) cs = comm_count_min(pl, &Ntot, &smin, &fail);
+      if (st != EFGP_OK) {
+        pl->err = local_err;
+      } else if (cs != EFGP_OK) {
+        st = cs;
+      } else if (fail) {
+        pl->err = "fit_hetero: the spreading failed on another rank (invalid input there); no rank solved";
+        st = EFGP_ERR_INVALID;
+      }
     }
     if (st == EFGP_OK) {
       pl->sigma2_sys = 1.0;

@@ -268,6 +268,7 @@ efgp_status spread_begin(efgp_plan *pl, cudaStream_t s) {
   EFGP_CUDA(cudaMemsetAsync(pl->g2, 0, c2 * sizeof(double), s));
   EFGP_CUDA(cudaMemsetAsync(pl->dflags, 0, sizeof(int) * 4, s));
   pl->spread_used = P.spread_method;
+  pl->spread_fallback = EFGP_FALLBACK_NONE;
   return EFGP_OK;
 }
 
@@ -277,17 +278,24 @@ efgp_status spread_points(efgp_plan *pl, const double *x, const double *y, int64
   if (method == EFGP_SPREAD_SORTED) {
     // the binning bulk-copies x and y (16-byte alignment); unaligned inputs fall back to GLOBAL
     // (same grids, same kernel)
+    // (same grids, same kernel); the fallback is recorded in efgp_info.spread_fallback
     if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0) {
       const efgp_status st = spread_sorted2(pl, x, y, N, s);
       if (st != EFGP_ERR_RESOURCE) return st;
       pl->err.clear();  // co-residency not available now: same grids, direct spreading below
+      pl->spread_fallback = EFGP_FALLBACK_CORESIDENCY;
+    } else {
+      pl->spread_fallback = EFGP_FALLBACK_UNALIGNED;
     }
     method = EFGP_SPREAD_GLOBAL;
+    pl->spread_used = method;
   } else if (method == EFGP_SPREAD_CELLSORT) {
     const efgp_status st = spread_cellsort(pl, x, y, N, s);
     if (st != EFGP_ERR_RESOURCE) return st;
     pl->err.clear();  // (N >= 2^32 in one call): same grids, direct spreading below
+    pl->spread_fallback = EFGP_FALLBACK_TOO_MANY_POINTS;
     method = EFGP_SPREAD_GLOBAL;
+    pl->spread_used = method;
   }
   switch (pl->P.d) {
     case 1: return dispatch_w<1>(pl, x, y, N, s, method);
@@ -295,12 +303,6 @@ efgp_status spread_points(efgp_plan *pl, const double *x, const double *y, int64
     case 3: return dispatch_w<3>(pl, x, y, N, s, method);
   }
   return EFGP_ERR_INVALID;
-}
-
-efgp_status spread_end(efgp_plan *pl, cudaStream_t s) {
-  (void)pl;
-  (void)s;
-  return EFGP_OK;
 }
 
 }  // namespace efgp

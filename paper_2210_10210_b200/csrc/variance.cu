@@ -485,7 +485,8 @@ static efgp_status setup_var(efgp_plan *pl, int64_t Bwant) {
 }
 
 template <int D>
-static efgp_status var_batch(efgp_plan *pl, const double *xt, int nt, double *out, cudaStream_t s, int *iters_max) {
+static efgp_status var_batch(efgp_plan *pl, const double *xt, int nt, double *out, cudaStream_t s, int *iters_max,
+                             int64_t *noconv) {
   const Params &P = pl->P;
   int64_t box = P.L / 2 + 1, Ld = P.L;
   for (int k = 0; k < D - 1; ++k) {
@@ -572,7 +573,10 @@ static efgp_status var_batch(efgp_plan *pl, const double *xt, int nt, double *ou
   std::vector<VarTarget> host(nt);
   EFGP_CUDA(cudaMemcpyAsync(host.data(), st, sizeof(VarTarget) * nt, cudaMemcpyDeviceToHost, s));
   EFGP_CUDA(cudaStreamSynchronize(s));
-  for (const auto &h : host) *iters_max = std::max(*iters_max, h.iters);
+  for (const auto &h : host) {
+    *iters_max = std::max(*iters_max, h.iters);
+    if (h.iters >= max_iter) ++*noconv;  // stopped by the cap, not by cg_tol
+  }
   return EFGP_OK;
 }
 
@@ -590,11 +594,17 @@ static efgp_status var_targets_d(efgp_plan *pl, const double *xt, int64_t q, dou
     pl->var_exec = nullptr;
   }
   int iters_max = 0;
+  int64_t noconv = 0;
   for (int64_t t0 = 0; t0 < q; t0 += pl->var_B) {
     const int nt = (int)std::min<int64_t>(pl->var_B, q - t0);
-    EFGP_TRY(var_batch<D>(pl, xt + t0 * D, nt, out + t0, s, &iters_max));
+    EFGP_TRY(var_batch<D>(pl, xt + t0 * D, nt, out + t0, s, &iters_max, &noconv));
   }
   pl->var_iters_max = iters_max;
+  if (noconv) {
+    pl->err = "predict_var: " + std::to_string(noconv) + " of " + std::to_string(q) +
+              " target CGs reached max_iter before cg_tol (their variances are CG iterates)";
+    return EFGP_ERR_NOCONVERGE;
+  }
   return EFGP_OK;
 }
 

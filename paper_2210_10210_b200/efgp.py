@@ -154,7 +154,10 @@ class EFGP:
 
     def fit_hetero(self, x, y, noise_sd):
         """NEXT-3: fit with per-point noise standard deviations noise_sd (N,) (reading G11): solves
-        (Phi^* S^-1 Phi + I) beta = Phi^* S^-1 y with one type-2 + one type-1 NUFFT per CG iteration."""
+        (Phi^* S^-1 Phi + I) beta = Phi^* S^-1 y.  Default solver (hetero="auto"/"toeplitz", reading
+        G11b): the weighted Toeplitz system D T(v^w) D + I (v^w from strengths 1/sigma_n^2, one extra
+        type-1 pass) with the FFT Toeplitz CG; hetero="nufft": one type-2 + one type-1 NUFFT per CG
+        iteration (the BBMM-style product of P:2762-2763)."""
         N = int(x.shape[0])
         px, kx = _ptr_and_keep(x)
         py, ky = _ptr_and_keep(y)
@@ -236,8 +239,8 @@ class EFGP:
             out = torch.empty(q, dtype=torch.float64, device=dev)
         px, kx = _ptr_and_keep(xt)
         with torch.cuda.device(self.device):
-            self._check(self._lib.efgp_predict_var(self._h, C.c_void_p(px), q, C.c_void_p(out.data_ptr())),
-                        allow_noconverge=False)
+            # EFGP_ERR_NOCONVERGE (a target's CG hit max_iter) warns, as fit does
+            self._check(self._lib.efgp_predict_var(self._h, C.c_void_p(px), q, C.c_void_p(out.data_ptr())))
         return out
 
     # ------------------------------------------------------------------ state
@@ -246,6 +249,7 @@ class EFGP:
         self._check(self._lib.efgp_get_info(self._h, C.byref(inf)), allow_noconverge=False)
         d = {k: getattr(inf, k) for k, _ in L.Info._fields_}
         d["spread_method"] = SPREAD_NAMES.get(d["spread_method"], d["spread_method"])
+        d["spread_fallback"] = L.FALLBACK_NAMES.get(d["spread_fallback"], d["spread_fallback"])
         return d
 
     def residual_history(self) -> np.ndarray:
@@ -272,8 +276,11 @@ class EFGP:
         return out
 
     def load_weights(self, beta_half) -> "EFGP":
-        arr = np.ascontiguousarray(beta_half, dtype=np.float64)
-        if arr.size != int(self._lib.efgp_weights_count(self._h)):
+        """Load a Hermitian-half weight vector (numpy array or torch tensor, host or device)."""
+        ptr, keep = _ptr_and_keep(beta_half)
+        n = keep.numel() if hasattr(keep, "numel") else keep.size
+        if n != int(self._lib.efgp_weights_count(self._h)):
             raise ValueError("weights length mismatch")
-        self._check(self._lib.efgp_load_weights(self._h, arr.ctypes.data_as(C.c_void_p)), allow_noconverge=False)
+        with self._torch.cuda.device(self.device):
+            self._check(self._lib.efgp_load_weights(self._h, C.c_void_p(ptr)), allow_noconverge=False)
         return self

@@ -1,0 +1,175 @@
+#!/usr/bin/env python
+"""Golden dumps of the oracle at the BASELINE configs' own sizes.
+
+Test infrastructure (lives in tests/, the only place besides smoke() and bench.py's cpu_baseline that
+may run the oracle): imports only ``oracle`` and ``efgp_data`` (never the product package).  For one
+config it runs Algorithm a1 exactly as the oracle states it:
+
+  * the type-1 sums v (eq 88) and F^*y (eq rhs) over ALL N points, split into index shards that
+    worker processes sum independently (the sum over n is linear; only the order of additions
+    changes), each shard regenerated from the seeded Philox recipe (efgp_data);
+  * CG twice: parity mode (cg_tol = eps/1000, reading G9) and production mode
+    (cg_tol = eps), both with the default cap, recording ||r_k||/||b||;
+    the Toeplitz product is the direct one (dense T when M <= 10^4) or, for c4 only, the host FFT
+    of reading G11;
+  * mu at the config's targets (eq muws) for both solutions.
+
+Output: tests/golden/full_<cfg>.npz (arrays) + full_<cfg>.json (metadata: sizes, (h, m), reading,
+iteration counts, per-stage oracle seconds, host cores/model, sha256 of oracle/efgp_oracle.py and of
+the data recipe).  The GPU test tests/test_gpu_golden.py regenerates the same inputs on the device
+and gates on these.
+
+  python tests/make_golden.py c2 [--N 1e6] [--workers 8]
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import math
+import multiprocessing as mp
+import os
+import platform
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))  # tests/ -> repo root
+sys.path.insert(0, ROOT)
+
+import oracle as O  # noqa: E402
+from efgp_data import CONFIGS, observations, points, targets  # noqa: E402
+
+DEFAULT_N = {"c5": 100_000_000}  # c5's 1e9 would take ~4 h of host time; 1e8 keeps the same path
+
+
+def sha256(path):
+    with open(path, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()
+
+
+def oracle_hash():
+    return sha256(os.path.join(ROOT, "oracle", "efgp_oracle.py"))
+
+
+def data_hash():
+    return hashlib.sha256(b"".join(open(os.path.join(ROOT, "efgp_data", f), "rb").read()
+                                   for f in ("configs.py", "philox.py"))).hexdigest()
+
+
+def host_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor()
+
+
+def _shard(args):
+    """Partial sums of v and F^*y over records [a, b) (eq 88, eq rhs), single-threaded BLAS."""
+    name, a, b, h, m = args
+    from threadpoolctl import threadpool_limits
+    cfg = CONFIGS[name]
+    with threadpool_limits(1):
+        x = points(cfg, a, b)
+        y = observations(cfg, x, a)
+        v = O.toeplitz_vector(x, h, m)
+        fy = O.rhs_Fy(x, y, h, m)
+    return v, fy
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config")
+    ap.add_argument("--N", type=float, default=None)
+    ap.add_argument("--workers", type=int, default=os.cpu_count())
+    ap.add_argument("--shard", type=int, default=None)
+    ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden"))
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    N = int(args.N) if args.N else DEFAULT_N.get(cfg.name, cfg.N)
+    q = cfg.q
+    h, m = O.choose_params(cfg.kernel, cfg.ell, cfg.d, cfg.eps, cfg.nu)
+    M = (2 * m + 1) ** cfg.d
+    shard = args.shard or (50_000 if cfg.d == 3 else 500_000)
+    t = {}
+    log = lambda s: print(f"[{cfg.name} {time.strftime('%H:%M:%S')}] {s}", flush=True)
+    log(f"N={N} q={q} h={h} m={m} M={M} workers={args.workers} shard={shard}")
+
+    t0 = time.perf_counter()
+    jobs = [(cfg.name, a, min(N, a + shard), h, m) for a in range(0, N, shard)]
+    v = np.zeros((4 * m + 1,) * cfg.d, dtype=np.complex128)
+    fy = np.zeros((2 * m + 1,) * cfg.d, dtype=np.complex128)
+    with mp.get_context("fork").Pool(args.workers) as pool:
+        for k, (vp, fp) in enumerate(pool.imap_unordered(_shard, jobs)):
+            v += vp
+            fy += fp
+            if (k + 1) % max(1, len(jobs) // 20) == 0:
+                log(f"type-1 sums {k + 1}/{len(jobs)} shards")
+    t["type1_sums_s"] = time.perf_counter() - t0
+    D = O.spectral_weights(cfg.kernel, cfg.ell, cfg.d, h, m, cfg.nu)
+    b = D * fy
+    log(f"type-1 sums {t['type1_sums_s']:.1f} s, v0={v[(2 * m,) * cfg.d].real:.1f}")
+
+    use_fft = cfg.name == "c4"          # reading G11: the one exception to the direct product
+    T = None
+    if not use_fft:
+        t0 = time.perf_counter()
+        T = O.toeplitz_matrix(v, m)      # dense T_pq = v_{j_p - j_q} (eq 223), M <= 9801
+        t["dense_T_s"] = time.perf_counter() - t0
+    A = lambda p: O.system_apply(v, D, cfg.sigma ** 2, p, T, fft=use_fft)
+
+    res = {}
+    for mode, tol in (("parity", cfg.eps / 1000), ("production", cfg.eps)):
+        cap = O.default_max_iter(N, cfg.sigma, tol)
+        t0 = time.perf_counter()
+        beta, iters, hist = O.cg(A, b, tol, cap)
+        t[f"cg_{mode}_s"] = time.perf_counter() - t0
+        true_rel = float(np.linalg.norm(A(beta) - b) / np.linalg.norm(b))
+        log(f"CG {mode}: tol {tol:g} iters {iters} (cap {cap}) true rel resid {true_rel:.2e} "
+            f"{t[f'cg_{mode}_s']:.1f} s")
+        res[mode] = (beta, iters, np.asarray(hist), true_rel, cap)
+
+    xt = targets(cfg, 0, q)
+    mus = {}
+    for mode in ("parity", "production"):
+        t0 = time.perf_counter()
+        mus[mode] = O.posterior_mean(res[mode][0], D, h, xt)
+        t[f"mu_{mode}_s"] = time.perf_counter() - t0
+    log(f"mu done; parity vs production rel {np.linalg.norm(mus['parity'] - mus['production']) / np.linalg.norm(mus['parity']):.2e}")
+
+    os.makedirs(args.out, exist_ok=True)
+    arrays = {"mu_parity": mus["parity"], "mu_production": mus["production"],
+              "hist_parity": res["parity"][2], "hist_production": res["production"][2]}
+    # small mode vectors in full; c4's (149^3 / 75^3) as norms + seeded samples
+    if v.size * 16 <= 4 << 20:
+        arrays.update(v=v, b=b, beta_parity=res["parity"][0])
+    else:
+        rng = np.random.default_rng(1234)
+        iv = rng.integers(0, v.size, 4096)
+        ib = rng.integers(0, b.size, 4096)
+        arrays.update(v_idx=iv, v_sample=v.reshape(-1)[iv], b_idx=ib, b_sample=b.reshape(-1)[ib],
+                      beta_parity_sample=res["parity"][0].reshape(-1)[ib])
+    base = os.path.join(args.out, f"full_{cfg.name}")
+    np.savez_compressed(base + ".npz", **arrays)
+    meta = {"config": cfg.name, "N": N, "q": q, "seed": cfg.seed, "h": h, "m": m, "M": M,
+            "reading": "A (Matern eps rescaling by ||k||_L2), G1 signs, G9 parity mode eps/1000",
+            "toeplitz_product": "host FFT (reading G11)" if use_fft else "direct (dense T)",
+            "v_norm": float(np.linalg.norm(v)), "b_norm": float(np.linalg.norm(b)),
+            "iters_parity": int(res["parity"][1]), "iters_production": int(res["production"][1]),
+            "cap_parity": int(res["parity"][4]), "cap_production": int(res["production"][4]),
+            "true_rel_resid_parity": res["parity"][3], "true_rel_resid_production": res["production"][3],
+            "oracle_sha256": oracle_hash(), "data_sha256": data_hash(),
+            "oracle_seconds": t, "host": {"cores": args.workers, "model": host_model()},
+            "written": time.strftime("%Y-%m-%dT%H:%M:%S")}
+    with open(base + ".json", "w") as f:
+        json.dump(meta, f, indent=1)
+    log(f"wrote {base}.npz/.json: {json.dumps({k: meta[k] for k in ('iters_parity', 'iters_production')})}")
+
+
+if __name__ == "__main__":
+    main()

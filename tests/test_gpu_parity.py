@@ -643,3 +643,66 @@ def test_cellsort_supercells_for_large_grids():
     assert out["auto"][2]["m"] == 94 and out["auto"][2]["spread_method"] == "cellsort"
     assert rel(out["auto"][0], out["global"][0]) < 1e-12
     assert rel(out["auto"][1], out["global"][1]) < 2 * out["auto"][2]["nufft_tol"]
+
+
+def test_unaligned_input_fallback_is_reported():
+    # SORTED bulk-copies x and y (16-byte alignment); an 8-byte-offset view falls back to GLOBAL and
+    # efgp_info says so (spread_method = the method that ran, spread_fallback = why), with the same v
+    import torch
+    c = CONFIGS["c5"]
+    x, y, _ = generate(c, N=30_000, q=1)
+    buf = torch.empty(2 * len(x) + 1, dtype=torch.float64, device="cuda")
+    xu = buf[1:].view(len(x), 2)
+    xu.copy_(torch.from_numpy(x))
+    assert xu.data_ptr() % 16 == 8
+    g = model(c, max_iter=1, spread="sorted")
+    with pytest.warns(RuntimeWarning):
+        g.fit(xu, dev(y))
+    inf = g.info()
+    assert inf["spread_method"] == "global" and inf["spread_fallback"] == "unaligned" and inf["sorted_t1"] == 0
+    v_u = g.vector("v")
+    with pytest.warns(RuntimeWarning):
+        g.fit(dev(x), dev(y))
+    inf = g.info()
+    assert inf["spread_method"] == "sorted" and inf["spread_fallback"] == "none" and inf["sorted_t1"] > 0
+    assert rel(v_u, g.vector("v")) < 1e-12
+    g.close()
+
+
+def test_variance_cap_reports_noconverge():
+    # a variance CG stopped by max_iter is reported (EFGP_ERR_NOCONVERGE -> RuntimeWarning), not OK
+    c = CONFIGS["c5"]
+    x, y, xt = generate(c, N=20_000, q=8)
+    g = model(c, max_iter=3)
+    with pytest.warns(RuntimeWarning):
+        g.fit(dev(x), dev(y))
+    with pytest.warns(RuntimeWarning, match="max_iter"):
+        var = g.predict_var(dev(xt))
+    assert g.last_status == 1 and var.numel() == 8 and bool(torch_isfinite(var))
+    g.close()
+
+
+def torch_isfinite(t):
+    import torch
+    return torch.isfinite(t).all()
+
+
+def test_load_and_get_weights_follow_the_callers_stream():
+    # efgp_load_weights / efgp_get_weights order themselves after the caller's stream (enter/leave):
+    # a device beta written by a kernel on the caller's stream just before the call is the one loaded
+    import torch
+    from paper_2210_10210_b200 import full_to_half
+    c = CONFIGS["c5"]
+    g = model(c)
+    n = g.info()["m"] * 2 + 1
+    rng = np.random.default_rng(3)
+    full = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+    full = 0.5 * (full + np.conj(full[::-1, ::-1]))
+    half = torch.from_numpy(full_to_half(full)).cuda()
+    s = torch.cuda.current_stream()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(50_000_000)                              # keep the stream busy (~tens of ms)
+        beta = half * 2.0                                           # written after the sleep
+        g.load_weights(beta)                                        # must see the finished product
+    assert np.allclose(g.weights(), 2.0 * full_to_half(full))
+    g.close()

@@ -177,3 +177,54 @@ def test_condition_number_bound_and_fig3_point():
 def test_default_max_iter_formula():
     # k <= log(1/eps) sqrt(N) / (2 sigma)
     assert O.default_max_iter(10_000, 0.1, 1e-6) == math.ceil(math.log(1e6) * 100 / 0.2)
+
+
+@pytest.mark.parametrize("d,m", [(1, 9), (2, 4), (3, 3)])
+def test_toeplitz_apply_fft_equals_direct_product(d, m):
+    # Reading G11: the host-FFT Toeplitz product (c4 only) against the direct convolution and the
+    # dense F^*F on 3 random vectors each (a wrong placement of v, a sign or an off-by-one in the
+    # extraction window fails these)
+    rng, x, _ = _small_problem(d=d, N=250, m=m, seed=11 + d)
+    h = 0.6
+    v = O.toeplitz_vector(x, h, m)
+    F = O.design_matrix(x, h, m, np.ones((2 * m + 1,) * d))
+    for _ in range(3):
+        beta = rng.normal(size=(2 * m + 1,) * d) + 1j * rng.normal(size=(2 * m + 1,) * d)
+        ref = (F.conj().T @ (F @ beta.reshape(-1))).reshape(beta.shape)
+        got = O.toeplitz_apply_fft(v, beta)
+        np.testing.assert_allclose(got, O.toeplitz_apply(v, beta), rtol=1e-12, atol=1e-10)
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-10)
+    # a non-Hermitian generating vector too (the placement must not rely on symmetry)
+    w = rng.normal(size=v.shape) + 1j * rng.normal(size=v.shape)
+    beta = rng.normal(size=(2 * m + 1,) * d) + 1j * rng.normal(size=(2 * m + 1,) * d)
+    np.testing.assert_allclose(O.toeplitz_apply_fft(w, beta), O.toeplitz_apply(w, beta), rtol=1e-12, atol=1e-10)
+
+
+def test_toeplitz_apply_fft_at_c4_size_sampled():
+    # c4's own m = 37 (M = 421875): the FFT product at 40 sampled outputs p against the direct sum
+    # sum_q v_{p-q} beta_q written out over all M q's, for 3 random vectors (reading G11's validation)
+    c = CONFIGS["c4"]
+    h, m = O.choose_params(c.kernel, c.ell, c.d, c.eps, c.nu)
+    assert m == 37
+    rng = np.random.default_rng(4)
+    v = rng.normal(size=(4 * m + 1,) * 3) + 1j * rng.normal(size=(4 * m + 1,) * 3)
+    J = O.mode_indices(m, 3)
+    for _ in range(3):
+        beta = rng.normal(size=(2 * m + 1,) * 3) + 1j * rng.normal(size=(2 * m + 1,) * 3)
+        got = O.toeplitz_apply_fft(v, beta)
+        bflat = beta.reshape(-1)
+        for _ in range(40):
+            p = rng.integers(-m, m + 1, 3)
+            dif = p[None, :] - J + 2 * m
+            direct = np.sum(v[dif[:, 0], dif[:, 1], dif[:, 2]] * bflat)
+            assert abs(got[tuple(p + m)] - direct) <= 1e-9 * np.sqrt(np.sum(np.abs(bflat) ** 2) * v.size)
+
+
+def test_fit_with_fft_toeplitz_equals_direct():
+    # efgp_fit(toeplitz_fft=True) runs the same CG as the direct product (same iterates up to roundoff)
+    rng, x, _ = _small_problem(d=3, N=600, m=3, seed=5)
+    y = np.sin(4 * x[:, 0]) + 0.1 * rng.normal(size=600)
+    a = O.efgp_fit(x, y, "matern", 0.2, 0.1, 1e-3, nu=0.5, h=0.4, m=3, cg_tol=1e-9)
+    b = O.efgp_fit(x, y, "matern", 0.2, 0.1, 1e-3, nu=0.5, h=0.4, m=3, cg_tol=1e-9, toeplitz_fft=True)
+    assert abs(a.iters - b.iters) <= 2
+    np.testing.assert_allclose(b.beta, a.beta, rtol=0, atol=1e-8 * np.max(np.abs(a.beta)))
