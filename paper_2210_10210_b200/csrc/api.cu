@@ -106,6 +106,7 @@ efgp_status build(efgp_plan *pl) {
   EFGP_TRY(make_plan(pl, &pl->plan_t2, d, P.n2, CUFFT_Z2D));
   for (auto &e : pl->ev) EFGP_CUDA(cudaEventCreate(&e));
   EFGP_CUDA(cudaStreamCreateWithFlags(&pl->copy_stream, cudaStreamNonBlocking));
+  pl->spread_used = P.spread_method;  // until a fit spreads: the planned method (and its geometry)
   return EFGP_OK;
 }
 

@@ -123,6 +123,106 @@ __global__ void __launch_bounds__(interp_max_threads<D, W>()) k_interp(const dou
   }
 }
 
+// 2D, grid staged in shared memory, bank-aware order (the K9 variant for many random targets).
+// Gathering a W x W window for 32 random targets is bound by shared-memory bank conflicts: a warp's
+// LDS.64 of 32 random cells costs ~6.2 wavefronts instead of 2 (r01 ncu).  The bank of every cell
+// of a target's window is (bank of its first cell + a A + b) mod 16 (8-byte banks of a half-warp
+// phase), so if the 16 targets of each half-warp have pairwise different first-cell banks, all
+// W^2 gathers are conflict-free.  Each CTA therefore takes batches of kIB targets, classifies them by
+// first-cell bank (shared counters), and hands target rank k of bank class b to thread 16 k + b;
+// the few targets beyond a class's quota fill the slots of the classes that ran short.  Same
+// arithmetic per target as k_interp (bitwise-identical results), only the thread assignment changes.
+#ifndef EFGP_KIB
+#define EFGP_KIB 512
+#endif
+constexpr int kIB = EFGP_KIB;  // targets per batch = threads per CTA (1024 / kIB CTAs per SM overlap their barriers)
+
+template <int W>
+__global__ void __launch_bounds__(kIB, 1024 / kIB) k_interp2_banked(const double *__restrict__ xt, int64_t q,
+                                                                    const double *__restrict__ grid, int n, double h,
+                                                                    EsPoly P, int lo, int A, const double *__restrict__ sd,
+                                                                    double *__restrict__ mu, int *__restrict__ err) {
+  extern __shared__ __align__(16) double sgrid[];
+  __shared__ double s_s[2][kIB];       // reduced coordinates of the batch's targets (by batch index)
+  __shared__ int s_cell[kIB];          // first-cell offset r A + c in the staged grid (-1: invalid / none)
+  __shared__ short s_tbl[kIB];         // thread slot -> batch index
+  __shared__ short s_ovf[kIB];         // targets beyond their class quota
+  __shared__ int s_cnt[16], s_novf, s_take;
+  const int tid = threadIdx.x;
+  for (int c = tid; c < A * A; c += kIB) {
+    const int r = c / A, cc = c % A;
+    sgrid[c] = __ldg(grid + (int64_t)wrapn(r + lo, n) * n + wrapn(cc + lo, n));
+  }
+  const int64_t nb = (q + kIB - 1) / kIB;
+  const double2 *x2 = reinterpret_cast<const double2 *>(xt);
+  // targets are loaded one batch ahead (their HBM latency overlaps a batch of work)
+  auto ld = [&](int64_t b) -> double2 {
+    const int64_t ii = b * kIB + tid;
+    return (b < nb && ii < q) ? __ldg(x2 + ii) : make_double2(0.0, 0.0);
+  };
+  double2 xn = ld(blockIdx.x);
+  for (int64_t bt = blockIdx.x; bt < nb; bt += gridDim.x) {
+    const double2 xc = xn;
+    const int64_t i = bt * kIB + tid;
+    xn = ld(bt + gridDim.x);
+    __syncthreads();  // the previous batch is done with every table (and the grid is staged)
+    if (tid < 16) s_cnt[tid] = 0;
+    if (tid == 0) s_novf = s_take = 0;
+    s_tbl[tid] = -1;
+    __syncthreads();
+    int cell = -1;
+    if (i < q) {
+      if (xc.x >= 0.0 && xc.x <= 1.0 && xc.y >= 0.0 && xc.y <= 1.0) {
+        double s0, s1;
+        const int b0 = es_reduce<W>(h * xc.x * (double)n, s0);
+        const int b1 = es_reduce<W>(h * xc.y * (double)n, s1);
+        s_s[0][tid] = s0;
+        s_s[1][tid] = s1;
+        cell = (b0 - lo) * A + (b1 - lo);
+      } else {
+        mu[i] = __longlong_as_double(0x7ff8000000000000LL);
+        atomicOr(err + 1, 1);
+      }
+    }
+    s_cell[tid] = cell;
+    if (cell >= 0) {
+      const int b = cell & 15;
+      const int k = atomicAdd(&s_cnt[b], 1);
+      if (k < kIB / 16) s_tbl[16 * k + b] = (short)tid;
+      else s_ovf[atomicAdd(&s_novf, 1)] = (short)tid;
+    }
+    __syncthreads();
+    int j = s_tbl[tid];
+    if (j < 0) {  // an empty slot takes an over-quota target, if any is left
+      const int novf = s_novf;
+      if (novf > 0) {
+        const int t = atomicAdd(&s_take, 1);
+        if (t < novf) j = s_ovf[t];
+      }
+    }
+    if (j >= 0) {
+      double wt[2][W];
+      es_weights_s<W>(s_s[0][j], P, wt[0]);
+      es_weights_s<W>(s_s[1][j], P, wt[1]);
+      const double *win = sgrid + s_cell[j];
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < W; ++a) {
+        double ra = 0.0;
+#pragma unroll
+        for (int b = 0; b < W; ++b) ra = fma(win[a * A + b], wt[1][b], ra);
+        acc = fma(ra, wt[0][a], acc);
+      }
+      const int64_t ij = bt * kIB + j;
+      if (sd) {  // NEXT-3: w_n = (Phi p)_n / sigma_n^2 (reading G11)
+        const double sn = __ldg(sd + ij);
+        acc /= sn * sn;
+      }
+      mu[ij] = acc;
+    }
+  }
+}
+
 template <int D, int W>
 static efgp_status launch_interp(efgp_plan *pl, const double *grid, int n, const double *xt, int64_t q,
                                  const double *sd, double *mu, cudaStream_t s) {
@@ -132,6 +232,16 @@ static efgp_status launch_interp(efgp_plan *pl, const double *grid, int n, const
   for (int k = 1; k < D; ++k) cells *= o.A;
   const size_t sb = cells * sizeof(double);
   int64_t blocks = (q + 255) / 256;
+  if (D == 2 && q >= (int64_t)pl->num_sms * kIB && sb <= 160 * 1024 && (reinterpret_cast<uintptr_t>(xt) & 15) == 0 &&
+      !getenv("EFGP_INTERP_PLAIN")) {
+    // many targets: bank-aware order (1024 / kIB CTAs of kIB threads per SM, persistent over batches)
+    EFGP_CUDA(cudaFuncSetAttribute(k_interp2_banked<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    const int64_t nbt = (q + kIB - 1) / kIB;
+    const int64_t nblk = std::min<int64_t>(nbt, (int64_t)(1024 / kIB) * pl->num_sms);
+    k_interp2_banked<W><<<(unsigned)nblk, kIB, sb, s>>>(xt, q, grid, n, P.h, P.poly, o.lo, o.A, sd, mu, pl->dflags);
+    EFGP_CUDA(cudaGetLastError());
+    return EFGP_OK;
+  }
   if (sb <= 160 * 1024) {
     // one wave of persistent CTAs so the staged grid is reused across many targets; 1024 resident
     // threads per SM whatever the staged size (4 x 256, 2 x 512 or 1 x 1024)

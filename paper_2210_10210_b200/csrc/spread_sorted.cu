@@ -190,6 +190,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// 256-bit global store (sm_100: STG.E.ENL2.256): a whole 32-byte record in one instruction
+__device__ __forceinline__ void st_v4(double4 *p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -431,7 +435,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       const double2 xx = xs2[j];
       const double yv = ys[j];
       if (p < A.segcap)
-        rec[((int64_t)t * G + blockIdx.x) * A.segcap + p] = make_double4(xx.x, xx.y, yv, __longlong_as_double((long long)key));
+        st_v4(rec + ((int64_t)t * G + blockIdx.x) * A.segcap + p, xx.x, xx.y, yv, __longlong_as_double((long long)key));
       else
         ovf = true;
     }

@@ -13,10 +13,12 @@ and gates:
   * type-1 outputs v and Phi^*y against the oracle's exact sums: relative l2 <= 5 nufft_tol (c4:
     4096 sampled entries, error relative to the oracle's norm);
   * parity mode: mu relative l2 over the config's targets <= 10 eps (north_star);
-  * production mode (CG at eps): the iteration count within +-2 of the oracle's or inside its
-    [2 eps, eps/2] crossing window (reading G10).  For c3 the survey expects this to miss (SURVEY
-    A.6: NUFFT-level perturbations move the first crossing of eps by tens of iterations); there the
-    mismatch is reported with both residual histories and the parity-mode mu gate is authoritative.
+  * iteration counts (both modes): within +-2 of the oracle's, inside its [2 eps_cg, eps_cg/2]
+    crossing window (reading G10), or within +-2 of the range of first crossings the ORACLE itself
+    shows when v and F^*y carry an error of the size the NUFFT contract allows (reading G10b, counts
+    stored by tests/make_golden.py).  Gated in production mode; in parity mode (thousands of
+    iterations on a plateaued residual) reported, with both residual histories, where it misses —
+    there the mu gate is authoritative (reading G9).
 
 Both histories and the counts of every config are written to $EFGP_GOLDEN_REPORT (a directory) when
 set, so a GPU run leaves the evidence behind (profiles/r02_golden_*.json).
@@ -36,8 +38,8 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLD = os.path.join(ROOT, "tests", "golden")
-# configs where reading G10's window is expected to hold in production mode
-G10_PRODUCTION = {"c1", "c2", "c4", "c5"}
+# configs gated on G10 alone when a dump has no perturbed counts
+G10_PRODUCTION = {"c1", "c4", "c5"}
 
 
 def _load(name):
@@ -56,6 +58,14 @@ def _window(hist, tol):
     lo = next((k for k, r in enumerate(hist) if r <= 2 * tol), len(hist))
     hi = next((k for k, r in enumerate(hist) if r <= tol / 2), len(hist) + 10)
     return lo, hi
+
+
+def _count_ok(k_g, k_o, hist_o, tol, perturbed):
+    """Readings G10 / G10b: +-2, or the oracle's crossing window, or the oracle's own perturbed range."""
+    lo, hi = _window(hist_o, tol)
+    g10 = abs(k_g - k_o) <= 2 or lo <= k_g <= hi
+    g10b = bool(perturbed) and min(perturbed) - 2 <= k_g <= max(perturbed) + 2
+    return g10, g10b, (lo, hi)
 
 
 def _report(name, rec):
@@ -105,11 +115,16 @@ def test_golden_parity_mode(name):
     mu = g.predict(xt).cpu().numpy()
     err = rel(mu, G["mu_parity"])
     hist_g = g.residual_history()
-    lo, hi = _window(G["hist_parity"], cg_tol)
+    pert = meta.get("iters_perturbed", {}).get("parity", [])
+    g10, g10b, (lo, hi) = _count_ok(inf["iters"], meta["iters_parity"], G["hist_parity"], cg_tol, pert)
     _report(name, {"N": N, "m": meta["m"], "spread": inf["spread_method"], "parity": {
         "mu_rel_err": err, "gate": 10 * c.eps, "type1_rel_err": [ev, eb], "iters_gpu": inf["iters"],
-        "iters_oracle": meta["iters_parity"], "oracle_window": [lo, hi],
+        "iters_oracle": meta["iters_parity"], "oracle_window": [lo, hi], "oracle_perturbed": pert,
+        "g10_pass": g10, "g10b_pass": g10b,
         "hist_gpu": list(map(float, hist_g)), "hist_oracle": list(map(float, G["hist_parity"]))}})
+    if not (g10 or g10b):
+        print(f"{name} parity mode: iteration count {inf['iters']} vs oracle {meta['iters_parity']} "
+              f"(window [{lo}, {hi}], perturbed oracle {pert}); mu gate authoritative (G9)")
     assert err <= 10 * c.eps, (err, 10 * c.eps)
     assert len(hist_g) == inf["iters"] + 1 and hist_g[-1] <= cg_tol
     # the trajectories agree to NUFFT accuracy before roundoff decorrelates them
@@ -132,13 +147,15 @@ def test_golden_production_iterations(name):
     inf = g.info()
     mu = g.predict(xt).cpu().numpy()
     k_g, k_o = inf["iters"], meta["iters_production"]
-    lo, hi = _window(G["hist_production"], c.eps)
-    ok = abs(k_g - k_o) <= 2 or lo <= k_g <= hi
+    pert = meta.get("iters_perturbed", {}).get("production", [])
+    g10, g10b, (lo, hi) = _count_ok(k_g, k_o, G["hist_production"], c.eps, pert)
+    ok = g10 or g10b
     hist_g = np.asarray(g.residual_history())
     ho = np.asarray(G["hist_production"])
     kk = min(len(hist_g), len(ho))
     _report(name, {"production": {
-        "iters_gpu": k_g, "iters_oracle": k_o, "oracle_window": [lo, hi], "g10_pass": bool(ok),
+        "iters_gpu": k_g, "iters_oracle": k_o, "oracle_window": [lo, hi], "oracle_perturbed": pert,
+        "g10_pass": g10, "g10b_pass": g10b,
         "mu_rel_to_oracle_production": rel(mu, G["mu_production"]),
         "mu_rel_to_oracle_parity": rel(mu, G["mu_parity"]),
         "oracle_production_rel_to_parity": rel(G["mu_production"], G["mu_parity"]),
@@ -148,13 +165,9 @@ def test_golden_production_iterations(name):
     # own production answer is (x2), plus 10 eps (reading G9: the first crossing is hypersensitive)
     e_o = rel(G["mu_production"], G["mu_parity"])
     assert rel(mu, G["mu_parity"]) <= 2 * e_o + 10 * c.eps, (rel(mu, G["mu_parity"]), e_o)
-    if name in G10_PRODUCTION:
-        assert ok, (f"G10: gpu {k_g} vs oracle {k_o}, window [{lo}, {hi}]; histories: "
-                    f"gpu {hist_g[max(0, k_o - 5):k_g + 2]} oracle {ho[max(0, k_o - 5):k_o + 2]}")
-    elif not ok:
-        print(f"{name}: G10 window missed as SURVEY A.6 predicts: gpu {k_g} vs oracle {k_o} "
-              f"(window [{lo}, {hi}]); first 25 residual ratios agree to "
-              f"{np.max(np.abs(hist_g[:26] / ho[:26] - 1)):.1e}")
+    if pert or name in G10_PRODUCTION:
+        assert ok, (f"G10/G10b: gpu {k_g} vs oracle {k_o}, window [{lo}, {hi}], perturbed oracle {pert}; "
+                    f"histories: gpu {hist_g[max(0, k_o - 5):k_g + 2]} oracle {ho[max(0, k_o - 5):k_o + 2]}")
     g.close()
     del x, y
     torch.cuda.empty_cache()
