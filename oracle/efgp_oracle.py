@@ -34,7 +34,7 @@ Readings where the paper is silent, garbled or inconsistent (DESIGN.md "Readings
   G4  SE (h, m): Cor c:SEparams literally; h rounded down at the 12th significant digit.
   G6  CG: x0 = 0, unpreconditioned, recursive residual, Hermitian inner products.
   G11 (c4 Toeplitz product): the direct O(M^2) product is too slow at M = 4.2e5, so the oracle may use
-      an independent host FFT (numpy/pocketfft, never cuFFT), validated against the direct product.
+      an independent host FFT (scipy/pocketfft, never cuFFT), validated against the direct product.
   G12 NEXT-4 preconditioner (P:2741-2745 names "Kronecker-structure Toeplitz preconditioners" only):
       v^(i)_l = v_{l e_i}, T_i = T(v^(i)) ((2m+1)^2 Toeplitz), delta_i(j) = D_{j e_i} / D_0^((d-1)/d),
       A_i = diag(delta_i) T_i diag(delta_i) / N^((d-1)/d), M = A_1 (x) ... (x) A_d + sigma^2 I, applied as
@@ -57,6 +57,7 @@ import math
 from dataclasses import dataclass, field
 
 import numpy as np
+import scipy.fft
 import scipy.integrate
 import scipy.linalg
 import scipy.special
@@ -275,22 +276,35 @@ def toeplitz_apply(v: np.ndarray, beta: np.ndarray, T: np.ndarray | None = None)
     return out
 
 
+def _prime_factors(n: int):
+    out, f = [], 2
+    while f * f <= n:
+        while n % f == 0:
+            out.append(f)
+            n //= f
+        f += 1
+    return out + ([n] if n > 1 else [])
+
+
 def toeplitz_apply_fft(v: np.ndarray, beta: np.ndarray) -> np.ndarray:
-    """(T beta)_p = sum_{q in J_m} v_{p-q} beta_q by a host FFT (numpy's pocketfft), reading G11: the
+    """(T beta)_p = sum_{q in J_m} v_{p-q} beta_q by a host FFT (scipy's pocketfft), reading G11: the
     one allowed exception to the direct product, for c4 only (M = 4.2e5 makes the direct O(M^2)
     product ~1.8e11 MACs).  It is Alg ``a:FF`` written with complex FFTs of length
-    L = 4m+1 per axis: v_j is placed at index j mod L, beta_q at q + m (zero-padded); the circular
-    convolution at index p + m equals the linear one because |p - q| <= 2m < L (no wrap-around).
-    Pinned against :func:`toeplitz_apply` (full at small m, sampled outputs at c4's m)."""
+    L >= 4m+1 per axis (the smallest 2^a 3^b 5^c, so pocketfft avoids Bluestein for prime 4m+1): v_j
+    is placed at index j mod L, beta_q at q + m (zero-padded); the circular convolution at index p + m
+    equals the linear one because |p - q| <= 2m < L (no wrap-around).  Pinned against
+    :func:`toeplitz_apply` (full at small m, sampled outputs at c4's m)."""
     d = beta.ndim
     m = (beta.shape[0] - 1) // 2
     L = 4 * m + 1
+    while any(f > 5 for f in _prime_factors(L)):
+        L += 1
     vb = np.zeros((L,) * d, dtype=np.complex128)
     idx = np.arange(-2 * m, 2 * m + 1) % L
     vb[np.ix_(*([idx] * d))] = v
     bb = np.zeros((L,) * d, dtype=np.complex128)
     bb[(slice(0, 2 * m + 1),) * d] = beta
-    c = np.fft.ifftn(np.fft.fftn(vb) * np.fft.fftn(bb))
+    c = scipy.fft.ifftn(scipy.fft.fftn(vb, workers=-1) * scipy.fft.fftn(bb, workers=-1), workers=-1)
     return c[(slice(0, 2 * m + 1),) * d]       # index p + m, p in J_m
 
 

@@ -224,7 +224,8 @@ def test_fit_with_fft_toeplitz_equals_direct():
     # efgp_fit(toeplitz_fft=True) runs the same CG as the direct product (same iterates up to roundoff)
     rng, x, _ = _small_problem(d=3, N=600, m=3, seed=5)
     y = np.sin(4 * x[:, 0]) + 0.1 * rng.normal(size=600)
-    a = O.efgp_fit(x, y, "matern", 0.2, 0.1, 1e-3, nu=0.5, h=0.4, m=3, cg_tol=1e-9)
-    b = O.efgp_fit(x, y, "matern", 0.2, 0.1, 1e-3, nu=0.5, h=0.4, m=3, cg_tol=1e-9, toeplitz_fft=True)
-    assert abs(a.iters - b.iters) <= 2
-    np.testing.assert_allclose(b.beta, a.beta, rtol=0, atol=1e-8 * np.max(np.abs(a.beta)))
+    # (a well-conditioned system, sigma = 1, so that roundoff does not move the stopping iteration)
+    a = O.efgp_fit(x, y, "matern", 0.2, 1.0, 1e-3, nu=0.5, h=0.4, m=3, cg_tol=1e-10)
+    b = O.efgp_fit(x, y, "matern", 0.2, 1.0, 1e-3, nu=0.5, h=0.4, m=3, cg_tol=1e-10, toeplitz_fft=True)
+    assert abs(a.iters - b.iters) <= 1
+    np.testing.assert_allclose(b.beta, a.beta, rtol=0, atol=1e-9 * np.max(np.abs(a.beta)))
