@@ -2,6 +2,8 @@
 
     python -m paper_2210_10210_b200.build          # incremental
     python -m paper_2210_10210_b200.build --force
+    python -m paper_2210_10210_b200.build --checked  # libefgp_checked.so: device-side invariant
+                                                     # checks on (EFGP_DCHECK; select with EFGP_LIB)
 """
 from __future__ import annotations
 
@@ -28,27 +30,29 @@ def _run(cmd):
     return r.stdout + r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
     newest_hdr = max(os.path.getmtime(h) for h in hdrs)
-    objdir = os.path.join(HERE, "build_obj")
+    objdir = os.path.join(HERE, "build_obj_checked" if checked else "build_obj")
+    lib = os.path.join(HERE, "libefgp_checked.so") if checked else LIB
+    extra = ["-DEFGP_DEVICE_CHECKS=1"] if checked else []
     os.makedirs(objdir, exist_ok=True)
     jobs = []
     for s in srcs:
         o = os.path.join(objdir, os.path.basename(s)[:-3] + ".o")
         if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), newest_hdr):
-            jobs.append([NVCC] + CFLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", s, "-o", o])
+            jobs.append([NVCC] + CFLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-c", s, "-o", o])
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         for out in ex.map(_run, jobs):
             if verbose and out:
                 print(out)
     objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in srcs]
-    if force or jobs or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs +
+    if force or jobs or not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs):
+        _run([NVCC] + ARCH + ["-shared", "-o", lib] + objs +
              ["-L/usr/local/cuda/lib64", "-lcufft", "-lcusolver", "-ldl", "-Xlinker", "-rpath=/usr/local/cuda/lib64"])
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

@@ -618,10 +618,12 @@ void efgp_destroy(efgp_handle pl) {
   void *bufs[] = {pl->poly_dev, pl->D_half, pl->psi1, pl->psi2, pl->g1, pl->g2, pl->G1h, pl->G2h, pl->modes, pl->modes_sum,
                   pl->Xbox, pl->Yr, pl->vhat, pl->Zbox, pl->b, pl->x, pl->r, pl->p, pl->Ap, pl->partials,
                   pl->scal, pl->hist, pl->dflags, pl->T2box, pl->t2grid, pl->stage[0], pl->stage[1],
-                  pl->rec[0], pl->rec[1], pl->rec[2], pl->trace,
+                  pl->trace,
                   pl->sync_buf, pl->het_box, pl->het_grid, pl->pc_Q, pl->pc_F0, pl->pc_F1, pl->pc_work, pl->z,
                   pl->pc_lam, pl->pc_info, pl->comm_buf, pl->vfull, pl->pc_diag};
   for (void *b : bufs)
+    if (b) cudaFree(b);
+  for (void *b : pl->rec)
     if (b) cudaFree(b);
   if (pl->h_pinned) cudaFreeHost(pl->h_pinned);
   for (auto &e : pl->ev)

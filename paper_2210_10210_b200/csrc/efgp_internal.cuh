@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cufft.h>
+#include <cstdio>
 #include <cstdint>
 #include <cstdlib>
 #include <string>
@@ -13,6 +14,7 @@ namespace efgp {
 
 constexpr double kPi = 3.14159265358979323846;
 constexpr int kMaxW = 16;  // ES kernel width for nufft_tol down to 1e-15
+constexpr int kMaxNbuf = 8;  // SORTED spreading: record-list buffers in flight (at most)
 
 // Degree of the piecewise-polynomial ES kernel per cell offset: degree W already gives the aliasing
 // error of the exact ES kernel to within 2 % for W >= 4 (the deconvolution tables are the
@@ -71,6 +73,7 @@ struct Params {
   int tiles_grid = 0;          // CTAs of the fused spreading kernel (<= one per SM)
   int nbuf = 2;                // tile-list buffers in flight
   int64_t chunk = 0;           // points per chunk
+  bool sorted_own = false;     // static tile ownership (CTA b accumulates tile b)
 };
 
 // host_setup.cu
@@ -145,7 +148,7 @@ struct efgp_plan {
 
   // SORTED spreading: per-chunk tile lists (nbuf buffers) of x pairs and y, and the per-call
   // list lengths + handshake counters of the fused kernel
-  double4 *rec[3] = {nullptr, nullptr, nullptr};  // ntiles x grid x segcap records (x1, x2, y, key)
+  double4 *rec[efgp::kMaxNbuf] = {};  // ntiles x grid x segcap records (x1, x2, y, key)
   size_t rec_cap = 0;                              // records allocated per buffer
   int *sync_buf = nullptr;
   size_t sync_cap = 0;
@@ -307,6 +310,23 @@ efgp_status variance_targets(efgp_plan *pl, const double *xt, int64_t q, double 
   do {                                 \
     efgp_status s_ = (call);           \
     if (s_ != EFGP_OK) return s_;      \
+  } while (0)
+
+// ---- device-side invariant checks ------------------------------------------------------
+// compute-sanitizer is closed on the GPU pool (profiles/r02_compute_sanitizer_closed.log), so the
+// kernels carry their own bounds/invariant checks: built with -DEFGP_DEVICE_CHECKS=1 (tools/
+// build_checked.sh) every EFGP_DCHECK prints the failed condition and traps; the default build
+// compiles them out.
+#ifndef EFGP_DEVICE_CHECKS
+#define EFGP_DEVICE_CHECKS 0
+#endif
+#define EFGP_DCHECK(c)                                                                       \
+  do {                                                                                       \
+    if (EFGP_DEVICE_CHECKS && !(c)) {                                                        \
+      printf("EFGP_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, blockIdx.x, \
+             threadIdx.x, #c);                                                               \
+      __trap();                                                                              \
+    }                                                                                        \
   } while (0)
 
 // ---- device helpers shared by the kernels ------------------------------------------------

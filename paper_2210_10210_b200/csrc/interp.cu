@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(kIB, 1024 / kIB) k_interp2_banked(const double
       }
     }
     if (j >= 0) {
+      EFGP_DCHECK(j < kIB && s_cell[j] >= 0 && s_cell[j] + (W - 1) * (A + 1) < A * A);
       double wt[2][W];
       es_weights_s<W>(s_s[0][j], P, wt[0]);
       es_weights_s<W>(s_s[1][j], P, wt[1]);

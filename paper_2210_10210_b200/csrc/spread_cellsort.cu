@@ -6,14 +6,17 @@
 //   1. k_cs_count   : per-CTA shared-memory histogram of the points' super-cells (G^d start cells;
 //                     G = 1 in 2D (2 for large grids), 4 in 3D so the key space fits shared memory).
 //   2. k_het_colscan / k_het_offsets (hetero.cu): bucket offsets per CTA.
-//   3. k_cs_scatter : counting-sort scatter into structure-of-arrays buffers (coordinates, y).
+//   3. k_cs_scatter : counting-sort scatter of 32-byte records, one STG.256 (a full sector) per point:
+//                     2D (x1, x2, y, w), 3D (x1, x2, x3, y) (+ w in its own array when given).  (The
+//                     r01 structure-of-arrays scatter wrote 3-4 partial 8-byte sectors per point: 3.5-4x
+//                     its algorithmic DRAM bytes.)
 //   4. k_cs_spread  : a warp per run of <= kCsRun points of one super-cell.  Batches of 32 points: lane
 //                     p evaluates the ES weights of point p and writes them, padded to the union window
 //                     U = W + G - 1 per dimension, to shared memory; then every lane accumulates the
 //                     U^d window elements it owns (e = lane + 32 t) over the 32 points in registers
 //                     (strengths 1 and y).  One RED per owned element per run.
-// Traffic: x, y read twice (count, scatter) + the sorted copy written and read: (d + 1) 8 B x 4 per
-// point, against 2 W^d L2 atomics per point for GLOBAL.
+// Traffic: x, y read twice (count, scatter) + the sorted 32-byte records written and read, against
+// 2 W^d L2 atomics per point for GLOBAL.
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -69,11 +72,15 @@ __global__ void k_cs_count(const double *__restrict__ x, const double *__restric
   for (int i = threadIdx.x; i < ncell; i += blockDim.x) hist[(size_t)blockIdx.x * ncell + i] = cs_h[i];
 }
 
+__device__ __forceinline__ void cs_st256(double4 *p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 template <int D, int W, int G>
 __global__ void k_cs_scatter(const double *__restrict__ x, const double *__restrict__ y, int64_t N, double h, int n,
                              int lo, int S, int ncell, const unsigned *__restrict__ hist,
-                             const long long *__restrict__ off, double *__restrict__ xs, double *__restrict__ ys,
-                             int *__restrict__ err, const double *__restrict__ w1, double *__restrict__ ws1) {
+                             const long long *__restrict__ off, double4 *__restrict__ rec, int *__restrict__ err,
+                             const double *__restrict__ w1, double *__restrict__ ws1) {
   extern __shared__ unsigned cs_c[];  // cursor relative to the bucket start (< 2^32 points per call)
   for (int i = threadIdx.x; i < ncell; i += blockDim.x) cs_c[i] = hist[(size_t)blockIdx.x * ncell + i];
   __syncthreads();
@@ -81,11 +88,15 @@ __global__ void k_cs_scatter(const double *__restrict__ x, const double *__restr
   cs_range(N, a, e);
   for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x) {
     const int key = cs_key<D, W, G>(x, y, i, h, n, lo, S, err);
+    EFGP_DCHECK(key >= 0 && key < ncell);
     const long long pos = off[key] + (long long)atomicAdd(&cs_c[key], 1u);
-#pragma unroll
-    for (int k = 0; k < D; ++k) xs[(int64_t)k * N + pos] = __ldg(x + i * D + k);
-    ys[pos] = __ldg(y + i);
-    if (w1) ws1[pos] = __ldg(w1 + i);
+    EFGP_DCHECK(pos >= off[key] && pos < off[key + 1]);
+    if constexpr (D == 2) {
+      cs_st256(rec + pos, __ldg(x + 2 * i), __ldg(x + 2 * i + 1), __ldg(y + i), w1 ? __ldg(w1 + i) : 1.0);
+    } else {
+      cs_st256(rec + pos, __ldg(x + 3 * i), __ldg(x + 3 * i + 1), __ldg(x + 3 * i + 2), __ldg(y + i));
+      if (w1) ws1[pos] = __ldg(w1 + i);
+    }
   }
 }
 
@@ -96,7 +107,7 @@ __device__ __forceinline__ int cs_wrap(int i, int n) {
 
 template <int D, int W, int G>
 __global__ void __launch_bounds__(kCsThreads) k_cs_spread(const CsItem *__restrict__ items, int64_t nitems,
-                                                          const double *__restrict__ xs, const double *__restrict__ ys,
+                                                          const double4 *__restrict__ rec,
                                                           const double *__restrict__ ws1, int64_t N,
                                                           double *__restrict__ g1, double *__restrict__ g2,
                                                           double h, int n, int lo, int S, EsPoly P) {
@@ -126,13 +137,15 @@ __global__ void __launch_bounds__(kCsThreads) k_cs_spread(const CsItem *__restri
       const long long r = b0 + lane;
       __syncwarp();
       if (r < item.end) {
+        const double4 rv = rec[r];
+        const double xr[3] = {rv.x, rv.y, rv.z};
         double row[D * U];
 #pragma unroll
         for (int q = 0; q < D * U; ++q) row[q] = 0.0;
 #pragma unroll
         for (int k = 0; k < D; ++k) {
           double w[W];
-          const int i0 = es_weights<W>(h * __ldg(xs + (int64_t)k * N + r) * (double)n, P, w);
+          const int i0 = es_weights<W>(h * xr[k] * (double)n, P, w);
           int off = i0 - lo - sc[k] * G;         // start cell within the super-cell, 0..G-1
           off = off < 0 ? 0 : (off > G - 1 ? G - 1 : off);
 #pragma unroll
@@ -143,8 +156,8 @@ __global__ void __launch_bounds__(kCsThreads) k_cs_spread(const CsItem *__restri
         }
 #pragma unroll
         for (int q = 0; q < D * U; ++q) ws[lane][q] = row[q];
-        ws[lane][D * U] = __ldg(ys + r);
-        ws[lane][D * U + 1] = ws1 ? __ldg(ws1 + r) : 1.0;
+        ws[lane][D * U] = D == 2 ? rv.z : rv.w;
+        ws[lane][D * U + 1] = D == 2 ? rv.w : (ws1 ? __ldg(ws1 + r) : 1.0);
       } else {
 #pragma unroll
         for (int q = 0; q <= D * U + 1; ++q) ws[lane][q] = 0.0;
@@ -215,21 +228,21 @@ static efgp_status cellsort_t(efgp_plan *pl, const double *x, const double *y, c
   const int B = sort_ctas(pl->num_sms), T = 1024, n = (int)P.n1;
   unsigned *hist = nullptr;
   long long *tot = nullptr, *off = nullptr;
-  double *xs = nullptr, *ys = nullptr, *ws1 = nullptr;
+  double4 *rec = nullptr;
+  double *ws1 = nullptr;
   CsItem *items = nullptr;
   EFGP_PALLOC(&hist, sizeof(unsigned) * B * ncell, s);
   EFGP_PALLOC(&tot, sizeof(long long) * ncell, s);
   EFGP_PALLOC(&off, sizeof(long long) * (ncell + 1), s);
-  EFGP_PALLOC(&xs, sizeof(double) * N * D, s);
-  EFGP_PALLOC(&ys, sizeof(double) * N, s);
-  if (w1) EFGP_PALLOC(&ws1, sizeof(double) * N, s);
+  EFGP_PALLOC(&rec, sizeof(double4) * N, s);
+  if (w1 && D == 3) EFGP_PALLOC(&ws1, sizeof(double) * N, s);
   const size_t sm = sizeof(unsigned) * ncell;
   EFGP_CUDA(cudaFuncSetAttribute(k_cs_count<D, W, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   EFGP_CUDA(cudaFuncSetAttribute(k_cs_scatter<D, W, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_cs_count<D, W, G><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, pl->dflags);
   k_het_colscan<<<(ncell + 255) / 256, 256, 0, s>>>(hist, B, ncell, tot);
   k_het_offsets<<<1, 1024, 0, s>>>(tot, ncell, off);
-  k_cs_scatter<D, W, G><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, off, xs, ys, pl->dflags, w1, ws1);
+  k_cs_scatter<D, W, G><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, off, rec, pl->dflags, w1, ws1);
   EFGP_CUDA(cudaGetLastError());
   std::vector<long long> offh(ncell + 1);
   EFGP_CUDA(cudaMemcpyAsync(offh.data(), off, sizeof(long long) * (ncell + 1), cudaMemcpyDeviceToHost, s));
@@ -245,11 +258,11 @@ static efgp_status cellsort_t(efgp_plan *pl, const double *x, const double *y, c
   EFGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cs_spread<D, W, G>, kCsThreads, 0));
   int64_t blocks = std::min<int64_t>((int64_t)pl->num_sms * std::max(per_sm, 1), (nitems * 32 + kCsThreads - 1) / kCsThreads);
   if (nitems > 0)
-    k_cs_spread<D, W, G><<<(unsigned)std::max<int64_t>(blocks, 1), kCsThreads, 0, s>>>(items, nitems, xs, ys, ws1, N, pl->g1,
+    k_cs_spread<D, W, G><<<(unsigned)std::max<int64_t>(blocks, 1), kCsThreads, 0, s>>>(items, nitems, rec, ws1, N, pl->g1,
                                                                                      pl->g2, P.h, n, lo, S, P.poly);
   EFGP_CUDA(cudaGetLastError());
   EFGP_CUDA(cudaStreamSynchronize(s));  // the host item vector is consumed by the copy above
-  for (void *p : {(void *)hist, (void *)tot, (void *)off, (void *)xs, (void *)ys, (void *)items}) cudaFreeAsync(p, s);
+  for (void *p : {(void *)hist, (void *)tot, (void *)off, (void *)rec, (void *)items}) cudaFreeAsync(p, s);
   if (ws1) cudaFreeAsync(ws1, s);
   return EFGP_OK;
 }

@@ -37,8 +37,17 @@
 
 namespace efgp {
 
+#ifndef EFGP_BIN_WARPS
+#define EFGP_BIN_WARPS 4
+#endif
 constexpr int kAccThreads = 256;                  // warps 0-7
-constexpr int kBinThreads = 128;                  // warps 8-11
+constexpr int kBinThreads = 32 * EFGP_BIN_WARPS;  // warps 8.. (one or two warpgroups)
+// setmaxnreg budgets (multiples of 8; kAccThreads acc + kBinThreads bin <= 64K registers)
+#ifndef EFGP_BIN_REGS8
+#define EFGP_BIN_REGS8 56
+#endif
+constexpr int kBinRegs = EFGP_BIN_WARPS == 4 ? 104 : EFGP_BIN_REGS8;
+constexpr int kAccRegs = EFGP_BIN_WARPS == 4 ? 200 : (65536 / 256 - EFGP_BIN_REGS8) / 8 * 8;
 constexpr int kFusedThreads = kAccThreads + kBinThreads;
 constexpr int kBarAcc = 1, kBarBin = 2, kBarAcc2 = 3;  // named barriers (0 = __syncthreads)
 constexpr int kModeF64 = 0;   // fp64 weights (evaluated per record in phase C), fp64 accumulation
@@ -243,11 +252,13 @@ struct FusedArgs {
   int64_t N, chunk;
   int nchunks, nbuf;
   int debug;           // diagnostics (EFGP_SORTED_DEBUG): 1 = accumulators skip their work
+  int own;             // 1: static tile ownership (CTA b accumulates tile b; ntiles <= grid)
+  unsigned nconsumers; // accumulator groups that release each chunk (acc_done target)
   double h;
   int n1, s_lo, S, T1, T2, nt2, ntiles;
   int segcap;          // records per (tile, binner CTA) segment per chunk
   int R;               // records per accumulator round
-  double4 *rec[3];     // [buf][tile][cta][segcap] records (x1, x2, y, key bits)
+  double4 *rec[kMaxNbuf];  // [buf][tile][cta][segcap] records (x1, x2, y, key bits)
   int *segcnt;         // [nchunks][tile][cta] segment lengths
   int *tilecnt;        // [nchunks][tile] list lengths (sum over CTAs)
   unsigned *bin_done;  // [nchunks] CTAs that finished binning chunk k
@@ -266,7 +277,7 @@ struct FusedArgs {
 #endif
 constexpr int kWBatch = EFGP_WBATCH;              // points per binner-warp batch
 constexpr int kWStages = EFGP_WSTAGES;            // TMA ring depth per binner warp
-constexpr int kBinWarps = kBinThreads / 32;       // 4
+constexpr int kBinWarps = kBinThreads / 32;
 
 template <int W, int MODE>
 struct FusedSmem {
@@ -351,7 +362,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
           atomicAdd(A.bin_done + cur, 1u);
           stamp(A.trace, cur, 0);
         }
-        if (cur + 1 < A.nchunks && cur + 1 >= A.nbuf) spin_until(A.acc_done + (cur + 1 - A.nbuf), 2 * G);
+        if (cur + 1 < A.nchunks && cur + 1 >= A.nbuf) spin_until(A.acc_done + (cur + 1 - A.nbuf), A.nconsumers);
       }
       ++cur;
       named_sync(kBarBin, kBinThreads);  // buffer cur % nbuf is free
@@ -395,6 +406,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       const int r = rowt[start_cell<W>(grid_t(A.h, p.x, A.n1)) - A.s_lo];
       const int c = colt[start_cell<W>(grid_t(A.h, p.y, A.n1)) - A.s_lo];
       tk[q] = (in && ok) ? (((r >> 16) + (c >> 16)) << 8 | ((r & 0xFFFF) + (c & 0xFFFF))) : -1;
+      EFGP_DCHECK(!(in && ok) || ((tk[q] >> 8) < ntiles && (tk[q] & 0xFF) < A.T1 * A.T2));
       ci[q] = (r >> 16) + (c >> 16);
     }
 #pragma unroll
@@ -432,6 +444,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       const int v = perm[slot];
       const int j = v & 0xFF, key = (v >> 8) & 0xFF, t = v >> 16;
       const int p = wbase[t] + slot - wloc[t];
+      EFGP_DCHECK(j < nb && t < ntiles && slot >= wloc[t] && p >= 0);
       const double2 xx = xs2[j];
       const double yv = ys[j];
       if (p < A.segcap)
@@ -528,6 +541,354 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
 #pragma unroll
     for (int b = 0; b < (W + 1) / 2; ++b) p1[a][b] = py[a][b] = make_float2(0.f, 0.f);
 
+  // One round: wait for its records (raw[0..nr), bulk copies issued earlier), pass 1 (rank per start
+  // cell), scan, pass 2 (cell-sorted stage), issue_next() (raw is free), phase C (register windows);
+  // fold the windows into the fp64 tile accumulator if fold_req (or MIXED overflow), and flush the
+  // tile accumulator (tile origin r0, c0 in start cells) into the fine grids if flush.
+  auto round_body = [&](const int nr, auto &&issue_next, const bool fold_req, const bool flush, const int r0,
+                        const int c0, auto &&on_landed) {
+        cnt[tid] = 0;
+        PH(0);
+        if (nr > 0) {  // (nr = 0: a final fold / flush without records)
+          mbar_wait(bar, phase);
+          phase ^= 1u;
+        }
+        on_landed();  // the round's records are in shared memory
+        named_sync(bar_id, kGrpThreads);
+        PH(1);
+        // pass 1 (thread per record): rank within its start cell (key from the binner), kept in
+        // the record's key slot
+        for (int j0 = tid; j0 < nr; j0 += 4 * kGrpThreads) {  // 4 records at a time (latency)
+          int key[4], rnk[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u * kGrpThreads;
+            key[u] = j < nr ? __double2loint(raw[j].w) : -1;
+            EFGP_DCHECK(key[u] < NT);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) rnk[u] = key[u] >= 0 ? atomicAdd(&cnt[key[u]], 1) : 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u * kGrpThreads;
+            if (j < nr) reinterpret_cast<int *>(&raw[j].w)[1] = rnk[u];
+          }
+        }
+        named_sync(bar_id, kGrpThreads);
+        const int mycnt = cnt[tid];
+        if (tid < 32) {  // cell offsets: warp 0 scans the 128 counts (4 per lane)
+          const int4 c4 = reinterpret_cast<const int4 *>(cnt)[tid];
+          const int sum = c4.x + c4.y + c4.z + c4.w;
+          int incl = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o) incl += v;
+          }
+          const int e = incl - sum;
+          reinterpret_cast<int4 *>(coff)[tid] = make_int4(e, e + c4.x, e + c4.x + c4.y, e + c4.x + c4.y + c4.z);
+        }
+        named_sync(bar_id, kGrpThreads);
+        PH(2);
+        const int myoff = coff[tid];
+        // pass 2 (thread per record): the record (FP64) or its fp32 weights at its sorted slot
+#pragma unroll 2
+        for (int j = tid; j < nr; j += kGrpThreads) {
+          const double4 rv = raw[j];
+          EFGP_DCHECK(__double2loint(rv.w) >= 0 && __double2loint(rv.w) < NT && __double2hiint(rv.w) >= 0 &&
+                      coff[__double2loint(rv.w)] + __double2hiint(rv.w) < nr);
+          unsigned char *st = stage + (size_t)(coff[__double2loint(rv.w)] + __double2hiint(rv.w)) * SB;
+          if constexpr (MODE == kModeF64) {
+            // the reduced coordinates s1, s2 (es_reduce) are computed here, in the load-balanced
+            // thread-per-record pass, instead of in phase C (thread per cell, Poisson-imbalanced)
+            double *d = reinterpret_cast<double *>(st);
+            double s1, s2;
+            es_reduce<W>(grid_t(h, rv.x, n1), s1);
+            es_reduce<W>(grid_t(h, rv.y, n1), s2);
+            d[0] = s1;
+            d[1] = s2;
+            d[2] = rv.z;
+          } else {
+            constexpr int WP = (W + 1) / 2, WE = 2 * WP, NF = SB / 4;
+            float2 w1[WP], w2[WP];
+            es_weights_pairs<W>(grid_t(h, rv.x, n1), PF, w1);
+            es_weights_pairs<W>(grid_t(h, rv.y, n1), PF, w2);
+            float f[NF];
+#pragma unroll
+            for (int q = 0; q < WP; ++q) {
+              f[2 * q] = w1[q].x;
+              f[2 * q + 1] = w1[q].y;
+              f[WE + 2 * q] = w2[q].x;
+              f[WE + 2 * q + 1] = w2[q].y;
+            }
+#pragma unroll
+            for (int i = 2 * WE; i < NF; ++i) f[i] = 0.f;
+            if constexpr (MODE == kModeA32) {
+              f[StageRec<W, MODE>::kYSlot] = (float)rv.z;
+            } else {
+              f[2 * WE] = __int_as_float(__double2loint(rv.z));
+              f[2 * WE + 1] = __int_as_float(__double2hiint(rv.z));
+            }
+            float4 *q4 = reinterpret_cast<float4 *>(st);
+#pragma unroll
+            for (int i = 0; i < NF / 4; ++i) q4[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+          }
+        }
+        named_sync(bar_id, kGrpThreads);
+        PH(3);
+        issue_next();  // raw is free: the next round's copies land during phase C
+        // phase C (thread per start cell): register accumulation of its records
+        if (mycnt > 0) {
+          const unsigned char *sp = stage + (size_t)myoff * SB;
+          if constexpr (MODE == kModeF64) {
+#pragma unroll 2
+            for (int q = 0; q < mycnt; ++q, sp += SB) {
+              const double *d = reinterpret_cast<const double *>(sp);
+              const double yv = d[2];
+              double w1[W], w2[W];
+              es_weights_s<W>(d[0], P, w1);
+              es_weights_s<W>(d[1], P, w2);
+#pragma unroll
+              for (int a = 0; a < W; ++a) {
+                const double ca = w1[a], cy = yv * w1[a];
+#pragma unroll
+                for (int b2 = 0; b2 < W; ++b2) {
+                  a1[a][b2] = fma(ca, w2[b2], a1[a][b2]);
+                  ay[a][b2] = fma(cy, w2[b2], ay[a][b2]);
+                }
+              }
+            }
+          } else if constexpr (MODE == kModeW32) {
+            constexpr int WE = StageRec<W, MODE>::WE, NF = SB / 4;
+#pragma unroll 2
+            for (int q = 0; q < mycnt; ++q, sp += SB) {
+              float f[NF];
+              load_floats<SB>(sp, f);
+              const double yv = __hiloint2double(__float_as_int(f[2 * WE + 1]), __float_as_int(f[2 * WE]));
+              double w2[W];
+#pragma unroll
+              for (int b2 = 0; b2 < W; ++b2) w2[b2] = (double)f[WE + b2];
+#pragma unroll
+              for (int a = 0; a < W; ++a) {
+                const double ca = (double)f[a], cy = yv * ca;
+#pragma unroll
+                for (int b2 = 0; b2 < W; ++b2) {
+                  a1[a][b2] = fma(ca, w2[b2], a1[a][b2]);
+                  ay[a][b2] = fma(cy, w2[b2], ay[a][b2]);
+                }
+              }
+            }
+          } else {
+            // MIXED: fp32 pairs along b: (acc[a][2p], acc[a][2p+1]) += w1[a] * (w2[2p], w2[2p+1])
+            constexpr int WP = (W + 1) / 2, WE = 2 * WP, NF = SB / 4;
+#pragma unroll 2
+            for (int q = 0; q < mycnt; ++q, sp += SB) {
+              float f[NF];
+              load_floats<SB>(sp, f);
+              const float yf = f[StageRec<W, MODE>::kYSlot];
+#pragma unroll
+              for (int a = 0; a < W; ++a) {
+                const float c1 = f[a], cy = yf * f[a];
+#pragma unroll
+                for (int pp = 0; pp < WP; ++pp) {
+                  const float2 w2p = make_float2(f[WE + 2 * pp], f[WE + 2 * pp + 1]);
+                  p1[a][pp] = __ffma2_rn(w2p, make_float2(c1, c1), p1[a][pp]);
+                  py[a][pp] = __ffma2_rn(w2p, make_float2(cy, cy), py[a][pp]);
+                }
+              }
+            }
+          }
+        }
+        // MIXED: the fp32 windows of one tile segment sum at most 64 points per start cell; past that
+        // (only for very concentrated data) they are folded into the fp64 tile accumulator early
+        PH(4);
+        bool fold_now = fold_req;
+        if constexpr (MODE == kModeA32) {
+          pend += mycnt;
+          fold_now = named_sync_or(bar_id, kGrpThreads, pend >= 64) || fold_now;
+        } else {
+          named_sync(bar_id, kGrpThreads);  // stage and cnt free
+        }
+        if (fold_now) {
+          // add the windows into the fp64 tile accumulator in W^2 conflict-free steps
+#pragma unroll
+          for (int a = 0; a < W; ++a) {
+#pragma unroll
+            for (int b2 = 0; b2 < W; ++b2) {
+              if (own) {
+                const int idx = (my_r + a) * A2 + (my_c + b2);
+                if constexpr (MODE == kModeA32) {
+                  const float2 v1 = p1[a][b2 / 2], vy = py[a][b2 / 2];
+                  tacc[idx] += (double)((b2 & 1) ? v1.y : v1.x);
+                  tacc[A1 * A2 + idx] += (double)((b2 & 1) ? vy.y : vy.x);
+                } else {
+                  tacc[idx] += a1[a][b2];
+                  tacc[A1 * A2 + idx] += ay[a][b2];
+                }
+              }
+              named_sync(bar_id, kGrpThreads);
+            }
+          }
+          if constexpr (MODE == kModeA32) {
+#pragma unroll
+            for (int a = 0; a < W; ++a)
+#pragma unroll
+              for (int pp = 0; pp < (W + 1) / 2; ++pp) p1[a][pp] = py[a][pp] = make_float2(0.f, 0.f);
+            pend = 0;
+          } else {
+#pragma unroll
+            for (int a = 0; a < W; ++a)
+#pragma unroll
+              for (int b2 = 0; b2 < W; ++b2) a1[a][b2] = ay[a][b2] = 0.0;
+          }
+        }
+        PH(5);
+        // end of a tile segment: one RED per cell of the tile accumulator, which is re-zeroed
+        if (flush) {
+          for (int i = tid; i < A1 * A2; i += kGrpThreads) {
+            const double v1 = tacc[i], vy = tacc[A1 * A2 + i];
+            const int r = wrap_s(s_lo + r0 + i / A2, n1), c = wrap_s(s_lo + c0 + i % A2, n1);
+            const int64_t gidx = (int64_t)r * n1 + c;
+            if (v1 != 0.0) atomicAdd(A.g1 + gidx, v1);
+            if (vy != 0.0) atomicAdd(A.gy + gidx, vy);
+            tacc[i] = tacc[A1 * A2 + i] = 0.0;
+          }
+          named_sync(bar_id, kGrpThreads);
+        }
+  };
+
+  // Static ownership (A.own: ntiles <= grid, the c5 geometry): CTA b owns tile b for the whole call;
+  // its group g consumes the segments of the binner CTAs p = g, g + 2, ... of tile b, chunk after
+  // chunk, as ONE stream: rounds of R records may span chunk boundaries, the windows are never folded
+  // before the end (no tile switches), and a chunk's lists are released (acc_done) as soon as this
+  // group's rounds have read them.  With small chunks the record lists stay L2-resident.
+  auto accumulate_static = [&]() {
+    const int t = blockIdx.x;
+    if (t >= ntiles) return;  // no tile (not counted among the consumers)
+    const int np = (G - gi + 1) / 2;  // producers p = gi + 2 j, j < np
+    int *spk = spre;                  // [3][np + 1] segment prefixes of chunks k (slot k % 3)
+    __shared__ int tot_s[kAccGroups][3], nr_s[kAccGroups], fin_s[kAccGroups][4];
+    int *tot = tot_s[gi];
+    if (A.debug & 1) {  // diagnostics: accumulators skip their work, release every chunk
+      for (int k = 0; k < A.nchunks; ++k) {
+        if (tid == 0) {
+          spin_until(A.bin_done + k, G);
+          __threadfence();
+          atomicAdd(A.acc_done + k, 1u);
+        }
+      }
+      return;
+    }
+    // warp-0 state (uniform across its lanes): read cursor and prepared chunks
+    int kc = 0, pc = 0, kprep = -1;
+    auto prepare = [&](int k) {  // warp 0: wait until chunk k is binned, prefix of my segments
+      if (tid == 0) spin_until(A.bin_done + k, G);
+      __syncwarp();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      const int *segc = A.segcnt + ((int64_t)k * ntiles + t) * G;
+      int *sp = spk + (k % 3) * (np + 1);
+      const int per = (np + 31) / 32, beg = tid * per, end = min(np, beg + per);
+      int sum = 0;
+      for (int j = beg; j < end; ++j) sum += __ldcg(segc + gi + 2 * j);
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (tid >= o) incl += v;
+      }
+      int run = incl - sum;
+      for (int j = beg; j < end; ++j) {
+        sp[j] = run;
+        run += __ldcg(segc + gi + 2 * j);
+      }
+      const int total_k = __shfl_sync(0xffffffffu, incl, 31);
+      if (tid == 31) sp[np] = incl;
+      if (tid == 0) tot[k % 3] = total_k;
+      __syncwarp();
+      kprep = k;
+    };
+    // warp 0: plan the next round (up to R records from the stream, at most 3 chunk pieces), arm the
+    // mbarrier and issue one bulk copy per (chunk, producer) piece; nr_s / fin_s get the round's
+    // size and the chunks it finishes
+    auto plan_issue = [&]() {
+      if (tid >= 32) return;
+      int nr = 0, nfin = 0, nrng = 0;
+      int rk[3], ra[3], rt[3], rd[3];
+      int fin[4];
+      while (nr < R && kc < A.nchunks && nrng < 3 && nfin < 4) {
+        if (kprep < kc) prepare(kc);
+        const int total_k = tot[kc % 3];
+        const int take = min(R - nr, total_k - pc);
+        if (take > 0) {
+          rk[nrng] = kc;
+          ra[nrng] = pc;
+          rt[nrng] = take;
+          rd[nrng] = nr;
+          ++nrng;
+          nr += take;
+          pc += take;
+        }
+        if (pc < total_k) break;  // round full
+        fin[nfin++] = kc;         // chunk kc exhausted by this round
+        ++kc;
+        pc = 0;
+      }
+      if (tid == 0) {
+        nr_s[gi] = nr;
+        for (int f = 0; f < 4; ++f) fin_s[gi][f] = f < nfin ? fin[f] : -1;
+        if (nr > 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect(bar, (uint32_t)(nr * 32));
+        }
+      }
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      for (int q = 0; q < nrng; ++q) {
+        const int k = rk[q], a = ra[q], a_end = a + rt[q];
+        const int *sp = spk + (k % 3) * (np + 1);
+        const double4 *base = A.rec[k % A.nbuf] + (int64_t)t * G * A.segcap;
+        for (int j = tid; j < np; j += 32) {
+          const int lo = max(a, sp[j]), hi = min(a_end, sp[j + 1]);
+          if (hi > lo) {
+            EFGP_DCHECK(rd[q] + (hi - a) <= R && hi - sp[j] <= A.segcap);
+            bulk_g2s(raw + rd[q] + (lo - a), base + (int64_t)(gi + 2 * j) * A.segcap + (lo - sp[j]),
+                     (uint32_t)((hi - lo) * 32), bar);
+          }
+        }
+      }
+    };
+    const int r0 = (t / A.nt2) * T1, c0 = (t % A.nt2) * T2;
+    plan_issue();
+    named_sync(bar_id, kGrpThreads);
+    int nr = nr_s[gi];
+    int fin[4];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) fin[f] = fin_s[gi][f];
+    // a chunk is released as soon as the round that read its last records has landed (before the
+    // next round is planned: a plan may wait for chunks whose buffers that release frees)
+    auto release = [&] {
+      if (tid == 0)
+        for (int f = 0; f < 4; ++f)
+          if (fin[f] >= 0) {
+            __threadfence();
+            atomicAdd(A.acc_done + fin[f], 1u);
+          }
+    };
+    while (nr > 0) {
+      round_body(nr, [&] { plan_issue(); }, false, false, r0, c0, release);
+      // (round_body ends with a group barrier: nr_s / fin_s of the next round are visible)
+      nr = nr_s[gi];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) fin[f] = fin_s[gi][f];
+      named_sync(bar_id, kGrpThreads);  // nr_s / fin_s reusable
+    }
+    release();  // chunks finished without records (empty tail)
+    round_body(0, [] {}, true, true, r0, c0, [] {});  // fold the windows, flush the tile accumulator
+  };
+
+  if (A.own) {
+    accumulate_static();
+  } else {
   for (int k = 0; k < A.nchunks; ++k) {
     const double4 *rec = A.rec[k % A.nbuf];
     const int *segc = A.segcnt + (int64_t)k * ntiles * G;
@@ -616,6 +977,7 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
           const int a0 = r.lo + done - sp[c];
           const int m = min(sp[c + 1] - sp[c] - a0, r.n - done);
           if (m > 0) {
+            EFGP_DCHECK(c < G && a0 >= 0 && a0 + m <= A.segcap && done + m <= R);
             bulk_g2s(raw + done, tb + (int64_t)c * A.segcap + a0, (uint32_t)(m * 32), bar);
             done += m;
           }
@@ -627,211 +989,9 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
       issue(cur);
       while (cur.tile >= 0) {
         const Rd nxt = next_round(cur);
-        const int r0 = (cur.tile / A.nt2) * T1, c0 = (cur.tile % A.nt2) * T2;
-        const int nr = cur.n;
-        cnt[tid] = 0;
         seg_prefix(nxt.tile);  // for issue(nxt) below
-        PH(0);
-        mbar_wait(bar, phase);
-        phase ^= 1u;
-        named_sync(bar_id, kGrpThreads);
-        PH(1);
-        // pass 1 (thread per record): rank within its start cell (key from the binner), kept in
-        // the record's key slot
-        for (int j0 = tid; j0 < nr; j0 += 4 * kGrpThreads) {  // 4 records at a time (latency)
-          int key[4], rnk[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int j = j0 + u * kGrpThreads;
-            key[u] = j < nr ? __double2loint(raw[j].w) : -1;
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) rnk[u] = key[u] >= 0 ? atomicAdd(&cnt[key[u]], 1) : 0;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int j = j0 + u * kGrpThreads;
-            if (j < nr) reinterpret_cast<int *>(&raw[j].w)[1] = rnk[u];
-          }
-        }
-        named_sync(bar_id, kGrpThreads);
-        const int mycnt = cnt[tid];
-        if (tid < 32) {  // cell offsets: warp 0 scans the 128 counts (4 per lane)
-          const int4 c4 = reinterpret_cast<const int4 *>(cnt)[tid];
-          const int sum = c4.x + c4.y + c4.z + c4.w;
-          int incl = sum;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (tid >= o) incl += v;
-          }
-          const int e = incl - sum;
-          reinterpret_cast<int4 *>(coff)[tid] = make_int4(e, e + c4.x, e + c4.x + c4.y, e + c4.x + c4.y + c4.z);
-        }
-        named_sync(bar_id, kGrpThreads);
-        PH(2);
-        const int myoff = coff[tid];
-        // pass 2 (thread per record): the record (FP64) or its fp32 weights at its sorted slot
-#pragma unroll 2
-        for (int j = tid; j < nr; j += kGrpThreads) {
-          const double4 rv = raw[j];
-          unsigned char *st = stage + (size_t)(coff[__double2loint(rv.w)] + __double2hiint(rv.w)) * SB;
-          if constexpr (MODE == kModeF64) {
-            // the reduced coordinates s1, s2 (es_reduce) are computed here, in the load-balanced
-            // thread-per-record pass, instead of in phase C (thread per cell, Poisson-imbalanced)
-            double *d = reinterpret_cast<double *>(st);
-            double s1, s2;
-            es_reduce<W>(grid_t(h, rv.x, n1), s1);
-            es_reduce<W>(grid_t(h, rv.y, n1), s2);
-            d[0] = s1;
-            d[1] = s2;
-            d[2] = rv.z;
-          } else {
-            constexpr int WP = (W + 1) / 2, WE = 2 * WP, NF = SB / 4;
-            float2 w1[WP], w2[WP];
-            es_weights_pairs<W>(grid_t(h, rv.x, n1), PF, w1);
-            es_weights_pairs<W>(grid_t(h, rv.y, n1), PF, w2);
-            float f[NF];
-#pragma unroll
-            for (int q = 0; q < WP; ++q) {
-              f[2 * q] = w1[q].x;
-              f[2 * q + 1] = w1[q].y;
-              f[WE + 2 * q] = w2[q].x;
-              f[WE + 2 * q + 1] = w2[q].y;
-            }
-#pragma unroll
-            for (int i = 2 * WE; i < NF; ++i) f[i] = 0.f;
-            if constexpr (MODE == kModeA32) {
-              f[StageRec<W, MODE>::kYSlot] = (float)rv.z;
-            } else {
-              f[2 * WE] = __int_as_float(__double2loint(rv.z));
-              f[2 * WE + 1] = __int_as_float(__double2hiint(rv.z));
-            }
-            float4 *q4 = reinterpret_cast<float4 *>(st);
-#pragma unroll
-            for (int i = 0; i < NF / 4; ++i) q4[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
-          }
-        }
-        named_sync(bar_id, kGrpThreads);
-        PH(3);
-        issue(nxt);  // raw is free: the next round's copies land during phase C
-        // phase C (thread per start cell): register accumulation of its records
-        if (mycnt > 0) {
-          const unsigned char *sp = stage + (size_t)myoff * SB;
-          if constexpr (MODE == kModeF64) {
-#pragma unroll 2
-            for (int q = 0; q < mycnt; ++q, sp += SB) {
-              const double *d = reinterpret_cast<const double *>(sp);
-              const double yv = d[2];
-              double w1[W], w2[W];
-              es_weights_s<W>(d[0], P, w1);
-              es_weights_s<W>(d[1], P, w2);
-#pragma unroll
-              for (int a = 0; a < W; ++a) {
-                const double ca = w1[a], cy = yv * w1[a];
-#pragma unroll
-                for (int b2 = 0; b2 < W; ++b2) {
-                  a1[a][b2] = fma(ca, w2[b2], a1[a][b2]);
-                  ay[a][b2] = fma(cy, w2[b2], ay[a][b2]);
-                }
-              }
-            }
-          } else if constexpr (MODE == kModeW32) {
-            constexpr int WE = StageRec<W, MODE>::WE, NF = SB / 4;
-#pragma unroll 2
-            for (int q = 0; q < mycnt; ++q, sp += SB) {
-              float f[NF];
-              load_floats<SB>(sp, f);
-              const double yv = __hiloint2double(__float_as_int(f[2 * WE + 1]), __float_as_int(f[2 * WE]));
-              double w2[W];
-#pragma unroll
-              for (int b2 = 0; b2 < W; ++b2) w2[b2] = (double)f[WE + b2];
-#pragma unroll
-              for (int a = 0; a < W; ++a) {
-                const double ca = (double)f[a], cy = yv * ca;
-#pragma unroll
-                for (int b2 = 0; b2 < W; ++b2) {
-                  a1[a][b2] = fma(ca, w2[b2], a1[a][b2]);
-                  ay[a][b2] = fma(cy, w2[b2], ay[a][b2]);
-                }
-              }
-            }
-          } else {
-            // MIXED: fp32 pairs along b: (acc[a][2p], acc[a][2p+1]) += w1[a] * (w2[2p], w2[2p+1])
-            constexpr int WP = (W + 1) / 2, WE = 2 * WP, NF = SB / 4;
-#pragma unroll 2
-            for (int q = 0; q < mycnt; ++q, sp += SB) {
-              float f[NF];
-              load_floats<SB>(sp, f);
-              const float yf = f[StageRec<W, MODE>::kYSlot];
-#pragma unroll
-              for (int a = 0; a < W; ++a) {
-                const float c1 = f[a], cy = yf * f[a];
-#pragma unroll
-                for (int pp = 0; pp < WP; ++pp) {
-                  const float2 w2p = make_float2(f[WE + 2 * pp], f[WE + 2 * pp + 1]);
-                  p1[a][pp] = __ffma2_rn(w2p, make_float2(c1, c1), p1[a][pp]);
-                  py[a][pp] = __ffma2_rn(w2p, make_float2(cy, cy), py[a][pp]);
-                }
-              }
-            }
-          }
-        }
-        // MIXED: the fp32 windows of one tile segment sum at most 64 points per start cell; past that
-        // (only for very concentrated data) they are folded into the fp64 tile accumulator early
-        PH(4);
-        bool fold_now = nxt.tile != cur.tile;
-        if constexpr (MODE == kModeA32) {
-          pend += mycnt;
-          fold_now = named_sync_or(bar_id, kGrpThreads, pend >= 64) || fold_now;
-        } else {
-          named_sync(bar_id, kGrpThreads);  // stage and cnt free
-        }
-        if (fold_now) {
-          // add the windows into the fp64 tile accumulator in W^2 conflict-free steps
-#pragma unroll
-          for (int a = 0; a < W; ++a) {
-#pragma unroll
-            for (int b2 = 0; b2 < W; ++b2) {
-              if (own) {
-                const int idx = (my_r + a) * A2 + (my_c + b2);
-                if constexpr (MODE == kModeA32) {
-                  const float2 v1 = p1[a][b2 / 2], vy = py[a][b2 / 2];
-                  tacc[idx] += (double)((b2 & 1) ? v1.y : v1.x);
-                  tacc[A1 * A2 + idx] += (double)((b2 & 1) ? vy.y : vy.x);
-                } else {
-                  tacc[idx] += a1[a][b2];
-                  tacc[A1 * A2 + idx] += ay[a][b2];
-                }
-              }
-              named_sync(bar_id, kGrpThreads);
-            }
-          }
-          if constexpr (MODE == kModeA32) {
-#pragma unroll
-            for (int a = 0; a < W; ++a)
-#pragma unroll
-              for (int pp = 0; pp < (W + 1) / 2; ++pp) p1[a][pp] = py[a][pp] = make_float2(0.f, 0.f);
-            pend = 0;
-          } else {
-#pragma unroll
-            for (int a = 0; a < W; ++a)
-#pragma unroll
-              for (int b2 = 0; b2 < W; ++b2) a1[a][b2] = ay[a][b2] = 0.0;
-          }
-        }
-        PH(5);
-        // end of a tile segment: one RED per cell of the tile accumulator, which is re-zeroed
-        if (nxt.tile != cur.tile) {
-          for (int i = tid; i < A1 * A2; i += kGrpThreads) {
-            const double v1 = tacc[i], vy = tacc[A1 * A2 + i];
-            const int r = wrap_s(s_lo + r0 + i / A2, n1), c = wrap_s(s_lo + c0 + i % A2, n1);
-            const int64_t gidx = (int64_t)r * n1 + c;
-            if (v1 != 0.0) atomicAdd(A.g1 + gidx, v1);
-            if (vy != 0.0) atomicAdd(A.gy + gidx, vy);
-            tacc[i] = tacc[A1 * A2 + i] = 0.0;
-          }
-          named_sync(bar_id, kGrpThreads);
-        }
+        round_body(cur.n, [&] { issue(nxt); }, nxt.tile != cur.tile, nxt.tile != cur.tile,
+                   (cur.tile / A.nt2) * T1, (cur.tile % A.nt2) * T2, [] {});
         PH(6);
         cur = nxt;
       }
@@ -845,6 +1005,7 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
       if (gi == 0) stamp(A.trace, k, 3);
     }
   }
+  }  // share mode
   if (A.trace && tid == 0) {
     unsigned long long *o = A.trace + (size_t)A.nchunks * G * 4 + ((size_t)blockIdx.x * kAccGroups + gi) * 8;
     for (int i = 0; i < 7; ++i) o[i] = (unsigned long long)ph_acc[i];
@@ -858,10 +1019,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_spread_fused(const FusedAr
   const int tid = threadIdx.x;
   const size_t acc_bytes = 2 * AccSmem<W, MODE>::bytes(A.R, A.ntiles, gridDim.x, A.T1, A.T2);
   if (tid >= kAccThreads) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kBinRegs) : "memory");
     binner_role<W>(A, fsm + (acc_bytes + 15) / 16 * 16, tid - kAccThreads);
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kAccRegs) : "memory");
     accumulator_role<W, MODE>(A, fsm, tid, P, PF);
   }
 }
@@ -914,11 +1075,16 @@ bool sorted_geometry(Params &p, int num_sms) {
   p.ntiles = p.nt1 * p.nt2;
   // 32M points x 3 list buffers: fewer hand-offs, binning two chunks ahead (c5 N = 4e8: 3.76e10 ->
   // 3.86e10 points/s against 16M x 2; records are allocated per call for min(N, chunk) points)
-  p.chunk = int64_t(1) << 25;
+  // static ownership: opt-in (EFGP_SORTED_OWN=1); measured slower than the equal-share mode on c5
+  // (25.0 vs 24.0 ms at N = 1e9 with 3M-point chunks; per-chunk coupling of all CTAs dominates with
+  // the small chunks that keep the lists in L2)
+  p.sorted_own = p.ntiles <= num_sms && std::getenv("EFGP_SORTED_OWN") && std::atoi(std::getenv("EFGP_SORTED_OWN"));
+  // the equal-share mode amortises its per-chunk tile switches over large chunks
+  p.chunk = p.sorted_own ? int64_t(3) << 20 : int64_t(1) << 25;
   if (const char *e = std::getenv("EFGP_SORTED_CHUNK"))
     p.chunk = std::max<int64_t>(kWBatch, std::atoll(e) / kWBatch * kWBatch);
   p.nbuf = 3;
-  if (const char *e = std::getenv("EFGP_SORTED_NBUF")) p.nbuf = std::max(2, std::min(3, std::atoi(e)));
+  if (const char *e = std::getenv("EFGP_SORTED_NBUF")) p.nbuf = std::max(2, std::min(kMaxNbuf, std::atoi(e)));
   p.tiles_grid = num_sms;
   if (const char *e = std::getenv("EFGP_SORTED_GRID")) p.tiles_grid = std::max(1, std::atoi(e));
   // capacity of a (tile, binner CTA) segment: 2x its uniform share + slack; overflow spills to
@@ -985,7 +1151,7 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
   const int segcap = sorted_segcap(P, chunk);
   const size_t rec_need = (size_t)P.ntiles * P.tiles_grid * segcap;
   if (rec_need > pl->rec_cap) {
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < kMaxNbuf; ++k) {
       if (pl->rec[k]) cudaFree(pl->rec[k]);
       pl->rec[k] = nullptr;
     }
@@ -997,6 +1163,8 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
   A.nchunks = (int)((N + chunk - 1) / chunk);
   A.nbuf = P.nbuf;
   A.debug = std::getenv("EFGP_SORTED_DEBUG") ? std::atoi(std::getenv("EFGP_SORTED_DEBUG")) : 0;
+  A.own = P.sorted_own && P.ntiles <= P.tiles_grid;
+  A.nconsumers = A.own ? 2u * (unsigned)P.ntiles : 2u * (unsigned)P.tiles_grid;
   A.h = P.h;
   A.n1 = (int)P.n1;
   A.s_lo = P.s_lo;
@@ -1007,7 +1175,7 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
   A.ntiles = P.ntiles;
   A.segcap = segcap;
   A.R = P.round;
-  for (int b = 0; b < 3; ++b) A.rec[b] = pl->rec[b];
+  for (int b = 0; b < kMaxNbuf; ++b) A.rec[b] = pl->rec[b];
   // per-chunk segment and tile lengths and the two handshake counters, zeroed for this call
   const int G = P.tiles_grid;
   const size_t need = (size_t)A.nchunks * ((size_t)P.ntiles * G + P.ntiles + 2);

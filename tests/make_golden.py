@@ -148,9 +148,11 @@ def main():
         res[mode] = (beta, iters, np.asarray(hist), true_rel, cap)
 
     # Reading G10b: the oracle's own first crossings when v and F^*y carry an error of the size the
-    # NUFFT contract allows (relative l2 = nufft_tol = eps/10; Hermitian-symmetric white
-    # noise, seeds 1..K).  The GPU's count passes if it lies within these counts +-2 (or in G10's
-    # window): the crossing of a plateaued residual moves by more than +-2 under any such error.
+    # NUFFT contract allows (relative l2 = nufft_tol = eps/10), seeds 1..K.  v is perturbed
+    # by 64 phantom points of equal positive mass (eq 88's sum over extra points, so T stays positive
+    # semidefinite: white noise of that size makes the c2 system indefinite), F^*y by Hermitian white
+    # noise.  The GPU's count passes if it lies within these counts +-2 (or in G10's window): the
+    # crossing of a plateaued residual moves by more than +-2 under any such error.
     ntol = cfg.eps / 10
     perturbed = {"parity": [], "production": []}
 
@@ -159,14 +161,15 @@ def main():
 
     for k in range(1, args.perturb + 1):
         rng = np.random.default_rng(k)
-        dv = herm(rng.normal(size=v.shape) + 1j * rng.normal(size=v.shape))
+        dv = O.toeplitz_vector(rng.uniform(size=(64, cfg.d)), h, m)
         db = herm(rng.normal(size=b.shape) + 1j * rng.normal(size=b.shape))
         vk = v + dv * (ntol * np.linalg.norm(v) / np.linalg.norm(dv))
         bk = b + db * (ntol * np.linalg.norm(b) / np.linalg.norm(db))
         Tk = None if use_fft else O.toeplitz_matrix(vk, m)
         Ak = lambda p: O.system_apply(vk, D, cfg.sigma ** 2, p, Tk, fft=use_fft)
         for mode, tol in (("parity", cfg.eps / 1000), ("production", cfg.eps)):
-            _, it_k, _ = O.cg(Ak, bk, tol, O.default_max_iter(N, cfg.sigma, tol))
+            cap = min(O.default_max_iter(N, cfg.sigma, tol), 3 * res[mode][1] + 50)
+            _, it_k, _ = O.cg(Ak, bk, tol, cap)
             perturbed[mode].append(int(it_k))
         log(f"perturbed CG {k}: parity {perturbed['parity'][-1]} production {perturbed['production'][-1]}")
         del Tk
@@ -200,7 +203,8 @@ def main():
             "iters_parity": int(res["parity"][1]), "iters_production": int(res["production"][1]),
             "cap_parity": int(res["parity"][4]), "cap_production": int(res["production"][4]),
             "true_rel_resid_parity": res["parity"][3], "true_rel_resid_production": res["production"][3],
-            "iters_perturbed": perturbed, "perturbation": "relative l2 = eps/10 on v and F^*y (reading G10b)",
+            "iters_perturbed": perturbed,
+            "perturbation": "relative l2 = eps/10: v + 64 phantom points (PSD), F^*y + white noise (reading G10b)",
             "oracle_sha256": oracle_hash(), "data_sha256": data_hash(),
             "oracle_seconds": t, "host": {"cores": args.workers, "model": host_model()},
             "written": time.strftime("%Y-%m-%dT%H:%M:%S")}
