@@ -88,7 +88,7 @@ efgp_status build(efgp_plan *pl) {
   EFGP_TRY(dalloc(pl, &pl->Zbox, box));
   EFGP_TRY(dalloc(pl, &pl->Yr, Ld));
   EFGP_TRY(dalloc(pl, &pl->vhat, Ld));
-  for (double2 **v : {&pl->b, &pl->x, &pl->r, &pl->p, &pl->Ap}) {
+  for (double2 **v : {&pl->b, &pl->x, &pl->r, &pl->p, &pl->Ap, &pl->p2}) {
     EFGP_TRY(dalloc(pl, v, P.Mh));
     EFGP_CUDA(cudaMemset(*v, 0, sizeof(double2) * P.Mh));
   }
@@ -620,7 +620,7 @@ void efgp_destroy(efgp_handle pl) {
                   pl->scal, pl->hist, pl->dflags, pl->T2box, pl->t2grid, pl->stage[0], pl->stage[1],
                   pl->trace,
                   pl->sync_buf, pl->het_box, pl->het_grid, pl->pc_Q, pl->pc_F0, pl->pc_F1, pl->pc_work, pl->z,
-                  pl->pc_lam, pl->pc_info, pl->comm_buf, pl->vfull, pl->pc_diag};
+                  pl->pc_lam, pl->pc_info, pl->comm_buf, pl->vfull, pl->pc_diag, pl->toep_part, pl->toep_cnt, pl->p2};
   for (void *b : bufs)
     if (b) cudaFree(b);
   for (void *b : pl->rec)

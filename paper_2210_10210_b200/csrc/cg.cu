@@ -28,6 +28,7 @@ struct CGState {
   int done;         // 1: converged, 2: hit max_iter
   int pad_;
   double rz;        // PCG: (r, z) of the current residual (NEXT-4)
+  double rrs[2];    // fused direct CG: ||r_j||^2 in slot j & 1 (written by k_cg_toep2f, read one iteration later)
 };
 
 constexpr int kCGThreads = 256;
@@ -82,6 +83,7 @@ __global__ void k_cg_init2(CGState *st, const double *__restrict__ part, int nbl
   if (threadIdx.x == 0) {
     st->rr = rr;
     st->rr_old = rr;
+    st->rrs[0] = rr;
     st->bnorm = sqrt(rr);
     st->iter = 0;
     st->done = (rr == 0.0) ? 1 : 0;
@@ -329,6 +331,288 @@ __global__ void __launch_bounds__(kToepThreads) k_cg_toep2(const double2 *__rest
   if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 
+// The same product split over the k1 rows so that all SMs work (k_cg_toep2 runs 2m+1 = 51 CTAs on
+// 148 SMs, FP64 pipe ~22 %, r01 ncu): CTA (row j1, split s) sums k1 in its range, every thread 4
+// consecutive outputs j2 over one k1 row and a chunk of the k2 range (sliding window as above); the
+// CTA's partial row goes to part[row][s]; the last CTA of a row (counter) adds the kToepSplits partials
+// in fixed order (deterministic), applies D and sigma^2 and writes the row's <p, Ap> partial.
+constexpr int kToepSplits = kToepSplitsHost, kToepSThreads = 256;
+__host__ __device__ constexpr int toeps_rows_per_split(int n) { return (n + kToepSplits - 1) / kToepSplits; }
+
+__global__ void __launch_bounds__(kToepSThreads) k_cg_toep2s(const double2 *__restrict__ vfull,
+                                                             const double2 *__restrict__ p,
+                                                             const double *__restrict__ Dh, double2 *__restrict__ Ap,
+                                                             int m, const CGState *st, double2 *__restrict__ tpart,
+                                                             unsigned *__restrict__ tcnt, double *__restrict__ part) {
+  extern __shared__ double2 tsm[];
+  __shared__ double sh[40];
+  __shared__ bool last_s;
+  pdl_trigger();
+  if (st->done) return;
+  const int n = 2 * m + 1, nv = 4 * m + 1, nout = m + 1, ngrp = (nout + 3) / 4;
+  const int row = (int)blockIdx.x % n, spl = (int)blockIdx.x / n, j1 = row - m;
+  const int nk = toeps_rows_per_split(n), k1a = spl * nk, k1b = min(n, k1a + nk), nkr = k1b - k1a;
+  const int nc = kToepSThreads / (ngrp * nk), clen = (n + nc - 1) / nc;  // k2 chunks
+  double2 *u = tsm;              // nk x n: u[(k1 - k1a) n + (k2 + m)]
+  double2 *vr = u + nk * n;      // nk x nv: v_{j1 - k1, .}
+  double2 *red = vr + nk * nv;   // [nk * nc][nout] partial sums
+  for (int idx = threadIdx.x; idx < nkr * n; idx += blockDim.x) {
+    int k1 = k1a + idx / n - m, k2 = idx % n - m;
+    const bool neg = k2 < 0 || (k2 == 0 && k1 < 0);  // canonical half (exactly Hermitian, see above)
+    if (neg) {
+      k1 = -k1;
+      k2 = -k2;
+    }
+    const int64_t q = (int64_t)(k1 + m) * (m + 1) + k2;
+    const double2 pp = p[q];
+    const double dq = Dh[q];
+    u[idx] = make_double2(dq * pp.x, neg ? -dq * pp.y : dq * pp.y);
+  }
+  for (int idx = threadIdx.x; idx < nkr * nv; idx += blockDim.x) {
+    const int k1 = k1a + idx / nv - m, sc = idx % nv;
+    vr[idx] = vfull[(int64_t)(j1 - k1 + 2 * m) * nv + sc];
+  }
+  for (int idx = threadIdx.x; idx < nk * nc * nout; idx += blockDim.x) red[idx] = make_double2(0.0, 0.0);
+  __syncthreads();
+  const int t = threadIdx.x, g4 = t % ngrp, kk = (t / ngrp) % nk, c = t / (ngrp * nk), j2b = 4 * g4;
+  if (c < nc && kk < nkr) {
+    const int c2a = c * clen, c2b = min(n, c2a + clen);
+    double re[4] = {0.0, 0.0, 0.0, 0.0}, im[4] = {0.0, 0.0, 0.0, 0.0};
+    const double2 *ur = u + kk * n, *vrow = vr + kk * nv;
+    double2 w[4];  // v_{j1-k1, j2b+o - k2} at k2 = c2a - m: index j2b + o - c2a + 3m
+#pragma unroll
+    for (int o = 0; o < 4; ++o) w[o] = (j2b + o <= m && c2a < c2b) ? vrow[j2b + o - c2a + 3 * m] : make_double2(0.0, 0.0);
+    for (int c2 = c2a; c2 < c2b; ++c2) {
+      const double2 b = ur[c2];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        re[o] = fma(w[o].x, b.x, fma(-w[o].y, b.y, re[o]));
+        im[o] = fma(w[o].x, b.y, fma(w[o].y, b.x, im[o]));
+      }
+#pragma unroll
+      for (int o = 3; o > 0; --o) w[o] = w[o - 1];
+      w[0] = (c2 + 1 < c2b) ? vrow[j2b - (c2 + 1) + 3 * m] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int o = 0; o < 4; ++o)
+      if (j2b + o <= m) red[(kk * nc + c) * nout + j2b + o] = make_double2(re[o], im[o]);
+  }
+  __syncthreads();
+  if (t < nout) {
+    double2 o = make_double2(0.0, 0.0);
+    for (int k = 0; k < nk * nc; ++k) {
+      o.x += red[k * nout + t].x;
+      o.y += red[k * nout + t].y;
+    }
+    tpart[((int64_t)row * kToepSplits + spl) * nout + t] = o;
+  }
+  __threadfence();
+  __syncthreads();
+  if (t == 0) last_s = atomicAdd(tcnt + row, 1u) == kToepSplits - 1;
+  __syncthreads();
+  if (!last_s) return;
+  __threadfence();  // the other splits' partials of this row are visible
+  double acc = 0.0;
+  if (t < nout && !(t == 0 && j1 < 0)) {  // (j1 < 0, 0) is written by row -j1 as the conjugate
+    double2 o = make_double2(0.0, 0.0);
+    for (int k = 0; k < kToepSplits; ++k) {
+      const double2 v = __ldcg(tpart + ((int64_t)row * kToepSplits + k) * nout + t);
+      o.x += v.x;
+      o.y += v.y;
+    }
+    const int64_t q = (int64_t)(j1 + m) * (m + 1) + t;
+    const double2 pp = p[q];
+    const double dq = Dh[q], s2 = st->sigma2;
+    double2 a = make_double2(dq * o.x + s2 * pp.x, dq * o.y + s2 * pp.y);
+    if (t == 0 && j1 == 0) a.y = s2 * pp.y;  // j = 0: (T u)_0 is real
+    Ap[q] = a;
+    acc = (t ? 2.0 : 1.0) * (pp.x * a.x + pp.y * a.y);
+    if (t == 0 && j1 > 0) {  // the mirrored entry (-j1, 0) = conj, with the canonical p
+      Ap[(int64_t)(m - j1) * (m + 1)] = make_double2(a.x, -a.y);
+      acc *= 2.0;
+    }
+  }
+  acc = block_sum(acc, sh);
+  if (t == 0) {
+    part[row] = acc;
+    tcnt[row] = 0;  // for the next product
+  }
+}
+
+static size_t toep2s_smem(int m) {
+  const int n = 2 * m + 1, nv = 4 * m + 1, nout = m + 1, ngrp = (nout + 3) / 4, nk = toeps_rows_per_split(n);
+  const int nc = kToepSThreads / (ngrp * nk);
+  return sizeof(double2) * ((size_t)nk * n + (size_t)nk * nv + (size_t)nk * nc * nout);
+}
+static bool toep_split() {
+  const char *e = getenv("EFGP_TOEP_SPLIT");
+  return !(e && e[0] == '0');
+}
+
+
+// ---- fused direct CG (2D, small m): two kernels per iteration instead of three -----------------
+// Iteration j (slot q = j & 1; the graph captures an even number of iterations, so the slot of a
+// captured iteration is fixed):
+//   k_cg_toep2f: rr_j = ||r_j||^2 from the previous k_cg_xr2's partials (redundantly in every CTA, same
+//                order), stop test (hist, done), beta = rr_j / rr_{j-1}, p_j = r_j + beta p_{j-1} formed on
+//                the fly from (r, p slot 1-q) and written to p slot q, then A p_j as k_cg_toep2s;
+//   k_cg_xr2   : alpha = rr_j / <p_j, A p_j>, x += alpha p_j, r -= alpha A p_j, ||r_{j+1}||^2 partials.
+// Same recurrences and stopping rule as k_cg_xr + k_cg_p (reading G6); one launch (~4-5 us of
+// dependency latency) fewer per iteration.
+__global__ void __launch_bounds__(kToepSThreads) k_cg_toep2f(
+    const double2 *__restrict__ vfull, const double2 *__restrict__ r, const double2 *__restrict__ p_old,
+    double2 *__restrict__ p_new, const double *__restrict__ Dh, double2 *__restrict__ Ap, int m, CGState *st,
+    double2 *__restrict__ tpart, unsigned *__restrict__ tcnt, double *__restrict__ part_pAp,
+    const double *__restrict__ part_rr, int nblk, double *__restrict__ hist, int q) {
+  extern __shared__ double2 tsm[];
+  __shared__ double sh[40];
+  __shared__ bool last_s;
+  pdl_wait();
+  pdl_trigger();
+  if (st->done) return;
+  const long long it = st->iter;
+  double beta = 0.0;
+  if (it > 0) {
+    const double rr = reduce_partials(part_rr, nblk, sh);
+    beta = rr / st->rrs[q ^ 1];
+    const double rel = sqrt(rr) / st->bnorm;
+    const int stop = rel <= st->tol ? 1 : (it >= st->max_iter ? 2 : 0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->rrs[q] = rr;
+      st->rr = rr;
+      hist[it] = rel;
+      if (stop) st->done = stop;
+    }
+    if (stop) return;
+  }
+  const int n = 2 * m + 1, nv = 4 * m + 1, nout = m + 1, ngrp = (nout + 3) / 4;
+  const int row = (int)blockIdx.x % n, spl = (int)blockIdx.x / n, j1 = row - m;
+  const int nk = toeps_rows_per_split(n), k1a = spl * nk, k1b = min(n, k1a + nk), nkr = k1b - k1a;
+  const int nc = kToepSThreads / (ngrp * nk), clen = (n + nc - 1) / nc;
+  double2 *u = tsm, *vr = u + nk * n, *red = vr + nk * nv;
+  for (int idx = threadIdx.x; idx < nkr * n; idx += blockDim.x) {
+    int k1 = k1a + idx / n - m, k2 = idx % n - m;
+    const bool neg = k2 < 0 || (k2 == 0 && k1 < 0);
+    if (neg) {
+      k1 = -k1;
+      k2 = -k2;
+    }
+    const int64_t qq = (int64_t)(k1 + m) * (m + 1) + k2;
+    const double2 rq = r[qq], po = p_old[qq];
+    const double2 pp = make_double2(rq.x + beta * po.x, rq.y + beta * po.y);
+    const double dq = Dh[qq];
+    u[idx] = make_double2(dq * pp.x, neg ? -dq * pp.y : dq * pp.y);
+  }
+  if (row == 0)  // p_j of this split's stored rows (every stored entry exactly once over the splits)
+    for (int idx = threadIdx.x; idx < nkr * (m + 1); idx += blockDim.x) {
+      const int64_t qq = (int64_t)k1a * (m + 1) + idx;
+      const double2 rq = r[qq], po = p_old[qq];
+      p_new[qq] = make_double2(rq.x + beta * po.x, rq.y + beta * po.y);
+    }
+  for (int idx = threadIdx.x; idx < nkr * nv; idx += blockDim.x) {
+    const int k1 = k1a + idx / nv - m, sc = idx % nv;
+    vr[idx] = vfull[(int64_t)(j1 - k1 + 2 * m) * nv + sc];
+  }
+  for (int idx = threadIdx.x; idx < nk * nc * nout; idx += blockDim.x) red[idx] = make_double2(0.0, 0.0);
+  __syncthreads();
+  const int t = threadIdx.x, g4 = t % ngrp, kk = (t / ngrp) % nk, c = t / (ngrp * nk), j2b = 4 * g4;
+  if (c < nc && kk < nkr) {
+    const int c2a = c * clen, c2b = min(n, c2a + clen);
+    double re[4] = {0.0, 0.0, 0.0, 0.0}, im[4] = {0.0, 0.0, 0.0, 0.0};
+    const double2 *ur = u + kk * n, *vrow = vr + kk * nv;
+    double2 w[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) w[o] = (j2b + o <= m && c2a < c2b) ? vrow[j2b + o - c2a + 3 * m] : make_double2(0.0, 0.0);
+    for (int c2 = c2a; c2 < c2b; ++c2) {
+      const double2 b = ur[c2];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        re[o] = fma(w[o].x, b.x, fma(-w[o].y, b.y, re[o]));
+        im[o] = fma(w[o].x, b.y, fma(w[o].y, b.x, im[o]));
+      }
+#pragma unroll
+      for (int o = 3; o > 0; --o) w[o] = w[o - 1];
+      w[0] = (c2 + 1 < c2b) ? vrow[j2b - (c2 + 1) + 3 * m] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int o = 0; o < 4; ++o)
+      if (j2b + o <= m) red[(kk * nc + c) * nout + j2b + o] = make_double2(re[o], im[o]);
+  }
+  __syncthreads();
+  if (t < nout) {
+    double2 o = make_double2(0.0, 0.0);
+    for (int k = 0; k < nk * nc; ++k) {
+      o.x += red[k * nout + t].x;
+      o.y += red[k * nout + t].y;
+    }
+    tpart[((int64_t)row * kToepSplits + spl) * nout + t] = o;
+  }
+  __threadfence();
+  __syncthreads();
+  if (t == 0) last_s = atomicAdd(tcnt + row, 1u) == kToepSplits - 1;
+  __syncthreads();
+  if (!last_s) return;
+  __threadfence();
+  double acc = 0.0;
+  if (t < nout && !(t == 0 && j1 < 0)) {
+    double2 o = make_double2(0.0, 0.0);
+    for (int k = 0; k < kToepSplits; ++k) {
+      const double2 v = __ldcg(tpart + ((int64_t)row * kToepSplits + k) * nout + t);
+      o.x += v.x;
+      o.y += v.y;
+    }
+    const int64_t qq = (int64_t)(j1 + m) * (m + 1) + t;
+    const double2 rq = r[qq], po = p_old[qq];
+    const double2 pp = make_double2(rq.x + beta * po.x, rq.y + beta * po.y);
+    const double dq = Dh[qq], s2 = st->sigma2;
+    double2 a = make_double2(dq * o.x + s2 * pp.x, dq * o.y + s2 * pp.y);
+    if (t == 0 && j1 == 0) a.y = s2 * pp.y;
+    Ap[qq] = a;
+    acc = (t ? 2.0 : 1.0) * (pp.x * a.x + pp.y * a.y);
+    if (t == 0 && j1 > 0) {
+      Ap[(int64_t)(m - j1) * (m + 1)] = make_double2(a.x, -a.y);
+      acc *= 2.0;
+    }
+  }
+  acc = block_sum(acc, sh);
+  if (t == 0) {
+    part_pAp[row] = acc;
+    tcnt[row] = 0;
+  }
+}
+
+__global__ void k_cg_xr2(double2 *__restrict__ x, double2 *__restrict__ r, const double2 *__restrict__ p,
+                         const double2 *__restrict__ Ap, int64_t Mh, int m, CGState *st,
+                         const double *__restrict__ part_pAp, int nrow, double *__restrict__ part_rr, int q) {
+  __shared__ double sh[40];
+  pdl_wait();
+  pdl_trigger();
+  if (st->done) return;
+  const double alpha = st->rrs[q] / reduce_partials(part_pAp, nrow, sh);
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Mh; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 pp = p[i], a = Ap[i];
+    double2 xx = x[i], rq = r[i];
+    xx.x += alpha * pp.x;
+    xx.y += alpha * pp.y;
+    rq.x -= alpha * a.x;
+    rq.y -= alpha * a.y;
+    x[i] = xx;
+    r[i] = rq;
+    acc += ((i % (m + 1)) ? 2.0 : 1.0) * (rq.x * rq.x + rq.y * rq.y);
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) {
+    part_rr[blockIdx.x] = acc;
+    if (blockIdx.x == 0) st->iter = st->iter + 1;
+  }
+}
+
+static bool cg_fused() {
+  const char *e = getenv("EFGP_CG_FUSED");
+  return !(e && e[0] == '0');
+}
+
 static size_t toep2_smem(int m) {
   const int n = 2 * m + 1, nv = 4 * m + 1;
   const int nout = m + 1, slices = kToepThreads / ((nout + 3) / 4);
@@ -360,14 +644,29 @@ static unsigned nblocks(int64_t n, int sms) {
 
 template <int D>
 static efgp_status enqueue_iteration(efgp_plan *pl, cudaStream_t s, CGState *st, int64_t box, int64_t Ld,
-                                     unsigned nb, unsigned nbox) {
+                                     unsigned nb, unsigned nbox, int slot) {
   const Params &P = pl->P;
   double *part_pAp = pl->partials, *part_rr = pl->partials + pl->cg_blocks;
   const bool direct = D == 2 && toeplitz_direct(P);
+  if (direct && pl->p2 && pl->toep_part && cg_fused() && toep_split()) {  // fused direct CG: two kernels per iteration
+    const int nrow = (int)(2 * P.m + 1);
+    double2 *pq = slot ? pl->p2 : pl->p, *pold = slot ? pl->p : pl->p2;
+    EFGP_CUDA(launch_pdl_smem(k_cg_toep2f, nrow * kToepSplits, kToepSThreads, toep2s_smem((int)P.m), s, pl->vfull,
+                              (const double2 *)pl->r, (const double2 *)pold, pq, (const double *)pl->D_half, pl->Ap,
+                              (int)P.m, st, pl->toep_part, pl->toep_cnt, part_pAp, (const double *)part_rr, (int)nb,
+                              pl->hist, slot));
+    EFGP_CUDA(launch_pdl(k_cg_xr2, nb, kCGThreads, s, pl->x, pl->r, (const double2 *)pq, (const double2 *)pl->Ap, P.Mh,
+                         (int)P.m, st, (const double *)part_pAp, nrow, part_rr, slot));
+    return EFGP_OK;
+  }
   if (direct) {  // the partials come from 2m+1 CTAs
     const int nrow = (int)(2 * P.m + 1);
-    k_cg_toep2<<<nrow, kToepThreads, toep2_smem((int)P.m), s>>>(pl->vfull, pl->p, pl->D_half, pl->Ap, (int)P.m, st,
-                                                                part_pAp);
+    if (toep_split() && pl->toep_part)
+      k_cg_toep2s<<<nrow * kToepSplits, kToepSThreads, toep2s_smem((int)P.m), s>>>(
+          pl->vfull, pl->p, pl->D_half, pl->Ap, (int)P.m, st, pl->toep_part, pl->toep_cnt, part_pAp);
+    else
+      k_cg_toep2<<<nrow, kToepThreads, toep2_smem((int)P.m), s>>>(pl->vfull, pl->p, pl->D_half, pl->Ap, (int)P.m, st,
+                                                                  part_pAp);
     EFGP_CUDA(launch_pdl(k_cg_xr, nb, kCGThreads, s, pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp,
                          part_rr, nrow, (const double *)nullptr));
   } else {
@@ -425,14 +724,16 @@ static efgp_status cg_solve_d(efgp_plan *pl, int64_t N_total) {
   if (D == 2 && toeplitz_direct(P))
     EFGP_CUDA(cudaFuncSetAttribute(k_cg_toep2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)toep2_smem((int)P.m)));
 
-  const int G = P.graph_iters;
+  int G = P.graph_iters;
+  const bool fused = D == 2 && toeplitz_direct(P) && pl->p2 && pl->toep_part && cg_fused() && toep_split();
+  if (fused) G += G & 1;  // the fused iterations alternate two p slots: an even count per graph
   if (!pl->cg_exec || pl->cg_exec_iters != G) {
     if (pl->cg_exec) cudaGraphExecDestroy(pl->cg_exec);
     pl->cg_exec = nullptr;
     cudaGraph_t graph;
     EFGP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     for (int it = 0; it < G; ++it) {
-      efgp_status e = enqueue_iteration<D>(pl, s, st, box, Ld, nb, nbox);
+      efgp_status e = enqueue_iteration<D>(pl, s, st, box, Ld, nb, nbox, it & 1);
       if (e != EFGP_OK) {
         cudaStreamEndCapture(s, &graph);
         return e;
@@ -602,8 +903,12 @@ static efgp_status enqueue_pcg_iteration(efgp_plan *pl, cudaStream_t s, CGState 
   const bool direct = D == 2 && toeplitz_direct(P);
   if (direct) {
     const int nrow = (int)(2 * P.m + 1);
-    k_cg_toep2<<<nrow, kToepThreads, toep2_smem((int)P.m), s>>>(pl->vfull, pl->p, pl->D_half, pl->Ap, (int)P.m, st,
-                                                                part_pAp);
+    if (toep_split() && pl->toep_part)
+      k_cg_toep2s<<<nrow * kToepSplits, kToepSThreads, toep2s_smem((int)P.m), s>>>(
+          pl->vfull, pl->p, pl->D_half, pl->Ap, (int)P.m, st, pl->toep_part, pl->toep_cnt, part_pAp);
+    else
+      k_cg_toep2<<<nrow, kToepThreads, toep2_smem((int)P.m), s>>>(pl->vfull, pl->p, pl->D_half, pl->Ap, (int)P.m, st,
+                                                                  part_pAp);
     // (x, r update: alpha from the toep2 partials, (r, z) from the previous dot's partials)
     EFGP_CUDA(launch_pdl(k_cg_xr_pc_direct, nb, kCGThreads, s, pl->x, pl->r, pl->p, (const double2 *)pl->Ap, P.Mh,
                          (int)P.m, st, (const double *)part_pAp, nrow, part_rr, (const double *)part_rz, (int)nb));

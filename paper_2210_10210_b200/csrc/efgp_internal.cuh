@@ -15,6 +15,10 @@ namespace efgp {
 constexpr double kPi = 3.14159265358979323846;
 constexpr int kMaxW = 16;  // ES kernel width for nufft_tol down to 1e-15
 constexpr int kMaxNbuf = 8;  // SORTED spreading: record-list buffers in flight (at most)
+#ifndef EFGP_TOEP_SPLITS
+#define EFGP_TOEP_SPLITS 8
+#endif
+constexpr int kToepSplitsHost = EFGP_TOEP_SPLITS;  // k1 splits of the split direct Toeplitz product (cg.cu kToepSplits)
 
 // Degree of the piecewise-polynomial ES kernel per cell offset: degree W already gives the aliasing
 // error of the exact ES kernel to within 2 % for W >= 4 (the deconvolution tables are the
@@ -127,8 +131,11 @@ struct efgp_plan {
   double *Yr = nullptr;       // L^d real
   double *vhat = nullptr;     // L^d real, C2R(v)/L^d
   double2 *vfull = nullptr;   // (4m+1)^2 complex, full v (direct Toeplitz product, small m, 2D)
+  double2 *toep_part = nullptr;  // split direct product: (2m+1) x kToepSplitsHost x (m+1) partial rows
+  unsigned *toep_cnt = nullptr;  // per output row: splits done (reset by the row's last CTA)
   double2 *Zbox = nullptr;    // R2C output
   double2 *b = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *Ap = nullptr;  // Mh each
+  double2 *p2 = nullptr;      // fused direct CG: second search-direction slot (Mh), zeroed at setup
   double *partials = nullptr; // 2 * cg_blocks
   double *scal = nullptr;     // device scalars (see cg.cu)
   double *hist = nullptr;     // residual history, hist_cap entries
@@ -455,6 +462,22 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl_smem(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                                   Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -171,6 +171,12 @@ efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s) {
   if (toeplitz_direct(P)) {  // small m: the CG applies T by direct convolution with the full v
     const int n = (int)(4 * P.m + 1);
     if (!pl->vfull) EFGP_CUDA(cudaMalloc((void **)&pl->vfull, sizeof(double2) * n * n));
+    if (!pl->toep_part) {  // split direct product (k_cg_toep2s): per-(row, split) partial rows + row counters
+      const int64_t nrow = 2 * P.m + 1;
+      EFGP_CUDA(cudaMalloc((void **)&pl->toep_part, sizeof(double2) * nrow * kToepSplitsHost * (P.m + 1)));
+      EFGP_CUDA(cudaMalloc((void **)&pl->toep_cnt, sizeof(unsigned) * nrow));
+      EFGP_CUDA(cudaMemsetAsync(pl->toep_cnt, 0, sizeof(unsigned) * nrow, s));
+    }
     k_expand_v2<<<grid_for((int64_t)n * n, 256, pl->num_sms), 256, 0, s>>>(vh, (int)P.m, pl->vfull);
     EFGP_CUDA(cudaGetLastError());
   }
