@@ -186,6 +186,27 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def host_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def golden_record(cfg):
+    """The oracle's full-size run of this config (tests/golden, written by tests/make_golden.py): its
+    N, per-stage host seconds and iteration counts, for the per-run metrics record."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", f"full_{cfg.name}.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def cpu_baseline(cfg, n_points: int, q_targets: int):
     """The oracle (as it stands) on a bounded sample of the workload, on the host cores."""
     import numpy as np
@@ -202,7 +223,8 @@ def cpu_baseline(cfg, n_points: int, q_targets: int):
     mu = O.efgp_predict(fit, xt)
     dt = time.perf_counter() - t0
     assert np.all(np.isfinite(mu))
-    return {"value": n_points / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": n_points / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "host_model": host_model(),
+            "host_cpus": os.cpu_count(),
             "sample": f"{cfg.name} recipe, first {n_points} points and {q_targets} targets "
                       f"(same N/q ratio as the workload), full fit+predict, {fit.iters} CG iterations, "
                       f"{dt:.1f} s"}
@@ -461,6 +483,42 @@ def main():
         except Exception as exc:
             hetero = {"error": f"{type(exc).__name__}: {exc}"[:200]}
 
+    # per-run metrics record: the production fit's residual history, and a parity-mode fit
+    # (CG to eps/1000, reading G9) of the same workload compared with the oracle's full-size dump
+    # (tests/golden) when it covers exactly this N and these targets
+    run_record = None
+    try:
+        hist = model.residual_history()
+        run_record = {"production": {"iters": int(len(hist) - 1), "rel_resid_first": [float(v) for v in hist[:6]],
+                                     "rel_resid_last": [float(v) for v in hist[-4:]]}}
+        if world == 1:
+            mpar = EFGP(cfg.kernel, cfg.ell, cfg.sigma, cfg.eps, cfg.d, cfg.nu, spread=args.spread,
+                        weights=args.weights, cg_tol=cfg.eps / 1000)
+            mpar.fit(x, y)
+            mu_par = mpar.predict(xt).cpu()
+            ip = mpar.info()
+            hp = mpar.residual_history()
+            rec = {"cg_tol": cfg.eps / 1000, "iters": ip["iters"], "solve_ms": ip["t_solve_ms"],
+                   "rel_resid_last": [float(v) for v in hp[-4:]]}
+            gold = golden_record(cfg)
+            if gold and gold["N"] == N and gold["q"] == q:
+                import numpy as np
+                G = np.load(os.path.join(ROOT, "tests", "golden", f"full_{cfg.name}.npz"))
+                ref = G["mu_parity"]
+                rec.update({"oracle_iters": gold["iters_parity"],
+                            "mu_rel_err_vs_oracle": float(np.linalg.norm(mu_par.numpy() - ref) / np.linalg.norm(ref)),
+                            "gate": 10 * cfg.eps})
+                run_record["production"].update({"oracle_iters": gold["iters_production"],
+                                                 "oracle_perturbed_iters": gold.get("iters_perturbed", {}).get("production")})
+            run_record["parity_mode"] = rec
+            mpar.close()
+        gold = golden_record(cfg)
+        if gold:
+            run_record["oracle_full_run"] = {"N": gold["N"], "seconds": gold["oracle_seconds"], "host": gold["host"],
+                                             "note": "tests/make_golden.py on the build host (not this box)"}
+    except Exception as exc:
+        run_record = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
     # e2e: same metric through the public API with host (pinned) buffers, copies inside the step
     e2e = None
     if not args.no_e2e:
@@ -529,7 +587,7 @@ def main():
                             "alg_bytes_per_launch": alg_bytes},
                "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "mu_at_training_points": interp_n,
                "posterior_variance": variance, "hetero_fit": hetero, "preconditioned_fit": precond,
-               "spread_variants": spread_variants}
+               "spread_variants": spread_variants, "run_record": run_record}
         if not args.no_cpu_baseline and world == 1:  # the oracle baseline: rank 0 at N = 1 only
             try:
                 ns = int(args.oracle_points)

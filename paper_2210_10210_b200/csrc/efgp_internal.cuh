@@ -74,6 +74,7 @@ struct Params {
   int nt1 = 0, nt2 = 0, ntiles = 0;
   int cap = 0;                 // records per (tile, binner CTA) segment per chunk
   int round = 0;               // records per shared-memory round
+  int round_w = 0;             // ... of the weighted one-pass mode (NEXT-3)
   int tiles_grid = 0;          // CTAs of the fused spreading kernel (<= one per SM)
   int nbuf = 2;                // tile-list buffers in flight
   int64_t chunk = 0;           // points per chunk
@@ -223,9 +224,13 @@ struct efgp_plan {
 
 namespace efgp {
 // spread.cu
-efgp_status spread_points(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s);
+// s1 (optional): per-point strength-1 weight (NEXT-3 one-pass: 1/sigma_n^2); only the SORTED and CELLSORT
+// spreaders take it — elsewhere EFGP_ERR_RESOURCE (the caller spreads the two strengths separately)
+efgp_status spread_points(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s,
+                          const double *s1 = nullptr);
 efgp_status spread_begin(efgp_plan *pl, cudaStream_t s);
-efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s);
+efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s,
+                           const double *s1 = nullptr);
 // spread_cellsort.cu: K1 CELLSORT (2D any W, 3D W <= 6); EFGP_ERR_RESOURCE if not applicable
 // w1 (optional): per-point weight of the strength-1 grid (default 1): the heteroskedastic TOEPLITZ
 // solver spreads (1/sigma_n^2, y_n/sigma_n^2) in one pass

@@ -569,11 +569,11 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
     // onto the v grid, then the homoskedastic Toeplitz machinery with sigma^2 -> 1 (reading G11b)
     double2 *vh = reinterpret_cast<double2 *>(pl->modes_sum), *fyh = vh + P.Kvh;
     bool one_pass = false;
-    if (P.spread_method == EFGP_SPREAD_CELLSORT) {
-      // CELLSORT spreads both weighted strengths in one pass: g1 = sum (1/sigma^2) phi (v^w),
-      // g2 = sum (y/sigma^2) phi, then the standard K2 for both
+    if (P.spread_method == EFGP_SPREAD_CELLSORT || P.spread_method == EFGP_SPREAD_SORTED) {
+      // SORTED (weighted one-pass mode) and CELLSORT spread both weighted strengths in one pass:
+      // g1 = sum (1/sigma^2) phi (v^w), g2 = sum (y/sigma^2) phi, then the standard K2 for both
       st = spread_begin(pl, s);
-      if (st == EFGP_OK) st = spread_cellsort(pl, x, w, N, s, iv);
+      if (st == EFGP_OK) st = spread_points(pl, x, w, N, s, iv);
       if (st == EFGP_OK) {
         one_pass = true;
         st = type1_modes(pl, pl->modes_sum, s);

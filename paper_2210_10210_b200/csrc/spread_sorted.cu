@@ -53,6 +53,8 @@ constexpr int kBarAcc = 1, kBarBin = 2, kBarAcc2 = 3;  // named barriers (0 = __
 constexpr int kModeF64 = 0;   // fp64 weights (evaluated per record in phase C), fp64 accumulation
 constexpr int kModeW32 = 1;   // fp32 weights (pass 2), fp64 accumulation
 [[maybe_unused]] constexpr int kModeA32 = 2;   // fp32 weights, fp32 (packed FFMA2) sums within a round, fp64 across
+constexpr int kModeF64W = 3;  // FP64 with a per-point strength-1 weight (NEXT-3: strengths 1/sigma_n^2 and
+                              // y_n/sigma_n^2 in ONE pass; records (x1, x2, w, y), start cell recomputed)
 
 __device__ __forceinline__ int wrap_s(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
 
@@ -161,7 +163,7 @@ __device__ __forceinline__ void es_weights_pairs(double t, const EsPolyP &P, flo
 template <int W>
 __device__ __noinline__ void spread_point_red(double x1, double x2, double yv, double h, int n1,
                                               const EsPoly *__restrict__ Pg, double *__restrict__ g1,
-                                              double *__restrict__ gy) {
+                                              double *__restrict__ gy, double s1v = 1.0) {
   double w1[W], w2[W];
   const int b1 = es_weights<W>(grid_t(h, x1, n1), *Pg, w1);
   const int b2 = es_weights<W>(grid_t(h, x2, n1), *Pg, w2);
@@ -172,7 +174,7 @@ __device__ __noinline__ void spread_point_red(double x1, double x2, double yv, d
     for (int b = 0; b < W; ++b) {
       const int64_t gi = row + wrap_s(b2 + b, n1);
       const double p = w1[a] * w2[b];
-      atomicAdd(g1 + gi, p);
+      atomicAdd(g1 + gi, p * s1v);
       atomicAdd(gy + gi, p * yv);
     }
   }
@@ -227,7 +229,7 @@ struct StageRec {
   // w1e[W] (W odd) or after w2e (W even); W32 stores it as fp64 after w2e.  16-byte padded.
   static constexpr int WE = (W + 1) / 2 * 2;
   static constexpr int kYSlot = (W & 1) ? W : 2 * WE;  // MIXED: float index of y
-  static constexpr int kBytes = MODE == kModeF64 ? 24
+  static constexpr int kBytes = MODE == kModeF64 ? 24 : MODE == kModeF64W ? 32
                                 : MODE == kModeW32 ? (8 * WE + 8 + 15) / 16 * 16
                                                    : (4 * (2 * WE + ((W & 1) ? 0 : 1)) + 15) / 16 * 16;
 };
@@ -249,6 +251,7 @@ __device__ __forceinline__ void load_floats(const unsigned char *sp, float (&f)[
 // All kernel arguments (passed by value; lives in the constant bank).
 struct FusedArgs {
   const double *x, *y;
+  const double *s1;    // kModeF64W: per-point strength-1 weight (NEXT-3: 1/sigma_n^2), else nullptr
   int64_t N, chunk;
   int nchunks, nbuf;
   int debug;           // diagnostics (EFGP_SORTED_DEBUG): 1 = accumulators skip their work
@@ -281,10 +284,11 @@ constexpr int kBinWarps = kBinThreads / 32;
 
 template <int W, int MODE>
 struct FusedSmem {
-  // binner: per warp a TMA ring (x pairs + y), per-tile count / offset / base, perm; shared: the
-  // CTA's running segment lengths and the start-cell tables
+  // binner: per warp a TMA ring (x pairs + y (+ the strength-1 weight)), per-tile count / offset /
+  // base, perm; shared: the CTA's running segment lengths and the start-cell tables
+  static constexpr int kPtBytes = MODE == kModeF64W ? 32 : 24;
   __host__ __device__ static size_t bin_warp_bytes(int ntiles) {
-    return (size_t)kWStages * kWBatch * 24 + 4 * (size_t)kWBatch + 4 * 3 * (size_t)ntiles;
+    return (size_t)kWStages * kWBatch * kPtBytes + 4 * (size_t)kWBatch + 4 * 3 * (size_t)ntiles;
   }
   __host__ __device__ static size_t bin_bytes(int ntiles, int S) {
     return kBinWarps * ((bin_warp_bytes(ntiles) + 15) / 16 * 16) + 4 * ((size_t)ntiles + 2 * (size_t)S);
@@ -296,14 +300,16 @@ struct FusedSmem {
 // points through its own TMA ring, ranks them per tile with warp-private shared counters, reserves
 // room in the CTA's segment of each tile with one shared atomic per (batch, tile), and writes the
 // records tile-contiguously.  Per-segment and per-tile lengths are published at each chunk's end.
-template <int W>
+template <int W, int MODE>
 __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..127 */) {
+  constexpr bool WGT = MODE == kModeF64W;
   const int lane = g & 31, wid = g >> 5, ntiles = A.ntiles, G = gridDim.x;
-  const size_t wbytes = (FusedSmem<W, 0>::bin_warp_bytes(ntiles) + 15) / 16 * 16;
+  const size_t wbytes = (FusedSmem<W, MODE>::bin_warp_bytes(ntiles) + 15) / 16 * 16;
   unsigned char *wsm = sm + wid * wbytes;
   double *xin = reinterpret_cast<double *>(wsm);                      // [stage][kWBatch * 2]
   double *yin = xin + kWStages * 2 * kWBatch;                         // [stage][kWBatch]
-  int *perm = reinterpret_cast<int *>(yin + kWStages * kWBatch);      // kWBatch
+  double *s1in = yin + kWStages * kWBatch;                            // [stage][kWBatch] (WGT only)
+  int *perm = reinterpret_cast<int *>(yin + (WGT ? 2 : 1) * kWStages * kWBatch);  // kWBatch
   int *wcnt = perm + kWBatch;                                         // ntiles
   int *wloc = wcnt + ntiles;                                          // ntiles
   int *wbase = wloc + ntiles;                                         // ntiles
@@ -333,9 +339,10 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     const int nb = (int)(A.N - i0 < kWBatch ? A.N - i0 : kWBatch);
     const int ne = nb & ~1;  // y copies need a multiple of 16 bytes; an odd tail is loaded by hand
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect(&bar[wid][s], (uint32_t)(nb * 16 + ne * 8));
+    mbar_expect(&bar[wid][s], (uint32_t)(nb * 16 + (WGT ? 2 : 1) * ne * 8));
     bulk_g2s(xin + s * 2 * kWBatch, A.x + 2 * i0, (uint32_t)(nb * 16), &bar[wid][s]);
     if (ne > 0) bulk_g2s(yin + s * kWBatch, A.y + i0, (uint32_t)(ne * 8), &bar[wid][s]);
+    if (WGT && ne > 0) bulk_g2s(s1in + s * kWBatch, A.s1 + i0, (uint32_t)(ne * 8), &bar[wid][s]);
   };
   for (int i = 0; i < kWStages; ++i) issue(i);
   uint32_t phases = 0;
@@ -383,7 +390,11 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     phases ^= 1u << s;
     const double2 *xs2 = reinterpret_cast<const double2 *>(xin + s * 2 * kWBatch);
     double *ys = yin + s * kWBatch;
-    if ((nb & 1) && lane == 0) ys[nb - 1] = A.y[i0 + nb - 1];
+    double *s1s = s1in + s * kWBatch;
+    if ((nb & 1) && lane == 0) {
+      ys[nb - 1] = A.y[i0 + nb - 1];
+      if (WGT) s1s[nb - 1] = A.s1[i0 + nb - 1];
+    }
     __syncwarp();
     int tk[kWBatch / 32], rk[kWBatch / 32];  // (tile << 8 | key), rank within the batch's tile
     // (written as independent predicated steps so the 8 points of a lane overlap their latencies)
@@ -447,8 +458,10 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       EFGP_DCHECK(j < nb && t < ntiles && slot >= wloc[t] && p >= 0);
       const double2 xx = xs2[j];
       const double yv = ys[j];
+      const double s1v = WGT ? s1s[j] : 0.0;
       if (p < A.segcap)
-        st_v4(rec + ((int64_t)t * G + blockIdx.x) * A.segcap + p, xx.x, xx.y, yv, __longlong_as_double((long long)key));
+        st_v4(rec + ((int64_t)t * G + blockIdx.x) * A.segcap + p, xx.x, xx.y, WGT ? s1v : yv,
+              WGT ? yv : __longlong_as_double((long long)key));  // WGT: (x1, x2, w, y), start cell recomputed
       else
         ovf = true;
     }
@@ -457,7 +470,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
         const int v = perm[slot];
         const int j = v & 0xFF, t = v >> 16;
         if (wbase[t] + slot - wloc[t] >= A.segcap)
-          spread_point_red<W>(xs2[j].x, xs2[j].y, ys[j], A.h, A.n1, A.poly_dev, A.g1, A.gy);
+          spread_point_red<W>(xs2[j].x, xs2[j].y, ys[j], A.h, A.n1, A.poly_dev, A.g1, A.gy, WGT ? s1s[j] : 1.0);
       }
     }
     __syncwarp();  // stage s consumed
@@ -476,7 +489,7 @@ struct AccSmem {
   // raw round (32 B records, bulk-copied), cell-sorted stage, per-cell counts, tile prefix, two
   // segment prefixes, fp64 tile accumulator; all 16-byte multiples
   __host__ __device__ static size_t bytes(int R, int ntiles, int grid, int T1, int T2) {
-    size_t b = 32 * (size_t)R + (size_t)R * StageRec<W, MODE>::kBytes;
+    size_t b = 32 * (size_t)R + (size_t)R * StageRec<W, MODE>::kBytes + (MODE == kModeF64W ? 4 * (size_t)R : 0);
     b += ((4 * (size_t)(2 * kGrpThreads + ntiles + 1 + 2 * (grid + 1))) + 15) / 16 * 16;
     b += 16 * (size_t)(T1 + W - 1) * (T2 + W - 1);
     return b;
@@ -502,6 +515,8 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
   int *spre = tpre + ntiles + 1;                                        // [2][G + 1]
   double *tacc = reinterpret_cast<double *>(
       gsm + 32 * (size_t)R + (size_t)R * SB + ((4 * (size_t)(2 * kGrpThreads + ntiles + 1 + 2 * (G + 1))) + 15) / 16 * 16);
+  // kModeF64W: key | rank << 8 of each raw record (the records carry (x1, x2, w, y), no key)
+  int *kr = reinterpret_cast<int *>(tacc + 2 * (size_t)(T1 + W - 1) * (T2 + W - 1));
   __shared__ int wsum_s[kAccGroups][8], total_s[kAccGroups], spre_tile_s[kAccGroups][2];
   __shared__ __align__(8) uint64_t bar_s[kAccGroups];
   int *wsum = wsum_s[gi], *spre_tile = spre_tile_s[gi];
@@ -563,7 +578,19 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int j = j0 + u * kGrpThreads;
-            key[u] = j < nr ? __double2loint(raw[j].w) : -1;
+            if constexpr (MODE == kModeF64W) {  // start cell recomputed from x (same roundings as the binner)
+              if (j < nr) {
+                const double4 rv = raw[j];
+                const int i1 = start_cell<W>(grid_t(h, rv.x, n1)) - s_lo - r0;
+                const int i2 = start_cell<W>(grid_t(h, rv.y, n1)) - s_lo - c0;
+                EFGP_DCHECK(i1 >= 0 && i1 < T1 && i2 >= 0 && i2 < T2);
+                key[u] = i1 * T2 + i2;
+              } else {
+                key[u] = -1;
+              }
+            } else {
+              key[u] = j < nr ? __double2loint(raw[j].w) : -1;
+            }
             EFGP_DCHECK(key[u] < NT);
           }
 #pragma unroll
@@ -571,7 +598,10 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int j = j0 + u * kGrpThreads;
-            if (j < nr) reinterpret_cast<int *>(&raw[j].w)[1] = rnk[u];
+            if (j < nr) {
+              if constexpr (MODE == kModeF64W) kr[j] = key[u] | rnk[u] << 8;
+              else reinterpret_cast<int *>(&raw[j].w)[1] = rnk[u];
+            }
           }
         }
         named_sync(bar_id, kGrpThreads);
@@ -595,10 +625,16 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
 #pragma unroll 2
         for (int j = tid; j < nr; j += kGrpThreads) {
           const double4 rv = raw[j];
-          EFGP_DCHECK(__double2loint(rv.w) >= 0 && __double2loint(rv.w) < NT && __double2hiint(rv.w) >= 0 &&
-                      coff[__double2loint(rv.w)] + __double2hiint(rv.w) < nr);
-          unsigned char *st = stage + (size_t)(coff[__double2loint(rv.w)] + __double2hiint(rv.w)) * SB;
-          if constexpr (MODE == kModeF64) {
+          const int kk = MODE == kModeF64W ? (kr[j] & 0xFF) : __double2loint(rv.w);
+          const int rr = MODE == kModeF64W ? (kr[j] >> 8) : __double2hiint(rv.w);
+          EFGP_DCHECK(kk >= 0 && kk < NT && rr >= 0 && coff[kk] + rr < nr);
+          unsigned char *st = stage + (size_t)(coff[kk] + rr) * SB;
+          if constexpr (MODE == kModeF64W) {
+            double s1, s2;
+            es_reduce<W>(grid_t(h, rv.x, n1), s1);
+            es_reduce<W>(grid_t(h, rv.y, n1), s2);
+            reinterpret_cast<double4 *>(st)[0] = make_double4(s1, s2, rv.z, rv.w);  // (s1, s2, w, y)
+          } else if constexpr (MODE == kModeF64) {
             // the reduced coordinates s1, s2 (es_reduce) are computed here, in the load-balanced
             // thread-per-record pass, instead of in phase C (thread per cell, Poisson-imbalanced)
             double *d = reinterpret_cast<double *>(st);
@@ -640,17 +676,18 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
         // phase C (thread per start cell): register accumulation of its records
         if (mycnt > 0) {
           const unsigned char *sp = stage + (size_t)myoff * SB;
-          if constexpr (MODE == kModeF64) {
+          if constexpr (MODE == kModeF64 || MODE == kModeF64W) {
 #pragma unroll 2
             for (int q = 0; q < mycnt; ++q, sp += SB) {
               const double *d = reinterpret_cast<const double *>(sp);
-              const double yv = d[2];
+              const double yv = MODE == kModeF64W ? d[3] : d[2];
+              const double wv = MODE == kModeF64W ? d[2] : 1.0;  // strength-1 weight (NEXT-3: 1/sigma_n^2)
               double w1[W], w2[W];
               es_weights_s<W>(d[0], P, w1);
               es_weights_s<W>(d[1], P, w2);
 #pragma unroll
               for (int a = 0; a < W; ++a) {
-                const double ca = w1[a], cy = yv * w1[a];
+                const double ca = MODE == kModeF64W ? wv * w1[a] : w1[a], cy = yv * w1[a];
 #pragma unroll
                 for (int b2 = 0; b2 < W; ++b2) {
                   a1[a][b2] = fma(ca, w2[b2], a1[a][b2]);
@@ -1020,7 +1057,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_spread_fused(const FusedAr
   const size_t acc_bytes = 2 * AccSmem<W, MODE>::bytes(A.R, A.ntiles, gridDim.x, A.T1, A.T2);
   if (tid >= kAccThreads) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kBinRegs) : "memory");
-    binner_role<W>(A, fsm + (acc_bytes + 15) / 16 * 16, tid - kAccThreads);
+    binner_role<W, MODE>(A, fsm + (acc_bytes + 15) / 16 * 16, tid - kAccThreads);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kAccRegs) : "memory");
     accumulator_role<W, MODE>(A, fsm, tid, P, PF);
@@ -1038,7 +1075,8 @@ static size_t fused_smem(int w, int mode, int R, int ntiles, int S, int grid, in
   case WW:                                                     \
     return mode == 0   ? fused_smem_bytes<WW, 0>(R, ntiles, S, grid, T1, T2) \
            : mode == 1 ? fused_smem_bytes<WW, 1>(R, ntiles, S, grid, T1, T2) \
-                       : fused_smem_bytes<WW, 2>(R, ntiles, S, grid, T1, T2);
+           : mode == 2 ? fused_smem_bytes<WW, 2>(R, ntiles, S, grid, T1, T2) \
+                       : fused_smem_bytes<WW, 3>(R, ntiles, S, grid, T1, T2);
     EFGP_SZ(2) EFGP_SZ(3) EFGP_SZ(4) EFGP_SZ(5) EFGP_SZ(6)
 #undef EFGP_SZ
   }
@@ -1097,6 +1135,10 @@ bool sorted_geometry(Params &p, int num_sms) {
     if (fused_smem(p.w, p.spread_mode, r, p.ntiles, S, p.tiles_grid, p.T1, p.T2) <= lim) R = r;
   if (const char *e = std::getenv("EFGP_SORTED_R")) R = std::max(256, std::min(R, std::atoi(e) / 128 * 128));
   p.round = R;
+  // the weighted one-pass mode (kModeF64W, NEXT-3) stages 8 more bytes per point and record
+  p.round_w = 0;
+  for (int r = 256; r <= 16384; r += 128)
+    if (fused_smem(p.w, kModeF64W, r, p.ntiles, S, p.tiles_grid, p.T1, p.T2) <= lim) p.round_w = r;
   return R >= 256;  // otherwise the lists / tables do not leave room for a round: use another method
 }
 
@@ -1140,7 +1182,8 @@ static efgp_status launch_fused(efgp_plan *pl, const FusedArgs &A, cudaStream_t 
   return EFGP_OK;
 }
 
-efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s) {
+efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s,
+                           const double *s1) {
   const Params &P = pl->P;
   FusedArgs A{};
   A.x = x;
@@ -1174,7 +1217,9 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
   A.nt2 = P.nt2;
   A.ntiles = P.ntiles;
   A.segcap = segcap;
-  A.R = P.round;
+  A.s1 = s1;
+  A.R = s1 ? P.round_w : P.round;
+  if (s1 && (P.spread_mode != kModeF64 || A.R < 256)) return EFGP_ERR_RESOURCE;  // caller: two passes
   for (int b = 0; b < kMaxNbuf; ++b) A.rec[b] = pl->rec[b];
   // per-chunk segment and tile lengths and the two handshake counters, zeroed for this call
   const int G = P.tiles_grid;
@@ -1207,13 +1252,14 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
   A.g1 = pl->g1;
   A.gy = pl->g2;
   A.err = pl->dflags;
-  const int mode = P.spread_mode;
+  const int mode = s1 ? kModeF64W : P.spread_mode;
   switch (P.w) {
 #define EFGP_CASE(WW)                                  \
   case WW:                                             \
     return mode == 0   ? launch_fused<WW, 0>(pl, A, s) \
            : mode == 1 ? launch_fused<WW, 1>(pl, A, s) \
-                       : launch_fused<WW, 2>(pl, A, s);
+           : mode == 2 ? launch_fused<WW, 2>(pl, A, s) \
+                       : launch_fused<WW, 3>(pl, A, s);
     EFGP_CASE(2) EFGP_CASE(3) EFGP_CASE(4) EFGP_CASE(5) EFGP_CASE(6)
 #undef EFGP_CASE
   }
