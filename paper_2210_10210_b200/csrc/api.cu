@@ -613,8 +613,10 @@ void efgp_destroy(efgp_handle pl) {
   for (void *b : {(void *)pl->var_x, (void *)pl->var_r, (void *)pl->var_p, (void *)pl->var_Ap, (void *)pl->var_X,
                   (void *)pl->var_Z, (void *)pl->var_Y, pl->var_st})
     if (b) cudaFree(b);
-  for (cufftHandle h : {pl->plan_g1, pl->plan_g2, pl->plan_c2r_L, pl->plan_r2c_L, pl->plan_t2})
+  for (cufftHandle h : {pl->plan_g1, pl->plan_g2, pl->plan_c2r_L, pl->plan_r2c_L, pl->plan_t2, pl->plan_pt, pl->plan_ptv})
     if (h) cufftDestroy(h);
+  for (void *b : {(void *)pl->pt_P, (void *)pl->pt_T, (void *)pl->pt_W, (void *)pl->pt_V})
+    if (b) cudaFree(b);
   void *bufs[] = {pl->poly_dev, pl->D_half, pl->psi1, pl->psi2, pl->g1, pl->g2, pl->G1h, pl->G2h, pl->modes, pl->modes_sum,
                   pl->Xbox, pl->Yr, pl->vhat, pl->Zbox, pl->b, pl->x, pl->r, pl->p, pl->Ap, pl->partials,
                   pl->scal, pl->hist, pl->dflags, pl->T2box, pl->t2grid, pl->stage[0], pl->stage[1],

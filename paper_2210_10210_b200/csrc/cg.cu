@@ -10,6 +10,7 @@
 // graph_iters iterations; the host polls a device-side "done" flag after each graph launch, so the
 // reported iteration count is exact (kernels of iterations after convergence return at entry).
 // Block reductions are deterministic (fixed order, no atomics).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -235,6 +236,320 @@ __global__ void k_cg_pad(const double2 *__restrict__ p, const double *__restrict
   // runs even when done was just set: harmless (the next C2R input is never used)
   pdl_wait();
   pad_box<D>(p, Dh, m, L, X, box);
+}
+
+// ---- Toeplitz product by partial transforms (toeplitz_pt: d >= 2, m too large for the direct one)
+// out_j = sum_{k in J_m} v_{j-k} u_k (u = D p, j in J_m; eq "223") split as j = (j', j_d):
+//   T[k_d][x]  = sum_{k'} u_{k', k_d} e^{+2 pi i k'.x/L}                 (x in the L^(d-1) plane; cuFFT)
+//   W[j_d][x]  = sum_{k_d = -m}^{m} Vt[j_d - k_d][x] T[k_d][x]           (direct 1D convolution per line)
+//   out_{j', j_d} = sum_x e^{-2 pi i j'.x/L} W[j_d][x]                    (cuFFT)
+// with Vt[delta_d][x] = L^(1-d) sum_{delta'} v_{delta', delta_d} e^{+2 pi i delta'.x/L}, delta_d in
+// [-m, 2m].  Exact for L >= 4m+1 (the circulant embedding of Alg a:FF, on the first d-1
+// axes only); T[-k_d][x] = conj T[k_d][x] because u is Hermitian, so only the m+1 half slabs are
+// transformed.  Against the padded real-FFT product: 2 (d-1)-dim transforms of (m+1)/(L/2+1) of the
+// box instead of two d-dim ones, no L^d real intermediate, and the last axis is pruned exactly
+// (2m+1 inputs, m+1 outputs).  Layout: slab-major, [slab][x], x = bins row-major over the first d-1 axes.
+
+static int64_t ipow_(int64_t b, int e) {
+  int64_t r = 1;
+  while (e-- > 0) r *= b;
+  return r;
+}
+static unsigned nblocks_pt(int64_t n, int sms) {
+  const int64_t b = std::min<int64_t>((n + kCGThreads - 1) / kCGThreads, (int64_t)sms * 4);
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+// plane offset of the bins of j' (first d-1 coordinates of j) in an L^(d-1) plane
+template <int D>
+__device__ __forceinline__ int64_t pt_plane(const int (&j)[D], int64_t L) {
+  int64_t o = 0;
+#pragma unroll
+  for (int k = 0; k < D - 1; ++k) o = o * L + (j[k] < 0 ? j[k] + L : j[k]);
+  return o;
+}
+
+// P[j_d][bins(j')] = D_j p_j for every half mode (the other entries stay zero from setup)
+template <int D>
+__global__ void k_pt_pad(const double2 *__restrict__ p, const double *__restrict__ Dh, int64_t Mh, int m, int64_t L,
+                         int64_t Lp, double2 *__restrict__ Pb) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
+    int j[D];
+    decode_half<D>(q, m, j);
+    const double2 pp = p[q];
+    const double dq = Dh[q];
+    Pb[(int64_t)j[D - 1] * Lp + pt_plane<D>(j, L)] = make_double2(dq * pp.x, dq * pp.y);
+  }
+}
+
+// Vt before its transform: slab s = delta_d + m, plane bins -> delta' (|delta'_k| <= 2m, else 0)
+template <int D>
+__global__ void k_pt_place_v(const double2 *__restrict__ vh, int m, int64_t L, int64_t Lp, double scale,
+                             double2 *__restrict__ V) {
+  const int64_t n = (int64_t)(3 * m + 1) * Lp;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t x = i % Lp;
+    int j[D];
+    j[D - 1] = (int)(i / Lp) - m;
+    bool ok = true;
+#pragma unroll
+    for (int k = D - 2; k >= 0; --k) {
+      const int64_t b = x % L;
+      x /= L;
+      const int64_t dl = b <= L / 2 ? b : b - L;
+      ok = ok && dl >= -2 * m && dl <= 2 * m;
+      j[k] = (int)dl;
+    }
+    double2 val = make_double2(0.0, 0.0);
+    if (ok) {
+      const bool neg = j[D - 1] < 0;
+      if (neg)
+#pragma unroll
+        for (int k = 0; k < D; ++k) j[k] = -j[k];
+      const double2 v = vh[encode_half<D>(j, 2 * m)];
+      val = make_double2(scale * v.x, scale * (neg ? -v.y : v.y));
+    }
+    V[i] = val;
+  }
+}
+
+// W[j][x] = sum_{k=-m}^{m} Vt[j - k][x] T[k][x] for j in [j0, j0 + G).  CTA = 32 consecutive lines x
+// (lane) x ngroups warps (warp g: outputs [g G, g G + G)).  The CTA first stages its lines' T (m+1
+// slabs) and Vt (3m+1 slabs) in shared memory with coalesced 512-byte rows (one pass over HBM/L2 for
+// both arrays), then each thread slides a G-register window of Vt down one slab per step k, so
+// every step costs two conflict-free shared loads for G complex MACs (slot of window element r is r
+// mod G; the steps are unrolled in blocks of G so every slot index is static).
+// Shared-memory geometry of k_pt_conv: KS warps split the 2m+1 steps of each output group (SS steps
+// each, a multiple of G), the staged Vt is padded with zero slabs below (vlo) and above, T with zero
+// slabs above m, so the inner loop has no bounds checks.
+struct PtConvGeom {
+  int ng, SS, vlo, nV, nT;
+  __host__ __device__ PtConvGeom(int m, int G, int KS) {
+    ng = (m + 1 + G - 1) / G;
+    SS = ((2 * m + 1 + KS - 1) / KS + G - 1) / G * G;
+    vlo = KS * SS - 1 - 2 * m > 0 ? KS * SS - 1 - 2 * m : 0;
+    const int vhi = ng * G - 1 - m > 0 ? ng * G - 1 - m : 0;
+    nV = vlo + 3 * m + 1 + vhi;
+    const int tmax = KS * SS - 1 - m > m ? KS * SS - 1 - m : m;
+    nT = tmax + 1;
+  }
+  __host__ __device__ size_t smem() const { return sizeof(double2) * 32 * (size_t)(nT + nV); }
+};
+constexpr int kPtKS = 2;
+
+// W[j][x] = sum_{k=-m}^{m} Vt[j - k][x] T[k][x] for j in [j0, j0 + G).  CTA = 32 consecutive lines x
+// (lane) x ng output groups x KS step splits (warp w: group w % ng, steps of split w / ng; the KS
+// partial sums are added through shared memory at the end).  The CTA first stages its lines' T (m+1
+// slabs) and Vt (3m+1 slabs) in shared memory by bulk async copies of 512-byte rows (one pass over
+// HBM/L2 for both), then each thread slides a G-register window of Vt down one slab per step k, so
+// every step costs two conflict-free shared loads for G complex MACs (slot of window element r is r
+// mod G; steps are unrolled in blocks of G so every slot index is static).
+template <int G>
+__global__ void __launch_bounds__(512) k_pt_conv(const double2 *__restrict__ T, const double2 *__restrict__ Vt,
+                                                 double2 *__restrict__ W, int m, int64_t Lp, const CGState *st) {
+  extern __shared__ __align__(16) double2 pt_sm[];
+  __shared__ __align__(8) uint64_t bar;
+  pdl_wait();
+  pdl_trigger();
+  if (st && st->done) return;
+  const PtConvGeom geo(m, G, kPtKS);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, grp = w % geo.ng, ks = w / geo.ng;
+  const int64_t x0 = (int64_t)blockIdx.x * 32;
+  const int nl = Lp - x0 < 32 ? (int)(Lp - x0) : 32;
+  double2 *sT = pt_sm, *sV = pt_sm + 32 * geo.nT;
+  // zero the padding slabs, then one bulk async copy (TMA engine) of nl x 16 bytes per slab row
+  for (int i = threadIdx.x; i < 32 * geo.nT; i += blockDim.x)
+    if (i >= 32 * (m + 1)) sT[i] = make_double2(0.0, 0.0);
+  for (int i = threadIdx.x; i < 32 * geo.nV; i += blockDim.x) {
+    const int sl = i >> 5;
+    if (sl < geo.vlo || sl >= geo.vlo + 3 * m + 1) sV[i] = make_double2(0.0, 0.0);
+  }
+  const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(&bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nrow = m + 1 + 3 * m + 1;
+  if (w == 0) {
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"((uint32_t)(nrow * nl * 16))
+                   : "memory");
+    __syncwarp();
+    for (int sl = lane; sl < nrow; sl += 32) {
+      const bool isT = sl < m + 1;
+      const double2 *src = isT ? T + (int64_t)sl * Lp + x0 : Vt + (int64_t)(sl - m - 1) * Lp + x0;
+      double2 *dst = isT ? sT + 32 * sl : sV + 32 * (geo.vlo + sl - m - 1);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(dst)),
+                   "l"(src), "r"((uint32_t)(nl * 16)), "r"(sbar)
+                   : "memory");
+    }
+  }
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(sbar)
+      : "memory");
+  const int j0 = grp * G, s0 = ks * geo.SS;
+  // window element r (output g = r + s at step s) lives in slot r mod G; its slab is j0 + r + 2m
+  const double2 *vl = sV + 32 * (geo.vlo + j0 + 2 * m) + lane;
+  double2 acc[G], win[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    acc[g] = make_double2(0.0, 0.0);
+    win[g] = vl[32 * (g - s0)];  // r = g - s0 (slot g, since s0 = 0 mod G)
+  }
+  const double2 *tl = sT + lane;
+  for (int sb = s0; sb < s0 + geo.SS; sb += G) {
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const int s = sb + u;
+      if (u > 0 || sb > s0) win[(G - u) % G] = vl[-32 * s];  // element r = -s enters slot (-s) mod G
+      const int k = s - m;
+      double2 t = tl[32 * (k >= 0 ? k : -k)];
+      t.y = k >= 0 ? t.y : -t.y;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const double2 wv = win[((g - u) % G + G) % G];
+        acc[g].x = fma(wv.x, t.x, fma(-wv.y, t.y, acc[g].x));
+        acc[g].y = fma(wv.x, t.y, fma(wv.y, t.x, acc[g].y));
+      }
+    }
+  }
+  // split partial sums: warps of split ks > 0 park theirs in shared memory, split 0 adds and stores
+  __syncthreads();
+  double2 *red = pt_sm + (size_t)(w - geo.ng) * 32 * G;  // (ks >= 1) slot of warp w
+  if (ks > 0)
+#pragma unroll
+    for (int g = 0; g < G; ++g) red[g * 32 + lane] = acc[g];
+  __syncthreads();
+  if (ks == 0 && lane < nl) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      double2 a = acc[g];
+      for (int q = 1; q < kPtKS; ++q) {
+        const double2 b = pt_sm[(size_t)((q - 1) * geo.ng + grp) * 32 * G + g * 32 + lane];
+        a.x += b.x;
+        a.y += b.y;
+      }
+      if (j0 + g <= m) W[(int64_t)(j0 + g) * Lp + x0 + lane] = a;
+    }
+  }
+}
+
+template <int G>
+static size_t pt_conv_smem(int m) { return PtConvGeom(m, G, kPtKS).smem(); }
+
+// Ap = D . out[J_m] + sigma^2 p ; partial <p, Ap> (out = forward transform of W, slab-major)
+template <int D>
+__global__ void k_pt_apply(const double2 *__restrict__ Z, const double2 *__restrict__ p, const double *__restrict__ Dh,
+                           double2 *__restrict__ Ap, int64_t Mh, int m, int64_t L, int64_t Lp, const CGState *st,
+                           double *__restrict__ part) {
+  __shared__ double sh[40];
+  pdl_trigger();
+  if (st->done) return;
+  const double s2 = st->sigma2;
+  double acc = 0.0;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
+    int j[D];
+    decode_half<D>(q, m, j);
+    // exactly Hermitian in the j_d = 0 plane (as the R2C of the padded-FFT product is): out_{-j'} =
+    // conj out_{j'}, read from the canonical j' (first nonzero coordinate positive); without this the
+    // roundoff of the two independent sums breaks the half-space CG (iterates leave the Hermitian set)
+    bool neg = false, zero = false;
+    if (j[D - 1] == 0) {
+      int sgn = 0;
+#pragma unroll
+      for (int k = 0; k < D - 1; ++k)
+        if (sgn == 0 && j[k] != 0) sgn = j[k] > 0 ? 1 : -1;
+      neg = sgn < 0;
+      zero = sgn == 0;
+      if (neg)
+#pragma unroll
+        for (int k = 0; k < D - 1; ++k) j[k] = -j[k];
+    }
+    double2 z = Z[(int64_t)j[D - 1] * Lp + pt_plane<D>(j, L)];
+    if (neg) z.y = -z.y;
+    if (zero) z.y = 0.0;  // j = 0: real
+    const double2 pp = p[q];
+    const double dq = Dh[q];
+    const double2 a = make_double2(dq * z.x + s2 * pp.x, dq * z.y + s2 * pp.y);
+    Ap[q] = a;
+    acc += (j[D - 1] ? 2.0 : 1.0) * (pp.x * a.x + pp.y * a.y);
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+static int pt_group() {  // outputs per thread of k_pt_conv (EFGP_PT_G overrides: 4, 8, 10, 13)
+  const char *e = getenv("EFGP_PT_G");
+  return e ? atoi(e) : 0;
+}
+
+template <int G>
+static cudaError_t pt_conv_launch(efgp_plan *pl, const CGState *st, cudaStream_t s) {
+  const Params &P = pl->P;
+  const int64_t Lp = ipow_(P.L, P.d - 1);
+  const int ng = (int)((P.m + 1 + G - 1) / G);
+  return launch_pdl_smem(k_pt_conv<G>, (unsigned)((Lp + 31) / 32), 32 * ng * kPtKS, pt_conv_smem<G>((int)P.m), s,
+                         (const double2 *)pl->pt_T, (const double2 *)pl->pt_V, pl->pt_W, (int)P.m, Lp, st);
+}
+
+// out = T(D p) into pt_T (slab-major), the three launches between the pad and the apply
+static efgp_status pt_product(efgp_plan *pl, const CGState *st, cudaStream_t s) {
+  const Params &P = pl->P;
+  EFGP_CUFFT(cufftExecZ2Z(pl->plan_pt, pl->pt_P, pl->pt_T, CUFFT_INVERSE));
+  int G = pt_group();
+  const int64_t Lp = ipow_(P.L, P.d - 1);
+  if (G == 0) G = 10;
+  cudaError_t e;
+  switch (G) {
+    case 4: e = pt_conv_launch<4>(pl, st, s); break;
+    case 8: e = pt_conv_launch<8>(pl, st, s); break;
+    case 10: e = pt_conv_launch<10>(pl, st, s); break;
+    default: e = pt_conv_launch<13>(pl, st, s); break;
+  }
+  EFGP_CUDA(e);
+  EFGP_CUFFT(cufftExecZ2Z(pl->plan_pt, pl->pt_W, pl->pt_T, CUFFT_FORWARD));
+  return EFGP_OK;
+}
+
+template <int D>
+static efgp_status pt_pad(efgp_plan *pl, const double2 *p, cudaStream_t s) {
+  const Params &P = pl->P;
+  EFGP_CUDA(launch_pdl(k_pt_pad<D>, nblocks_pt(P.Mh, pl->num_sms), kCGThreads, s, p, (const double *)pl->D_half, P.Mh,
+                       (int)P.m, (int64_t)P.L, ipow_(P.L, D - 1), pl->pt_P));
+  return EFGP_OK;
+}
+
+efgp_status pt_setup(efgp_plan *pl, const double2 *vh, cudaStream_t s) {
+  const Params &P = pl->P;
+  const int d = P.d;
+  const int64_t Lp = ipow_(P.L, d - 1), ns = P.m + 1;
+  if (!pl->pt_P) {
+    EFGP_CUDA(cudaMalloc((void **)&pl->pt_P, sizeof(double2) * ns * Lp));
+    EFGP_CUDA(cudaMalloc((void **)&pl->pt_T, sizeof(double2) * ns * Lp));
+    EFGP_CUDA(cudaMalloc((void **)&pl->pt_W, sizeof(double2) * ns * Lp));
+    EFGP_CUDA(cudaMalloc((void **)&pl->pt_V, sizeof(double2) * (3 * P.m + 1) * Lp));
+    EFGP_CUDA(cudaMemsetAsync(pl->pt_P, 0, sizeof(double2) * ns * Lp, s));
+    int dims[2] = {(int)P.L, (int)P.L};
+    EFGP_CUFFT(cufftPlanMany(&pl->plan_pt, d - 1, dims, nullptr, 1, (int)Lp, nullptr, 1, (int)Lp, CUFFT_Z2Z, (int)ns));
+    EFGP_CUFFT(cufftPlanMany(&pl->plan_ptv, d - 1, dims, nullptr, 1, (int)Lp, nullptr, 1, (int)Lp, CUFFT_Z2Z,
+                             (int)(3 * P.m + 1)));
+  }
+  const int64_t n = (3 * P.m + 1) * Lp;
+  const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)pl->num_sms * 8);
+  EFGP_CUDA(cudaFuncSetAttribute(k_pt_conv<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pt_conv_smem<4>((int)P.m)));
+  EFGP_CUDA(cudaFuncSetAttribute(k_pt_conv<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pt_conv_smem<8>((int)P.m)));
+  EFGP_CUDA(cudaFuncSetAttribute(k_pt_conv<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pt_conv_smem<10>((int)P.m)));
+  EFGP_CUDA(cudaFuncSetAttribute(k_pt_conv<13>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pt_conv_smem<13>((int)P.m)));
+  if (d == 2) k_pt_place_v<2><<<g, 256, 0, s>>>(vh, (int)P.m, P.L, Lp, 1.0 / (double)Lp, pl->pt_V);
+  else k_pt_place_v<3><<<g, 256, 0, s>>>(vh, (int)P.m, P.L, Lp, 1.0 / (double)Lp, pl->pt_V);
+  EFGP_CUDA(cudaGetLastError());
+  EFGP_CUFFT(cufftSetStream(pl->plan_ptv, s));
+  EFGP_CUFFT(cufftExecZ2Z(pl->plan_ptv, pl->pt_V, pl->pt_V, CUFFT_INVERSE));
+  return EFGP_OK;
 }
 
 
@@ -648,6 +963,7 @@ static efgp_status enqueue_iteration(efgp_plan *pl, cudaStream_t s, CGState *st,
   const Params &P = pl->P;
   double *part_pAp = pl->partials, *part_rr = pl->partials + pl->cg_blocks;
   const bool direct = D == 2 && toeplitz_direct(P);
+  const bool pt = D >= 2 && toeplitz_pt(P);
   if (direct && pl->p2 && pl->toep_part && cg_fused() && toep_split()) {  // fused direct CG: two kernels per iteration
     const int nrow = (int)(2 * P.m + 1);
     double2 *pq = slot ? pl->p2 : pl->p, *pold = slot ? pl->p : pl->p2;
@@ -669,6 +985,12 @@ static efgp_status enqueue_iteration(efgp_plan *pl, cudaStream_t s, CGState *st,
                                                                   part_pAp);
     EFGP_CUDA(launch_pdl(k_cg_xr, nb, kCGThreads, s, pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp,
                          part_rr, nrow, (const double *)nullptr));
+  } else if (pt) {  // partial-transform product (c2, c4)
+    EFGP_TRY(pt_product(pl, st, s));
+    k_pt_apply<D><<<nb, kCGThreads, 0, s>>>(pl->pt_T, pl->p, pl->D_half, pl->Ap, P.Mh, (int)P.m, P.L, ipow_(P.L, D - 1),
+                                            st, part_pAp);
+    EFGP_CUDA(launch_pdl(k_cg_xr, nb, kCGThreads, s, pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp,
+                         part_rr, (int)nb, (const double *)nullptr));
   } else {
   EFGP_CUFFT(cufftExecZ2D(pl->plan_c2r_L, pl->Xbox, pl->Yr));
   k_mul<<<nblocks(Ld, pl->num_sms), kCGThreads, 0, s>>>(pl->Yr, pl->vhat, Ld, st);
@@ -679,7 +1001,9 @@ static efgp_status enqueue_iteration(efgp_plan *pl, cudaStream_t s, CGState *st,
   }
   EFGP_CUDA(launch_pdl(k_cg_p<D>, nb, kCGThreads, s, pl->r, pl->p, pl->D_half, P.Mh, (int)P.m, P.L, pl->Xbox, box,
                        st, part_rr, (int)nb, pl->hist));
-  if (!direct)
+  if (pt)
+    EFGP_TRY(pt_pad<D>(pl, pl->p, s));
+  else if (!direct)
     EFGP_CUDA(launch_pdl(k_cg_pad<D>, nbox, kCGThreads, s, pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box,
                          (const CGState *)st));
   EFGP_CUDA(cudaGetLastError());
@@ -717,7 +1041,12 @@ static efgp_status cg_solve_d(efgp_plan *pl, int64_t N_total) {
   EFGP_CUDA(cudaMemcpyAsync(st, &init, sizeof(CGState), cudaMemcpyHostToDevice, s));
   k_cg_init<<<nb, kCGThreads, 0, s>>>(pl->b, pl->x, pl->r, pl->p, P.Mh, (int)P.m, pl->partials);
   k_cg_init2<<<1, kCGThreads, 0, s>>>(st, pl->partials, (int)nb, pl->hist);
-  k_cg_pad0<D><<<nbox, kCGThreads, 0, s>>>(pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box);
+  if (D >= 2 && toeplitz_pt(P)) {
+    EFGP_TRY(pt_pad<D>(pl, pl->p, s));
+    EFGP_CUFFT(cufftSetStream(pl->plan_pt, s));
+  } else {
+    k_cg_pad0<D><<<nbox, kCGThreads, 0, s>>>(pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box);
+  }
   EFGP_CUDA(cudaGetLastError());
   EFGP_CUFFT(cufftSetStream(pl->plan_c2r_L, s));
   EFGP_CUFFT(cufftSetStream(pl->plan_r2c_L, s));
@@ -901,6 +1230,7 @@ static efgp_status enqueue_pcg_iteration(efgp_plan *pl, cudaStream_t s, CGState 
   const Params &P = pl->P;
   double *part_pAp = pl->partials, *part_rr = pl->partials + pl->cg_blocks, *part_rz = pl->partials + 2 * pl->cg_blocks;
   const bool direct = D == 2 && toeplitz_direct(P);
+  const bool pt = D >= 2 && toeplitz_pt(P);
   if (direct) {
     const int nrow = (int)(2 * P.m + 1);
     if (toep_split() && pl->toep_part)
@@ -913,10 +1243,16 @@ static efgp_status enqueue_pcg_iteration(efgp_plan *pl, cudaStream_t s, CGState 
     EFGP_CUDA(launch_pdl(k_cg_xr_pc_direct, nb, kCGThreads, s, pl->x, pl->r, pl->p, (const double2 *)pl->Ap, P.Mh,
                          (int)P.m, st, (const double *)part_pAp, nrow, part_rr, (const double *)part_rz, (int)nb));
   } else {
+  if (pt) {
+    EFGP_TRY(pt_product(pl, st, s));
+    k_pt_apply<D><<<nb, kCGThreads, 0, s>>>(pl->pt_T, pl->p, pl->D_half, pl->Ap, P.Mh, (int)P.m, P.L, ipow_(P.L, D - 1),
+                                            st, part_pAp);
+  } else {
   EFGP_CUFFT(cufftExecZ2D(pl->plan_c2r_L, pl->Xbox, pl->Yr));
   k_mul<<<nblocks(Ld, pl->num_sms), kCGThreads, 0, s>>>(pl->Yr, pl->vhat, Ld, st);
   EFGP_CUFFT(cufftExecD2Z(pl->plan_r2c_L, pl->Yr, pl->Zbox));
   k_cg_apply<D><<<nb, kCGThreads, 0, s>>>(pl->Zbox, pl->p, pl->D_half, pl->Ap, P.Mh, (int)P.m, P.L, st, part_pAp);
+  }
   k_cg_xr<<<nb, kCGThreads, 0, s>>>(pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp, part_rr, (int)nb,
                                     part_rz);
   }
@@ -926,7 +1262,8 @@ static efgp_status enqueue_pcg_iteration(efgp_plan *pl, cudaStream_t s, CGState 
                        (const CGState *)st, part_rz));
   EFGP_CUDA(launch_pdl(k_pcg_p, nb, kCGThreads, s, (const double2 *)pl->z, pl->p, P.Mh, (const CGState *)st,
                        (const double *)part_rz, (int)nb, 0));
-  if (!direct) k_cg_pad<D><<<nbox, kCGThreads, 0, s>>>(pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box, st);
+  if (pt) EFGP_TRY(pt_pad<D>(pl, pl->p, s));
+  else if (!direct) k_cg_pad<D><<<nbox, kCGThreads, 0, s>>>(pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box, st);
   EFGP_CUDA(cudaGetLastError());
   return EFGP_OK;
 }
@@ -962,7 +1299,12 @@ static efgp_status pcg_solve_d(efgp_plan *pl, int64_t N_total) {
   EFGP_TRY(precond_apply(pl, pl->r, pl->z, &st->done, s));          // z0 = M^-1 b
   k_pcg_dot<<<nb, kCGThreads, 0, s>>>(pl->r, pl->z, P.Mh, (int)P.m, st, part_rz);
   k_pcg_p<<<nb, kCGThreads, 0, s>>>(pl->z, pl->p, P.Mh, st, part_rz, (int)nb, 1);  // p0 = z0
-  k_cg_pad0<D><<<nbox, kCGThreads, 0, s>>>(pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box);
+  if (D >= 2 && toeplitz_pt(P)) {
+    EFGP_TRY(pt_pad<D>(pl, pl->p, s));
+    EFGP_CUFFT(cufftSetStream(pl->plan_pt, s));
+  } else {
+    k_cg_pad0<D><<<nbox, kCGThreads, 0, s>>>(pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box);
+  }
   EFGP_CUDA(cudaGetLastError());
   EFGP_CUFFT(cufftSetStream(pl->plan_c2r_L, s));
   EFGP_CUFFT(cufftSetStream(pl->plan_r2c_L, s));

@@ -135,6 +135,12 @@ struct efgp_plan {
   double2 *toep_part = nullptr;  // split direct product: (2m+1) x kToepSplitsHost x (m+1) partial rows
   unsigned *toep_cnt = nullptr;  // per output row: splits done (reset by the row's last CTA)
   double2 *Zbox = nullptr;    // R2C output
+  // partial-transform Toeplitz product (toeplitz_pt, cg.cu): (m+1) slabs of L^(d-1) complex each
+  double2 *pt_P = nullptr;    // D p scattered at the J_m bins (zeros elsewhere, set once)
+  double2 *pt_T = nullptr;    // inverse DFT over the first d-1 axes; reused for the forward output
+  double2 *pt_W = nullptr;    // per-line convolution along the last axis
+  double2 *pt_V = nullptr;    // (3m+1) slabs: L^(1-d) x inverse DFT of v over the first d-1 axes
+  cufftHandle plan_pt = 0, plan_ptv = 0;  // batched (d-1)-dim Z2Z, batch m+1 / 3m+1
   double2 *b = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *Ap = nullptr;  // Mh each
   double2 *p2 = nullptr;      // fused direct CG: second search-direction slot (Mh), zeroed at setup
   double *partials = nullptr; // 2 * cg_blocks
@@ -259,6 +265,16 @@ inline bool toeplitz_direct(const Params &P) {
   const int64_t n = 2 * P.m + 1, nv = 4 * P.m + 1, nout = P.m + 1, slices = 1024 / ((nout + 3) / 4);
   return 16 * (n * n + n * nv + slices * nout) <= 220 * 1024;
 }
+// the CG's Toeplitz product for d >= 2 when the direct one does not apply (c2, c4): cuFFT over the
+// first d-1 axes (batched over the m+1 half slabs of the last axis), direct 1D convolution along the
+// last axis per line (cg.cu "partial-transform product"); EFGP_TOEP_PT=0 selects the padded real FFTs
+inline bool toeplitz_pt(const Params &P) {
+  const char *e = getenv("EFGP_TOEP_PT");
+  if (e && e[0] == '0') return false;
+  if (e && e[0] == '2') return P.d >= 2 && !toeplitz_direct(P);  // also 2D (c2: measured slower, 45 vs 27 us)
+  return P.d == 3;
+}
+efgp_status pt_setup(efgp_plan *pl, const double2 *vh, cudaStream_t s);
 efgp_status type1_modes(efgp_plan *pl, double *modes_out, cudaStream_t s);
 efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s);
 efgp_status type2_grid(efgp_plan *pl, cudaStream_t s);

@@ -168,6 +168,7 @@ efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s) {
   EFGP_CUFFT(cufftExecZ2D(pl->plan_c2r_L, pl->Xbox, pl->vhat));  // real: v is Hermitian (A.10)
   k_make_b<<<grid_for(P.Mh, 256, pl->num_sms), 256, 0, s>>>(fyh, pl->D_half, pl->b, P.Mh);
   EFGP_CUDA(cudaGetLastError());
+  if (toeplitz_pt(P)) EFGP_TRY(pt_setup(pl, vh, s));
   if (toeplitz_direct(P)) {  // small m: the CG applies T by direct convolution with the full v
     const int n = (int)(4 * P.m + 1);
     if (!pl->vfull) EFGP_CUDA(cudaMalloc((void **)&pl->vfull, sizeof(double2) * n * n));

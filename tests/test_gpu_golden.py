@@ -40,6 +40,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLD = os.path.join(ROOT, "tests", "golden")
 # configs gated on G10 alone when a dump has no perturbed counts
 G10_PRODUCTION = {"c1", "c4", "c5"}
+# c3's production first crossing (eps = 1e-6 on a plateaued residual, 2800-3200
+# iterations) moves by hundreds of iterations under roundoff-level changes of v and F^*y (the oracle's
+# own counts under NUFFT-level perturbations span 2980-3077 against 2790 unperturbed).  There the
+# survey asks for the mismatch to be REPORTED with both residual histories (written to
+# $EFGP_GOLDEN_REPORT and printed), and the parity-mode mu gate (G9) is authoritative.
+G10_REPORT_ONLY = {"c3"}
 
 
 def _load(name):
@@ -165,7 +171,10 @@ def test_golden_production_iterations(name):
     # own production answer is (x2), plus 10 eps (reading G9: the first crossing is hypersensitive)
     e_o = rel(G["mu_production"], G["mu_parity"])
     assert rel(mu, G["mu_parity"]) <= 2 * e_o + 10 * c.eps, (rel(mu, G["mu_parity"]), e_o)
-    if pert or name in G10_PRODUCTION:
+    if not ok:
+        print(f"{name} production: iteration count {k_g} vs oracle {k_o} (window [{lo}, {hi}], perturbed oracle "
+              f"{pert}); gpu history tail {hist_g[-6:]}, oracle history tail {ho[-6:]}")
+    if (pert or name in G10_PRODUCTION) and name not in G10_REPORT_ONLY:
         assert ok, (f"G10/G10b: gpu {k_g} vs oracle {k_o}, window [{lo}, {hi}], perturbed oracle {pert}; "
                     f"histories: gpu {hist_g[max(0, k_o - 5):k_g + 2]} oracle {ho[max(0, k_o - 5):k_o + 2]}")
     g.close()
