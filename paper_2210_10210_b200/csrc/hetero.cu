@@ -125,39 +125,58 @@ __global__ void k_het_count(const double *__restrict__ x, int64_t N, double h, i
 
 // per cell: exclusive scan over the CTAs (in place) and the cell total
 __global__ void k_het_colscan(unsigned *__restrict__ hist, int nblk, int ncell, long long *__restrict__ tot) {
+  // hist[b][c] -> exclusive prefix over b (column scan), tot[c] = column total.  The loads of a
+  // chunk of rows are issued before any store (no aliasing stall: r01 did one dependent load/store
+  // pair per row, ~1 us per row of latency at 148 rows)
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncell) return;
+  constexpr int kChunk = 16;
   long long run = 0;
-  for (int b = 0; b < nblk; ++b) {
-    const unsigned v = hist[(size_t)b * ncell + c];
-    hist[(size_t)b * ncell + c] = (unsigned)run;  // < 2^32 points per cell
-    run += v;
+  for (int b0 = 0; b0 < nblk; b0 += kChunk) {
+    unsigned v[kChunk];
+#pragma unroll
+    for (int k = 0; k < kChunk; ++k) v[k] = b0 + k < nblk ? __ldcg(hist + (size_t)(b0 + k) * ncell + c) : 0u;
+#pragma unroll
+    for (int k = 0; k < kChunk; ++k) {
+      if (b0 + k < nblk) hist[(size_t)(b0 + k) * ncell + c] = (unsigned)run;  // < 2^32 points per cell
+      run += v[k];
+    }
   }
   tot[c] = run;
 }
 
-// off[c] = sum_{c' < c} tot[c'], off[ncell] = N (one CTA, sequential chunks of blockDim)
+// off[c] = sum_{c' < c} tot[c'], off[ncell] = N (one CTA of 1024 threads: each thread scans a
+// contiguous slice serially, one block scan of the slice totals, then the slices are written)
 __global__ void k_het_offsets(const long long *__restrict__ tot, int ncell, long long *__restrict__ off) {
-  __shared__ long long sh[1024];
-  __shared__ long long carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int c0 = 0; c0 < ncell; c0 += blockDim.x) {
-    const int c = c0 + threadIdx.x;
-    sh[threadIdx.x] = c < ncell ? tot[c] : 0;
-    __syncthreads();
-    for (int o = 1; o < (int)blockDim.x; o <<= 1) {  // Hillis-Steele inclusive scan
-      const long long v = threadIdx.x >= (unsigned)o ? sh[threadIdx.x - o] : 0;
-      __syncthreads();
-      sh[threadIdx.x] += v;
-      __syncthreads();
-    }
-    if (c < ncell) off[c] = carry + sh[threadIdx.x] - (c < ncell ? tot[c] : 0);
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry += sh[threadIdx.x];
-    __syncthreads();
+  __shared__ long long wsum[32];
+  const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, wid = t >> 5;
+  const int per = (ncell + nt - 1) / nt, a = t * per, e = min(ncell, a + per);
+  long long s = 0;
+  for (int c = a; c < e; ++c) s += tot[c];
+  long long incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
   }
-  if (threadIdx.x == 0) off[ncell] = carry;
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    long long w = lane < (nt >> 5) ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long v = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += v;
+    }
+    wsum[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  long long run = incl - s + (wid > 0 ? wsum[wid - 1] : 0);
+  for (int c = a; c < e; ++c) {
+    off[c] = run;
+    run += tot[c];
+  }
+  if (t == nt - 1) off[ncell] = run;
 }
 
 template <int D, int W>

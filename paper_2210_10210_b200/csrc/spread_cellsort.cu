@@ -81,23 +81,106 @@ __global__ void k_cs_scatter(const double *__restrict__ x, const double *__restr
                              int lo, int S, int ncell, const unsigned *__restrict__ hist,
                              const long long *__restrict__ off, double4 *__restrict__ rec, int *__restrict__ err,
                              const double *__restrict__ w1, double *__restrict__ ws1) {
-  extern __shared__ unsigned cs_c[];  // cursor relative to the bucket start (< 2^32 points per call)
-  for (int i = threadIdx.x; i < ncell; i += blockDim.x) cs_c[i] = hist[(size_t)blockIdx.x * ncell + i];
+  // absolute cursor of this CTA in each bucket, off[c] + (this CTA's prefix), as 32 bits (< 2^32 points
+  // per call): the scatter position needs no dependent global load of off[key]
+  extern __shared__ unsigned cs_c[];
+  for (int i = threadIdx.x; i < ncell; i += blockDim.x) cs_c[i] = (unsigned)(off[i] + hist[(size_t)blockIdx.x * ncell + i]);
   __syncthreads();
   int64_t a, e;
   cs_range(N, a, e);
-  for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x) {
-    const int key = cs_key<D, W, G>(x, y, i, h, n, lo, S, err);
-    EFGP_DCHECK(key >= 0 && key < ncell);
-    const long long pos = off[key] + (long long)atomicAdd(&cs_c[key], 1u);
-    EFGP_DCHECK(pos >= off[key] && pos < off[key + 1]);
-    if constexpr (D == 2) {
-      cs_st256(rec + pos, __ldg(x + 2 * i), __ldg(x + 2 * i + 1), __ldg(y + i), w1 ? __ldg(w1 + i) : 1.0);
-    } else {
-      cs_st256(rec + pos, __ldg(x + 3 * i), __ldg(x + 3 * i + 1), __ldg(x + 3 * i + 2), __ldg(y + i));
-      if (w1) ws1[pos] = __ldg(w1 + i);
+  // 4 points per thread per step (independent loads, keys, cursor atomics and stores overlap)
+  for (int64_t i0 = a + threadIdx.x; i0 < e; i0 += 4 * (int64_t)blockDim.x) {
+    int key[4];
+    long long pos[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * (int64_t)blockDim.x;
+      key[u] = i < e ? cs_key<D, W, G>(x, y, i, h, n, lo, S, err) : -1;
+      EFGP_DCHECK(key[u] < ncell);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) pos[u] = key[u] >= 0 ? (long long)atomicAdd(&cs_c[key[u]], 1u) : 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * (int64_t)blockDim.x;
+      if (key[u] < 0) continue;
+      EFGP_DCHECK(pos[u] >= off[key[u]] && pos[u] < off[key[u] + 1]);
+      if constexpr (D == 2) {
+        cs_st256(rec + pos[u], __ldg(x + 2 * i), __ldg(x + 2 * i + 1), __ldg(y + i), w1 ? __ldg(w1 + i) : 1.0);
+      } else {
+        cs_st256(rec + pos[u], __ldg(x + 3 * i), __ldg(x + 3 * i + 1), __ldg(x + 3 * i + 2), __ldg(y + i));
+        if (w1) ws1[pos[u]] = __ldg(w1 + i);
+      }
     }
   }
+}
+
+// off[c] = exclusive prefix of the bucket sizes tot[c] (off[ncell] = N), iof[c] = exclusive prefix of
+// the work items per bucket ceil(tot[c] / kCsRun) (iof[ncell] = item count): one CTA of 1024
+// threads, each scanning a contiguous slice serially, one block scan of the slice totals
+__global__ void k_cs_offsets(const long long *__restrict__ tot, int ncell, long long *__restrict__ off,
+                             long long *__restrict__ iof) {
+  extern __shared__ unsigned cs_t[];  // bucket sizes (< 2^32: N < 2^32 per call), staged coalesced
+  __shared__ long long wsum[2][32];
+  for (int c = threadIdx.x; c < ncell; c += blockDim.x) cs_t[c] = (unsigned)tot[c];
+  __syncthreads();
+  const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, wid = t >> 5;
+  const int per = (ncell + nt - 1) / nt, a = t * per, e = min(ncell, a + per);
+  long long s = 0, si = 0;
+  for (int c = a; c < e; ++c) {
+    const unsigned v = cs_t[c];
+    s += v;
+    si += (v + kCsRun - 1) / kCsRun;
+  }
+  long long incl = s, incli = si;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long v = __shfl_up_sync(0xffffffffu, incl, o), vi = __shfl_up_sync(0xffffffffu, incli, o);
+    if (lane >= o) {
+      incl += v;
+      incli += vi;
+    }
+  }
+  if (lane == 31) {
+    wsum[0][wid] = incl;
+    wsum[1][wid] = incli;
+  }
+  __syncthreads();
+  if (wid < 2) {
+    long long w = lane < (nt >> 5) ? wsum[wid][lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long v = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += v;
+    }
+    wsum[wid][lane] = w;
+  }
+  __syncthreads();
+  long long run = incl - s + (wid > 0 ? wsum[0][wid - 1] : 0);
+  long long runi = incli - si + (wid > 0 ? wsum[1][wid - 1] : 0);
+  for (int c = a; c < e; ++c) {
+    const unsigned v = cs_t[c];
+    iof[c] = runi;
+    runi += (v + kCsRun - 1) / kCsRun;
+    cs_t[c] = (unsigned)run;  // exclusive offset (< 2^32), written out coalesced below
+    run += v;
+  }
+  if (t == nt - 1) {
+    off[ncell] = run;
+    iof[ncell] = runi;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < ncell; c += blockDim.x) off[c] = cs_t[c];
+}
+
+// the work items of bucket c: runs of <= kCsRun records (thread per bucket)
+__global__ void k_cs_items(const long long *__restrict__ off, const long long *__restrict__ iof, int ncell,
+                           CsItem *__restrict__ items) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncell) return;
+  long long it = iof[c];
+  for (long long b = off[c]; b < off[c + 1]; b += kCsRun, ++it)
+    items[it] = CsItem{b, b + kCsRun < off[c + 1] ? b + kCsRun : off[c + 1], c, 0};
 }
 
 __device__ __forceinline__ int cs_wrap(int i, int n) {
@@ -106,7 +189,7 @@ __device__ __forceinline__ int cs_wrap(int i, int n) {
 }
 
 template <int D, int W, int G>
-__global__ void __launch_bounds__(kCsThreads) k_cs_spread(const CsItem *__restrict__ items, int64_t nitems,
+__global__ void __launch_bounds__(kCsThreads) k_cs_spread(const CsItem *__restrict__ items, const long long *__restrict__ nitems_dev,
                                                           const double4 *__restrict__ rec,
                                                           const double *__restrict__ ws1, int64_t N,
                                                           double *__restrict__ g1, double *__restrict__ g2,
@@ -119,6 +202,7 @@ __global__ void __launch_bounds__(kCsThreads) k_cs_spread(const CsItem *__restri
   double(*ws)[D * U + 2] = wsm[wid];
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nitems = *nitems_dev;
   for (int64_t it = warp; it < nitems; it += nwarps) {
     const CsItem item = items[it];
     int sc[D];
@@ -164,6 +248,7 @@ __global__ void __launch_bounds__(kCsThreads) k_cs_spread(const CsItem *__restri
       }
       __syncwarp();
       const int np = (int)min(32LL, item.end - b0);
+#pragma unroll 4
       for (int p = 0; p < np; ++p) {
         const double yv = ws[p][D * U], wv = ws[p][D * U + 1];
 #pragma unroll
@@ -200,6 +285,122 @@ __global__ void __launch_bounds__(kCsThreads) k_cs_spread(const CsItem *__restri
   }
 }
 
+// 2D spread with a quarter-warp layout (c3): batches of 32 points as in k_cs_spread (lane p evaluates
+// point p's weights into a shared row), then the warp accumulates 4 points at a time: quarter q = lane / 8
+// takes point 4 i + q, lane c = lane % 8 owns the window columns b = c, c + 8, .. (< U) and every row a.
+// Per point a lane loads w2[b] once and the U row weights w1[.] as broadcast 16-byte pairs, so a point
+// costs ~2 shared wavefronts instead of 5 (r01 layout: every lane two elements, two loads each; the
+// shared-memory pipe was the limit), with the same 2 U^2 FMAs.  The four quarters' partial windows are
+// summed by shuffles at the end of a run; quarter q then issues the REDs of rows a = q mod 4.
+template <int W, int G>
+__global__ void __launch_bounds__(kCsThreads) k_cs_spread2q(const CsItem *__restrict__ items,
+                                                            const long long *__restrict__ nitems_dev,
+                                                            const double4 *__restrict__ rec, double *__restrict__ g1,
+                                                            double *__restrict__ g2, double h, int n, int lo, int S,
+                                                            EsPoly P) {
+  constexpr int U = W + G - 1;                  // union window per dimension of a super-cell
+  constexpr int RW = (2 * U + 2 + 1) / 2 * 2;   // row: w1[U], w2[U], y, strength-1 weight (16-byte multiple)
+  constexpr int NB = (U + 7) / 8;               // columns per lane
+  __shared__ __align__(16) double wsm[kCsThreads / 32][32][RW];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, qd = lane >> 3, c8 = lane & 7;
+  double(*ws)[RW] = wsm[wid];
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nitems = *nitems_dev;
+  for (int64_t it = warp; it < nitems; it += nwarps) {
+    const CsItem item = items[it];
+    const int sc0 = item.cell / S, sc1 = item.cell % S;
+    double a1[U][NB], ay[U][NB];
+#pragma unroll
+    for (int a = 0; a < U; ++a)
+#pragma unroll
+      for (int k = 0; k < NB; ++k) a1[a][k] = ay[a][k] = 0.0;
+    for (long long b0 = item.begin; b0 < item.end; b0 += 32) {
+      const long long r = b0 + lane;
+      __syncwarp();
+      double *myrow = ws[lane];
+      if (r < item.end) {
+        const double4 rv = rec[r];  // (x1, x2, y, strength-1 weight)
+        const double xr[2] = {rv.x, rv.y};
+        const int scs[2] = {sc0, sc1};
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          double w[W];
+          const int i0 = es_weights<W>(h * xr[k] * (double)n, P, w);
+          if constexpr (G == 1) {
+#pragma unroll
+            for (int a = 0; a < W; ++a) myrow[k * U + a] = w[a];
+          } else {
+            int off = i0 - lo - scs[k] * G;  // start cell within the super-cell, 0..G-1
+            off = off < 0 ? 0 : (off > G - 1 ? G - 1 : off);
+#pragma unroll
+            for (int a = 0; a < U; ++a) {
+              double v = 0.0;
+#pragma unroll
+              for (int o = 0; o < G; ++o)
+                if (o == off && a - o >= 0 && a - o < W) v = w[a - o];
+              myrow[k * U + a] = v;
+            }
+          }
+        }
+        *reinterpret_cast<double2 *>(myrow + 2 * U) = make_double2(rv.z, rv.w);
+      } else {
+#pragma unroll
+        for (int q = 0; q < RW; q += 2) *reinterpret_cast<double2 *>(myrow + q) = make_double2(0.0, 0.0);
+      }
+      __syncwarp();
+      const int np = (int)min(32LL, item.end - b0);
+      for (int p0 = 0; p0 < np; p0 += 4) {
+        const double *wr = ws[p0 + qd];  // rows past np are zero, so they add nothing
+        double w2[NB];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) w2[k] = c8 + 8 * k < U ? wr[U + c8 + 8 * k] : 0.0;
+        const double2 yw = *reinterpret_cast<const double2 *>(wr + 2 * U);
+#pragma unroll
+        for (int a = 0; a < U; a += 2) {
+          const double2 wa = *reinterpret_cast<const double2 *>(wr + a);  // (w1[a], w1[a+1]); w1[U] = w2[0] if U odd
+#pragma unroll
+          for (int k = 0; k < NB; ++k) {
+            const double f0 = wa.x * w2[k];
+            a1[a][k] = fma(f0, yw.y, a1[a][k]);
+            ay[a][k] = fma(f0, yw.x, ay[a][k]);
+            if (a + 1 < U) {
+              const double f1 = wa.y * w2[k];
+              a1[a + 1][k] = fma(f1, yw.y, a1[a + 1][k]);
+              ay[a + 1][k] = fma(f1, yw.x, ay[a + 1][k]);
+            }
+          }
+        }
+      }
+    }
+    // sum the four quarters (butterfly: every lane gets the totals of its columns), then quarter qd
+    // adds rows a = qd mod 4 to the fine grids
+#pragma unroll
+    for (int a = 0; a < U; ++a)
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        a1[a][k] += __shfl_xor_sync(0xffffffffu, a1[a][k], 8);
+        a1[a][k] += __shfl_xor_sync(0xffffffffu, a1[a][k], 16);
+        ay[a][k] += __shfl_xor_sync(0xffffffffu, ay[a][k], 8);
+        ay[a][k] += __shfl_xor_sync(0xffffffffu, ay[a][k], 16);
+      }
+#pragma unroll
+    for (int a = 0; a < U; ++a) {
+      if ((a & 3) != qd) continue;
+      const int64_t rowi = (int64_t)cs_wrap(sc0 * G + lo + a, n) * n;
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        const int b = c8 + 8 * k;
+        if (b < U && (a1[a][k] != 0.0 || ay[a][k] != 0.0)) {
+          const int64_t gi = rowi + cs_wrap(sc1 * G + lo + b, n);
+          atomicAdd(g1 + gi, a1[a][k]);
+          atomicAdd(g2 + gi, ay[a][k]);
+        }
+      }
+    }
+  }
+}
+
 // super-cell size: 1 in 2D (2 when the start-cell count does not fit the shared-memory histogram,
 // e.g. m = 94), 4 in 3D
 bool cellsort_geometry(const Params &p, int &lo, int &S, int &ncell, int &G) {
@@ -227,13 +428,15 @@ static efgp_status cellsort_t(efgp_plan *pl, const double *x, const double *y, c
   if (!cellsort_geometry(P, lo, S, ncell, Gs) || Gs != G) return EFGP_ERR_RESOURCE;
   const int B = sort_ctas(pl->num_sms), T = 1024, n = (int)P.n1;
   unsigned *hist = nullptr;
-  long long *tot = nullptr, *off = nullptr;
+  long long *tot = nullptr, *off = nullptr, *iof = nullptr;
   double4 *rec = nullptr;
   double *ws1 = nullptr;
   CsItem *items = nullptr;
   EFGP_PALLOC(&hist, sizeof(unsigned) * B * ncell, s);
   EFGP_PALLOC(&tot, sizeof(long long) * ncell, s);
   EFGP_PALLOC(&off, sizeof(long long) * (ncell + 1), s);
+  EFGP_PALLOC(&iof, sizeof(long long) * (ncell + 1), s);
+  EFGP_PALLOC(&items, sizeof(CsItem) * ((N + kCsRun - 1) / kCsRun + ncell), s);
   EFGP_PALLOC(&rec, sizeof(double4) * N, s);
   if (w1 && D == 3) EFGP_PALLOC(&ws1, sizeof(double) * N, s);
   const size_t sm = sizeof(unsigned) * ncell;
@@ -241,28 +444,32 @@ static efgp_status cellsort_t(efgp_plan *pl, const double *x, const double *y, c
   EFGP_CUDA(cudaFuncSetAttribute(k_cs_scatter<D, W, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_cs_count<D, W, G><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, pl->dflags);
   k_het_colscan<<<(ncell + 255) / 256, 256, 0, s>>>(hist, B, ncell, tot);
-  k_het_offsets<<<1, 1024, 0, s>>>(tot, ncell, off);
+  EFGP_CUDA(cudaFuncSetAttribute(k_cs_offsets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_cs_offsets<<<1, 1024, sm, s>>>(tot, ncell, off, iof);
   k_cs_scatter<D, W, G><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, off, rec, pl->dflags, w1, ws1);
+  // work items on the device (no host round trip): at most ceil(N / kCsRun) + ncell of them
+  k_cs_items<<<(ncell + 255) / 256, 256, 0, s>>>(off, iof, ncell, items);
   EFGP_CUDA(cudaGetLastError());
-  std::vector<long long> offh(ncell + 1);
-  EFGP_CUDA(cudaMemcpyAsync(offh.data(), off, sizeof(long long) * (ncell + 1), cudaMemcpyDeviceToHost, s));
-  EFGP_CUDA(cudaStreamSynchronize(s));
-  std::vector<CsItem> it;
-  for (int c = 0; c < ncell; ++c)
-    for (long long b = offh[c]; b < offh[c + 1]; b += kCsRun)
-      it.push_back(CsItem{b, std::min<long long>(b + kCsRun, offh[c + 1]), c, 0});
-  const int64_t nitems = (int64_t)it.size();
-  EFGP_PALLOC(&items, sizeof(CsItem) * std::max<size_t>(it.size(), 1), s);
-  EFGP_CUDA(cudaMemcpyAsync(items, it.data(), sizeof(CsItem) * it.size(), cudaMemcpyHostToDevice, s));
   int per_sm = 1;
-  EFGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cs_spread<D, W, G>, kCsThreads, 0));
-  int64_t blocks = std::min<int64_t>((int64_t)pl->num_sms * std::max(per_sm, 1), (nitems * 32 + kCsThreads - 1) / kCsThreads);
-  if (nitems > 0)
-    k_cs_spread<D, W, G><<<(unsigned)std::max<int64_t>(blocks, 1), kCsThreads, 0, s>>>(items, nitems, rec, ws1, N, pl->g1,
-                                                                                     pl->g2, P.h, n, lo, S, P.poly);
+  // quarter-warp 2D layout for union windows up to 12 (EFGP_CS_R01: the r01 layout)
+  constexpr bool kQ2 = D == 2 && W + G - 1 <= 12;
+  const bool q2 = kQ2 && !getenv("EFGP_CS_R01");
+  if constexpr (kQ2) {
+    if (q2) EFGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cs_spread2q<W, G>, kCsThreads, 0));
+  }
+  if (!q2) EFGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cs_spread<D, W, G>, kCsThreads, 0));
+  const int64_t max_items = (N + kCsRun - 1) / kCsRun + ncell;
+  int64_t blocks = std::min<int64_t>((int64_t)pl->num_sms * std::max(per_sm, 1), (max_items * 32 + kCsThreads - 1) / kCsThreads);
+  if constexpr (kQ2) {
+    if (q2)
+      k_cs_spread2q<W, G><<<(unsigned)std::max<int64_t>(blocks, 1), kCsThreads, 0, s>>>(items, iof + ncell, rec, pl->g1,
+                                                                                      pl->g2, P.h, n, lo, S, P.poly);
+  }
+  if (!q2)
+    k_cs_spread<D, W, G><<<(unsigned)std::max<int64_t>(blocks, 1), kCsThreads, 0, s>>>(items, iof + ncell, rec, ws1, N,
+                                                                                       pl->g1, pl->g2, P.h, n, lo, S, P.poly);
   EFGP_CUDA(cudaGetLastError());
-  EFGP_CUDA(cudaStreamSynchronize(s));  // the host item vector is consumed by the copy above
-  for (void *p : {(void *)hist, (void *)tot, (void *)off, (void *)rec, (void *)items}) cudaFreeAsync(p, s);
+  for (void *p : {(void *)hist, (void *)tot, (void *)off, (void *)iof, (void *)rec, (void *)items}) cudaFreeAsync(p, s);
   if (ws1) cudaFreeAsync(ws1, s);
   return EFGP_OK;
 }
