@@ -216,9 +216,19 @@ __global__ void k_cg_p(const double2 *__restrict__ r, double2 *__restrict__ p, c
   const double bcg = rr_new / st->rr_old;
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Mh; q += (int64_t)gridDim.x * blockDim.x) {
     const double2 rq = r[q], pp = p[q];
-    p[q] = make_double2(rq.x + bcg * pp.x, rq.y + bcg * pp.y);
+    const double2 pn = make_double2(rq.x + bcg * pp.x, rq.y + bcg * pp.y);
+    p[q] = pn;
+    if (X) {  // partial-transform product (toeplitz_pt): scatter D p into its slab (X = pt_P, box = L^(d-1))
+      int j[D];
+      decode_half<D>(q, m, j);
+      int64_t o = 0;
+#pragma unroll
+      for (int k = 0; k < D - 1; ++k) o = o * L + (j[k] < 0 ? j[k] + L : j[k]);
+      const double dq = Dh[q];
+      X[(int64_t)j[D - 1] * box + o] = make_double2(dq * pn.x, dq * pn.y);
+    }
   }
-  // grid-wide dependency: the pad below reads p written by other blocks -> separate kernel
+  // grid-wide dependency: the padded-FFT path's pad reads p written by other blocks -> separate kernel
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->rr = rr_new;
     const long long it = st->iter + 1;
@@ -999,11 +1009,10 @@ static efgp_status enqueue_iteration(efgp_plan *pl, cudaStream_t s, CGState *st,
   EFGP_CUDA(launch_pdl(k_cg_xr, nb, kCGThreads, s, pl->x, pl->r, pl->p, pl->Ap, P.Mh, (int)P.m, st, part_pAp,
                        part_rr, (int)nb, (const double *)nullptr));
   }
-  EFGP_CUDA(launch_pdl(k_cg_p<D>, nb, kCGThreads, s, pl->r, pl->p, pl->D_half, P.Mh, (int)P.m, P.L, pl->Xbox, box,
-                       st, part_rr, (int)nb, pl->hist));
-  if (pt)
-    EFGP_TRY(pt_pad<D>(pl, pl->p, s));
-  else if (!direct)
+  EFGP_CUDA(launch_pdl(k_cg_p<D>, nb, kCGThreads, s, pl->r, pl->p, pl->D_half, P.Mh, (int)P.m, P.L,
+                       pt ? pl->pt_P : (double2 *)nullptr, pt ? ipow_(P.L, D - 1) : (int64_t)0, st, part_rr, (int)nb,
+                       pl->hist));
+  if (!direct && !pt)
     EFGP_CUDA(launch_pdl(k_cg_pad<D>, nbox, kCGThreads, s, pl->p, pl->D_half, (int)P.m, P.L, pl->Xbox, box,
                          (const CGState *)st));
   EFGP_CUDA(cudaGetLastError());

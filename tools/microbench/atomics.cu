@@ -28,6 +28,10 @@ __global__ void __launch_bounds__(1024) k_smem(double* out, int iters, int words
       int a=(s>>8)&(mask_u-7); 
       #pragma unroll
       for(int c=0;c<5;++c) atomicAdd(&su[a+c], s+c); }
+    else if(MODE==4){ // int64 fixed-point accumulation (survey §7 step 4(d)): 64-bit integer shared atomics
+      unsigned long long* sl=(unsigned long long*)sm; atomicAdd(&sl[(s>>8)&mask_d], (unsigned long long)s); }
+    else if(MODE==5){ // fp32 shared atomicAdd (native RED/ATOMS.ADD.F32)
+      float* sf=(float*)sm; atomicAdd(&sf[(s>>8)&mask_u], (float)(s&255)); }
   }
   __syncthreads();
   if(threadIdx.x==0){ double t=0; for(int i=0;i<64;++i) t+=su[i]; out[blockIdx.x]=t+acc; }
@@ -64,9 +68,12 @@ int main(){
   CK(cudaFuncSetAttribute(k_smem<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CK(cudaFuncSetAttribute(k_smem<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CK(cudaFuncSetAttribute(k_smem<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CK(cudaFuncSetAttribute(k_smem<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CK(cudaFuncSetAttribute(k_smem<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int words=32768; // 128 KB region
-  const char* names[4]={"smem_u32_atomicAdd","smem_f64_atomicAdd_CAS","smem_f64_nonatomic_RMW","smem_u32_atomicAdd_5consec"};
-  for(int mode=0;mode<4;++mode){
+  const char* names[6]={"smem_u32_atomicAdd","smem_f64_atomicAdd_CAS","smem_f64_nonatomic_RMW","smem_u32_atomicAdd_5consec",
+                        "smem_u64_atomicAdd_fixedpoint","smem_f32_atomicAdd"};
+  for(int mode=0;mode<6;++mode){
     for(int thr: {256,1024}){
       int iters=4096;
       for(int rep=0;rep<2;++rep){
@@ -75,6 +82,8 @@ int main(){
         if(mode==1) k_smem<1><<<nsm,thr,smem>>>(out,iters,words);
         if(mode==2) k_smem<2><<<nsm,thr,smem>>>(out,iters,words);
         if(mode==3) k_smem<3><<<nsm,thr,smem>>>(out,iters,words);
+        if(mode==4) k_smem<4><<<nsm,thr,smem>>>(out,iters,words);
+        if(mode==5) k_smem<5><<<nsm,thr,smem>>>(out,iters,words);
         cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
         float ms; cudaEventElapsedTime(&ms,e0,e1);
         double ops=(double)nsm*thr*iters*(mode==3?5:1);
