@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define EFGP_ABI_VERSION 5
+#define EFGP_ABI_VERSION 6
 
 typedef struct efgp_plan *efgp_handle;
 
@@ -140,6 +140,8 @@ typedef struct {
   int64_t precond;       /* preconditioner the last fit used (NONE, KRON or JACOBI; AUTO resolved; NONE after a NUFFT-pair hetero fit) */
   int64_t comm_size;     /* ranks of the handle's NCCL communicator (0: none) */
   int64_t spread_fallback; /* efgp_spread_fallback of the last fit (NONE: the planned method ran) */
+  int64_t cg_persist_split; /* direct 2D CG (c3, c5): k1 splits of the persistent one-kernel loop of the
+                              last fit; 0 when the launched per-iteration kernels ran */
 } efgp_info;
 
 /* Fill *opt with defaults (all zero / automatic). */

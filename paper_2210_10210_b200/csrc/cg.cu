@@ -933,6 +933,287 @@ __global__ void k_cg_xr2(double2 *__restrict__ x, double2 *__restrict__ r, const
   }
 }
 
+// ---- persistent direct CG (2D, small m: c3, c5) ------------------------------------------------
+// The whole CG loop of the direct path (same recurrences and stopping rule as k_cg_xr + k_cg_p,
+// reading G6) as ONE cooperative kernel with ONE grid barrier per iteration:
+//   phase 1: p_j = r_j + beta_j p_{j-1}, then the split direct product A p_j (CTA (row, split); the
+//            last CTA of a row adds the row's splits in fixed order, applies D and sigma^2 and writes
+//            the row's <p, Ap> partial);
+//   grid barrier;
+//   phase 2: alpha = rr_j / <p_j, A p_j>, r_{j+1} = r_j - alpha A p_j and ||r_{j+1}||^2, beta_{j+1},
+//            the stop test.
+// The M_h-entry vectors r and p are small (21 KB each for c5), so EVERY CTA keeps its own copy in
+// shared memory and updates all of it in phase 2 from the exchanged A p_j: the sums of phase 2 are
+// formed in the same fixed order in every CTA, so all CTAs hold bitwise-equal r, p, rr and take the
+// same stop decision, and the second grid-wide reduction of the launched path (||r||^2 before
+// beta) needs no barrier.  Only A p_j and the <p, Ap> row partials cross CTAs; they are
+// double-buffered by iteration parity (a CTA can be at most one phase ahead of the slowest: the
+// barrier of iteration j+1 waits for everyone's phase 2 of iteration j).  x is updated by the CTA
+// that owns each entry.  The v rows a CTA convolves with are staged once for all iterations.
+// Data written by other CTAs is read with ld.global.cg (L2), never through the non-coherent paths.
+__device__ __forceinline__ unsigned ld_acq_gpu(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+struct PersistGeom {  // CTA (row, split) of the persistent direct CG; nsplit is a launch parameter
+  int n, nv, nout, ngrp, nk, nc, Mh;
+  __host__ __device__ PersistGeom(int m, int nsplit, int threads) {
+    n = 2 * m + 1;
+    nv = 4 * m + 1;
+    nout = m + 1;
+    ngrp = (nout + 3) / 4;
+    nk = (n + nsplit - 1) / nsplit;
+    nc = threads / (ngrp * nk);
+    Mh = n * nout;
+  }
+  __host__ __device__ bool ok() const { return nc >= 1; }  // every (output group, k1 row) has a thread
+  __host__ __device__ size_t smem() const {
+    return sizeof(double2) * ((size_t)nk * n + (size_t)nk * nv + (size_t)nk * nc * nout + 2 * (size_t)Mh);
+  }
+};
+constexpr int kPersistThreads = 256;
+
+__global__ void __launch_bounds__(kPersistThreads) k_cg_toep2_persist(
+    const double2 *__restrict__ vfull, const double *__restrict__ Dh, double2 *x, double2 *r, double2 *p0,
+    double2 *ap0, double2 *ap1, int m, int nsplit, CGState *st, double2 *tpart, unsigned *tcnt, double *part_pAp,
+    double *hist, unsigned *gbar) {
+  extern __shared__ double2 tsm[];
+  __shared__ double sh[40];
+  __shared__ bool last_s;
+  const PersistGeom G(m, nsplit, kPersistThreads);
+  const int n = G.n, nv = G.nv, nout = G.nout, ngrp = G.ngrp, nk = G.nk, nc = G.nc, Mh = G.Mh;
+  const int row = (int)blockIdx.x % n, spl = (int)blockIdx.x / n, j1 = row - m;
+  const int k1a = min(n, spl * nk), k1b = min(n, k1a + nk), nkr = k1b - k1a;
+  const int clen = (n + nc - 1) / nc;
+  double2 *u = tsm, *vr = u + nk * n, *red = vr + nk * nv, *rs = red + nk * nc * nout, *ps = rs + Mh;
+  for (int idx = threadIdx.x; idx < nkr * nv; idx += blockDim.x) {  // once for all iterations
+    const int k1 = k1a + idx / nv - m, sc = idx % nv;
+    vr[idx] = vfull[(int64_t)(j1 - k1 + 2 * m) * nv + sc];
+  }
+  for (int i = threadIdx.x; i < Mh; i += blockDim.x) rs[i] = ps[i] = r[i];  // r_0 = b (k_cg_init)
+  const int t = threadIdx.x, g4 = t % ngrp, kk = (t / ngrp) % nk, c = t / (ngrp * nk), j2b = 4 * g4;
+  const double tol = st->tol, bnorm = st->bnorm, s2 = st->sigma2;
+  const long long max_iter = st->max_iter;
+  long long it = st->iter;
+  if (st->done) return;  // (rr = 0: decided by k_cg_init2, the same in every CTA)
+  double rr = st->rrs[0], beta = 0.0;
+  unsigned target = 0;
+  const int own_lo = (int)blockIdx.x * kPersistThreads, own_hi = min(Mh, own_lo + kPersistThreads);
+  __syncthreads();
+  for (;;) {
+    const int q = (int)(it & 1);
+    double2 *Ap = q ? ap1 : ap0;
+    double *pAp = part_pAp + q * n;
+    // phase 1: p_j (all entries, every CTA), u = D p_j on this split's k1 rows (canonical half:
+    // exactly Hermitian, see k_cg_toep2), the product
+    for (int i = threadIdx.x; i < Mh; i += blockDim.x) {
+      const double2 rq = rs[i], po = ps[i];
+      ps[i] = make_double2(rq.x + beta * po.x, rq.y + beta * po.y);
+    }
+    for (int idx = threadIdx.x; idx < nk * nc * nout; idx += blockDim.x) red[idx] = make_double2(0.0, 0.0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nkr * n; idx += blockDim.x) {
+      int k1 = k1a + idx / n - m, k2 = idx % n - m;
+      const bool neg = k2 < 0 || (k2 == 0 && k1 < 0);
+      if (neg) {
+        k1 = -k1;
+        k2 = -k2;
+      }
+      const int qq = (k1 + m) * (m + 1) + k2;
+      const double2 pp = ps[qq];
+      const double dq = Dh[qq];
+      u[idx] = make_double2(dq * pp.x, neg ? -dq * pp.y : dq * pp.y);
+    }
+    __syncthreads();
+    if (c < nc && kk < nkr) {
+      const int c2a = c * clen, c2b = min(n, c2a + clen);
+      double re[4] = {0.0, 0.0, 0.0, 0.0}, im[4] = {0.0, 0.0, 0.0, 0.0};
+      const double2 *ur = u + kk * n, *vrow = vr + kk * nv;
+      double2 w[4];
+#pragma unroll
+      for (int o = 0; o < 4; ++o)
+        w[o] = (j2b + o <= m && c2a < c2b) ? vrow[j2b + o - c2a + 3 * m] : make_double2(0.0, 0.0);
+      for (int c2 = c2a; c2 < c2b; ++c2) {
+        const double2 b = ur[c2];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+          re[o] = fma(w[o].x, b.x, fma(-w[o].y, b.y, re[o]));
+          im[o] = fma(w[o].x, b.y, fma(w[o].y, b.x, im[o]));
+        }
+#pragma unroll
+        for (int o = 3; o > 0; --o) w[o] = w[o - 1];
+        w[0] = (c2 + 1 < c2b) ? vrow[j2b - (c2 + 1) + 3 * m] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int o = 0; o < 4; ++o)
+        if (j2b + o <= m) red[(kk * nc + c) * nout + j2b + o] = make_double2(re[o], im[o]);
+    }
+    __syncthreads();
+    {  // the nk nc partial rows of this CTA, in two fixed-order stages (u is free: it holds them)
+      const int spl2 = min(kPersistThreads / nout, nk * n / nout), np = nk * nc;
+      if (t < spl2 * nout) {
+        const int o = t % nout, g = t / nout;
+        double2 a = make_double2(0.0, 0.0);
+        for (int k = g; k < np; k += spl2) {
+          a.x += red[k * nout + o].x;
+          a.y += red[k * nout + o].y;
+        }
+        u[g * nout + o] = a;
+      }
+      __syncthreads();
+      if (t < nout) {
+        double2 o = make_double2(0.0, 0.0);
+        for (int g = 0; g < spl2; ++g) {
+          o.x += u[g * nout + t].x;
+          o.y += u[g * nout + t].y;
+        }
+        tpart[((int64_t)row * nsplit + spl) * nout + t] = o;
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (t == 0) last_s = atomicAdd(tcnt + row, 1u) == (unsigned)nsplit - 1;
+    __syncthreads();
+    if (last_s) {
+      __threadfence();
+      double acc = 0.0;
+      if (t < nout && !(t == 0 && j1 < 0)) {  // (j1 < 0, 0) is written by row -j1 as the conjugate
+        double2 tv[kToepSplitsHost];  // all loads first, then the fixed-order sum
+#pragma unroll
+        for (int k = 0; k < kToepSplitsHost; ++k)
+          tv[k] = k < nsplit ? __ldcg(tpart + ((int64_t)row * nsplit + k) * nout + t) : make_double2(0.0, 0.0);
+        double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < kToepSplitsHost; ++k) {
+          o.x += tv[k].x;
+          o.y += tv[k].y;
+        }
+        const int qq = (j1 + m) * (m + 1) + t;
+        const double2 pp = ps[qq];
+        const double dq = Dh[qq];
+        double2 a = make_double2(dq * o.x + s2 * pp.x, dq * o.y + s2 * pp.y);
+        if (t == 0 && j1 == 0) a.y = s2 * pp.y;  // j = 0: (T u)_0 is real
+        Ap[qq] = a;
+        acc = (t ? 2.0 : 1.0) * (pp.x * a.x + pp.y * a.y);
+        if (t == 0 && j1 > 0) {  // the mirrored entry (-j1, 0) = conj, with the canonical p
+          Ap[(m - j1) * (m + 1)] = make_double2(a.x, -a.y);
+          acc *= 2.0;
+        }
+      }
+      acc = block_sum(acc, sh);
+      if (t == 0) {
+        pAp[row] = acc;
+        tcnt[row] = 0;  // for the next product
+        __threadfence();
+        atomicAdd(gbar, 1u);  // the row is complete (arrivals: one per row, 2m+1 per iteration)
+      }
+    }
+    // grid barrier: every row's A p_j and <p, Ap> partial are written
+    target += n;
+    if (t == 0)
+      while (ld_acq_gpu(gbar) < target) {
+      }
+    __syncthreads();
+    // phase 2 (every CTA, the same fixed order): alpha, x (owned entries), r and ||r||^2, beta, stop
+    double v = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) v += __ldcg(pAp + i);
+    v = block_sum(v, sh);
+    if (threadIdx.x == 0) sh[32] = v;
+    __syncthreads();
+    const double alpha = rr / sh[32];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < Mh; i += blockDim.x) {
+      const double2 a = __ldcg(Ap + i), pp = ps[i];
+      double2 rq = rs[i];
+      rq.x -= alpha * a.x;
+      rq.y -= alpha * a.y;
+      rs[i] = rq;
+      acc += ((i % (m + 1)) ? 2.0 : 1.0) * (rq.x * rq.x + rq.y * rq.y);
+      if (i >= own_lo && i < own_hi) {
+        double2 xx = x[i];
+        xx.x += alpha * pp.x;
+        xx.y += alpha * pp.y;
+        x[i] = xx;
+        r[i] = rq;
+        p0[i] = pp;
+      }
+    }
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) sh[33] = acc;
+    __syncthreads();
+    const double rr_new = sh[33];
+    ++it;
+    beta = rr_new / rr;
+    const double rr_prev = rr;
+    rr = rr_new;
+    const double rel = sqrt(rr_new) / bnorm;
+    const int stop = rel <= tol ? 1 : (it >= max_iter ? 2 : 0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->rr = rr_new;
+      st->rr_old = rr_prev;
+      st->rrs[it & 1] = rr_new;
+      st->iter = it;
+      hist[it] = rel;
+      if (stop) st->done = stop;
+    }
+    if (stop) return;
+    __syncthreads();  // sh[32], sh[33] reusable
+  }
+}
+
+static int persist_split_env() {
+  const char *e = getenv("EFGP_CG_PSPLIT");
+  return (e && atoi(e) > 0) ? atoi(e) : 0;
+}
+static bool cg_persist() {
+  const char *e = getenv("EFGP_CG_PERSIST");
+  return !(e && e[0] == '0');
+}
+
+// One cooperative launch runs the whole CG (returns cudaErrorNotSupported when the grid cannot be
+// co-resident: the caller then takes the launched path).
+static cudaError_t launch_persist_cg(efgp_plan *pl, CGState *st, cudaStream_t s) {
+  const Params &P = pl->P;
+  const int m = (int)P.m, n = 2 * m + 1;
+  int dev = 0, coop = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop) return cudaErrorNotSupported;
+  int nsplit = persist_split_env() ? persist_split_env() : kToepSplitsHost;
+  for (; nsplit >= 1; --nsplit) {
+    const PersistGeom G(m, nsplit, kPersistThreads);
+    const size_t smem = G.smem();
+    if (!G.ok() || smem > 200 * 1024 || 2 * n > pl->cg_blocks) continue;
+    cudaError_t e = cudaFuncSetAttribute(k_cg_toep2_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_toep2_persist, kPersistThreads, smem);
+    if (e != cudaSuccess) return e;
+    if ((int64_t)per_sm * pl->num_sms < (int64_t)n * nsplit || nsplit > kToepSplitsHost) continue;
+    if (!pl->cg_gbar) {
+      e = cudaMalloc((void **)&pl->cg_gbar, sizeof(unsigned));
+      if (e != cudaSuccess) return e;
+    }
+    e = cudaMemsetAsync(pl->cg_gbar, 0, sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    double *part_pAp = pl->partials;  // two slots of 2m+1 row partials (cg_blocks >= 2 (2m+1))
+    const double2 *vfull = pl->vfull;
+    const double *Dh = pl->D_half;
+    double2 *x = pl->x, *r = pl->r, *p0 = pl->p, *ap0 = pl->Ap, *ap1 = pl->p2, *tpart = pl->toep_part;
+    unsigned *tcnt = pl->toep_cnt, *gbar = pl->cg_gbar;
+    double *hist = pl->hist;
+    void *args[] = {(void *)&vfull, (void *)&Dh, (void *)&x, (void *)&r, (void *)&p0, (void *)&ap0, (void *)&ap1,
+                    (void *)&m, (void *)&nsplit, (void *)&st, (void *)&tpart, (void *)&tcnt, (void *)&part_pAp,
+                    (void *)&hist, (void *)&gbar};
+    pl->cg_persist_split = nsplit;
+    return cudaLaunchCooperativeKernel((const void *)k_cg_toep2_persist, dim3((unsigned)(n * nsplit)),
+                                       dim3(kPersistThreads), args, smem, s);
+  }
+  return cudaErrorNotSupported;
+}
+
 static bool cg_fused() {
   const char *e = getenv("EFGP_CG_FUSED");
   return !(e && e[0] == '0');
@@ -1064,6 +1345,25 @@ static efgp_status cg_solve_d(efgp_plan *pl, int64_t N_total) {
 
   int G = P.graph_iters;
   const bool fused = D == 2 && toeplitz_direct(P) && pl->p2 && pl->toep_part && cg_fused() && toep_split();
+  pl->cg_persist_split = 0;
+  if (fused && cg_persist()) {  // the whole loop in one cooperative kernel
+    const cudaError_t e = launch_persist_cg(pl, st, s);
+    if (e == cudaSuccess) {
+      CGState host{};
+      EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned, st, sizeof(CGState), cudaMemcpyDeviceToHost, s));
+      EFGP_CUDA(cudaStreamSynchronize(s));
+      std::memcpy(&host, pl->h_pinned, sizeof(CGState));
+      pl->iters = host.iter;
+      pl->rel_resid = host.bnorm > 0 ? std::sqrt(host.rr) / host.bnorm : 0.0;
+      return host.done == 2 ? EFGP_ERR_NOCONVERGE : EFGP_OK;
+    }
+    pl->cg_persist_split = 0;
+    if (e != cudaErrorNotSupported && e != cudaErrorCooperativeLaunchTooLarge) {
+      pl->err = "persistent CG launch failed";
+      return EFGP_ERR_CUDA;
+    }
+    cudaGetLastError();  // not co-resident: the launched path below
+  }
   if (fused) G += G & 1;  // the fused iterations alternate two p slots: an even count per graph
   if (!pl->cg_exec || pl->cg_exec_iters != G) {
     if (pl->cg_exec) cudaGraphExecDestroy(pl->cg_exec);

@@ -132,6 +132,8 @@ struct efgp_plan {
   double *Yr = nullptr;       // L^d real
   double *vhat = nullptr;     // L^d real, C2R(v)/L^d
   double2 *vfull = nullptr;   // (4m+1)^2 complex, full v (direct Toeplitz product, small m, 2D)
+  unsigned *cg_gbar = nullptr;    // persistent direct CG: software grid-barrier counter
+  int cg_persist_split = 0;       // k1 splits of the last persistent direct CG launch (0: not used)
   double2 *toep_part = nullptr;  // split direct product: (2m+1) x kToepSplitsHost x (m+1) partial rows
   unsigned *toep_cnt = nullptr;  // per output row: splits done (reset by the row's last CTA)
   double2 *Zbox = nullptr;    // R2C output

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in declared_functions() if not hasattr(lib, n)]
     assert not missing, missing
     assert set(declared_functions()) <= set(_lib.SIGNATURES)
-    assert _lib.load().efgp_abi_version() == 5
+    assert _lib.load().efgp_abi_version() == 6
 
 
 def test_library_is_sm100a_only():

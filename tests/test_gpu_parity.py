@@ -706,3 +706,38 @@ def test_load_and_get_weights_follow_the_callers_stream():
         g.load_weights(beta)                                        # must see the finished product
     assert np.allclose(g.weights(), 2.0 * full_to_half(full))
     g.close()
+
+
+@pytest.mark.parametrize("name", ["c5", "c3"])
+def test_persistent_direct_cg_matches_launched(name, monkeypatch):
+    # k_cg_toep2_persist (the whole direct CG in one cooperative kernel, the default for c3/c5) against
+    # the launched per-iteration kernels on the SAME v and F^*y (one spread, two solves), parity mode
+    # (eps/1000, reading G9): the two differ only in the order of floating-point sums, so beta agrees
+    # to the CG's own sensitivity (the launched path against itself with v, F^*y x (1 + 1e-13 n): 3.5e-5
+    # / 3.6e-6 at N = 1e7, tools/cg_persist_check.py) and the counts to a few percent; the persistent
+    # kernel is deterministic (two runs bitwise equal); max_iter is honoured
+    import torch
+    c = CONFIGS[name]
+    x, y, _ = generate(c, N=200_000, q=10)
+    g = model(c, cg_tol=c.eps / 1000)
+    modes = g.fit_local(dev(x), dev(y))
+    N = x.shape[0]
+    monkeypatch.setenv("EFGP_CG_PERSIST", "0")
+    g.fit_solve(modes, N)
+    it0, b0 = g.info()["iters"], g.weights()
+    assert g.info()["cg_persist_split"] == 0
+    monkeypatch.delenv("EFGP_CG_PERSIST")
+    g.fit_solve(modes, N)
+    it1, b1 = g.info()["iters"], g.weights()
+    assert g.info()["cg_persist_split"] >= 1
+    g.fit_solve(modes, N)
+    assert np.array_equal(g.weights(), b1) and g.info()["iters"] == it1
+    assert abs(it1 - it0) <= max(2, 0.1 * it0), (it0, it1)
+    assert np.abs(b1 - b0).max() <= 1e-4 * np.abs(b0).max(), np.abs(b1 - b0).max() / np.abs(b0).max()
+    torch.cuda.synchronize()
+    g2 = model(c, max_iter=7)
+    with pytest.warns(RuntimeWarning, match="max_iter"):
+        g2.fit_solve(modes, N)
+    assert g2.last_status == 1 and g2.info()["iters"] == 7 and len(g2.residual_history()) == 8
+    g.close()
+    g2.close()
