@@ -34,23 +34,54 @@ struct CsItem {
 };
 
 
-// super-cell key of point i; validates x in [0,1]^d and finite y (raises *err)
+// super-cell key of a point from its loaded coordinates; ok is false for x outside [0,1]^d or a
+// non-finite y (the caller raises *err once per batch: an atomic between the loads of a batch would
+// keep the compiler from hoisting the later loads above it)
 template <int D, int W, int G>
-__device__ __forceinline__ int cs_key(const double *__restrict__ x, const double *__restrict__ y, int64_t i, double h,
-                                      int n, int lo, int S, int *__restrict__ err) {
+__device__ __forceinline__ int cs_key_of(const double (&xv)[D], double yv, double h, int n, int lo, int S, bool &ok) {
   int key = 0;
-  bool ok = isfinite(__ldg(y + i));
+  ok = isfinite(yv);
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    const double xv = __ldg(x + i * D + k);
-    ok = ok && xv >= 0.0 && xv <= 1.0;
-    const double t = h * xv * (double)n;  // the expression es_weights' callers use (K1, K9)
+    ok = ok && xv[k] >= 0.0 && xv[k] <= 1.0;
+    const double t = h * xv[k] * (double)n;  // the expression es_weights' callers use (K1, K9)
     int c = ((int)ceil(__dsub_rn(t, 0.5 * W)) - lo) / G;
     c = c < 0 ? 0 : (c >= S ? S - 1 : c);
     key = key * S + c;
   }
-  if (!ok) atomicOr(err, 1);
   return key;
+}
+
+// kCsBatch points per thread per step: all loads first, then keys, cursor atomics and stores
+constexpr int kCsBatch = 4;
+template <int D>
+struct CsPts {
+  double x[kCsBatch][D], y[kCsBatch], w[kCsBatch];
+  int key[kCsBatch];
+};
+template <int D, int W, int G>
+__device__ __forceinline__ bool cs_load_batch(const double *__restrict__ x, const double *__restrict__ y,
+                                              const double *__restrict__ w1, int64_t i0, int64_t stride, int64_t e,
+                                              double h, int n, int lo, int S, CsPts<D> &P) {
+#pragma unroll
+  for (int u = 0; u < kCsBatch; ++u) {
+    const int64_t i = i0 + u * stride;
+    const int64_t j = i < e ? i : i0;  // (i0 < e: a valid index for the masked lanes)
+#pragma unroll
+    for (int k = 0; k < D; ++k) P.x[u][k] = __ldg(x + j * D + k);
+    P.y[u] = __ldg(y + j);
+    P.w[u] = w1 ? __ldg(w1 + j) : 1.0;
+  }
+  bool bad = false;
+#pragma unroll
+  for (int u = 0; u < kCsBatch; ++u) {
+    bool ok;
+    const int k = cs_key_of<D, W, G>(P.x[u], P.y[u], h, n, lo, S, ok);
+    const bool in = i0 + u * stride < e;
+    bad |= in && !ok;
+    P.key[u] = in ? k : -1;
+  }
+  return bad;
 }
 
 __device__ __forceinline__ void cs_range(int64_t N, int64_t &a, int64_t &e) {
@@ -60,14 +91,22 @@ __device__ __forceinline__ void cs_range(int64_t N, int64_t &a, int64_t &e) {
 }
 
 template <int D, int W, int G>
-__global__ void k_cs_count(const double *__restrict__ x, const double *__restrict__ y, int64_t N, double h, int n,
+__global__ void __launch_bounds__(1024) k_cs_count(const double *__restrict__ x, const double *__restrict__ y, int64_t N, double h, int n,
                            int lo, int S, int ncell, unsigned *__restrict__ hist, int *__restrict__ err) {
   extern __shared__ unsigned cs_h[];
   for (int i = threadIdx.x; i < ncell; i += blockDim.x) cs_h[i] = 0;
   __syncthreads();
   int64_t a, e;
   cs_range(N, a, e);
-  for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&cs_h[cs_key<D, W, G>(x, y, i, h, n, lo, S, err)], 1u);
+  bool bad = false;
+  for (int64_t i0 = a + threadIdx.x; i0 < e; i0 += kCsBatch * (int64_t)blockDim.x) {
+    CsPts<D> P;
+    bad |= cs_load_batch<D, W, G>(x, y, nullptr, i0, blockDim.x, e, h, n, lo, S, P);
+#pragma unroll
+    for (int u = 0; u < kCsBatch; ++u)
+      if (P.key[u] >= 0) atomicAdd(&cs_h[P.key[u]], 1u);
+  }
+  if (bad) atomicOr(err, 1);
   __syncthreads();
   for (int i = threadIdx.x; i < ncell; i += blockDim.x) hist[(size_t)blockIdx.x * ncell + i] = cs_h[i];
 }
@@ -77,7 +116,7 @@ __device__ __forceinline__ void cs_st256(double4 *p, double a, double b, double 
 }
 
 template <int D, int W, int G>
-__global__ void k_cs_scatter(const double *__restrict__ x, const double *__restrict__ y, int64_t N, double h, int n,
+__global__ void __launch_bounds__(1024) k_cs_scatter(const double *__restrict__ x, const double *__restrict__ y, int64_t N, double h, int n,
                              int lo, int S, int ncell, const unsigned *__restrict__ hist,
                              const long long *__restrict__ off, double4 *__restrict__ rec, int *__restrict__ err,
                              const double *__restrict__ w1, double *__restrict__ ws1) {
@@ -88,31 +127,29 @@ __global__ void k_cs_scatter(const double *__restrict__ x, const double *__restr
   __syncthreads();
   int64_t a, e;
   cs_range(N, a, e);
-  // 4 points per thread per step (independent loads, keys, cursor atomics and stores overlap)
-  for (int64_t i0 = a + threadIdx.x; i0 < e; i0 += 4 * (int64_t)blockDim.x) {
-    int key[4];
-    long long pos[4];
+  bool bad = false;
+  for (int64_t i0 = a + threadIdx.x; i0 < e; i0 += kCsBatch * (int64_t)blockDim.x) {
+    CsPts<D> P;
+    bad |= cs_load_batch<D, W, G>(x, y, w1, i0, blockDim.x, e, h, n, lo, S, P);
+    unsigned pos[kCsBatch];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t i = i0 + u * (int64_t)blockDim.x;
-      key[u] = i < e ? cs_key<D, W, G>(x, y, i, h, n, lo, S, err) : -1;
-      EFGP_DCHECK(key[u] < ncell);
+    for (int u = 0; u < kCsBatch; ++u) {
+      EFGP_DCHECK(P.key[u] < ncell);
+      pos[u] = P.key[u] >= 0 ? atomicAdd(&cs_c[P.key[u]], 1u) : 0u;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) pos[u] = key[u] >= 0 ? (long long)atomicAdd(&cs_c[key[u]], 1u) : 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t i = i0 + u * (int64_t)blockDim.x;
-      if (key[u] < 0) continue;
-      EFGP_DCHECK(pos[u] >= off[key[u]] && pos[u] < off[key[u] + 1]);
+    for (int u = 0; u < kCsBatch; ++u) {
+      if (P.key[u] < 0) continue;
+      EFGP_DCHECK(pos[u] >= off[P.key[u]] && pos[u] < off[P.key[u] + 1]);
       if constexpr (D == 2) {
-        cs_st256(rec + pos[u], __ldg(x + 2 * i), __ldg(x + 2 * i + 1), __ldg(y + i), w1 ? __ldg(w1 + i) : 1.0);
+        cs_st256(rec + pos[u], P.x[u][0], P.x[u][1], P.y[u], P.w[u]);
       } else {
-        cs_st256(rec + pos[u], __ldg(x + 3 * i), __ldg(x + 3 * i + 1), __ldg(x + 3 * i + 2), __ldg(y + i));
-        if (w1) ws1[pos[u]] = __ldg(w1 + i);
+        cs_st256(rec + pos[u], P.x[u][0], P.x[u][1], P.x[u][2], P.y[u]);
+        if (w1) ws1[pos[u]] = P.w[u];
       }
     }
   }
+  if (bad) atomicOr(err, 1);
 }
 
 // off[c] = exclusive prefix of the bucket sizes tot[c] (off[ncell] = N), iof[c] = exclusive prefix of

@@ -32,13 +32,21 @@ def main():
             os.environ.update(env)
             g = EFGP(c.kernel, c.ell, c.sigma, c.eps, c.d, c.nu, max_iter=a.iters, cg_tol=1e-30)
             ts = []
-            for _ in range(3):
-                g.fit(x, y)
-                ts.append(g.info()["t_solve_ms"])
+            try:
+                for _ in range(3):
+                    g.fit(x, y)
+                    ts.append(g.info()["t_solve_ms"])
+            except Exception as ex:  # report and go on with the other variants
+                print(f"{name} {mode}: {ex}", flush=True)
+                g.close()
+                os.environ.pop("EFGP_PT_G", None)
+                os.environ.pop("EFGP_PT_CONV", None)
+                continue
             inf = g.info()
             out[mode] = (g.weights(), inf["iters"], min(ts))
             g.close()
             os.environ.pop("EFGP_PT_G", None)
+            os.environ.pop("EFGP_PT_CONV", None)
         ref = out["fft"][0]
         for mode, (w, it, t) in out.items():
             err = float(np.linalg.norm(w - ref) / np.linalg.norm(ref))
