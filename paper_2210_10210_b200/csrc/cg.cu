@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdio>
+#include <vector>
 
 #include "efgp_internal.cuh"
 
@@ -974,14 +976,24 @@ struct PersistGeom {  // CTA (row, split) of the persistent direct CG; nsplit is
   }
 };
 constexpr int kPersistThreads = 256;
+constexpr int kPersistPer = 9;  // M_h entries per thread in phase 2: M_h <= 9 x 256 covers m <= 32
+constexpr int kPersistU = 3;    // u entries per thread (nk (2m+1) <= 3 x 256: checked at launch)
 
-__global__ void __launch_bounds__(kPersistThreads) k_cg_toep2_persist(
+__global__ void __launch_bounds__(kPersistThreads, 2) k_cg_toep2_persist(
     const double2 *__restrict__ vfull, const double *__restrict__ Dh, double2 *x, double2 *r, double2 *p0,
     double2 *ap0, double2 *ap1, int m, int nsplit, CGState *st, double2 *tpart, unsigned *tcnt, double *part_pAp,
-    double *hist, unsigned *gbar) {
+    double *hist, unsigned *gbar, long long *trace) {
   extern __shared__ double2 tsm[];
   __shared__ double sh[40];
   __shared__ bool last_s;
+  // optional phase timing (EFGP_CG_TRACE): clock64 cycles per phase, thread 0, summed over iterations
+  long long tr_acc[6] = {0, 0, 0, 0, 0, 0}, tr_t = clock64();
+#define TR(i)                       \
+  if (trace && threadIdx.x == 0) {  \
+    const long long t_ = clock64(); \
+    tr_acc[(i)] += t_ - tr_t;       \
+    tr_t = t_;                      \
+  }
   const PersistGeom G(m, nsplit, kPersistThreads);
   const int n = G.n, nv = G.nv, nout = G.nout, ngrp = G.ngrp, nk = G.nk, nc = G.nc, Mh = G.Mh;
   const int row = (int)blockIdx.x % n, spl = (int)blockIdx.x / n, j1 = row - m;
@@ -1001,6 +1013,29 @@ __global__ void __launch_bounds__(kPersistThreads) k_cg_toep2_persist(
   double rr = st->rrs[0], beta = 0.0;
   unsigned target = 0;
   const int own_lo = (int)blockIdx.x * kPersistThreads, own_hi = min(Mh, own_lo + kPersistThreads);
+  // this thread's entries of u = D p on the split's k1 rows, fixed for all iterations: the stored
+  // (canonical-half) index << 1 | conjugate flag, and D (-1: no entry)
+  int uq[kPersistU];
+  double ud[kPersistU];
+#pragma unroll
+  for (int k = 0; k < kPersistU; ++k) {
+    const int idx = threadIdx.x + k * kPersistThreads;
+    uq[k] = -1;
+    ud[k] = 0.0;
+    if (idx < nkr * n) {
+      int k1 = k1a + idx / n - m, k2 = idx % n - m;
+      const bool neg = k2 < 0 || (k2 == 0 && k1 < 0);
+      if (neg) {
+        k1 = -k1;
+        k2 = -k2;
+      }
+      const int qq = (k1 + m) * (m + 1) + k2;
+      uq[k] = qq << 1 | (neg ? 1 : 0);
+      ud[k] = Dh[qq];
+    }
+  }
+  __shared__ double2 xs[kPersistThreads];
+  xs[t] = own_lo + t < own_hi ? x[own_lo + t] : make_double2(0.0, 0.0);
   __syncthreads();
   for (;;) {
     const int q = (int)(it & 1);
@@ -1014,19 +1049,15 @@ __global__ void __launch_bounds__(kPersistThreads) k_cg_toep2_persist(
     }
     for (int idx = threadIdx.x; idx < nk * nc * nout; idx += blockDim.x) red[idx] = make_double2(0.0, 0.0);
     __syncthreads();
-    for (int idx = threadIdx.x; idx < nkr * n; idx += blockDim.x) {
-      int k1 = k1a + idx / n - m, k2 = idx % n - m;
-      const bool neg = k2 < 0 || (k2 == 0 && k1 < 0);
-      if (neg) {
-        k1 = -k1;
-        k2 = -k2;
+#pragma unroll
+    for (int k = 0; k < kPersistU; ++k)
+      if (uq[k] >= 0) {
+        const int idx = threadIdx.x + k * kPersistThreads;
+        const double2 pp = ps[uq[k] >> 1];
+        u[idx] = make_double2(ud[k] * pp.x, (uq[k] & 1) ? -ud[k] * pp.y : ud[k] * pp.y);
       }
-      const int qq = (k1 + m) * (m + 1) + k2;
-      const double2 pp = ps[qq];
-      const double dq = Dh[qq];
-      u[idx] = make_double2(dq * pp.x, neg ? -dq * pp.y : dq * pp.y);
-    }
     __syncthreads();
+    TR(0);
     if (c < nc && kk < nkr) {
       const int c2a = c * clen, c2b = min(n, c2a + clen);
       double re[4] = {0.0, 0.0, 0.0, 0.0}, im[4] = {0.0, 0.0, 0.0, 0.0};
@@ -1072,10 +1103,12 @@ __global__ void __launch_bounds__(kPersistThreads) k_cg_toep2_persist(
         tpart[((int64_t)row * nsplit + spl) * nout + t] = o;
       }
     }
+    TR(1);
     __threadfence();
     __syncthreads();
     if (t == 0) last_s = atomicAdd(tcnt + row, 1u) == (unsigned)nsplit - 1;
     __syncthreads();
+    TR(2);
     if (last_s) {
       __threadfence();
       double acc = 0.0;
@@ -1110,40 +1143,49 @@ __global__ void __launch_bounds__(kPersistThreads) k_cg_toep2_persist(
         atomicAdd(gbar, 1u);  // the row is complete (arrivals: one per row, 2m+1 per iteration)
       }
     }
+    TR(3);
     // grid barrier: every row's A p_j and <p, Ap> partial are written
     target += n;
     if (t == 0)
       while (ld_acq_gpu(gbar) < target) {
       }
     __syncthreads();
-    // phase 2 (every CTA, the same fixed order): alpha, x (owned entries), r and ||r||^2, beta, stop
-    double v = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) v += __ldcg(pAp + i);
+    TR(4);
+    // phase 2 (every CTA, the same fixed order): alpha, x (owned entries), r and ||r||^2, beta, stop.
+    // Every load of the phase is issued before the first use (A p_j entries in registers)
+    double2 av[kPersistPer];
+#pragma unroll
+    for (int k = 0; k < kPersistPer; ++k) {
+      const int i = t + k * kPersistThreads;
+      av[k] = i < Mh ? __ldcg(Ap + i) : make_double2(0.0, 0.0);
+    }
+    double v = t < n ? __ldcg(pAp + t) : 0.0;
     v = block_sum(v, sh);
     if (threadIdx.x == 0) sh[32] = v;
     __syncthreads();
     const double alpha = rr / sh[32];
     double acc = 0.0;
-    for (int i = threadIdx.x; i < Mh; i += blockDim.x) {
-      const double2 a = __ldcg(Ap + i), pp = ps[i];
-      double2 rq = rs[i];
-      rq.x -= alpha * a.x;
-      rq.y -= alpha * a.y;
-      rs[i] = rq;
-      acc += ((i % (m + 1)) ? 2.0 : 1.0) * (rq.x * rq.x + rq.y * rq.y);
-      if (i >= own_lo && i < own_hi) {
-        double2 xx = x[i];
-        xx.x += alpha * pp.x;
-        xx.y += alpha * pp.y;
-        x[i] = xx;
-        r[i] = rq;
-        p0[i] = pp;
+#pragma unroll
+    for (int k = 0; k < kPersistPer; ++k) {
+      const int i = t + k * kPersistThreads;
+      if (i < Mh) {
+        const double2 a = av[k], pp = ps[i];
+        double2 rq = rs[i];
+        rq.x -= alpha * a.x;
+        rq.y -= alpha * a.y;
+        rs[i] = rq;
+        acc += ((i % (m + 1)) ? 2.0 : 1.0) * (rq.x * rq.x + rq.y * rq.y);
+        if (i >= own_lo && i < own_hi) {  // x of the owned entries lives in shared memory until the end
+          xs[t].x += alpha * pp.x;
+          xs[t].y += alpha * pp.y;
+        }
       }
     }
     acc = block_sum(acc, sh);
     if (threadIdx.x == 0) sh[33] = acc;
     __syncthreads();
     const double rr_new = sh[33];
+    TR(5);
     ++it;
     beta = rr_new / rr;
     const double rr_prev = rr;
@@ -1158,10 +1200,22 @@ __global__ void __launch_bounds__(kPersistThreads) k_cg_toep2_persist(
       hist[it] = rel;
       if (stop) st->done = stop;
     }
-    if (stop) return;
+    if (stop) {  // x (owned entries), r and p to global memory
+      if (trace && t == 0)
+        for (int k = 0; k < 6; ++k) trace[(size_t)blockIdx.x * 8 + k] = tr_acc[k];
+      if (trace && t == 0) trace[(size_t)blockIdx.x * 8 + 6] = last_s ? 1 : 0;
+      if (own_lo + t < own_hi) {
+        const int i = own_lo + t;
+        x[i] = xs[t];
+        r[i] = rs[i];
+        p0[i] = ps[i];
+      }
+      return;
+    }
     __syncthreads();  // sh[32], sh[33] reusable
   }
 }
+#undef TR
 
 static int persist_split_env() {
   const char *e = getenv("EFGP_CG_PSPLIT");
@@ -1185,7 +1239,9 @@ static cudaError_t launch_persist_cg(efgp_plan *pl, CGState *st, cudaStream_t s)
   for (; nsplit >= 1; --nsplit) {
     const PersistGeom G(m, nsplit, kPersistThreads);
     const size_t smem = G.smem();
-    if (!G.ok() || smem > 200 * 1024 || 2 * n > pl->cg_blocks) continue;
+    if (!G.ok() || smem > 200 * 1024 || 2 * n > pl->cg_blocks || G.Mh > kPersistPer * kPersistThreads ||
+        n > kPersistThreads || G.nk * n > kPersistU * kPersistThreads)
+      continue;
     cudaError_t e = cudaFuncSetAttribute(k_cg_toep2_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -1204,12 +1260,35 @@ static cudaError_t launch_persist_cg(efgp_plan *pl, CGState *st, cudaStream_t s)
     double2 *x = pl->x, *r = pl->r, *p0 = pl->p, *ap0 = pl->Ap, *ap1 = pl->p2, *tpart = pl->toep_part;
     unsigned *tcnt = pl->toep_cnt, *gbar = pl->cg_gbar;
     double *hist = pl->hist;
+    long long *trace = nullptr;
+    const bool want_trace = getenv("EFGP_CG_TRACE") != nullptr;
+    if (want_trace) {
+      e = cudaMallocAsync((void **)&trace, sizeof(long long) * 8 * n * nsplit, s);
+      if (e != cudaSuccess) return e;
+      cudaMemsetAsync(trace, 0, sizeof(long long) * 8 * n * nsplit, s);
+    }
     void *args[] = {(void *)&vfull, (void *)&Dh, (void *)&x, (void *)&r, (void *)&p0, (void *)&ap0, (void *)&ap1,
                     (void *)&m, (void *)&nsplit, (void *)&st, (void *)&tpart, (void *)&tcnt, (void *)&part_pAp,
-                    (void *)&hist, (void *)&gbar};
+                    (void *)&hist, (void *)&gbar, (void *)&trace};
     pl->cg_persist_split = nsplit;
-    return cudaLaunchCooperativeKernel((const void *)k_cg_toep2_persist, dim3((unsigned)(n * nsplit)),
-                                       dim3(kPersistThreads), args, smem, s);
+    e = cudaLaunchCooperativeKernel((const void *)k_cg_toep2_persist, dim3((unsigned)(n * nsplit)),
+                                    dim3(kPersistThreads), args, smem, s);
+    if (want_trace && e == cudaSuccess) {  // diagnostics: mean cycles per phase over CTAs (stderr)
+      std::vector<long long> h((size_t)8 * n * nsplit);
+      cudaMemcpyAsync(h.data(), trace, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      CGState hs{};
+      cudaMemcpy(&hs, st, sizeof(CGState), cudaMemcpyDeviceToHost);
+      double mean[6] = {0, 0, 0, 0, 0, 0};
+      for (int b = 0; b < n * nsplit; ++b)
+        for (int k = 0; k < 6; ++k) mean[k] += (double)h[(size_t)b * 8 + k] / (n * nsplit);
+      const double it = hs.iter > 0 ? (double)hs.iter : 1.0;
+      fprintf(stderr, "cg persist trace (cycles/iteration, mean over %d CTAs, %lld iterations): p-update+u %.0f, "
+              "product+partials %.0f, fence+row atomic %.0f, last-CTA row %.0f, barrier wait %.0f, phase 2 %.0f\n",
+              n * nsplit, hs.iter, mean[0] / it, mean[1] / it, mean[2] / it, mean[3] / it, mean[4] / it, mean[5] / it);
+      cudaFreeAsync(trace, s);
+    }
+    return e;
   }
   return cudaErrorNotSupported;
 }
