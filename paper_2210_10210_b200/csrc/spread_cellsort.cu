@@ -285,6 +285,30 @@ __global__ void __launch_bounds__(kCsThreads) k_cs_spread(const CsItem *__restri
       }
       __syncwarp();
       const int np = (int)min(32LL, item.end - b0);
+      if constexpr (D == 3 && U == 8) {
+        // 3D, U = 8 (c4: W = 5, G = 4): element t = 2a + k of lane l is (a, b = l/8 + 4k, c = l%8), so
+        // the strengths and the (b, c) weights fold into two per-point column factors and every
+        // element costs 2 FMAs; the row weights w1[a] are broadcast loads (r01: 2 products, 2 FMAs
+        // and 3 shared loads per element)
+        const int cc = lane & 7, bb = lane >> 3;
+#pragma unroll 2
+        for (int p = 0; p < np; ++p) {
+          const double *wr = ws[p];
+          const double yv = wr[3 * U], wv = wr[3 * U + 1];
+          const double w3 = wr[2 * U + cc], w3s = w3 * wv, w3y = w3 * yv;
+          const double w2a = wr[U + bb], w2b = wr[U + bb + 4];
+          const double gs0 = w2a * w3s, gy0 = w2a * w3y, gs1 = w2b * w3s, gy1 = w2b * w3y;
+#pragma unroll
+          for (int a = 0; a < U; ++a) {
+            const double w1 = wr[a];
+            a1[2 * a] = fma(w1, gs0, a1[2 * a]);
+            ay[2 * a] = fma(w1, gy0, ay[2 * a]);
+            a1[2 * a + 1] = fma(w1, gs1, a1[2 * a + 1]);
+            ay[2 * a + 1] = fma(w1, gy1, ay[2 * a + 1]);
+          }
+        }
+        continue;
+      }
 #pragma unroll 4
       for (int p = 0; p < np; ++p) {
         const double yv = ws[p][D * U], wv = ws[p][D * U + 1];
@@ -393,18 +417,24 @@ __global__ void __launch_bounds__(kCsThreads) k_cs_spread2q(const CsItem *__rest
 #pragma unroll
         for (int k = 0; k < NB; ++k) w2[k] = c8 + 8 * k < U ? wr[U + c8 + 8 * k] : 0.0;
         const double2 yw = *reinterpret_cast<const double2 *>(wr + 2 * U);
+        // the strengths folded into the column weight once per point: 2 FMAs per (row, column)
+        // instead of a product and 2 FMAs
+        double w2s[NB], w2y[NB];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          w2s[k] = w2[k] * yw.y;
+          w2y[k] = w2[k] * yw.x;
+        }
 #pragma unroll
         for (int a = 0; a < U; a += 2) {
           const double2 wa = *reinterpret_cast<const double2 *>(wr + a);  // (w1[a], w1[a+1]); w1[U] = w2[0] if U odd
 #pragma unroll
           for (int k = 0; k < NB; ++k) {
-            const double f0 = wa.x * w2[k];
-            a1[a][k] = fma(f0, yw.y, a1[a][k]);
-            ay[a][k] = fma(f0, yw.x, ay[a][k]);
+            a1[a][k] = fma(wa.x, w2s[k], a1[a][k]);
+            ay[a][k] = fma(wa.x, w2y[k], ay[a][k]);
             if (a + 1 < U) {
-              const double f1 = wa.y * w2[k];
-              a1[a + 1][k] = fma(f1, yw.y, a1[a + 1][k]);
-              ay[a + 1][k] = fma(f1, yw.x, ay[a + 1][k]);
+              a1[a + 1][k] = fma(wa.y, w2s[k], a1[a + 1][k]);
+              ay[a + 1][k] = fma(wa.y, w2y[k], ay[a + 1][k]);
             }
           }
         }
