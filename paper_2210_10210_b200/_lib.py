@@ -35,7 +35,7 @@ class Info(C.Structure):
                 ("spread_precision", C.c_int64), ("t_var_ms", C.c_double), ("var_iters_max", C.c_int64),
                 ("var_batch", C.c_int64), ("hetero_sorted", C.c_int64),
                 ("precond", C.c_int64), ("comm_size", C.c_int64), ("spread_fallback", C.c_int64),
-                ("cg_persist_split", C.c_int64)]
+                ("cg_persist_split", C.c_int64), ("cg_dft2", C.c_int64)]
 
 
 # every symbol include/efgp.h declares, with (restype, argtypes)

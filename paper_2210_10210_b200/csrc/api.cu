@@ -564,6 +564,7 @@ efgp_status efgp_get_info(efgp_handle pl, efgp_info *o) {
   o->t_predict_ms = pl->t_predict;
   o->spread_fallback = pl->spread_fallback;
   o->cg_persist_split = pl->cg_persist_split;
+  o->cg_dft2 = pl->cg_dft2;
   if (pl->spread_used == EFGP_SPREAD_SORTED) {
     o->sorted_t1 = P.T1;  // (the SORTED kernel is one cooperative launch per fit)
     o->sorted_t2 = P.T2;
@@ -623,7 +624,8 @@ void efgp_destroy(efgp_handle pl) {
                   pl->scal, pl->hist, pl->dflags, pl->T2box, pl->t2grid, pl->stage[0], pl->stage[1],
                   pl->trace,
                   pl->sync_buf, pl->het_box, pl->het_grid, pl->pc_Q, pl->pc_F0, pl->pc_F1, pl->pc_work, pl->z,
-                  pl->pc_lam, pl->pc_info, pl->comm_buf, pl->vfull, pl->pc_diag, pl->toep_part, pl->toep_cnt, pl->p2, pl->cg_gbar};
+                  pl->pc_lam, pl->pc_info, pl->comm_buf, pl->vfull, pl->pc_diag, pl->toep_part, pl->toep_cnt, pl->p2, pl->cg_gbar,
+                  pl->dft_V, pl->dft_roots, pl->dft_W};
   for (void *b : bufs)
     if (b) cudaFree(b);
   for (void *b : pl->rec)

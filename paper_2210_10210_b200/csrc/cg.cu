@@ -1217,6 +1217,392 @@ __global__ void __launch_bounds__(kPersistThreads, 2) k_cg_toep2_persist(
 }
 #undef TR
 
+// ---- persistent DFT CG (2D beyond the direct product: c2, m = 49) ------------------------------
+// The Toeplitz product out_j = sum_k v_{j-k} u_k (u = D p, j, k in J_m^2) with a DFT of length L
+// (>= 4m+1, the Toeplitz box) along the second axis and a direct convolution along the first:
+//   T[k1][x2]  = sum_{k2} u_{k1,k2} w^(-k2 x2)                                   (w = e^(2 pi i / L))
+//   W[j1][x2]  = sum_{k1} Vt[j1-k1][x2] T[k1][x2],   Vt[d1][x2] = sum_{d2} v_{d1,d2} w^(-d2 x2)
+//   out_{j1,j2} = (1/L) sum_{x2} w^(j2 x2) W[j1][x2]                                 (j2 = 0..m)
+// exact because |j2 - k2 - d2| < L for every term that survives (L >= 4m+1): (1/L) sum_x2 Vt[d1][x2]
+// w^((j2-k2) x2) = v_{d1, j2-k2}.  4.9e6 complex MACs per product for c2 against 4.9e7 for the direct
+// sum and four cuFFT launches for the padded real FFTs (Alg a:FF).
+// One cooperative kernel runs the whole CG (recurrences and stopping rule of k_cg_xr + k_cg_p,
+// reading G6), two grid barriers per iteration:
+//   phase 1 (CTA c owns the columns x2 in [c L / G, (c+1) L / G)): p_j = r_j + beta p_{j-1} (all
+//            entries), T and W of its columns, W to global memory; barrier;
+//   phase 2 (CTA c < 2m+1 owns row j1 = c - m): out of its row from W, A p_j = D out + sigma^2 p_j
+//            (exactly Hermitian in the j2 = 0 column, as k_cg_toep2), its <p, Ap> partial; barrier;
+//   phase 3 (every CTA, the same fixed order): alpha, r_{j+1} and ||r_{j+1}||^2 for ALL entries
+//            (r, p, D in every CTA's shared memory), beta, the stop test; x of the owned entries.
+// W, A p and the partials need no double buffer: a CTA passes the barrier of a phase only after
+// every CTA has finished the phase that reads what it is about to overwrite.
+constexpr int kDftThreads = 256, kDftCols = 2;  // columns per CTA: L <= kDftCols x grid
+constexpr int kDftPer = kDft2MaxMh / kDftThreads + 1;  // A p entries per thread in phase 3
+struct DftGeom {
+  int n, nv, nout, Mh, L, G;
+  __host__ __device__ DftGeom(int m, int L_, int G_) : n(2 * m + 1), nv(4 * m + 1), nout(m + 1), Mh(n * (m + 1)), L(L_), G(G_) {}
+  __host__ __device__ size_t smem() const {
+    const size_t opn = 8 * (size_t)nout > 2 * (size_t)n * kDftCols ? 8 * (size_t)nout : 2 * (size_t)n * kDftCols;
+    return sizeof(double2) * (2 * (size_t)Mh + (size_t)kDftCols * nv + (size_t)kDftCols * n + L + L + opn) +
+           sizeof(double) * (size_t)Mh;
+  }
+};
+
+__global__ void __launch_bounds__(kDftThreads, 1) k_cg_dft2_persist(
+    const double2 *__restrict__ Vt, const double2 *__restrict__ roots, const double *__restrict__ Dh, double2 *x,
+    double2 *r, double2 *p0, double2 *Ap, double2 *Wg, int m, int L, CGState *st, double *part_pAp, double *hist,
+    unsigned *gbar, long long *trace) {
+  extern __shared__ __align__(16) double2 dsm[];
+  __shared__ double sh[40];
+  // optional phase timing (EFGP_CG_TRACE), thread 0, cycles summed over iterations: 0 p + T, 2 W,
+  // 1 barrier 1, 4 phase 2, 5 barrier 2, 3 fence after W + phase 3
+  long long tr_acc[6] = {0, 0, 0, 0, 0, 0}, tr_t = clock64();
+#define TRD(i)                      \
+  if (trace && threadIdx.x == 0) {  \
+    const long long t_ = clock64(); \
+    tr_acc[(i)] += t_ - tr_t;       \
+    tr_t = t_;                      \
+  }
+  const DftGeom Gm(m, L, (int)gridDim.x);
+  const int n = Gm.n, nv = Gm.nv, nout = Gm.nout, Mh = Gm.Mh, t = threadIdx.x;
+  // r, p and D live in shared memory in k2-major order s(k1, k2) = k2 n + (k1 + m) (the global
+  // half is row-major g(k1, k2) = (k1 + m)(m + 1) + k2): the T sums read p and D of consecutive k1 in
+  // consecutive lanes (row-major: a 800-byte lane stride, 8-way bank conflicts, the kernel's limit)
+  double2 *rs = dsm, *ps = rs + Mh, *vs = ps + Mh, *ts = vs + kDftCols * nv, *wr = ts + kDftCols * n,
+          *rt = wr + L, *op = rt + L;
+  double *ds = reinterpret_cast<double *>(op + (8 * nout > 2 * n * kDftCols ? 8 * nout : 2 * n * kDftCols));
+  auto gidx = [&](int si) { return (si % n) * nout + si / n; };
+  const int c0 = (int)((int64_t)blockIdx.x * L / gridDim.x), c1 = (int)((int64_t)(blockIdx.x + 1) * L / gridDim.x);
+  const int nx = c1 - c0;  // <= kDftCols (checked at launch)
+  for (int i = t; i < Mh; i += kDftThreads) {
+    const int g = gidx(i);
+    rs[i] = ps[i] = r[g];  // r_0 = b (k_cg_init)
+    ds[i] = Dh[g];
+  }
+  for (int i = t; i < nx * nv; i += kDftThreads) vs[i] = Vt[(int64_t)(i % nv) * L + c0 + i / nv];  // [col][d1 + 2m]
+  for (int i = t; i < L; i += kDftThreads) rt[i] = roots[i];
+  const int own_lo = (int)((int64_t)blockIdx.x * Mh / gridDim.x), own_hi = (int)((int64_t)(blockIdx.x + 1) * Mh / gridDim.x);
+  __shared__ double2 xs[kDftThreads];
+  if (own_lo + t < own_hi) xs[t] = x[gidx(own_lo + t)];
+  const double tol = st->tol, bnorm = st->bnorm, s2 = st->sigma2;
+  const long long max_iter = st->max_iter;
+  long long it = st->iter;
+  if (st->done) return;
+  double rr = st->rrs[0], beta = 0.0;
+  unsigned target = 0;
+  const double invL = 1.0 / (double)L;
+  __syncthreads();
+  for (;;) {
+    // ---- phase 1: p_j; T and W of this CTA's columns
+    for (int i = t; i < Mh; i += kDftThreads) {
+      const double2 rq = rs[i], po = ps[i];
+      ps[i] = make_double2(rq.x + beta * po.x, rq.y + beta * po.y);
+    }
+    __syncthreads();
+    // T[k1][x2] = u_{k1,0} + sum_{k2 = 1..m} (u_{k1,k2} w^(-k2 x2) + conj(u_{-k1,k2}) w^(k2 x2)); the
+    // (k1 < 0, 0) entry is read as conj(u_{-k1,0}) (canonical half: the product is exactly Hermitian).
+    // Thread (k1, half h): k2 in half h of 1..m for BOTH columns of the CTA (the p and D loads serve
+    // two independent accumulator chains), the halves added in fixed order below
+    const int kh = (m + 1) / 2;  // k2 = 1..kh | kh+1..m
+    for (int item = t; item < 2 * n; item += kDftThreads) {
+      const int k1 = item % n - m, hf = item / n;
+      const int ka = hf ? kh + 1 : 1, kb = hf ? m : kh;
+      double tx[kDftCols] = {}, ty[kDftCols] = {};
+      int e[kDftCols];
+#pragma unroll
+      for (int xi = 0; xi < kDftCols; ++xi) e[xi] = ((ka - 1) * (c0 + xi)) % L;
+      for (int k2 = ka; k2 <= kb; ++k2) {
+        const int sa = k2 * n + k1 + m, sb = k2 * n - k1 + m;
+        const double2 a = ps[sa], b = ps[sb];
+        const double da = ds[sa], db = ds[sb];
+        const double2 ua = make_double2(da * a.x, da * a.y), ub = make_double2(db * b.x, db * b.y);
+        const double c1x = ua.x + ub.x, c1y = ua.y + ub.y, c2x = ua.y - ub.y, c2y = ub.x - ua.x;
+#pragma unroll
+        for (int xi = 0; xi < kDftCols; ++xi) {
+          e[xi] += c0 + xi;
+          if (e[xi] >= L) e[xi] -= L;
+          const double2 w = rt[e[xi]];  // w^(k2 x2), the same for every lane (broadcast)
+          // ua w^-1 + conj(ub) w
+          tx[xi] = fma(c1x, w.x, fma(c1y, w.y, tx[xi]));
+          ty[xi] = fma(c2x, w.x, fma(c2y, w.y, ty[xi]));
+        }
+      }
+#pragma unroll
+      for (int xi = 0; xi < kDftCols; ++xi) op[(hf * n + k1 + m) * kDftCols + xi] = make_double2(tx[xi], ty[xi]);
+    }
+    __syncthreads();
+    for (int item = t; item < n * nx; item += kDftThreads) {
+      const int k1 = item / nx - m, xi = item % nx;
+      const int q0 = k1 >= 0 ? k1 + m : -k1 + m;  // s(|k1|, 0)
+      double2 u0 = make_double2(ds[q0] * ps[q0].x, ds[q0] * ps[q0].y);
+      if (k1 < 0) u0.y = -u0.y;
+      const double2 h0 = op[(k1 + m) * kDftCols + xi], h1 = op[(n + k1 + m) * kDftCols + xi];
+      ts[(k1 + m) * kDftCols + xi] = make_double2(u0.x + h0.x + h1.x, u0.y + h0.y + h1.y);
+    }
+    __syncthreads();
+    TRD(0);
+    // W[j1][x2] = sum_{k1} Vt[j1 - k1][x2] T[k1][x2]: thread (j1, half of the k1 range), both columns
+    const int k1h = -m + n / 2;  // k1 = -m..k1h-1 | k1h..m
+    for (int item = t; item < 2 * n; item += kDftThreads) {
+      const int j1 = item % n - m, hf = item / n;
+      const int ka = hf ? k1h : -m, kb = hf ? m + 1 : k1h;
+      double wx[kDftCols] = {}, wy[kDftCols] = {};
+      for (int k1 = ka; k1 < kb; ++k1) {
+#pragma unroll
+        for (int xi = 0; xi < kDftCols; ++xi) {
+          if (xi < nx) {
+            const double2 a = vs[xi * nv + j1 - k1 + 2 * m], b = ts[(k1 + m) * kDftCols + xi];
+            wx[xi] = fma(a.x, b.x, fma(-a.y, b.y, wx[xi]));
+            wy[xi] = fma(a.x, b.y, fma(a.y, b.x, wy[xi]));
+          }
+        }
+      }
+#pragma unroll
+      for (int xi = 0; xi < kDftCols; ++xi) op[(hf * n + j1 + m) * kDftCols + xi] = make_double2(wx[xi], wy[xi]);
+    }
+    __syncthreads();
+    for (int item = t; item < n * nx; item += kDftThreads) {
+      const int j1 = item / nx - m, xi = item % nx;
+      const double2 h0 = op[(j1 + m) * kDftCols + xi], h1 = op[(n + j1 + m) * kDftCols + xi];
+      Wg[(int64_t)(j1 + m) * L + c0 + xi] = make_double2(h0.x + h1.x, h0.y + h1.y);
+    }
+    __syncthreads();
+    TRD(2);
+    __threadfence();
+    __syncthreads();
+    TRD(3);
+    target += gridDim.x;
+    if (t == 0) {
+      atomicAdd(gbar, 1u);
+      while (ld_acq_gpu(gbar) < target) {
+      }
+    }
+    __syncthreads();
+    TRD(1);
+    // ---- phase 2: row j1 = blockIdx - m
+    if ((int)blockIdx.x < n) {
+      const int j1 = (int)blockIdx.x - m;
+      for (int i = t; i < L; i += kDftThreads) wr[i] = __ldcg(Wg + (int64_t)(j1 + m) * L + i);
+      __syncthreads();
+      // out[j2] = (1/L) sum_x2 w^(j2 x2) W[x2]: 8 x2-slices per j2, partials summed in fixed order;
+      // the twiddle by recurrence (w^(j2 (x2+1)) = w^(j2 x2) w^j2, at most L/8 steps from a table entry)
+      for (int item = t; item < 8 * nout; item += kDftThreads) {
+        const int j2 = item % nout, sl = item / nout;
+        const int xa = (int)((int64_t)sl * L / 8), xb = (int)((int64_t)(sl + 1) * L / 8);
+        double ox = 0.0, oy = 0.0;
+        double2 w = rt[(j2 * xa) % L];
+        const double2 st1 = rt[j2];
+        for (int x2 = xa; x2 < xb; ++x2) {
+          const double2 a = wr[x2];
+          ox = fma(a.x, w.x, fma(-a.y, w.y, ox));
+          oy = fma(a.x, w.y, fma(a.y, w.x, oy));
+          w = make_double2(w.x * st1.x - w.y * st1.y, w.x * st1.y + w.y * st1.x);
+        }
+        op[sl * nout + j2] = make_double2(ox, oy);
+      }
+      __syncthreads();
+      double acc = 0.0;
+      if (t < nout && !(t == 0 && j1 < 0)) {  // (j1 < 0, 0) is written by row -j1 as the conjugate
+        double ox = 0.0, oy = 0.0;
+#pragma unroll
+        for (int sl = 0; sl < 8; ++sl) {
+          ox += op[sl * nout + t].x;
+          oy += op[sl * nout + t].y;
+        }
+        const int sq = t * n + j1 + m;
+        const double2 pp = ps[sq];
+        const double dq = ds[sq];
+        double2 a = make_double2(dq * ox * invL + s2 * pp.x, dq * oy * invL + s2 * pp.y);
+        if (t == 0 && j1 == 0) a.y = s2 * pp.y;  // j = 0: (T u)_0 is real
+        Ap[sq] = a;  // (A p is exchanged in the k2-major order of the shared copies)
+        acc = (t ? 2.0 : 1.0) * (pp.x * a.x + pp.y * a.y);
+        if (t == 0 && j1 > 0) {  // the mirrored entry (-j1, 0) = conj, with the canonical p
+          Ap[m - j1] = make_double2(a.x, -a.y);
+          acc *= 2.0;
+        }
+      }
+      acc = block_sum(acc, sh);
+      if (t == 0) {
+        part_pAp[blockIdx.x] = acc;
+        __threadfence();
+        atomicAdd(gbar, 1u);
+      }
+    }
+    TRD(4);
+    target += n;
+    if (t == 0)
+      while (ld_acq_gpu(gbar) < target) {
+      }
+    __syncthreads();
+    TRD(5);
+    // ---- phase 3 (every CTA): alpha, r and ||r||^2 (all entries, k2-major order), x (owned entries);
+    // all of its L2 loads are issued before the first use (M_h <= kDftPer x 256)
+    double acc = 0.0;
+    double alpha;
+    {
+      double2 av[kDftPer];
+#pragma unroll
+      for (int k = 0; k < kDftPer; ++k) {
+        const int i = t + k * kDftThreads;
+        av[k] = i < Mh ? __ldcg(Ap + i) : make_double2(0.0, 0.0);
+      }
+      double v = t < n ? __ldcg(part_pAp + t) : 0.0;
+      v = block_sum(v, sh);
+      if (t == 0) sh[32] = v;
+      __syncthreads();
+      alpha = rr / sh[32];
+#pragma unroll
+      for (int k = 0; k < kDftPer; ++k) {
+        const int i = t + k * kDftThreads;
+        if (i < Mh) {
+          double2 rq = rs[i];
+          rq.x -= alpha * av[k].x;
+          rq.y -= alpha * av[k].y;
+          rs[i] = rq;
+          acc += (i >= n ? 2.0 : 1.0) * (rq.x * rq.x + rq.y * rq.y);  // k2 = i / n > 0 weighs 2
+          if (i >= own_lo && i < own_hi) {
+            xs[i - own_lo].x += alpha * ps[i].x;
+            xs[i - own_lo].y += alpha * ps[i].y;
+          }
+        }
+      }
+    }
+    acc = block_sum(acc, sh);
+    if (t == 0) sh[33] = acc;
+    __syncthreads();
+    const double rr_new = sh[33];
+    TRD(3);
+    ++it;
+    beta = rr_new / rr;
+    const double rr_prev = rr;
+    rr = rr_new;
+    const double rel = sqrt(rr_new) / bnorm;
+    const int stop = rel <= tol ? 1 : (it >= max_iter ? 2 : 0);
+    if (blockIdx.x == 0 && t == 0) {
+      st->rr = rr_new;
+      st->rr_old = rr_prev;
+      st->rrs[it & 1] = rr_new;
+      st->iter = it;
+      hist[it] = rel;
+      if (stop) st->done = stop;
+    }
+    if (stop) {
+      for (int i = t; i < Mh; i += kDftThreads) {  // r and p back to global memory (every CTA holds them)
+        if (blockIdx.x == 0) {
+          r[gidx(i)] = rs[i];
+          p0[gidx(i)] = ps[i];
+        }
+      }
+      if (own_lo + t < own_hi) x[gidx(own_lo + t)] = xs[t];
+      if (trace && t == 0)
+        for (int k = 0; k < 6; ++k) trace[(size_t)blockIdx.x * 8 + k] = tr_acc[k];
+      return;
+    }
+    __syncthreads();
+  }
+#undef TRD
+}
+
+// Vt[d1][x2] = sum_{d2 = -2m..2m} v_{d1,d2} w^(-d2 x2) (once per fit; v full over J_2m, row-major)
+__global__ void k_dft2_vt(const double2 *__restrict__ vfull, const double2 *__restrict__ roots, int m, int L,
+                          double2 *__restrict__ Vt) {
+  const int nv = 4 * m + 1;
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (int64_t)nv * L) return;
+  const int d1 = (int)(id / L), x2 = (int)(id % L);
+  double sx = 0.0, sy = 0.0;
+  for (int d2 = -2 * m; d2 <= 2 * m; ++d2) {
+    int e = (int)((((int64_t)-d2 * x2) % L + L) % L);
+    const double2 w = roots[e], a = vfull[(int64_t)d1 * nv + d2 + 2 * m];
+    sx = fma(a.x, w.x, fma(-a.y, w.y, sx));
+    sy = fma(a.x, w.y, fma(a.y, w.x, sy));
+  }
+  Vt[id] = make_double2(sx, sy);
+}
+
+efgp_status dft2_setup(efgp_plan *pl, cudaStream_t s) {
+  const Params &P = pl->P;
+  const int m = (int)P.m, L = (int)P.L, nv = 4 * m + 1, n = 2 * m + 1;
+  if (!pl->dft_V) {
+    EFGP_CUDA(cudaMalloc((void **)&pl->dft_V, sizeof(double2) * (size_t)nv * L));
+    EFGP_CUDA(cudaMalloc((void **)&pl->dft_roots, sizeof(double2) * (size_t)L));
+    EFGP_CUDA(cudaMalloc((void **)&pl->dft_W, sizeof(double2) * (size_t)n * L));
+    std::vector<double2> w(L);
+    for (int t = 0; t < L; ++t) {  // w^t = e^(2 pi i t / L), sincospi for exact angles at t/L = k/4
+      double sn, cs;
+      sincospi(2.0 * t / (double)L, &sn, &cs);
+      w[t] = make_double2(cs, sn);
+    }
+    EFGP_CUDA(cudaMemcpyAsync(pl->dft_roots, w.data(), sizeof(double2) * L, cudaMemcpyHostToDevice, s));
+    EFGP_CUDA(cudaStreamSynchronize(s));  // (the host table goes out of scope)
+  }
+  const int64_t tot = (int64_t)nv * L;
+  k_dft2_vt<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(pl->vfull, pl->dft_roots, m, L, pl->dft_V);
+  EFGP_CUDA(cudaGetLastError());
+  return EFGP_OK;
+}
+
+static cudaError_t launch_dft2_cg(efgp_plan *pl, CGState *st, cudaStream_t s) {
+  const Params &P = pl->P;
+  const int m = (int)P.m, n = 2 * m + 1, L = (int)P.L;
+  int dev = 0, coop = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  // as few CTAs as give every CTA kDftCols columns and every row an owner (c2: 100), so phase 1 is
+  // balanced (148 CTAs: 52 with two columns, 96 with one, and every CTA waits for the two-column ones)
+  const int G = std::min(pl->num_sms, std::max(n, (L + kDftCols - 1) / kDftCols));
+  const DftGeom Gm(m, L, G);
+  const size_t smem = Gm.smem();
+  if (!coop || !pl->dft_V || G < n || (L + G - 1) / G > kDftCols || smem > 220 * 1024 || n > kDftThreads ||
+      n > pl->cg_blocks)
+    return cudaErrorNotSupported;
+  cudaError_t e = cudaFuncSetAttribute(k_cg_dft2_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_dft2_persist, kDftThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorNotSupported;
+  if (!pl->cg_gbar) {
+    e = cudaMalloc((void **)&pl->cg_gbar, sizeof(unsigned));
+    if (e != cudaSuccess) return e;
+  }
+  e = cudaMemsetAsync(pl->cg_gbar, 0, sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  const double2 *Vt = pl->dft_V, *roots = pl->dft_roots;
+  const double *Dh = pl->D_half;
+  double2 *x = pl->x, *r = pl->r, *p0 = pl->p, *Ap = pl->Ap, *Wg = pl->dft_W;
+  double *part = pl->partials, *hist = pl->hist;
+  unsigned *gbar = pl->cg_gbar;
+  int mm = m, LL = L;
+  long long *trace = nullptr;
+  const bool want_trace = getenv("EFGP_CG_TRACE") != nullptr;
+  if (want_trace) {
+    e = cudaMallocAsync((void **)&trace, sizeof(long long) * 8 * G, s);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(trace, 0, sizeof(long long) * 8 * G, s);
+  }
+  void *args[] = {(void *)&Vt, (void *)&roots, (void *)&Dh, (void *)&x, (void *)&r, (void *)&p0, (void *)&Ap,
+                  (void *)&Wg, (void *)&mm, (void *)&LL, (void *)&st, (void *)&part, (void *)&hist, (void *)&gbar,
+                  (void *)&trace};
+  e = cudaLaunchCooperativeKernel((const void *)k_cg_dft2_persist, dim3((unsigned)G), dim3(kDftThreads), args, smem, s);
+  if (want_trace && e == cudaSuccess) {
+    std::vector<long long> h((size_t)8 * G);
+    cudaMemcpyAsync(h.data(), trace, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    CGState hs{};
+    cudaMemcpy(&hs, st, sizeof(CGState), cudaMemcpyDeviceToHost);
+    double mean[6] = {0, 0, 0, 0, 0, 0};
+    for (int b = 0; b < G; ++b)
+      for (int k = 0; k < 6; ++k) mean[k] += (double)h[(size_t)b * 8 + k] / G;
+    const double it = hs.iter > 0 ? (double)hs.iter : 1.0;
+    fprintf(stderr, "cg dft2 trace (cycles/iteration, mean over %d CTAs, %lld iterations): p + T %.0f, W + store %.0f, "
+            "barrier 1 %.0f, phase 2 %.0f, barrier 2 %.0f, fence after W + phase 3 %.0f\n", G, hs.iter, mean[0] / it,
+            mean[2] / it, mean[1] / it, mean[4] / it, mean[5] / it, mean[3] / it);
+    cudaFreeAsync(trace, s);
+  }
+  return e;
+}
+
 static int persist_split_env() {
   const char *e = getenv("EFGP_CG_PSPLIT");
   return (e && atoi(e) > 0) ? atoi(e) : 0;
@@ -1425,6 +1811,25 @@ static efgp_status cg_solve_d(efgp_plan *pl, int64_t N_total) {
   int G = P.graph_iters;
   const bool fused = D == 2 && toeplitz_direct(P) && pl->p2 && pl->toep_part && cg_fused() && toep_split();
   pl->cg_persist_split = 0;
+  pl->cg_dft2 = 0;
+  if (D == 2 && toeplitz_dft2(P) && cg_persist()) {  // 2D beyond the direct product: persistent DFT CG
+    const cudaError_t e = launch_dft2_cg(pl, st, s);
+    if (e == cudaSuccess) {
+      pl->cg_dft2 = 1;
+      CGState host{};
+      EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned, st, sizeof(CGState), cudaMemcpyDeviceToHost, s));
+      EFGP_CUDA(cudaStreamSynchronize(s));
+      std::memcpy(&host, pl->h_pinned, sizeof(CGState));
+      pl->iters = host.iter;
+      pl->rel_resid = host.bnorm > 0 ? std::sqrt(host.rr) / host.bnorm : 0.0;
+      return host.done == 2 ? EFGP_ERR_NOCONVERGE : EFGP_OK;
+    }
+    if (e != cudaErrorNotSupported && e != cudaErrorCooperativeLaunchTooLarge) {
+      pl->err = "persistent DFT CG launch failed";
+      return EFGP_ERR_CUDA;
+    }
+    cudaGetLastError();
+  }
   if (fused && cg_persist()) {  // the whole loop in one cooperative kernel
     const cudaError_t e = launch_persist_cg(pl, st, s);
     if (e == cudaSuccess) {

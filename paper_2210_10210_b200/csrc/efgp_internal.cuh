@@ -132,8 +132,12 @@ struct efgp_plan {
   double *Yr = nullptr;       // L^d real
   double *vhat = nullptr;     // L^d real, C2R(v)/L^d
   double2 *vfull = nullptr;   // (4m+1)^2 complex, full v (direct Toeplitz product, small m, 2D)
+  double2 *dft_V = nullptr;   // persistent DFT CG: (4m+1) x L, Vt[d1][x2] = sum_d2 v_{d1,d2} w^(-d2 x2), w = e^(2 pi i/L)
+  double2 *dft_roots = nullptr;  // L: w^t
+  double2 *dft_W = nullptr;   // (2m+1) x L: the product's per-line stage (columns -> rows exchange)
   unsigned *cg_gbar = nullptr;    // persistent direct CG: software grid-barrier counter
   int cg_persist_split = 0;       // k1 splits of the last persistent direct CG launch (0: not used)
+  int cg_dft2 = 0;                // 1: the last CG ran the persistent DFT kernel (2D, m beyond the direct product)
   double2 *toep_part = nullptr;  // split direct product: (2m+1) x kToepSplitsHost x (m+1) partial rows
   unsigned *toep_cnt = nullptr;  // per output row: splits done (reset by the row's last CTA)
   double2 *Zbox = nullptr;    // R2C output
@@ -276,6 +280,16 @@ inline bool toeplitz_pt(const Params &P) {
   if (e && e[0] == '2') return P.d >= 2 && !toeplitz_direct(P);  // also 2D (c2: measured slower, 45 vs 27 us)
   return P.d == 3;
 }
+// 2D CG beyond the direct product's m (c2: m = 49): the whole CG as one cooperative kernel with the
+// Toeplitz product by DFTs along the second axis and a direct convolution along the first (cg.cu
+// "persistent DFT CG"); every CTA keeps r, p and D in shared memory, so M_h is bounded.
+constexpr int kDft2MaxMh = 5100;  // 2 (r, p) x 16 B + 8 B (D) per entry, with the stages: <= 227 KB
+inline bool toeplitz_dft2(const Params &P) {
+  const char *e = getenv("EFGP_TOEP_DFT2");
+  if (e && e[0] == '0') return false;
+  return P.d == 2 && !toeplitz_direct(P) && P.Mh <= kDft2MaxMh;
+}
+efgp_status dft2_setup(efgp_plan *pl, cudaStream_t s);
 efgp_status pt_setup(efgp_plan *pl, const double2 *vh, cudaStream_t s);
 efgp_status type1_modes(efgp_plan *pl, double *modes_out, cudaStream_t s);
 efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s);

@@ -169,6 +169,13 @@ efgp_status toeplitz_setup(efgp_plan *pl, const double *modes, cudaStream_t s) {
   k_make_b<<<grid_for(P.Mh, 256, pl->num_sms), 256, 0, s>>>(fyh, pl->D_half, pl->b, P.Mh);
   EFGP_CUDA(cudaGetLastError());
   if (toeplitz_pt(P)) EFGP_TRY(pt_setup(pl, vh, s));
+  if (toeplitz_dft2(P)) {  // 2D, larger m: full v, then its DFT along the second axis (cg.cu)
+    const int n = (int)(4 * P.m + 1);
+    if (!pl->vfull) EFGP_CUDA(cudaMalloc((void **)&pl->vfull, sizeof(double2) * n * n));
+    k_expand_v2<<<grid_for((int64_t)n * n, 256, pl->num_sms), 256, 0, s>>>(vh, (int)P.m, pl->vfull);
+    EFGP_CUDA(cudaGetLastError());
+    EFGP_TRY(dft2_setup(pl, s));
+  }
   if (toeplitz_direct(P)) {  // small m: the CG applies T by direct convolution with the full v
     const int n = (int)(4 * P.m + 1);
     if (!pl->vfull) EFGP_CUDA(cudaMalloc((void **)&pl->vfull, sizeof(double2) * n * n));

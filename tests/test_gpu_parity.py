@@ -718,26 +718,61 @@ def test_persistent_direct_cg_matches_launched(name, monkeypatch):
     # kernel is deterministic (two runs bitwise equal); max_iter is honoured
     import torch
     c = CONFIGS[name]
-    x, y, _ = generate(c, N=200_000, q=10)
+    x, y, xt = generate(c, N=200_000, q=2000)
     g = model(c, cg_tol=c.eps / 1000)
     modes = g.fit_local(dev(x), dev(y))
     N = x.shape[0]
     monkeypatch.setenv("EFGP_CG_PERSIST", "0")
     g.fit_solve(modes, N)
-    it0, b0 = g.info()["iters"], g.weights()
+    it0, b0, mu0 = g.info()["iters"], g.weights(), g.predict(dev(xt)).cpu().numpy()
     assert g.info()["cg_persist_split"] == 0
     monkeypatch.delenv("EFGP_CG_PERSIST")
     g.fit_solve(modes, N)
-    it1, b1 = g.info()["iters"], g.weights()
+    it1, b1, mu1 = g.info()["iters"], g.weights(), g.predict(dev(xt)).cpu().numpy()
     assert g.info()["cg_persist_split"] >= 1
     g.fit_solve(modes, N)
     assert np.array_equal(g.weights(), b1) and g.info()["iters"] == it1
     assert abs(it1 - it0) <= max(2, 0.1 * it0), (it0, it1)
-    assert np.abs(b1 - b0).max() <= 1e-4 * np.abs(b0).max(), np.abs(b1 - b0).max() / np.abs(b0).max()
+    # beta of a chaotic CG differs in its last digits between summation orders; the posterior mean,
+    # what the north star gates (10 eps against the oracle), agrees far inside eps
+    assert rel(mu1, mu0) <= c.eps, rel(mu1, mu0)
+    assert np.abs(b1 - b0).max() <= 1e-2 * np.abs(b0).max()
     torch.cuda.synchronize()
     g2 = model(c, max_iter=7)
     with pytest.warns(RuntimeWarning, match="max_iter"):
         g2.fit_solve(modes, N)
     assert g2.last_status == 1 and g2.info()["iters"] == 7 and len(g2.residual_history()) == 8
+    g.close()
+    g2.close()
+
+
+def test_persistent_dft_cg_matches_fft(monkeypatch):
+    # k_cg_dft2_persist (2D beyond the direct product: c2's m = 49; the Toeplitz product by DFTs along
+    # the second axis and a direct convolution along the first, the whole CG in one cooperative kernel)
+    # against the padded real-FFT CG (EFGP_TOEP_DFT2=0) on the SAME v and F^*y, parity mode (reading
+    # G9): beta to the CG's own sensitivity, counts within a few percent, bitwise-repeatable, max_iter
+    c = CONFIGS["c2"]
+    x, y, xt = generate(c, N=200_000, q=2000)
+    g = model(c, cg_tol=c.eps / 1000)
+    modes = g.fit_local(dev(x), dev(y))
+    N = x.shape[0]
+    assert g.info()["m"] == 49
+    monkeypatch.setenv("EFGP_TOEP_DFT2", "0")
+    g.fit_solve(modes, N)
+    it0, b0, mu0 = g.info()["iters"], g.weights(), g.predict(dev(xt)).cpu().numpy()
+    assert g.info()["cg_dft2"] == 0
+    monkeypatch.delenv("EFGP_TOEP_DFT2")
+    g.fit_solve(modes, N)
+    it1, b1, mu1 = g.info()["iters"], g.weights(), g.predict(dev(xt)).cpu().numpy()
+    assert g.info()["cg_dft2"] == 1
+    g.fit_solve(modes, N)
+    assert np.array_equal(g.weights(), b1) and g.info()["iters"] == it1
+    assert abs(it1 - it0) <= max(2, 0.1 * it0), (it0, it1)
+    assert rel(mu1, mu0) <= c.eps, rel(mu1, mu0)
+    assert np.abs(b1 - b0).max() <= 1e-2 * np.abs(b0).max()
+    g2 = model(c, max_iter=9)
+    with pytest.warns(RuntimeWarning, match="max_iter"):
+        g2.fit_solve(modes, N)
+    assert g2.last_status == 1 and g2.info()["iters"] == 9 and g2.info()["cg_dft2"] == 1
     g.close()
     g2.close()
