@@ -288,7 +288,7 @@ struct FusedSmem {
   // base, perm; shared: the CTA's running segment lengths and the start-cell tables
   static constexpr int kPtBytes = MODE == kModeF64W ? 32 : 24;
   __host__ __device__ static size_t bin_warp_bytes(int ntiles) {
-    return (size_t)kWStages * kWBatch * kPtBytes + 4 * (size_t)kWBatch + 4 * 3 * (size_t)ntiles;
+    return (size_t)kWStages * kWBatch * kPtBytes + 4 * (size_t)kWBatch + 4 * 4 * (size_t)ntiles;
   }
   __host__ __device__ static size_t bin_bytes(int ntiles, int S) {
     return kBinWarps * ((bin_warp_bytes(ntiles) + 15) / 16 * 16) + 4 * ((size_t)ntiles + 2 * (size_t)S);
@@ -312,7 +312,11 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
   int *perm = reinterpret_cast<int *>(yin + (WGT ? 2 : 1) * kWStages * kWBatch);  // kWBatch
   int *wcnt = perm + kWBatch;                                         // ntiles
   int *wloc = wcnt + ntiles;                                          // ntiles
-  int *wbase = wloc + ntiles;                                         // ntiles
+  // per tile, for this batch: the record offset of batch slot 0 in the tile's list buffer (segment
+  // start + reserved base - slot base; a record index, < 2^31 by the host's check) and the slot bound
+  // (slot < wlim <=> the record fits the segment): the copy-out's address is one add per point
+  int *woff = wloc + ntiles;                                          // ntiles
+  int *wlim = woff + ntiles;                                          // ntiles
   int *off = reinterpret_cast<int *>(sm + kBinWarps * wbytes);        // ntiles (CTA-shared)
   int *rowt = off + ntiles;                                           // S
   int *colt = rowt + A.S;                                             // S
@@ -440,7 +444,9 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     for (int t = tb; t < te; ++t) {
       const int c = wcnt[t];
       wloc[t] = run;
-      wbase[t] = c ? atomicAdd(&off[t], c) : 0;
+      const int wb = c ? atomicAdd(&off[t], c) : 0;
+      woff[t] = (t * G + (int)blockIdx.x) * A.segcap + wb - run;
+      wlim[t] = A.segcap - wb + run;
       wcnt[t] = 0;
       run += c;
     }
@@ -454,13 +460,12 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     for (int slot = lane; slot < nv; slot += 32) {
       const int v = perm[slot];
       const int j = v & 0xFF, key = (v >> 8) & 0xFF, t = v >> 16;
-      const int p = wbase[t] + slot - wloc[t];
-      EFGP_DCHECK(j < nb && t < ntiles && slot >= wloc[t] && p >= 0);
+      EFGP_DCHECK(j < nb && t < ntiles && slot >= wloc[t] && woff[t] + slot >= (t * G + (int)blockIdx.x) * A.segcap);
       const double2 xx = xs2[j];
       const double yv = ys[j];
       const double s1v = WGT ? s1s[j] : 0.0;
-      if (p < A.segcap)
-        st_v4(rec + ((int64_t)t * G + blockIdx.x) * A.segcap + p, xx.x, xx.y, WGT ? s1v : yv,
+      if (slot < wlim[t])
+        st_v4(rec + (woff[t] + slot), xx.x, xx.y, WGT ? s1v : yv,
               WGT ? yv : __longlong_as_double((long long)key));  // WGT: (x1, x2, w, y), start cell recomputed
       else
         ovf = true;
@@ -469,7 +474,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       for (int slot = lane; slot < nv; slot += 32) {  // kept out of the hot loop above
         const int v = perm[slot];
         const int j = v & 0xFF, t = v >> 16;
-        if (wbase[t] + slot - wloc[t] >= A.segcap)
+        if (slot >= wlim[t])
           spread_point_red<W>(xs2[j].x, xs2[j].y, ys[j], A.h, A.n1, A.poly_dev, A.g1, A.gy, WGT ? s1s[j] : 1.0);
       }
     }
@@ -1193,6 +1198,10 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
   const int64_t chunk = std::min<int64_t>(P.chunk, (N + kWBatch - 1) / kWBatch * kWBatch);
   const int segcap = sorted_segcap(P, chunk);
   const size_t rec_need = (size_t)P.ntiles * P.tiles_grid * segcap;
+  if (rec_need >= ((size_t)1 << 31)) {  // the binner addresses a list buffer with 32-bit record offsets
+    pl->err = "internal: SORTED list buffer over 2^31 records";
+    return EFGP_ERR_RESOURCE;
+  }
   if (rec_need > pl->rec_cap) {
     for (int k = 0; k < kMaxNbuf; ++k) {
       if (pl->rec[k]) cudaFree(pl->rec[k]);
