@@ -37,6 +37,9 @@
 
 namespace efgp {
 
+#ifndef EFGP_SORTED_BTRACE
+#define EFGP_SORTED_BTRACE 0  // binner phase clocks in the EFGP_SORTED_TRACE buffer (diagnostic builds)
+#endif
 #ifndef EFGP_BIN_WARPS
 #define EFGP_BIN_WARPS 4
 #endif
@@ -380,11 +383,28 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     }
   };
   const int tper = (ntiles + 31) / 32, tb = lane * tper, te = min(ntiles, tb + tper);
+  // optional phase timing (EFGP_SORTED_TRACE): lane 0 of each binner warp, clock64 cycles summed over
+  // the launch: 0 chunk hand-off, 1 TMA wait, 2 load + classify + rank atomics, 3 tile scan + reserve,
+  // 4 permutation, 5 copy-out (+ overflow), 6 batches
+  // (compiled in only with -DEFGP_SORTED_BTRACE=1: the counters cost registers in the binner role)
+#if EFGP_SORTED_BTRACE
+  long long bt_acc[7] = {0, 0, 0, 0, 0, 0, 0}, bt_t = clock64();
+#define BT(i)                               \
+  if (A.trace && lane == 0) {               \
+    const long long t_ = clock64();         \
+    bt_acc[(i)] += t_ - bt_t;               \
+    bt_t = t_;                              \
+  }
+#else
+#define BT(i)
+#endif
   for (int64_t i = 0;; ++i) {
     const int64_t b = gw + i * nw;
     // every warp walks the chunks in order; a warp with no batch left in a chunk still enters it
     const int k = b < nbatch ? (int)(b / bpc) : A.nchunks;
+    BT(5);
     if (k != cur) enter_chunk(k);
+    BT(0);
     if (b >= nbatch) break;
     const int s = (int)(i % kWStages);
     const int64_t i0 = b * kWBatch;
@@ -392,6 +412,10 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     double4 *rec = A.rec[k % A.nbuf];
     mbar_wait(&bar[wid][s], (phases >> s) & 1u);
     phases ^= 1u << s;
+    BT(1);
+#if EFGP_SORTED_BTRACE
+    if (A.trace && lane == 0) ++bt_acc[6];
+#endif
     const double2 *xs2 = reinterpret_cast<const double2 *>(xin + s * 2 * kWBatch);
     double *ys = yin + s * kWBatch;
     double *s1s = s1in + s * kWBatch;
@@ -428,6 +452,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     for (int q = 0; q < kWBatch / 32; ++q) rk[q] = tk[q] >= 0 ? atomicAdd(&wcnt[ci[q]], 1) : 0;
     if (bad) atomicOr(A.err, 1);
     __syncwarp();
+    BT(2);
     // warp scan of the per-tile counts -> slot offsets; reserve room in the CTA's segments
     int sum = 0;
 #pragma unroll 8
@@ -451,10 +476,12 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       run += c;
     }
     __syncwarp();
+    BT(3);
 #pragma unroll
     for (int q = 0; q < kWBatch / 32; ++q)
       if (tk[q] >= 0) perm[wloc[tk[q] >> 8] + rk[q]] = (q * 32 + lane) | (tk[q] << 8);
     __syncwarp();
+    BT(4);
     bool ovf = false;
 #pragma unroll 4
     for (int slot = lane; slot < nv; slot += 32) {
@@ -481,6 +508,13 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     __syncwarp();  // stage s consumed
     issue(i + kWStages);
   }
+#if EFGP_SORTED_BTRACE
+  if (A.trace && lane == 0) {
+    unsigned long long *o = A.trace + (size_t)A.nchunks * G * 4 + (size_t)G * 2 * 8 + ((size_t)blockIdx.x * kBinWarps + wid) * 8;
+    for (int q = 0; q < 7; ++q) o[q] = (unsigned long long)bt_acc[q];
+  }
+#endif
+#undef BT
 }
 
 // -------------------------------------------------------------------------- accumulator role
@@ -1247,7 +1281,7 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
   A.acc_done = A.bin_done + A.nchunks;
   A.trace = nullptr;
   if (std::getenv("EFGP_SORTED_TRACE")) {
-    const size_t tn = (size_t)A.nchunks * G * 4 + (size_t)G * kAccGroups * 8;
+    const size_t tn = (size_t)A.nchunks * G * 4 + (size_t)G * kAccGroups * 8 + (size_t)G * kBinWarps * 8;
     if (tn > pl->trace_cap) {
       if (pl->trace) cudaFree(pl->trace);
       EFGP_CUDA(cudaMalloc((void **)&pl->trace, tn * sizeof(unsigned long long)));

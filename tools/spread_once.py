@@ -41,8 +41,14 @@ def main():
         buf = np.zeros(n, dtype=np.uint64)
         g._lib.efgp_debug_trace(g._h, buf.ctypes.data_as(C.c_void_p), n)
         G = 148
-        nch = (n - G * 2 * 8) // (G * 4)
-        ph = buf[nch * G * 4:].reshape(G * 2, 8).astype(np.float64)[:, :7]
+        nch = (n - G * 2 * 8 - G * 4 * 8) // (G * 4)
+        ph = buf[nch * G * 4:nch * G * 4 + G * 2 * 8].reshape(G * 2, 8).astype(np.float64)[:, :7]
+        bph = buf[nch * G * 4 + G * 2 * 8:].reshape(G * 4, 8).astype(np.float64)
+        bnames = ["chunk hand-off", "TMA wait", "load+classify+rank", "tile scan+reserve", "permutation", "copy-out"]
+        nb = bph[:, 6].sum()
+        if nb > 0:  # (a build with -DEFGP_SORTED_BTRACE=1, e.g. tools/build_variant.sh)
+            print("binner phases (lane 0 of each binner warp, cycles per batch of 256 points, mean over warps):",
+                  ", ".join(f"{nm} {bph[:, q].sum() / nb:.0f}" for q, nm in enumerate(bnames)))
         names = ["wait/chunk", "tma wait", "pass1+scan", "pass2", "phaseC", "fold", "flush"]
         tot = ph.sum(axis=1, keepdims=True)
         frac = (ph / tot).mean(axis=0)
