@@ -284,6 +284,7 @@ struct FusedArgs {
 constexpr int kWBatch = EFGP_WBATCH;              // points per binner-warp batch
 constexpr int kWStages = EFGP_WSTAGES;            // TMA ring depth per binner warp
 constexpr int kBinWarps = kBinThreads / 32;
+constexpr int kTper = 8;  // tiles per binner lane handled by the fixed-trip scan (ntiles <= 256; else a loop)
 
 template <int W, int MODE>
 struct FusedSmem {
@@ -453,27 +454,60 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     if (bad) atomicOr(A.err, 1);
     __syncwarp();
     BT(2);
-    // warp scan of the per-tile counts -> slot offsets; reserve room in the CTA's segments
-    int sum = 0;
-#pragma unroll 8
-    for (int t = tb; t < te; ++t) sum += wcnt[t];
-    int incl = sum;
+    // warp scan of the per-tile counts -> slot offsets; reserve room in the CTA's segments.  A lane's
+    // tiles (<= kTper of them: fixed-trip, predicated) have their counts loaded and their segment
+    // reservations (shared atomics with a return value) issued back to back before any result is
+    // used: a loop that used each atomic's result before issuing the next serialised kTper round trips
+    int nv;
+    if (tper <= kTper) {
+      int cnt[kTper], wbv[kTper];
+      int sum = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int nv = __shfl_sync(0xffffffffu, incl, 31);
-    int run = incl - sum;
-#pragma unroll 8
-    for (int t = tb; t < te; ++t) {
-      const int c = wcnt[t];
-      wloc[t] = run;
-      const int wb = c ? atomicAdd(&off[t], c) : 0;
-      woff[t] = (t * G + (int)blockIdx.x) * A.segcap + wb - run;
-      wlim[t] = A.segcap - wb + run;
-      wcnt[t] = 0;
-      run += c;
+      for (int u = 0; u < kTper; ++u) {
+        cnt[u] = tb + u < te ? wcnt[tb + u] : 0;
+        sum += cnt[u];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      nv = __shfl_sync(0xffffffffu, incl, 31);
+#pragma unroll
+      for (int u = 0; u < kTper; ++u) wbv[u] = cnt[u] ? atomicAdd(&off[tb + u], cnt[u]) : 0;
+      int run = incl - sum;
+#pragma unroll
+      for (int u = 0; u < kTper; ++u) {
+        const int t = tb + u;
+        if (t < te) {
+          wloc[t] = run;
+          woff[t] = (t * G + (int)blockIdx.x) * A.segcap + wbv[u] - run;
+          wlim[t] = A.segcap - wbv[u] + run;
+          wcnt[t] = 0;
+          run += cnt[u];
+        }
+      }
+    } else {
+      int sum = 0;
+      for (int t = tb; t < te; ++t) sum += wcnt[t];
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      nv = __shfl_sync(0xffffffffu, incl, 31);
+      int run = incl - sum;
+      for (int t = tb; t < te; ++t) {
+        const int c = wcnt[t];
+        wloc[t] = run;
+        const int wb = c ? atomicAdd(&off[t], c) : 0;
+        woff[t] = (t * G + (int)blockIdx.x) * A.segcap + wb - run;
+        wlim[t] = A.segcap - wb + run;
+        wcnt[t] = 0;
+        run += c;
+      }
     }
     __syncwarp();
     BT(3);
