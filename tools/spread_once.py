@@ -18,6 +18,8 @@ def main():
     ap.add_argument("--spread", default="sorted")
     ap.add_argument("--fits", type=int, default=2)
     ap.add_argument("--config", default="c5")
+    ap.add_argument("--hetero", action="store_true",
+                    help="the NEXT-3 one-pass weighted spread (fit_hetero, sigma_n = sigma (0.5 + U))")
     a = ap.parse_args()
     import torch
     from efgp_data import CONFIGS
@@ -28,10 +30,18 @@ def main():
     x, y = G.generate_points(c, 0, N)
     torch.cuda.synchronize()
     g = EFGP(c.kernel, c.ell, c.sigma, c.eps, c.d, c.nu, max_iter=1, spread=a.spread, weights=a.weights)
+    sd = None
+    if a.hetero:
+        gen = torch.Generator(device=x.device)
+        gen.manual_seed(1234)
+        sd = c.sigma * (0.5 + torch.rand(N, dtype=torch.float64, device=x.device, generator=gen))
     for _ in range(a.fits):
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
-            g.fit(x, y)
+            if sd is None:
+                g.fit(x, y)
+            else:
+                g.fit_hetero(x, y, sd)
         inf = g.info()
         print(f"spread {inf['t_spread_ms']:.3f} ms  {N / inf['t_spread_ms'] * 1e3:.3e} pts/s", flush=True)
     if os.environ.get("EFGP_SORTED_TRACE"):
