@@ -732,9 +732,10 @@ def test_persistent_direct_cg_matches_launched(name, monkeypatch):
     assert g.info()["cg_persist_split"] >= 1
     g.fit_solve(modes, N)
     assert np.array_equal(g.weights(), b1) and g.info()["iters"] == it1
-    assert abs(it1 - it0) <= max(2, 0.1 * it0), (it0, it1)
-    # beta of a chaotic CG differs in its last digits between summation orders; the posterior mean,
-    # what the north star gates (10 eps against the oracle), agrees far inside eps
+    # parity-mode counts of a plateaued CG move by ~10 % under any change of summation order (the
+    # launched path against itself with v x (1 + 1e-13 n): 5313 -> 5869 on c5); the posterior mean,
+    # what the north star gates (10 eps against the oracle, reading G9), agrees far inside eps
+    assert abs(it1 - it0) <= max(2, 0.25 * it0), (it0, it1)
     assert rel(mu1, mu0) <= c.eps, rel(mu1, mu0)
     assert np.abs(b1 - b0).max() <= 1e-2 * np.abs(b0).max()
     torch.cuda.synchronize()
@@ -767,7 +768,7 @@ def test_persistent_dft_cg_matches_fft(monkeypatch):
     assert g.info()["cg_dft2"] == 1
     g.fit_solve(modes, N)
     assert np.array_equal(g.weights(), b1) and g.info()["iters"] == it1
-    assert abs(it1 - it0) <= max(2, 0.1 * it0), (it0, it1)
+    assert abs(it1 - it0) <= max(2, 0.25 * it0), (it0, it1)  # (chaotic parity-mode counts, see above)
     assert rel(mu1, mu0) <= c.eps, rel(mu1, mu0)
     assert np.abs(b1 - b0).max() <= 1e-2 * np.abs(b0).max()
     g2 = model(c, max_iter=9)
@@ -776,3 +777,34 @@ def test_persistent_dft_cg_matches_fft(monkeypatch):
     assert g2.last_status == 1 and g2.info()["iters"] == 9 and g2.info()["cg_dft2"] == 1
     g.close()
     g2.close()
+
+
+# 2D CG paths by half-width m (c5's kernel and data, h of c5): the persistent direct kernel (m <= 28:
+# toeplitz_direct's shared-memory bound; including degenerate tiny m), the persistent DFT kernel
+# (beyond it, M_h within its shared-memory bound,
+# odd and even Toeplitz boxes L), the launched padded-FFT CG beyond it.  Whole path against the
+# oracle in parity mode (reading G9): mu within 10 eps.
+@pytest.mark.parametrize("m_over,path", [(1, "direct"), (3, "direct"), (17, "direct"), (28, "direct"),
+                                         (29, "dft2"), (41, "dft2"), (41, "fft")])
+def test_2d_cg_paths_by_m(m_over, path, monkeypatch):
+    # (m = 49 is c2's own, gated at full size by the golden test; the FFT CG is also what M_h beyond the
+    # DFT kernel's shared-memory bound (m >= 50) takes: forced here with EFGP_TOEP_DFT2=0)
+    if path == "fft":
+        monkeypatch.setenv("EFGP_TOEP_DFT2", "0")
+    c = CONFIGS["c5"]
+    x, y, xt = generate(c, N=4000, q=500)
+    h0, _ = O.choose_params(c.kernel, c.ell, c.d, c.eps, c.nu)
+    cg_tol = c.eps / 1000
+    g = model(c, cg_tol=cg_tol, h=h0, m=m_over)
+    g.fit(dev(x), dev(y))
+    inf = g.info()
+    assert inf["m"] == m_over
+    got = "direct" if inf["cg_persist_split"] > 0 else ("dft2" if inf["cg_dft2"] else "fft")
+    assert got == path, (got, path, inf["L"])
+    mu = g.predict(dev(xt)).cpu().numpy()
+    fit = O.efgp_fit(x, y, c.kernel, c.ell, c.sigma, c.eps, nu=c.nu, cg_tol=cg_tol, h=h0, m=m_over)
+    ref = O.efgp_predict(fit, xt)
+    assert rel(mu, ref) <= 10 * c.eps, rel(mu, ref)
+    hist = g.residual_history()
+    assert len(hist) == inf["iters"] + 1 and hist[-1] <= cg_tol
+    g.close()
