@@ -143,7 +143,8 @@ __global__ void __launch_bounds__(kIB, 1024 / kIB) k_interp2_banked(const double
                                                                     EsPoly P, int lo, int A, const double *__restrict__ sd,
                                                                     double *__restrict__ mu, int *__restrict__ err) {
   extern __shared__ __align__(16) double sgrid[];
-  __shared__ double s_s[2][kIB];       // reduced coordinates of the batch's targets (by batch index)
+  __shared__ double2 s_s[kIB];         // reduced coordinates (s0, s1) of the batch's targets (by batch
+                                       // index): one 16-byte access in the permuted read
   __shared__ int s_cell[kIB];          // first-cell offset r A + c in the staged grid (-1: invalid / none)
   __shared__ short s_tbl[kIB];         // thread slot -> batch index
   __shared__ short s_ovf[kIB];         // targets beyond their class quota
@@ -176,8 +177,7 @@ __global__ void __launch_bounds__(kIB, 1024 / kIB) k_interp2_banked(const double
         double s0, s1;
         const int b0 = es_reduce<W>(h * xc.x * (double)n, s0);
         const int b1 = es_reduce<W>(h * xc.y * (double)n, s1);
-        s_s[0][tid] = s0;
-        s_s[1][tid] = s1;
+        s_s[tid] = make_double2(s0, s1);
         cell = (b0 - lo) * A + (b1 - lo);
       } else {
         mu[i] = __longlong_as_double(0x7ff8000000000000LL);
@@ -203,8 +203,9 @@ __global__ void __launch_bounds__(kIB, 1024 / kIB) k_interp2_banked(const double
     if (j >= 0) {
       EFGP_DCHECK(j < kIB && s_cell[j] >= 0 && s_cell[j] + (W - 1) * (A + 1) < A * A);
       double wt[2][W];
-      es_weights_s<W>(s_s[0][j], P, wt[0]);
-      es_weights_s<W>(s_s[1][j], P, wt[1]);
+      const double2 sj = s_s[j];
+      es_weights_s<W>(sj.x, P, wt[0]);
+      es_weights_s<W>(sj.y, P, wt[1]);
       const double *win = sgrid + s_cell[j];
       double acc = 0.0;
 #pragma unroll
