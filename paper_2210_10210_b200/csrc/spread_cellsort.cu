@@ -69,7 +69,7 @@ __device__ __forceinline__ bool cs_load_batch(const double *__restrict__ x, cons
     const int64_t j = i < e ? i : i0;  // (i0 < e: a valid index for the masked lanes)
 #pragma unroll
     for (int k = 0; k < D; ++k) P.x[u][k] = __ldg(x + j * D + k);
-    P.y[u] = __ldg(y + j);
+    P.y[u] = y ? __ldg(y + j) : 0.0;
     P.w[u] = w1 ? __ldg(w1 + j) : 1.0;
   }
   bool bad = false;
@@ -218,6 +218,104 @@ __global__ void k_cs_items(const long long *__restrict__ off, const long long *_
   long long it = iof[c];
   for (long long b = off[c]; b < off[c + 1]; b += kCsRun, ++it)
     items[it] = CsItem{b, b + kCsRun < off[c + 1] ? b + kCsRun : off[c + 1], c, 0};
+}
+
+// Column scan of the per-CTA histograms, global bucket offsets and work items in one kernel (r02;
+// replaces k_het_colscan + k_cs_offsets (one CTA) + k_cs_items: 22 + 37 + 5 us cold on c3).  CTA b
+// (logical index from a ticket, so every predecessor has started) owns cells [256 b, 256 b + 256):
+// thread c scans its column of hist over the B histogram rows (exclusive, in place) to the bucket size
+// tot_c, the CTA scans (tot, ceil(tot / kCsRun)) and publishes its aggregate, then looks back over the
+// predecessors' published words (decoupled look-back) for its exclusive prefix.  A status word packs
+// flag (2 bits: 1 aggregate, 2 inclusive prefix) | items (30 bits) | points (32 bits): one 64-bit
+// store publishes it, no torn reads (N < 2^32 and fewer than 2^30 items per call).
+constexpr int kScanThreads = 256;
+__global__ void __launch_bounds__(kScanThreads) k_cs_scan(unsigned *__restrict__ hist, int nblk, int ncell,
+                                                          long long N, long long *__restrict__ off,
+                                                          long long *__restrict__ iof, CsItem *__restrict__ items,
+                                                          unsigned long long *st) {
+  __shared__ unsigned ws_p[kScanThreads / 32], ws_i[kScanThreads / 32];
+  __shared__ unsigned long long pre_s;
+  __shared__ int bid_s;
+  if (threadIdx.x == 0) bid_s = (int)atomicAdd(reinterpret_cast<unsigned *>(st + gridDim.x), 1u);
+  __syncthreads();
+  const int b = bid_s, t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int c = b * kScanThreads + t;
+  unsigned tot = 0;
+  if (c < ncell) {  // column scan (loads of a chunk of rows before any store, as k_het_colscan)
+    constexpr int kChunk = 16;
+    unsigned run = 0;
+    for (int b0 = 0; b0 < nblk; b0 += kChunk) {
+      unsigned v[kChunk];
+#pragma unroll
+      for (int k = 0; k < kChunk; ++k) v[k] = b0 + k < nblk ? __ldcg(hist + (size_t)(b0 + k) * ncell + c) : 0u;
+#pragma unroll
+      for (int k = 0; k < kChunk; ++k) {
+        if (b0 + k < nblk) hist[(size_t)(b0 + k) * ncell + c] = run;
+        run += v[k];
+      }
+    }
+    tot = run;
+  }
+  const unsigned nit = (tot + kCsRun - 1) / kCsRun;
+  // CTA scan of (tot, nit)
+  unsigned ip = tot, ii = nit;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned vp = __shfl_up_sync(0xffffffffu, ip, o), vi = __shfl_up_sync(0xffffffffu, ii, o);
+    if (lane >= o) {
+      ip += vp;
+      ii += vi;
+    }
+  }
+  if (lane == 31) {
+    ws_p[wid] = ip;
+    ws_i[wid] = ii;
+  }
+  __syncthreads();
+  unsigned bp = 0, bi = 0, ap = 0, ai = 0;  // warp prefix, CTA aggregate
+  for (int w = 0; w < kScanThreads / 32; ++w) {
+    if (w < wid) {
+      bp += ws_p[w];
+      bi += ws_i[w];
+    }
+    ap += ws_p[w];
+    ai += ws_i[w];
+  }
+  if (t == 0) {
+    const unsigned long long agg = (unsigned long long)ai << 32 | ap;
+    unsigned long long excl = 0;  // (items << 32 | points) of the predecessors
+    if (b == 0) {
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(st + b), "l"(agg | (2ull << 62)) : "memory");
+    } else {
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(st + b), "l"(agg | (1ull << 62)) : "memory");
+      for (int p = b - 1; p >= 0;) {
+        unsigned long long w;
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(st + p) : "memory");
+        const unsigned fl = (unsigned)(w >> 62);
+        if (fl == 0) continue;  // not published yet: spin
+        excl += w & ~(3ull << 62);
+        if (fl == 2) break;
+        --p;
+      }
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(st + b), "l"((excl + agg) | (2ull << 62)) : "memory");
+    }
+    pre_s = excl;
+  }
+  __syncthreads();
+  const unsigned long long pre = pre_s;
+  if (c < ncell) {
+    const long long o = (long long)(pre & 0xFFFFFFFFull) + bp + (ip - tot);
+    const long long io = (long long)(pre >> 32) + bi + (ii - nit);
+    off[c] = o;
+    iof[c] = io;
+    long long it = io;
+    for (long long a = o; a < o + tot; a += kCsRun, ++it)
+      items[it] = CsItem{a, a + kCsRun < o + tot ? a + kCsRun : o + tot, c, 0};
+    if (c == ncell - 1) {
+      off[ncell] = N;
+      iof[ncell] = io + nit;
+    }
+  }
 }
 
 __device__ __forceinline__ int cs_wrap(int i, int n) {
@@ -509,13 +607,25 @@ static efgp_status cellsort_t(efgp_plan *pl, const double *x, const double *y, c
   const size_t sm = sizeof(unsigned) * ncell;
   EFGP_CUDA(cudaFuncSetAttribute(k_cs_count<D, W, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   EFGP_CUDA(cudaFuncSetAttribute(k_cs_scatter<D, W, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_cs_count<D, W, G><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, pl->dflags);
-  k_het_colscan<<<(ncell + 255) / 256, 256, 0, s>>>(hist, B, ncell, tot);
-  EFGP_CUDA(cudaFuncSetAttribute(k_cs_offsets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_cs_offsets<<<1, 1024, sm, s>>>(tot, ncell, off, iof);
-  k_cs_scatter<D, W, G><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, off, rec, pl->dflags, w1, ws1);
-  // work items on the device (no host round trip): at most ceil(N / kCsRun) + ncell of them
-  k_cs_items<<<(ncell + 255) / 256, 256, 0, s>>>(off, iof, ncell, items);
+  // (the count reads x only: y does not change a key, and the scatter validates y)
+  k_cs_count<D, W, G><<<B, T, sm, s>>>(x, nullptr, N, P.h, n, lo, S, ncell, hist, pl->dflags);
+  if (getenv("EFGP_CS_SCAN3")) {  // r02 before the fused scan: three launches
+    k_het_colscan<<<(ncell + 255) / 256, 256, 0, s>>>(hist, B, ncell, tot);
+    EFGP_CUDA(cudaFuncSetAttribute(k_cs_offsets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_cs_offsets<<<1, 1024, sm, s>>>(tot, ncell, off, iof);
+    k_cs_scatter<D, W, G><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, off, rec, pl->dflags, w1, ws1);
+    k_cs_items<<<(ncell + 255) / 256, 256, 0, s>>>(off, iof, ncell, items);
+  } else {
+    // column scan + global bucket offsets (decoupled look-back) + work items in ONE kernel
+    const int nsb = (ncell + kScanThreads - 1) / kScanThreads;
+    unsigned long long *scan_st = nullptr;
+    EFGP_PALLOC(&scan_st, sizeof(unsigned long long) * (nsb + 1), s);
+    EFGP_CUDA(cudaMemsetAsync(scan_st, 0, sizeof(unsigned long long) * (nsb + 1), s));
+    k_cs_scan<<<nsb, kScanThreads, 0, s>>>(hist, B, ncell, N, off, iof, items, scan_st);
+    k_cs_scatter<D, W, G><<<B, T, sm, s>>>(x, y, N, P.h, n, lo, S, ncell, hist, off, rec, pl->dflags, w1, ws1);
+    cudaFreeAsync(scan_st, s);
+  }
+  // (work items on the device, no host round trip: at most ceil(N / kCsRun) + ncell of them)
   EFGP_CUDA(cudaGetLastError());
   int per_sm = 1;
   // quarter-warp 2D layout for union windows up to 12 (EFGP_CS_R01: the r01 layout)
