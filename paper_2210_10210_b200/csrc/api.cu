@@ -183,6 +183,7 @@ efgp_status fit_local_impl(efgp_plan *pl, const double *x, const double *y, int6
     return EFGP_ERR_INVALID;
   }
   cudaStream_t s = pl->stream;
+  NvtxRange nv("efgp: type-1 (spread + modes)");
   EFGP_TRY(enter(pl));
   EFGP_CUDA(cudaEventRecord(pl->ev[0], s));
   EFGP_TRY(spread_begin(pl, s));
@@ -221,6 +222,7 @@ efgp_status fit_solve_impl(efgp_plan *pl, const double *modes, int64_t N_total) 
   cudaStream_t s = pl->stream;
   pl->fitted = false;
   pl->t2_valid = false;
+  NvtxRange nv("efgp: Toeplitz setup + CG");
   EFGP_TRY(enter(pl));
   EFGP_CUDA(cudaEventRecord(pl->ev[3], s));
   EFGP_CUDA(cudaMemcpyAsync(pl->modes_sum, modes, sizeof(double) * 2 * (P.Kvh + P.Mh), cudaMemcpyDefault, s));
@@ -305,6 +307,7 @@ efgp_status efgp_setup(efgp_handle *out, efgp_kernel kernel, double nu, double e
 }
 
 efgp_status efgp_fit(efgp_handle pl, const double *x, const double *y, int64_t N) {
+  efgp::NvtxRange nv_call("efgp_fit");
   if (!pl) return EFGP_ERR_INVALID;
   const efgp_status st = fit_local_impl(pl, x, y, N, pl->modes);
   if (pl->comm) {
@@ -342,6 +345,7 @@ efgp_status efgp_comm_init(efgp_handle pl, const void *id, int nranks, int rank)
 }
 
 efgp_status efgp_fit_hetero(efgp_handle pl, const double *x, const double *y, const double *noise_sd, int64_t N) {
+  efgp::NvtxRange nv_call("efgp_fit_hetero");
   if (!pl) return EFGP_ERR_INVALID;
   if (N < 1 || !x || !y || !noise_sd) {
     pl->err = "fit_hetero: N must be >= 1 and pointers non-null";
@@ -389,6 +393,7 @@ efgp_status efgp_fit_solve(efgp_handle pl, const double *modes, int64_t N_total)
 }
 
 efgp_status efgp_predict(efgp_handle pl, const double *xt, int64_t q, double *mu_out) {
+  efgp::NvtxRange nv_call("efgp_predict");
   if (!pl) return EFGP_ERR_INVALID;
   if (!pl->fitted) {
     pl->err = "predict before a successful fit or load_weights";
@@ -437,6 +442,7 @@ efgp_status efgp_predict(efgp_handle pl, const double *xt, int64_t q, double *mu
 }
 
 efgp_status efgp_predict_var(efgp_handle pl, const double *xt, int64_t q, double *var_out) {
+  efgp::NvtxRange nv_call("efgp_predict_var");
   if (!pl) return EFGP_ERR_INVALID;
   if (!pl->fitted || !pl->op_valid) {
     pl->err = "predict_var before a successful fit (the variance needs the fit's Toeplitz operator)";

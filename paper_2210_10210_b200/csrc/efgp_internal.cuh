@@ -10,6 +10,18 @@
 
 #include "../../include/efgp.h"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost a few ns without a tool attached
+
+namespace efgp {
+// NVTX range for the scope of a C-ABI call or one of its phases (nsys / ncu --nvtx timelines)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+}  // namespace efgp
+
 namespace efgp {
 
 constexpr double kPi = 3.14159265358979323846;
