@@ -142,8 +142,9 @@ typedef struct {
   int64_t spread_fallback; /* efgp_spread_fallback of the last fit (NONE: the planned method ran) */
   int64_t cg_persist_split; /* direct 2D CG (c3, c5): k1 splits of the persistent one-kernel loop of the
                               last fit; 0 when the launched per-iteration kernels ran */
-  int64_t cg_dft2;          /* 2D CG beyond the direct product (c2): 1 when the last fit ran the
-                              persistent DFT kernel (one cooperative launch), 0 otherwise */
+  int64_t cg_dft2;          /* one-launch CG kernels other than the direct 2D one: 1 when the last fit ran
+                              the persistent DFT kernel (2D beyond the direct product, c2), 2 the one-CTA
+                              1D kernel (c1), 0 otherwise */
 } efgp_info;
 
 /* Fill *opt with defaults (all zero / automatic). */

@@ -1603,6 +1603,119 @@ static cudaError_t launch_dft2_cg(efgp_plan *pl, CGState *st, cudaStream_t s) {
   return e;
 }
 
+// ---- 1D CG in one CTA (c1: m = 15) -------------------------------------------------------------
+// In 1D the system is tiny (M_h = m + 1 entries; c1: 16), and the launched loop (pad, C2R, multiply,
+// R2C, apply, x/r, p: 7 launches per iteration, ~17 us) is all dependent-launch latency.  One CTA runs
+// the whole CG with every vector in shared memory and the Toeplitz product by its direct sum
+// out_j = sum_{k=-m}^{m} v_{j-k} u_k (u = D p, u_{-k} = conj u_k; out_0 forced real, as the FFT
+// path's C2R projects), the recurrences and stopping rule of k_cg_xr + k_cg_p (reading G6).
+constexpr int kCg1Threads = 256, kCg1MaxM = 256;
+__device__ __forceinline__ double cg1_sum(double v, double *sh) {  // block sum, valid in every thread
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) sh[32] = v;
+  __syncthreads();
+  const double r = sh[32];
+  __syncthreads();
+  return r;
+}
+__global__ void __launch_bounds__(kCg1Threads) k_cg_1d(const double2 *__restrict__ vh, const double *__restrict__ Dh,
+                                                       double2 *x, double2 *r, double2 *p0, int m, CGState *st,
+                                                       double *hist) {
+  extern __shared__ __align__(16) double2 c1sm[];
+  __shared__ double sh[40];
+  const int Mh = m + 1, t = threadIdx.x;
+  double2 *vs = c1sm, *us = vs + 4 * m + 1, *rs = us + 2 * m + 1, *ps = rs + Mh, *xs = ps + Mh;
+  double *ds = reinterpret_cast<double *>(xs + Mh);
+  for (int d = t; d <= 4 * m; d += kCg1Threads) {  // v over J_2m: v_{-d} = conj v_d
+    const int dl = d - 2 * m;
+    const double2 v = vh[dl >= 0 ? dl : -dl];
+    vs[d] = dl >= 0 ? v : make_double2(v.x, -v.y);
+  }
+  for (int i = t; i < Mh; i += kCg1Threads) {
+    rs[i] = ps[i] = r[i];  // r_0 = b (k_cg_init)
+    xs[i] = x[i];
+    ds[i] = Dh[i];
+  }
+  const double tol = st->tol, bnorm = st->bnorm, s2 = st->sigma2;
+  const long long max_iter = st->max_iter;
+  long long it = st->iter;
+  if (st->done) return;
+  double rr = st->rrs[0], beta = 0.0;
+  __syncthreads();
+  for (;;) {
+    for (int i = t; i < Mh; i += kCg1Threads) {
+      const double2 rq = rs[i], po = ps[i];
+      ps[i] = make_double2(rq.x + beta * po.x, rq.y + beta * po.y);
+    }
+    __syncthreads();
+    for (int k = t; k <= 2 * m; k += kCg1Threads) {
+      const int kk = k - m, a = kk >= 0 ? kk : -kk;
+      const double2 pp = ps[a];
+      us[k] = make_double2(ds[a] * pp.x, kk >= 0 ? ds[a] * pp.y : -ds[a] * pp.y);
+    }
+    __syncthreads();
+    double acc = 0.0;
+    double2 apv[(kCg1MaxM + kCg1Threads) / kCg1Threads];
+#pragma unroll
+    for (int q = 0; q < (kCg1MaxM + kCg1Threads) / kCg1Threads; ++q) {
+      const int j = t + q * kCg1Threads;
+      if (j < Mh) {
+        double ox = 0.0, oy = 0.0;
+        for (int k = 0; k <= 2 * m; ++k) {  // v_{j-k} u_k, k = -m..m
+          const double2 v = vs[j - (k - m) + 2 * m], u = us[k];
+          ox = fma(v.x, u.x, fma(-v.y, u.y, ox));
+          oy = fma(v.x, u.y, fma(v.y, u.x, oy));
+        }
+        const double2 pp = ps[j];
+        double2 a = make_double2(ds[j] * ox + s2 * pp.x, ds[j] * oy + s2 * pp.y);
+        if (j == 0) a.y = s2 * pp.y;  // j = 0: (T u)_0 is real
+        apv[q] = a;
+        acc += (j ? 2.0 : 1.0) * (pp.x * a.x + pp.y * a.y);
+      }
+    }
+    const double alpha = rr / cg1_sum(acc, sh);
+    double racc = 0.0;
+#pragma unroll
+    for (int q = 0; q < (kCg1MaxM + kCg1Threads) / kCg1Threads; ++q) {
+      const int j = t + q * kCg1Threads;
+      if (j < Mh) {
+        const double2 pp = ps[j];
+        double2 rq = rs[j], xq = xs[j];
+        xq.x += alpha * pp.x;
+        xq.y += alpha * pp.y;
+        rq.x -= alpha * apv[q].x;
+        rq.y -= alpha * apv[q].y;
+        xs[j] = xq;
+        rs[j] = rq;
+        racc += (j ? 2.0 : 1.0) * (rq.x * rq.x + rq.y * rq.y);
+      }
+    }
+    const double rr_new = cg1_sum(racc, sh);
+    ++it;
+    beta = rr_new / rr;
+    const double rr_prev = rr;
+    rr = rr_new;
+    const double rel = sqrt(rr_new) / bnorm;
+    const int stop = rel <= tol ? 1 : (it >= max_iter ? 2 : 0);
+    if (t == 0) {
+      st->rr = rr_new;
+      st->rr_old = rr_prev;
+      st->rrs[it & 1] = rr_new;
+      st->iter = it;
+      hist[it] = rel;
+      if (stop) st->done = stop;
+    }
+    if (stop) {
+      for (int i = t; i < Mh; i += kCg1Threads) {
+        x[i] = xs[i];
+        r[i] = rs[i];
+        p0[i] = ps[i];
+      }
+      return;
+    }
+  }
+}
+
 static int persist_split_env() {
   const char *e = getenv("EFGP_CG_PSPLIT");
   return (e && atoi(e) > 0) ? atoi(e) : 0;
@@ -1812,6 +1925,23 @@ static efgp_status cg_solve_d(efgp_plan *pl, int64_t N_total) {
   const bool fused = D == 2 && toeplitz_direct(P) && pl->p2 && pl->toep_part && cg_fused() && toep_split();
   pl->cg_persist_split = 0;
   pl->cg_dft2 = 0;
+  if (D == 1 && P.m <= kCg1MaxM && cg_persist()) {  // 1D: the whole CG in one CTA
+    const int m = (int)P.m;
+    const size_t smem = sizeof(double2) * ((4 * (size_t)m + 1) + (2 * (size_t)m + 1) + 3 * ((size_t)m + 1)) +
+                        sizeof(double) * ((size_t)m + 1);
+    EFGP_CUDA(cudaFuncSetAttribute(k_cg_1d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_cg_1d<<<1, kCg1Threads, smem, s>>>(reinterpret_cast<const double2 *>(pl->modes_sum), pl->D_half, pl->x, pl->r,
+                                         pl->p, m, st, pl->hist);
+    EFGP_CUDA(cudaGetLastError());
+    pl->cg_dft2 = 2;  // (info: 2 = the one-CTA 1D kernel)
+    CGState host{};
+    EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned, st, sizeof(CGState), cudaMemcpyDeviceToHost, s));
+    EFGP_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(&host, pl->h_pinned, sizeof(CGState));
+    pl->iters = host.iter;
+    pl->rel_resid = host.bnorm > 0 ? std::sqrt(host.rr) / host.bnorm : 0.0;
+    return host.done == 2 ? EFGP_ERR_NOCONVERGE : EFGP_OK;
+  }
   if (D == 2 && toeplitz_dft2(P) && cg_persist()) {  // 2D beyond the direct product: persistent DFT CG
     const cudaError_t e = launch_dft2_cg(pl, st, s);
     if (e == cudaSuccess) {

@@ -808,3 +808,30 @@ def test_2d_cg_paths_by_m(m_over, path, monkeypatch):
     hist = g.residual_history()
     assert len(hist) == inf["iters"] + 1 and hist[-1] <= cg_tol
     g.close()
+
+
+def test_one_cta_1d_cg_matches_launched(monkeypatch):
+    # k_cg_1d (1D, m <= 256: the whole CG in one CTA, direct product) against the launched FFT CG on
+    # the same modes (c1, parity mode): mu far inside eps, counts close, bitwise-repeatable, max_iter
+    c = CONFIGS["c1"]
+    x, y, xt = generate(c, N=10_000, q=1000)
+    g = model(c, cg_tol=c.eps / 1000)
+    modes = g.fit_local(dev(x), dev(y))
+    monkeypatch.setenv("EFGP_CG_PERSIST", "0")
+    g.fit_solve(modes, 10_000)
+    it0, mu0 = g.info()["iters"], g.predict(dev(xt)).cpu().numpy()
+    assert g.info()["cg_dft2"] == 0
+    monkeypatch.delenv("EFGP_CG_PERSIST")
+    g.fit_solve(modes, 10_000)
+    it1, b1, mu1 = g.info()["iters"], g.weights(), g.predict(dev(xt)).cpu().numpy()
+    assert g.info()["cg_dft2"] == 2
+    g.fit_solve(modes, 10_000)
+    assert np.array_equal(g.weights(), b1) and g.info()["iters"] == it1
+    assert abs(it1 - it0) <= max(2, 0.25 * it0), (it0, it1)
+    assert rel(mu1, mu0) <= c.eps, rel(mu1, mu0)
+    g2 = model(c, max_iter=4)
+    with pytest.warns(RuntimeWarning, match="max_iter"):
+        g2.fit_solve(modes, 10_000)
+    assert g2.last_status == 1 and g2.info()["iters"] == 4 and len(g2.residual_history()) == 5
+    g.close()
+    g2.close()
