@@ -982,7 +982,9 @@ constexpr int kPersistU = 3;    // u entries per thread (nk (2m+1) <= 3 x 256: c
 __global__ void __launch_bounds__(kPersistThreads, 2) k_cg_toep2_persist(
     const double2 *__restrict__ vfull, const double *__restrict__ Dh, double2 *x, double2 *r, double2 *p0,
     double2 *ap0, double2 *ap1, int m, int nsplit, CGState *st, double2 *tpart, unsigned *tcnt, double *part_pAp,
-    double *hist, unsigned *gbar, long long *trace) {
+    double *hist, unsigned *gbar, long long *trace, const double2 *vh0) {
+  // vh0 != nullptr: Jacobi PCG (reading G12b, NEXT-4): z = r / (D^2 v_0 + sigma^2), p = z + beta p with
+  // beta = (r, z)_new / (r, z), alpha = (r, z) / (p, Ap); the stop test stays on ||r|| (as pcg_solve)
   extern __shared__ double2 tsm[];
   __shared__ double sh[40];
   __shared__ bool last_s;
@@ -1013,6 +1015,21 @@ __global__ void __launch_bounds__(kPersistThreads, 2) k_cg_toep2_persist(
   double rr = st->rrs[0], beta = 0.0;
   unsigned target = 0;
   const int own_lo = (int)blockIdx.x * kPersistThreads, own_hi = min(Mh, own_lo + kPersistThreads);
+  const bool jac = vh0 != nullptr;
+  const double v0 = jac ? vh0->x : 0.0;
+  auto inv_diag = [&](int i) { const double d = Dh[i]; return 1.0 / (d * d * v0 + s2); };
+  double rz = 0.0;  // Jacobi: (r, z), the same fixed-order sum in every CTA
+  if (jac) {
+    double a = 0.0;
+    for (int i = threadIdx.x; i < Mh; i += blockDim.x) {
+      const double2 rq = rs[i];
+      a += ((i % (m + 1)) ? 2.0 : 1.0) * (rq.x * rq.x + rq.y * rq.y) * inv_diag(i);
+    }
+    a = block_sum(a, sh);
+    if (threadIdx.x == 0) sh[34] = a;
+    __syncthreads();
+    rz = sh[34];
+  }
   // this thread's entries of u = D p on the split's k1 rows, fixed for all iterations: the stored
   // (canonical-half) index << 1 | conjugate flag, and D (-1: no entry)
   int uq[kPersistU];
@@ -1044,7 +1061,12 @@ __global__ void __launch_bounds__(kPersistThreads, 2) k_cg_toep2_persist(
     // phase 1: p_j (all entries, every CTA), u = D p_j on this split's k1 rows (canonical half:
     // exactly Hermitian, see k_cg_toep2), the product
     for (int i = threadIdx.x; i < Mh; i += blockDim.x) {
-      const double2 rq = rs[i], po = ps[i];
+      double2 rq = rs[i];
+      if (jac) {
+        const double w = inv_diag(i);
+        rq = make_double2(rq.x * w, rq.y * w);  // z = M^-1 r
+      }
+      const double2 po = ps[i];
       ps[i] = make_double2(rq.x + beta * po.x, rq.y + beta * po.y);
     }
     for (int idx = threadIdx.x; idx < nk * nc * nout; idx += blockDim.x) red[idx] = make_double2(0.0, 0.0);
@@ -1163,8 +1185,8 @@ __global__ void __launch_bounds__(kPersistThreads, 2) k_cg_toep2_persist(
     v = block_sum(v, sh);
     if (threadIdx.x == 0) sh[32] = v;
     __syncthreads();
-    const double alpha = rr / sh[32];
-    double acc = 0.0;
+    const double alpha = (jac ? rz : rr) / sh[32];
+    double acc = 0.0, accz = 0.0;
 #pragma unroll
     for (int k = 0; k < kPersistPer; ++k) {
       const int i = t + k * kPersistThreads;
@@ -1174,7 +1196,9 @@ __global__ void __launch_bounds__(kPersistThreads, 2) k_cg_toep2_persist(
         rq.x -= alpha * a.x;
         rq.y -= alpha * a.y;
         rs[i] = rq;
-        acc += ((i % (m + 1)) ? 2.0 : 1.0) * (rq.x * rq.x + rq.y * rq.y);
+        const double e = ((i % (m + 1)) ? 2.0 : 1.0) * (rq.x * rq.x + rq.y * rq.y);
+        acc += e;
+        if (jac) accz += e * inv_diag(i);
         if (i >= own_lo && i < own_hi) {  // x of the owned entries lives in shared memory until the end
           xs[t].x += alpha * pp.x;
           xs[t].y += alpha * pp.y;
@@ -1185,9 +1209,17 @@ __global__ void __launch_bounds__(kPersistThreads, 2) k_cg_toep2_persist(
     if (threadIdx.x == 0) sh[33] = acc;
     __syncthreads();
     const double rr_new = sh[33];
+    if (jac) {
+      accz = block_sum(accz, sh);
+      if (threadIdx.x == 0) sh[35] = accz;
+      __syncthreads();
+      const double rz_new = sh[35];
+      beta = rz_new / rz;
+      rz = rz_new;
+    }
     TR(5);
     ++it;
-    beta = rr_new / rr;
+    if (!jac) beta = rr_new / rr;
     const double rr_prev = rr;
     rr = rr_new;
     const double rel = sqrt(rr_new) / bnorm;
@@ -1251,7 +1283,8 @@ struct DftGeom {
 __global__ void __launch_bounds__(kDftThreads, 1) k_cg_dft2_persist(
     const double2 *__restrict__ Vt, const double2 *__restrict__ roots, const double *__restrict__ Dh, double2 *x,
     double2 *r, double2 *p0, double2 *Ap, double2 *Wg, int m, int L, CGState *st, double *part_pAp, double *hist,
-    unsigned *gbar, long long *trace) {
+    unsigned *gbar, long long *trace, const double2 *vh0) {
+  // vh0 != nullptr: Jacobi PCG (reading G12b), as k_cg_toep2_persist
   extern __shared__ __align__(16) double2 dsm[];
   __shared__ double sh[40];
   // optional phase timing (EFGP_CG_TRACE), thread 0, cycles summed over iterations: 0 p + T, 2 W,
@@ -1292,10 +1325,30 @@ __global__ void __launch_bounds__(kDftThreads, 1) k_cg_dft2_persist(
   unsigned target = 0;
   const double invL = 1.0 / (double)L;
   __syncthreads();
+  const bool jac = vh0 != nullptr;
+  const double v0 = jac ? vh0->x : 0.0;
+  auto inv_diag = [&](int i) { const double d = ds[i]; return 1.0 / (d * d * v0 + s2); };
+  double rz = 0.0;  // Jacobi: (r, z) in one fixed order (k2-major), the same in every CTA
+  if (jac) {
+    double a = 0.0;
+    for (int i = t; i < Mh; i += kDftThreads) {
+      const double2 rq = rs[i];
+      a += (i >= n ? 2.0 : 1.0) * (rq.x * rq.x + rq.y * rq.y) * inv_diag(i);
+    }
+    a = block_sum(a, sh);
+    if (t == 0) sh[34] = a;
+    __syncthreads();
+    rz = sh[34];
+  }
   for (;;) {
     // ---- phase 1: p_j; T and W of this CTA's columns
     for (int i = t; i < Mh; i += kDftThreads) {
-      const double2 rq = rs[i], po = ps[i];
+      double2 rq = rs[i];
+      if (jac) {
+        const double w = inv_diag(i);
+        rq = make_double2(rq.x * w, rq.y * w);  // z = M^-1 r
+      }
+      const double2 po = ps[i];
       ps[i] = make_double2(rq.x + beta * po.x, rq.y + beta * po.y);
     }
     __syncthreads();
@@ -1437,7 +1490,7 @@ __global__ void __launch_bounds__(kDftThreads, 1) k_cg_dft2_persist(
     TRD(5);
     // ---- phase 3 (every CTA): alpha, r and ||r||^2 (all entries, k2-major order), x (owned entries);
     // all of its L2 loads are issued before the first use (M_h <= kDftPer x 256)
-    double acc = 0.0;
+    double acc = 0.0, accz = 0.0;
     double alpha;
     {
       double2 av[kDftPer];
@@ -1450,7 +1503,7 @@ __global__ void __launch_bounds__(kDftThreads, 1) k_cg_dft2_persist(
       v = block_sum(v, sh);
       if (t == 0) sh[32] = v;
       __syncthreads();
-      alpha = rr / sh[32];
+      alpha = (jac ? rz : rr) / sh[32];
 #pragma unroll
       for (int k = 0; k < kDftPer; ++k) {
         const int i = t + k * kDftThreads;
@@ -1459,7 +1512,9 @@ __global__ void __launch_bounds__(kDftThreads, 1) k_cg_dft2_persist(
           rq.x -= alpha * av[k].x;
           rq.y -= alpha * av[k].y;
           rs[i] = rq;
-          acc += (i >= n ? 2.0 : 1.0) * (rq.x * rq.x + rq.y * rq.y);  // k2 = i / n > 0 weighs 2
+          const double e = (i >= n ? 2.0 : 1.0) * (rq.x * rq.x + rq.y * rq.y);  // k2 = i / n > 0 weighs 2
+          acc += e;
+          if (jac) accz += e * inv_diag(i);
           if (i >= own_lo && i < own_hi) {
             xs[i - own_lo].x += alpha * ps[i].x;
             xs[i - own_lo].y += alpha * ps[i].y;
@@ -1471,9 +1526,17 @@ __global__ void __launch_bounds__(kDftThreads, 1) k_cg_dft2_persist(
     if (t == 0) sh[33] = acc;
     __syncthreads();
     const double rr_new = sh[33];
+    if (jac) {
+      accz = block_sum(accz, sh);
+      if (t == 0) sh[35] = accz;
+      __syncthreads();
+      const double rz_new = sh[35];
+      beta = rz_new / rz;
+      rz = rz_new;
+    }
     TRD(3);
     ++it;
-    beta = rr_new / rr;
+    if (!jac) beta = rr_new / rr;
     const double rr_prev = rr;
     rr = rr_new;
     const double rel = sqrt(rr_new) / bnorm;
@@ -1542,7 +1605,7 @@ efgp_status dft2_setup(efgp_plan *pl, cudaStream_t s) {
   return EFGP_OK;
 }
 
-static cudaError_t launch_dft2_cg(efgp_plan *pl, CGState *st, cudaStream_t s) {
+static cudaError_t launch_dft2_cg(efgp_plan *pl, CGState *st, cudaStream_t s, const double2 *vh0 = nullptr) {
   const Params &P = pl->P;
   const int m = (int)P.m, n = 2 * m + 1, L = (int)P.L;
   int dev = 0, coop = 0;
@@ -1583,7 +1646,7 @@ static cudaError_t launch_dft2_cg(efgp_plan *pl, CGState *st, cudaStream_t s) {
   }
   void *args[] = {(void *)&Vt, (void *)&roots, (void *)&Dh, (void *)&x, (void *)&r, (void *)&p0, (void *)&Ap,
                   (void *)&Wg, (void *)&mm, (void *)&LL, (void *)&st, (void *)&part, (void *)&hist, (void *)&gbar,
-                  (void *)&trace};
+                  (void *)&trace, (void *)&vh0};
   e = cudaLaunchCooperativeKernel((const void *)k_cg_dft2_persist, dim3((unsigned)G), dim3(kDftThreads), args, smem, s);
   if (want_trace && e == cudaSuccess) {
     std::vector<long long> h((size_t)8 * G);
@@ -1727,7 +1790,7 @@ static bool cg_persist() {
 
 // One cooperative launch runs the whole CG (returns cudaErrorNotSupported when the grid cannot be
 // co-resident: the caller then takes the launched path).
-static cudaError_t launch_persist_cg(efgp_plan *pl, CGState *st, cudaStream_t s) {
+static cudaError_t launch_persist_cg(efgp_plan *pl, CGState *st, cudaStream_t s, const double2 *vh0 = nullptr) {
   const Params &P = pl->P;
   const int m = (int)P.m, n = 2 * m + 1;
   int dev = 0, coop = 0;
@@ -1768,7 +1831,7 @@ static cudaError_t launch_persist_cg(efgp_plan *pl, CGState *st, cudaStream_t s)
     }
     void *args[] = {(void *)&vfull, (void *)&Dh, (void *)&x, (void *)&r, (void *)&p0, (void *)&ap0, (void *)&ap1,
                     (void *)&m, (void *)&nsplit, (void *)&st, (void *)&tpart, (void *)&tcnt, (void *)&part_pAp,
-                    (void *)&hist, (void *)&gbar, (void *)&trace};
+                    (void *)&hist, (void *)&gbar, (void *)&trace, (void *)&vh0};
     pl->cg_persist_split = nsplit;
     e = cudaLaunchCooperativeKernel((const void *)k_cg_toep2_persist, dim3((unsigned)(n * nsplit)),
                                     dim3(kPersistThreads), args, smem, s);
@@ -2219,6 +2282,35 @@ static efgp_status pcg_solve_d(efgp_plan *pl, int64_t N_total) {
   EFGP_CUDA(cudaMemcpyAsync(st, &init, sizeof(CGState), cudaMemcpyHostToDevice, s));
   k_cg_init<<<nb, kCGThreads, 0, s>>>(pl->b, pl->x, pl->r, pl->p, P.Mh, (int)P.m, pl->partials);
   k_cg_init2<<<1, kCGThreads, 0, s>>>(st, pl->partials, (int)nb, pl->hist);
+  pl->cg_persist_split = 0;
+  pl->cg_dft2 = 0;
+  if (D == 2 && P.precond == EFGP_PRECOND_JACOBI && cg_persist()) {
+    // Jacobi PCG in the persistent 2D kernels (z = r / (D^2 v_0 + sigma^2) formed in place)
+    const double2 *vh0 = reinterpret_cast<const double2 *>(pl->modes_sum) + (int64_t)(2 * P.m) * (2 * P.m + 1);
+    cudaError_t e = cudaErrorNotSupported;
+    if (toeplitz_direct(P) && pl->p2 && pl->toep_part) {
+      e = launch_persist_cg(pl, st, s, vh0);
+    } else if (toeplitz_dft2(P)) {
+      e = launch_dft2_cg(pl, st, s, vh0);
+      if (e == cudaSuccess) pl->cg_dft2 = 1;
+    }
+    if (e == cudaSuccess) {
+      CGState host{};
+      EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned, st, sizeof(CGState), cudaMemcpyDeviceToHost, s));
+      EFGP_CUDA(cudaStreamSynchronize(s));
+      std::memcpy(&host, pl->h_pinned, sizeof(CGState));
+      pl->iters = host.iter;
+      pl->rel_resid = host.bnorm > 0 ? std::sqrt(host.rr) / host.bnorm : 0.0;
+      return host.done == 2 ? EFGP_ERR_NOCONVERGE : EFGP_OK;
+    }
+    pl->cg_persist_split = 0;
+    pl->cg_dft2 = 0;
+    if (e != cudaErrorNotSupported && e != cudaErrorCooperativeLaunchTooLarge) {
+      pl->err = "persistent PCG launch failed";
+      return EFGP_ERR_CUDA;
+    }
+    cudaGetLastError();
+  }
   EFGP_TRY(precond_apply(pl, pl->r, pl->z, &st->done, s));          // z0 = M^-1 b
   k_pcg_dot<<<nb, kCGThreads, 0, s>>>(pl->r, pl->z, P.Mh, (int)P.m, st, part_rz);
   k_pcg_p<<<nb, kCGThreads, 0, s>>>(pl->z, pl->p, P.Mh, st, part_rz, (int)nb, 1);  // p0 = z0
