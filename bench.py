@@ -425,6 +425,18 @@ def main():
                        "iters_plain_cg": statistics.median(iters), "solve_ms": ip["t_solve_ms"],
                        "solve_ms_plain_cg": statistics.median(solve_ms),
                        "fit_ms": ip["t_spread_ms"] + ip["t_modes_ms"] + ip["t_solve_ms"], "wall_ms": wall}
+            if not args.no_variance:
+                # NEXT-2 on the preconditioned fit: the variance CGs follow the fit's preconditioner
+                qv = min(int(args.var_targets), xt.shape[0])
+                var = torch.empty(qv, dtype=torch.float64, device=dev)
+                mp.predict_var(xt[:qv], out=var)  # warm-up (buffers, graph)
+                mp.predict_var(xt[:qv], out=var)
+                iv = mp.info()
+                precond["posterior_variance"] = {
+                    "q": qv, "ms": iv["t_var_ms"], "targets_per_s": qv / (iv["t_var_ms"] / 1e3),
+                    "cg_iters_max": iv["var_iters_max"], "batch": iv["var_batch"],
+                    "cg_iters_max_plain_cg": (variance or {}).get("cg_iters_max")}
+                del var
             mp.close()
         except Exception as exc:
             precond = {"error": f"{type(exc).__name__}: {exc}"[:200]}

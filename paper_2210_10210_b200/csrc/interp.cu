@@ -6,6 +6,7 @@
 // dflags[1].
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "efgp_internal.cuh"
 
@@ -225,6 +226,149 @@ __global__ void __launch_bounds__(kIB, 1024 / kIB) k_interp2_banked(const double
   }
 }
 
+// 2D, C shifted copies of the staged grid, no bank-class overflow (r02b successor of k_interp2_banked).
+// The banked kernel gives each of the 16 lanes of a half-warp one first-cell bank class; a class with
+// more than its quota of a batch's targets spills them into other classes' slots, where every one of
+// their W^2 gathers conflicts (~7 % of targets, ~1.2 extra wavefronts per target at c5, r02 ncu).
+// Here the grid is staged C times, copy j at a shared offset = j R (mod 16) doubles (R = 16 / C), so a
+// target whose first cell is in bank class b can be read through bank class b + j R: only its residue
+// b mod R is fixed.  Target rank k of residue c goes to half-warp k / C, lane c + (k mod C) R, read from
+// the copy that maps its class onto that lane — the per-residue quota (C HW) is far above the batch's
+// mean count, so practically no target spills, and half-warps only run short at the tail.  The per
+// batch tables are triple-buffered so one CTA barrier per batch suffices: a batch's classification
+// (writes set it % 3, resets set (it + 1) % 3) overlaps the previous batch's gathers (reads set
+// (it - 1) % 3).  Same arithmetic per target as k_interp (bitwise-identical results).
+template <int W, int C, int T, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_interp2_copies(const double *__restrict__ xt, int64_t q,
+                                                                  const double *__restrict__ grid, int n, double h,
+                                                                  EsPoly P, int lo, int A, int Sg,
+                                                                  const double *__restrict__ sd,
+                                                                  double *__restrict__ mu, int *__restrict__ err) {
+  constexpr int R = 16 / C;   // residue classes
+  constexpr int QC = (NT / 16) * C;  // slots per residue class and batch
+  static_assert(16 % C == 0 && T <= NT && T <= 32767, "k_interp2_copies shape");
+  // dynamic shared memory: the C grid copies (copy j at j Sg doubles, Sg = R mod 16, Sg even), then
+  // the triple-buffered tables
+  extern __shared__ __align__(16) double sgrid[];
+  auto s_s = reinterpret_cast<double2 (*)[T]>(sgrid + (size_t)C * Sg);  // reduced coordinates by batch index
+  auto s_cell = reinterpret_cast<int (*)[T]>(s_s + 3);                   // first-cell offset in a copy
+  auto s_tbl = reinterpret_cast<short (*)[NT]>(s_cell + 3);              // slot -> batch index (-1: empty)
+  auto s_ovf = reinterpret_cast<short (*)[T]>(s_tbl + 3);                // targets beyond their residue's quota
+  __shared__ int s_cnt[3][R], s_novf[3], s_take[3];
+  const int tid = threadIdx.x;
+  for (int c = tid; c < A * A; c += NT) {
+    const int r = c / A, cc = c % A;
+    const double g = __ldg(grid + (int64_t)wrapn(r + lo, n) * n + wrapn(cc + lo, n));
+#pragma unroll
+    for (int j = 0; j < C; ++j) sgrid[j * Sg + c] = g;
+  }
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    s_tbl[p][tid] = -1;
+    if (tid < R) s_cnt[p][tid] = 0;
+    if (tid == 0) s_novf[p] = s_take[p] = 0;
+  }
+  __syncthreads();
+  const int64_t nb = (q + T - 1) / T;
+  const double2 *x2 = reinterpret_cast<const double2 *>(xt);
+  auto ld = [&](int64_t b) -> double2 {
+    const int64_t ii = b * T + tid;
+    return (tid < T && b < nb && ii < q) ? __ldg(x2 + ii) : make_double2(0.0, 0.0);
+  };
+  double2 xn = ld(blockIdx.x);
+  const int lane16 = tid & 15;
+  int it = 0;
+  for (int64_t bt = blockIdx.x; bt < nb; bt += gridDim.x, ++it) {
+    const int p = it % 3, pn = (it + 1) % 3;
+    const double2 xc = xn;
+    const int64_t i = bt * T + tid;
+    xn = ld(bt + gridDim.x);
+    // classify into set p; set pn (last read two batches ago) is cleared for the next batch
+    if (tid < R) s_cnt[pn][tid] = 0;
+    if (tid == 0) s_novf[pn] = s_take[pn] = 0;
+    if (tid < T && i < q) {
+      if (xc.x >= 0.0 && xc.x <= 1.0 && xc.y >= 0.0 && xc.y <= 1.0) {
+        double s0, s1;
+        const int b0 = es_reduce<W>(h * xc.x * (double)n, s0);
+        const int b1 = es_reduce<W>(h * xc.y * (double)n, s1);
+        s_s[p][tid] = make_double2(s0, s1);
+        const int cell = (b0 - lo) * A + (b1 - lo);
+        s_cell[p][tid] = cell;
+        const int c = cell & (R - 1);
+        const int k = atomicAdd(&s_cnt[p][c], 1);
+        if (k < QC) s_tbl[p][16 * (k / C) + c + (k % C) * R] = (short)tid;
+        else s_ovf[p][atomicAdd(&s_novf[p], 1)] = (short)tid;
+      } else {
+        mu[i] = __longlong_as_double(0x7ff8000000000000LL);
+        atomicOr(err + 1, 1);
+      }
+    }
+    __syncthreads();
+    // gathers from set p
+    int j = s_tbl[p][tid];
+    s_tbl[p][tid] = -1;  // (re-filled three batches on, after two more barriers)
+    if (j < 0) {
+      const int novf = s_novf[p];
+      if (novf > 0) {
+        const int t = atomicAdd(&s_take[p], 1);
+        if (t < novf) j = s_ovf[p][t];
+      }
+    }
+    if (j >= 0) {
+      const int cell = s_cell[p][j];
+      EFGP_DCHECK(j < T && cell >= 0 && cell + (W - 1) * (A + 1) < A * A);
+      double wt[2][W];
+      const double2 sj = s_s[p][j];
+      es_weights_s<W>(sj.x, P, wt[0]);
+      es_weights_s<W>(sj.y, P, wt[1]);
+      // the copy whose shift maps this cell's bank class onto this lane (exact for in-quota targets)
+      const int cp = ((lane16 - cell) & 15) / R;
+      const double *win = sgrid + cp * Sg + cell;
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < W; ++a) {
+        double ra = 0.0;
+#pragma unroll
+        for (int b = 0; b < W; ++b) ra = fma(win[a * A + b], wt[1][b], ra);
+        acc = fma(ra, wt[0][a], acc);
+      }
+      const int64_t ij = bt * T + j;
+      if (sd) {  // NEXT-3: w_n = (Phi p)_n / sigma_n^2 (reading G11)
+        const double sn = __ldg(sd + ij);
+        acc /= sn * sn;
+      }
+      mu[ij] = acc;
+    }
+  }
+}
+
+// dynamic shared bytes of the triple-buffered tables of k_interp2_copies<W, C, T, NT>
+template <int C, int T, int NT>
+constexpr size_t interp_copies_tables() {
+  return 3 * ((size_t)T * (16 + 4 + 2) + (size_t)NT * 2);
+}
+
+template <int W, int C, int T, int NT>
+static bool try_interp_copies(efgp_plan *pl, const double *grid, int n, const double *xt, int64_t q,
+                              const double *sd, double *mu, int lo, int A, cudaStream_t s) {
+  constexpr int R = 16 / C;
+  const int Sg = ((A * A + 15) / 16) * 16 + R;  // copy stride = R (mod 16) doubles (R even: 16-byte tables)
+  const size_t sb = (size_t)Sg * C * sizeof(double) + interp_copies_tables<C, T, NT>();
+  const size_t per_cta = sb + 1024;
+  const int ctas = 1024 / NT;
+  if (per_cta * ctas > 227 * 1024) return false;
+  if (cudaFuncSetAttribute(k_interp2_copies<W, C, T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  const int64_t nbt = (q + T - 1) / T;
+  const int64_t nblk = std::min<int64_t>(nbt, (int64_t)ctas * pl->num_sms);
+  k_interp2_copies<W, C, T, NT><<<(unsigned)nblk, NT, sb, s>>>(xt, q, grid, n, pl->P.h, pl->P.poly, lo, A, Sg, sd,
+                                                               mu, pl->dflags);
+  return true;
+}
+
 template <int D, int W>
 static efgp_status launch_interp(efgp_plan *pl, const double *grid, int n, const double *xt, int64_t q,
                                  const double *sd, double *mu, cudaStream_t s) {
@@ -234,6 +378,20 @@ static efgp_status launch_interp(efgp_plan *pl, const double *grid, int n, const
   for (int k = 1; k < D; ++k) cells *= o.A;
   const size_t sb = cells * sizeof(double);
   int64_t blocks = (q + 255) / 256;
+  if constexpr (D == 2) {
+    // many targets: shifted grid copies (EFGP_K9 = banked | c2 | c4 selects the variant for A/B runs)
+    const char *k9 = getenv("EFGP_K9");
+    const bool aligned = (reinterpret_cast<uintptr_t>(xt) & 15) == 0 && !getenv("EFGP_INTERP_PLAIN");
+    if (aligned && q >= (int64_t)pl->num_sms * 512 && !(k9 && !strcmp(k9, "banked"))) {
+      const bool c2 = k9 && !strcmp(k9, "c2");
+      const bool ok = c2 ? try_interp_copies<W, 2, 384, 512>(pl, grid, n, xt, q, sd, mu, o.lo, o.A, s)
+                         : try_interp_copies<W, 4, 768, 1024>(pl, grid, n, xt, q, sd, mu, o.lo, o.A, s);
+      if (ok) {
+        EFGP_CUDA(cudaGetLastError());
+        return EFGP_OK;
+      }
+    }
+  }
   if (D == 2 && q >= (int64_t)pl->num_sms * kIB && sb <= 160 * 1024 && (reinterpret_cast<uintptr_t>(xt) & 15) == 0 &&
       !getenv("EFGP_INTERP_PLAIN")) {
     // many targets: bank-aware order (1024 / kIB CTAs of kIB threads per SM, persistent over batches)

@@ -835,3 +835,46 @@ def test_one_cta_1d_cg_matches_launched(monkeypatch):
     assert g2.last_status == 1 and g2.info()["iters"] == 4 and len(g2.residual_history()) == 5
     g.close()
     g2.close()
+
+
+@pytest.mark.parametrize("eps", [1e-1, 1e-3, 1e-6])
+def test_type2_many_target_variants_bitwise(eps, monkeypatch):
+    # K9 for many 2D targets: the bank-aware kernel and the shifted-copy kernels (C = 2, C = 4) only
+    # change which thread evaluates which target, so every mu must equal the plain kernel's bit for bit
+    # (ragged last batch, invalid targets -> NaN + error flag); the plain kernel is checked against the
+    # oracle's direct sum on a sample
+    from paper_2210_10210_b200 import EFGP, EFGPError, full_to_half
+    m = 12
+    g = EFGP("matern", 0.1, 0.1, eps, 2, 1.5, m=m, h=0.4)
+    inf = g.info()
+    rng = np.random.default_rng(11)
+    full = rng.normal(size=(2 * m + 1,) * 2) + 1j * rng.normal(size=(2 * m + 1,) * 2)
+    full = 0.5 * (full + np.conj(full[::-1, ::-1]))
+    g.load_weights(full_to_half(full))
+    q = 148 * 1024 * 3 + 777
+    xt = rng.uniform(0, 1, (q, 2))
+    xt[[5, 1000, q - 1], 0] = 0.0
+    xt[[6, 2000], 1] = 1.0
+    out = {}
+    for v in ("plain", "banked", "c2", "c4"):
+        monkeypatch.delenv("EFGP_INTERP_PLAIN", raising=False)
+        monkeypatch.delenv("EFGP_K9", raising=False)
+        if v == "plain":
+            monkeypatch.setenv("EFGP_INTERP_PLAIN", "1")
+        else:
+            monkeypatch.setenv("EFGP_K9", v)
+        out[v] = g.predict(dev(xt)).cpu().numpy()
+    for v in ("banked", "c2", "c4"):
+        assert np.array_equal(out[v], out["plain"]), (v, int(np.sum(out[v] != out["plain"])))
+    D = O.spectral_weights("matern", 0.1, 2, 0.4, m, 1.5)
+    idx = np.concatenate([rng.choice(q, 400, replace=False), [5, 6, 1000, 2000, q - 1]])
+    ref = O.posterior_mean(full, D, 0.4, xt[idx])
+    assert rel(out["plain"][idx], ref) <= 5 * inf["nufft_tol"]
+    bad = xt.copy()
+    bad[[3, q // 2], 1] = 1.5
+    bad[q - 2, 0] = np.nan
+    monkeypatch.setenv("EFGP_K9", "c4")
+    monkeypatch.delenv("EFGP_INTERP_PLAIN", raising=False)
+    with pytest.raises(EFGPError, match="INVALID"):
+        g.predict(dev(bad))
+    g.close()
