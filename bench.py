@@ -560,6 +560,9 @@ def main():
             e2e = {"value": N / (float(te.item()) / 1e3), "unit": UNIT,
                    "h2d_bytes_per_step": int(xh.numel() * 8 + yh.numel() * 8 + th.numel() * 8) * world,
                    "d2h_bytes_per_step": int(muh.numel() * 8) * world}
+            # what bounds it: the host->device link (bytes per rank / step time)
+            e2e["h2d_GBps_per_gpu"] = (xh.numel() + yh.numel() + th.numel()) * 8 / (float(te.item()) / 1e3) / 1e9
+            e2e["ms_per_step"] = float(te.item())
             del xh, yh, th, muh
         except Exception as exc:  # pinned allocation of 24 GB can fail on small hosts
             e2e = {"value": None, "unit": UNIT, "error": f"{type(exc).__name__}: {exc}"[:200]}

@@ -383,9 +383,11 @@ static efgp_status launch_interp(efgp_plan *pl, const double *grid, int n, const
     const char *k9 = getenv("EFGP_K9");
     const bool aligned = (reinterpret_cast<uintptr_t>(xt) & 15) == 0 && !getenv("EFGP_INTERP_PLAIN");
     if (aligned && q >= (int64_t)pl->num_sms * 512 && !(k9 && !strcmp(k9, "banked"))) {
+      // C = 4, 896 targets per batch (r02 A/B at q = 2e8: 2.69 ms against 2.79 for 768 and 2.84 for the
+      // banked kernel; C = 2 with two CTAs per SM 2.89)
       const bool c2 = k9 && !strcmp(k9, "c2");
       const bool ok = c2 ? try_interp_copies<W, 2, 384, 512>(pl, grid, n, xt, q, sd, mu, o.lo, o.A, s)
-                         : try_interp_copies<W, 4, 768, 1024>(pl, grid, n, xt, q, sd, mu, o.lo, o.A, s);
+                         : try_interp_copies<W, 4, 896, 1024>(pl, grid, n, xt, q, sd, mu, o.lo, o.A, s);
       if (ok) {
         EFGP_CUDA(cudaGetLastError());
         return EFGP_OK;
