@@ -67,10 +67,13 @@ def _window(hist, tol):
 
 
 def _count_ok(k_g, k_o, hist_o, tol, perturbed):
-    """Readings G10 / G10b: +-2, or the oracle's crossing window, or the oracle's own perturbed range."""
+    """Readings G10 / G10b: +-2, or the oracle's crossing window, or (G10b) the span of the oracle's own
+    counts from exact inputs (k_o) to inputs carrying the NUFFT contract's error (the perturbed runs),
+    +-2: the GPU's type-1 error lies between the two."""
     lo, hi = _window(hist_o, tol)
     g10 = abs(k_g - k_o) <= 2 or lo <= k_g <= hi
-    g10b = bool(perturbed) and min(perturbed) - 2 <= k_g <= max(perturbed) + 2
+    span = list(perturbed) + [k_o]
+    g10b = bool(perturbed) and min(span) - 2 <= k_g <= max(span) + 2
     return g10, g10b, (lo, hi)
 
 
