@@ -14,9 +14,9 @@ and gates:
     4096 sampled entries, error relative to the oracle's norm);
   * parity mode: mu relative l2 over the config's targets <= 10 eps (north_star);
   * iteration counts (both modes): within +-2 of the oracle's, inside its [2 eps_cg, eps_cg/2]
-    crossing window (reading G10), or within +-2 of the range of first crossings the ORACLE itself
-    shows when v and F^*y carry an error of the size the NUFFT contract allows (reading G10b, counts
-    stored by tests/make_golden.py).  Gated in production mode; in parity mode (thousands of
+    crossing window (reading G10), or within +-2 of the span of first crossings the ORACLE itself
+    shows from exact v and F^*y to v and F^*y carrying an error of the size the NUFFT contract allows
+    (reading G10b, counts stored by tests/make_golden.py).  Gated in production mode; in parity mode (thousands of
     iterations on a plateaued residual) reported, with both residual histories, where it misses —
     there the mu gate is authoritative (reading G9).
 
