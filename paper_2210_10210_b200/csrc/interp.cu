@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kIB, 1024 / kIB) k_interp2_banked(const double
 // (writes set it % 3, resets set (it + 1) % 3) overlaps the previous batch's gathers (reads set
 // (it - 1) % 3).  Same arithmetic per target as k_interp (bitwise-identical results).
 template <int W, int C, int T, int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) k_interp2_copies(const double *__restrict__ xt, int64_t q,
+__global__ void __launch_bounds__(NT, (NT <= 512 ? 1024 / NT : 1)) k_interp2_copies(const double *__restrict__ xt, int64_t q,
                                                                   const double *__restrict__ grid, int n, double h,
                                                                   EsPoly P, int lo, int A, int Sg,
                                                                   const double *__restrict__ sd,
@@ -355,7 +355,7 @@ static bool try_interp_copies(efgp_plan *pl, const double *grid, int n, const do
   const int Sg = ((A * A + 15) / 16) * 16 + R;  // copy stride = R (mod 16) doubles (R even: 16-byte tables)
   const size_t sb = (size_t)Sg * C * sizeof(double) + interp_copies_tables<C, T, NT>();
   const size_t per_cta = sb + 1024;
-  const int ctas = 1024 / NT;
+  const int ctas = NT <= 512 ? 1024 / NT : 1;
   if (per_cta * ctas > 227 * 1024) return false;
   if (cudaFuncSetAttribute(k_interp2_copies<W, C, T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb) !=
       cudaSuccess) {
@@ -385,9 +385,10 @@ static efgp_status launch_interp(efgp_plan *pl, const double *grid, int n, const
     if (aligned && q >= (int64_t)pl->num_sms * 512 && !(k9 && !strcmp(k9, "banked"))) {
       // C = 4, 896 targets per batch (r02 A/B at q = 2e8: 2.69 ms against 2.79 for 768 and 2.84 for the
       // banked kernel; C = 2 with two CTAs per SM 2.89)
-      const bool c2 = k9 && !strcmp(k9, "c2");
-      const bool ok = c2 ? try_interp_copies<W, 2, 384, 512>(pl, grid, n, xt, q, sd, mu, o.lo, o.A, s)
-                         : try_interp_copies<W, 4, 896, 1024>(pl, grid, n, xt, q, sd, mu, o.lo, o.A, s);
+      const bool c2 = k9 && !strcmp(k9, "c2"), c4r = k9 && !strcmp(k9, "c4r");
+      const bool ok = c2    ? try_interp_copies<W, 2, 384, 512>(pl, grid, n, xt, q, sd, mu, o.lo, o.A, s)
+                      : c4r ? try_interp_copies<W, 4, 640, 768>(pl, grid, n, xt, q, sd, mu, o.lo, o.A, s)
+                            : try_interp_copies<W, 4, 896, 1024>(pl, grid, n, xt, q, sd, mu, o.lo, o.A, s);
       if (ok) {
         EFGP_CUDA(cudaGetLastError());
         return EFGP_OK;

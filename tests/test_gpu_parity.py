@@ -856,7 +856,7 @@ def test_type2_many_target_variants_bitwise(eps, monkeypatch):
     xt[[5, 1000, q - 1], 0] = 0.0
     xt[[6, 2000], 1] = 1.0
     out = {}
-    for v in ("plain", "banked", "c2", "c4"):
+    for v in ("plain", "banked", "c2", "c4", "c4r"):
         monkeypatch.delenv("EFGP_INTERP_PLAIN", raising=False)
         monkeypatch.delenv("EFGP_K9", raising=False)
         if v == "plain":
@@ -864,7 +864,7 @@ def test_type2_many_target_variants_bitwise(eps, monkeypatch):
         else:
             monkeypatch.setenv("EFGP_K9", v)
         out[v] = g.predict(dev(xt)).cpu().numpy()
-    for v in ("banked", "c2", "c4"):
+    for v in ("banked", "c2", "c4", "c4r"):
         assert np.array_equal(out[v], out["plain"]), (v, int(np.sum(out[v] != out["plain"])))
     D = O.spectral_weights("matern", 0.1, 2, 0.4, m, 1.5)
     idx = np.concatenate([rng.choice(q, 400, replace=False), [5, 6, 1000, 2000, q - 1]])

@@ -9,7 +9,7 @@ import warnings
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-VARIANTS = ("plain", "banked", "c2", "c4")
+VARIANTS = ("plain", "banked", "c2", "c4", "c4r")
 
 
 def set_variant(v):
