@@ -250,11 +250,14 @@ namespace efgp {
 // spread.cu
 // s1 (optional): per-point strength-1 weight (NEXT-3 one-pass: 1/sigma_n^2); only the SORTED and CELLSORT
 // spreaders take it — elsewhere EFGP_ERR_RESOURCE (the caller spreads the two strengths separately)
+// raw_minbits (optional, with s1): y and s1 are the RAW observations y_n and noise sds sigma_n; the SORTED
+// kernel validates sigma_n (dflags[2]), takes min sigma_n into *raw_minbits (IEEE bits, preset to ~0)
+// and forms the two strengths itself — no prep pass and no N-sized temporaries; SORTED only
 efgp_status spread_points(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s,
-                          const double *s1 = nullptr);
+                          const double *s1 = nullptr, unsigned long long *raw_minbits = nullptr);
 efgp_status spread_begin(efgp_plan *pl, cudaStream_t s);
 efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s,
-                           const double *s1 = nullptr);
+                           const double *s1 = nullptr, unsigned long long *raw_minbits = nullptr);
 // spread_cellsort.cu: K1 CELLSORT (2D any W, 3D W <= 6); EFGP_ERR_RESOURCE if not applicable
 // w1 (optional): per-point weight of the strength-1 grid (default 1): the heteroskedastic TOEPLITZ
 // solver spreads (1/sigma_n^2, y_n/sigma_n^2) in one pass

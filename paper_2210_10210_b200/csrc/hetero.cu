@@ -562,34 +562,71 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
   pl->t2_valid = false;  // the type-2 grid is rebuilt from beta by the next predict
   // G11b route: the weighted Toeplitz system, where the y spreading grid is the v grid (n_rhs = n1)
   const bool tz = P.hetero_method != EFGP_HETERO_NUFFT && P.n_rhs == P.n1;
+  // SORTED one-pass route: the spreading kernel reads the raw (y_n, sigma_n), validates sigma_n, takes
+  // min sigma_n and forms the strengths 1/sigma_n^2, y_n/sigma_n^2 in its balanced pass 2 — no prep
+  // pass (32 B/point of HBM traffic) and no N-sized temporaries.  Every other route preps first.
+  const bool raw = tz && P.spread_method == EFGP_SPREAD_SORTED;
   double *w = nullptr, *iv = nullptr;
-  EFGP_PALLOC(&w, sizeof(double) * N, s);
-  if (tz) EFGP_PALLOC(&iv, sizeof(double) * N, s);
   unsigned long long *minbits = reinterpret_cast<unsigned long long *>(pl->scal + 24);
+  int flags[4] = {0, 0, 0, 0};
+  unsigned long long mb = 0;
   EFGP_CUDA(cudaEventRecord(pl->ev[0], s));
   EFGP_CUDA(cudaMemsetAsync(minbits, 0xff, sizeof(unsigned long long), s));
-  EFGP_CUDA(cudaMemsetAsync(pl->dflags + 2, 0, sizeof(int), s));
-  k_het_prep<<<grid_for(N, pl->num_sms), 256, 0, s>>>(y, sd, N, w, minbits, pl->dflags, iv);
-  EFGP_CUDA(cudaGetLastError());
-  int flags[4];
-  unsigned long long mb = 0;
-  EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned, pl->dflags, sizeof(int) * 4, cudaMemcpyDeviceToHost, s));
-  EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned + 8, minbits, sizeof(mb), cudaMemcpyDeviceToHost, s));
-  EFGP_CUDA(cudaStreamSynchronize(s));
-  std::memcpy(flags, pl->h_pinned, sizeof(flags));
-  std::memcpy(&mb, pl->h_pinned + 8, sizeof(mb));
-  efgp_status st = EFGP_OK;
-  if (flags[2]) {
-    pl->err = "fit_hetero: every noise standard deviation must be finite and > 0";
-    st = EFGP_ERR_INVALID;
-  }
+  auto prep = [&]() -> efgp_status {  // w = y / sigma^2 (and iv = 1 / sigma^2), sigma_n checked, min sigma_n
+    EFGP_PALLOC(&w, sizeof(double) * N, s);
+    if (tz) EFGP_PALLOC(&iv, sizeof(double) * N, s);
+    EFGP_CUDA(cudaMemsetAsync(minbits, 0xff, sizeof(unsigned long long), s));
+    EFGP_CUDA(cudaMemsetAsync(pl->dflags + 2, 0, sizeof(int), s));
+    k_het_prep<<<grid_for(N, pl->num_sms), 256, 0, s>>>(y, sd, N, w, minbits, pl->dflags, iv);
+    EFGP_CUDA(cudaGetLastError());
+    EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned, pl->dflags, sizeof(int) * 4, cudaMemcpyDeviceToHost, s));
+    EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned + 8, minbits, sizeof(mb), cudaMemcpyDeviceToHost, s));
+    EFGP_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(flags, pl->h_pinned, sizeof(flags));
+    std::memcpy(&mb, pl->h_pinned + 8, sizeof(mb));
+    if (flags[2]) {
+      pl->err = "fit_hetero: every noise standard deviation must be finite and > 0";
+      return EFGP_ERR_INVALID;
+    }
+    return EFGP_OK;
+  };
+  auto free_tmp = [&]() {
+    if (w) cudaFreeAsync(w, s);
+    if (iv) cudaFreeAsync(iv, s);
+    w = iv = nullptr;
+  };
+  efgp_status st = raw ? EFGP_OK : prep();
   if (st == EFGP_OK && tz) {
     // v^w (J_2m) from strengths 1/sigma_n^2 and F^*(y/sigma^2) (J_m), both spread as the "y" strength
     // onto the v grid, then the homoskedastic Toeplitz machinery with sigma^2 -> 1 (reading G11b)
     double2 *vh = reinterpret_cast<double2 *>(pl->modes_sum), *fyh = vh + P.Kvh;
     bool one_pass = false;
-    if (P.spread_method == EFGP_SPREAD_CELLSORT || P.spread_method == EFGP_SPREAD_SORTED) {
-      // SORTED (weighted one-pass mode) and CELLSORT spread both weighted strengths in one pass:
+    if (raw) {
+      st = spread_begin(pl, s);  // clears dflags[0..3]
+      if (st == EFGP_OK) st = spread_points(pl, x, y, N, s, sd, minbits);
+      if (st == EFGP_OK) {
+        one_pass = true;
+        st = type1_modes(pl, pl->modes_sum, s);
+        EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned, pl->dflags, sizeof(int) * 4, cudaMemcpyDeviceToHost, s));
+        EFGP_CUDA(cudaMemcpyAsync(pl->h_pinned + 8, minbits, sizeof(mb), cudaMemcpyDeviceToHost, s));
+        EFGP_CUDA(cudaStreamSynchronize(s));
+        std::memcpy(flags, pl->h_pinned, sizeof(flags));
+        std::memcpy(&mb, pl->h_pinned + 8, sizeof(mb));
+        if (st == EFGP_OK && flags[2]) {
+          pl->err = "fit_hetero: every noise standard deviation must be finite and > 0";
+          st = EFGP_ERR_INVALID;
+        } else if (st == EFGP_OK && flags[0]) {
+          pl->err = "fit_hetero: a coordinate is outside [0,1] or non-finite, or an observation is non-finite";
+          st = EFGP_ERR_INVALID;
+        }
+      } else if (st == EFGP_ERR_RESOURCE) {
+        // (unaligned inputs, no co-residency, 2^32 points and more in one call): prep, then the
+        // two-pass route below
+        pl->err.clear();
+        st = prep();
+      }
+    } else if (P.spread_method == EFGP_SPREAD_CELLSORT) {
+      // CELLSORT spreads both weighted strengths in one pass:
       // g1 = sum (1/sigma^2) phi (v^w), g2 = sum (y/sigma^2) phi, then the standard K2 for both
       st = spread_begin(pl, s);
       if (st == EFGP_OK) st = spread_points(pl, x, w, N, s, iv);
@@ -671,8 +708,7 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
       }
       if (st == EFGP_ERR_NOCONVERGE) pl->err = "CG reached max_iter before the relative residual reached cg_tol";
     }
-    cudaFreeAsync(w, s);
-    if (iv) cudaFreeAsync(iv, s);
+    free_tmp();
     EFGP_CUDA(cudaStreamSynchronize(s));
     return st;
   }
@@ -753,8 +789,7 @@ efgp_status fit_hetero_device(efgp_plan *pl, const double *x, const double *y, c
     }
     if (st == EFGP_ERR_NOCONVERGE) pl->err = "CG reached max_iter before the relative residual reached cg_tol";
   }
-  cudaFreeAsync(w, s);
-  if (iv) cudaFreeAsync(iv, s);
+  free_tmp();
   EFGP_CUDA(cudaStreamSynchronize(s));
   return st;
 }

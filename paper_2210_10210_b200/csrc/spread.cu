@@ -273,13 +273,14 @@ efgp_status spread_begin(efgp_plan *pl, cudaStream_t s) {
 }
 
 efgp_status spread_points(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s,
-                          const double *s1) {
+                          const double *s1, unsigned long long *raw_minbits) {
   if (N <= 0) return EFGP_OK;
   int method = pl->P.spread_method;
   if (s1) {  // weighted strength 1: the SORTED kernel's one-pass mode, or CELLSORT; nothing else
     if (method == EFGP_SPREAD_SORTED && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
                                           reinterpret_cast<uintptr_t>(s1)) & 15) == 0)
-      return spread_sorted2(pl, x, y, N, s, s1);
+      return spread_sorted2(pl, x, y, N, s, s1, raw_minbits);
+    if (raw_minbits) return EFGP_ERR_RESOURCE;  // raw (y, sigma_n) strengths: the SORTED kernel only
     if (method == EFGP_SPREAD_CELLSORT) return spread_cellsort(pl, x, y, N, s, s1);
     return EFGP_ERR_RESOURCE;
   }

@@ -255,6 +255,9 @@ __device__ __forceinline__ void load_floats(const unsigned char *sp, float (&f)[
 struct FusedArgs {
   const double *x, *y;
   const double *s1;    // kModeF64W: per-point strength-1 weight (NEXT-3: 1/sigma_n^2), else nullptr
+  int wraw;            // kModeF64W: y is the raw observation and s1 the raw noise sd sigma_n; the kernel
+                       // validates sigma_n (err[2]), takes min sigma_n (minbits) and weights in pass 2
+  unsigned long long *minbits;  // wraw: min sigma_n as IEEE bits (ordered like the value for sigma_n > 0)
   int64_t N, chunk;
   int nchunks, nbuf;
   int debug;           // diagnostics (EFGP_SORTED_DEBUG): 1 = accumulators skip their work
@@ -399,6 +402,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
 #else
 #define BT(i)
 #endif
+  [[maybe_unused]] unsigned long long sdmin = ~0ull;  // wraw: this lane's min sigma_n (IEEE bits)
   for (int64_t i = 0;; ++i) {
     const int64_t b = gw + i * nw;
     // every warp walks the chunks in order; a warp with no batch left in a chunk still enters it
@@ -429,19 +433,28 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     // (written as independent predicated steps so the 8 points of a lane overlap their latencies)
     double2 pv[kWBatch / 32];
     double yvv[kWBatch / 32];
+    unsigned sdbad = 0;  // wraw: bit q = sigma_n of point q is not a finite positive number
 #pragma unroll
     for (int q = 0; q < kWBatch / 32; ++q) {
       const int j = min(q * 32 + lane, nb - 1);
       pv[q] = xs2[j];
       yvv[q] = ys[j];
+      if (WGT && A.wraw) {
+        const double sdv = s1s[j];
+        const bool sok = sdv > 0.0 && isfinite(sdv);
+        sdbad |= sok ? 0u : 1u << q;
+        const unsigned long long sb = (unsigned long long)__double_as_longlong(sdv);
+        if (sok && sb < sdmin) sdmin = sb;
+      }
     }
     bool bad = false;
     int ci[kWBatch / 32];
 #pragma unroll
     for (int q = 0; q < kWBatch / 32; ++q) {
       const bool in = q * 32 + lane < nb;
-      const bool ok = pv[q].x >= 0.0 && pv[q].x <= 1.0 && pv[q].y >= 0.0 && pv[q].y <= 1.0 && isfinite(yvv[q]);
+      bool ok = pv[q].x >= 0.0 && pv[q].x <= 1.0 && pv[q].y >= 0.0 && pv[q].y <= 1.0 && isfinite(yvv[q]);
       bad |= in && !ok;
+      if (WGT) ok = ok && !((sdbad >> q) & 1u);  // a point with an invalid sigma_n is dropped (the fit fails)
       const double2 p = ok ? pv[q] : make_double2(0.0, 0.0);
       const int r = rowt[start_cell<W>(grid_t(A.h, p.x, A.n1)) - A.s_lo];
       const int c = colt[start_cell<W>(grid_t(A.h, p.y, A.n1)) - A.s_lo];
@@ -452,6 +465,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
 #pragma unroll
     for (int q = 0; q < kWBatch / 32; ++q) rk[q] = tk[q] >= 0 ? atomicAdd(&wcnt[ci[q]], 1) : 0;
     if (bad) atomicOr(A.err, 1);
+    if (WGT && sdbad) atomicOr(A.err + 2, 1);
     __syncwarp();
     BT(2);
     // warp scan of the per-tile counts -> slot offsets; reserve room in the CTA's segments.  A lane's
@@ -535,12 +549,27 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       for (int slot = lane; slot < nv; slot += 32) {  // kept out of the hot loop above
         const int v = perm[slot];
         const int j = v & 0xFF, t = v >> 16;
-        if (slot >= wlim[t])
-          spread_point_red<W>(xs2[j].x, xs2[j].y, ys[j], A.h, A.n1, A.poly_dev, A.g1, A.gy, WGT ? s1s[j] : 1.0);
+        if (slot >= wlim[t]) {
+          double yo = ys[j], wo = WGT ? s1s[j] : 1.0;
+          if (WGT && A.wraw) {  // the strengths of pass 2, same roundings
+            const double v = wo * wo;
+            wo = 1.0 / v;
+            yo = yo / v;
+          }
+          spread_point_red<W>(xs2[j].x, xs2[j].y, yo, A.h, A.n1, A.poly_dev, A.g1, A.gy, wo);
+        }
       }
     }
     __syncwarp();  // stage s consumed
     issue(i + kWStages);
+  }
+  if (WGT && A.wraw) {  // min sigma_n over this warp's points (P:1766's iteration cap uses min sigma_n, G11)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long t = __shfl_xor_sync(0xffffffffu, sdmin, o);
+      sdmin = t < sdmin ? t : sdmin;
+    }
+    if (lane == 0 && sdmin != ~0ull) atomicMin(A.minbits, sdmin);
   }
 #if EFGP_SORTED_BTRACE
   if (A.trace && lane == 0) {
@@ -579,6 +608,7 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
   const int VG = G * kAccGroups, vb = blockIdx.x * kAccGroups + gi;  // virtual CTA
   if (R <= 0) __trap();  // the host never launches without a round (sorted_geometry checks)
   const double h = A.h;
+  [[maybe_unused]] const bool wraw = A.wraw != 0;
   unsigned char *gsm = sm + gi * AccSmem<W, MODE>::bytes(R, ntiles, G, T1, T2);
   double4 *raw = reinterpret_cast<double4 *>(gsm);                      // R records
   unsigned char *stage = reinterpret_cast<unsigned char *>(raw + R);    // R * SB, cell-sorted
@@ -706,7 +736,13 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
             double s1, s2;
             es_reduce<W>(grid_t(h, rv.x, n1), s1);
             es_reduce<W>(grid_t(h, rv.y, n1), s2);
-            reinterpret_cast<double4 *>(st)[0] = make_double4(s1, s2, rv.z, rv.w);  // (s1, s2, w, y)
+            double wz = rv.z, wy = rv.w;
+            if (wraw) {  // raw (sigma_n, y_n) -> strengths 1/sigma_n^2 and y_n/sigma_n^2 (k_het_prep's roundings)
+              const double v = rv.z * rv.z;
+              wz = 1.0 / v;
+              wy = rv.w / v;
+            }
+            reinterpret_cast<double4 *>(st)[0] = make_double4(s1, s2, wz, wy);  // (s1, s2, w, y)
           } else if constexpr (MODE == kModeF64) {
             // the reduced coordinates s1, s2 (es_reduce) are computed here, in the load-balanced
             // thread-per-record pass, instead of in phase C (thread per cell, Poisson-imbalanced)
@@ -1256,7 +1292,7 @@ static efgp_status launch_fused(efgp_plan *pl, const FusedArgs &A, cudaStream_t 
 }
 
 efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int64_t N, cudaStream_t s,
-                           const double *s1) {
+                           const double *s1, unsigned long long *raw_minbits) {
   const Params &P = pl->P;
   FusedArgs A{};
   A.x = x;
@@ -1295,6 +1331,8 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
   A.ntiles = P.ntiles;
   A.segcap = segcap;
   A.s1 = s1;
+  A.wraw = s1 && raw_minbits ? 1 : 0;
+  A.minbits = raw_minbits;
   A.R = s1 ? P.round_w : P.round;
   if (s1 && (P.spread_mode != kModeF64 || A.R < 256)) return EFGP_ERR_RESOURCE;  // caller: two passes
   for (int b = 0; b < kMaxNbuf; ++b) A.rec[b] = pl->rec[b];

@@ -257,3 +257,36 @@ def test_nufft_solver_reports_no_preconditioner():
     assert g.info()["precond"] == 0 and g.info()["hetero_sorted"] in (0, 1)
     assert np.all(np.isfinite(g.predict(dev(xt)).cpu().numpy()))
     g.close()
+
+
+def test_hetero_sorted_raw_one_pass_matches_prep_routes():
+    # SORTED reads the raw (y_n, sigma_n) and forms 1/sigma_n^2, y_n/sigma_n^2 in its own pass 2 (no prep
+    # pass); CELLSORT takes the prep kernel's strengths (one pass), and an unaligned sigma array makes
+    # SORTED fall back to prep + two passes.  Same strengths, same grids: the right-hand sides agree to the
+    # rounding of the fp64 atomics, the iteration cap (min sigma_n) exactly, mu to the parity gate.
+    import torch
+    c = CONFIGS["c5"]
+    N = 300_001
+    x, y, xt = generate(c, N=N, q=300)
+    sd = noise_sd(c, N, 11)
+    sd[777] = 0.25 * c.sigma                                        # a unique minimum
+    gs = model(c, cg_tol=c.eps / 1000, spread="sorted")
+    gs.fit_hetero(dev(x), dev(y), dev(sd))
+    assert gs.info()["spread_method"] == "sorted" and gs.info()["spread_fallback"] == "none"
+    gg = model(c, cg_tol=c.eps / 1000, spread="cellsort")
+    gg.fit_hetero(dev(x), dev(y), dev(sd))
+    assert gg.info()["spread_method"] == "cellsort"
+    bs, bg = gs.vector("rhs"), gg.vector("rhs")
+    assert rel(bs, bg) < 1e-12, rel(bs, bg)
+    assert gs.info()["max_iter"] == gg.info()["max_iter"]
+    mu_s = gs.predict(dev(xt)).cpu().numpy()
+    mu_g = gg.predict(dev(xt)).cpu().numpy()
+    assert rel(mu_s, mu_g) <= 10 * c.eps
+    # 8-byte-aligned (not 16) sigma: the bulk copies cannot take it -> prep + two passes, same answer
+    buf = torch.empty(N + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = torch.from_numpy(sd)
+    gs.fit_hetero(dev(x), dev(y), buf[1:])
+    assert rel(gs.vector("rhs"), bg) < 1e-12
+    assert gs.info()["max_iter"] == gg.info()["max_iter"]
+    gs.close()
+    gg.close()
