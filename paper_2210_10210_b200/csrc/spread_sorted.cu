@@ -31,6 +31,7 @@
 // Register budget: setmaxnreg moves registers from the binner warpgroup to the accumulators.
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstdlib>
 
 #include "efgp_internal.cuh"
@@ -259,6 +260,11 @@ struct FusedArgs {
                        // validates sigma_n (err[2]), takes min sigma_n (minbits) and weights in pass 2
   unsigned long long *minbits;  // wraw: min sigma_n as IEEE bits (ordered like the value for sigma_n > 0)
   int64_t N, chunk;
+  // ramp-down of the last chunks (in batches): batches >= tail_b0 fall into 5 chunks that halve in
+  // size (cut points tail_c[0..3] relative to tail_b0), so the accumulators' drain after the last
+  // binned chunk is a 1/16-size chunk instead of a full one; tail_b0 = INT64_MAX: uniform chunks
+  int64_t tail_b0, tail_c[4];
+  int tail_k0;
   int nchunks, nbuf;
   int debug;           // diagnostics (EFGP_SORTED_DEBUG): 1 = accumulators skip their work
   int own;             // 1: static tile ownership (CTA b accumulates tile b; ntiles <= grid)
@@ -406,7 +412,15 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
   for (int64_t i = 0;; ++i) {
     const int64_t b = gw + i * nw;
     // every warp walks the chunks in order; a warp with no batch left in a chunk still enters it
-    const int k = b < nbatch ? (int)(b / bpc) : A.nchunks;
+    int k = A.nchunks;
+    if (b < nbatch) {
+      if (b < A.tail_b0) {
+        k = (int)(b / bpc);
+      } else {
+        const int64_t r = b - A.tail_b0;
+        k = A.tail_k0 + (r >= A.tail_c[0]) + (r >= A.tail_c[1]) + (r >= A.tail_c[2]) + (r >= A.tail_c[3]);
+      }
+    }
     BT(5);
     if (k != cur) enter_chunk(k);
     BT(0);
@@ -1317,6 +1331,31 @@ efgp_status spread_sorted2(efgp_plan *pl, const double *x, const double *y, int6
   }
   A.chunk = chunk;
   A.nchunks = (int)((N + chunk - 1) / chunk);
+  A.tail_b0 = INT64_MAX;
+  {
+    // A run ends one chunk's accumulation after its last chunk is binned.  With few chunks that drain
+    // is a large share of the run, so the last C..2C batches are cut into chunks of 1/2, 1/4, 1/8,
+    // 1/16, 1/16 of that tail (the drain shrinks 8-16x for 4 more chunk hand-offs).  Measured (c5,
+    // profiles/r02_sorted_tail_ab.log): N = 4e7 1.44 -> 1.32 ms; N = 1e9 (30 chunks) 23.99 -> 24.16 ms
+    // and N = 1e6 0.09 -> 0.18 ms (a hand-off costs ~20 us), so it is on for at most 4 full chunks
+    // before the tail and pieces of >= 1M points.  EFGP_SORTED_TAIL=0 / 1: never / whenever the
+    // smallest piece has >= 16 batches (tests).
+    const int64_t C = chunk / kWBatch, nb = (N + kWBatch - 1) / kWBatch;
+    const char *e = std::getenv("EFGP_SORTED_TAIL");
+    const int force = e ? std::atoi(e) : -1;
+    if (force != 0 && !P.sorted_own && nb >= C && C > 0) {
+      const int64_t kf = nb / C - 1, Lt = nb - kf * C;  // Lt in [C, 2C)
+      if (force > 0 ? Lt / 16 >= 16 : (kf <= 3 && Lt / 16 >= 4096)) {
+        A.tail_b0 = kf * C;
+        A.tail_k0 = (int)kf;
+        A.tail_c[0] = Lt / 2;
+        A.tail_c[1] = Lt / 2 + Lt / 4;
+        A.tail_c[2] = A.tail_c[1] + Lt / 8;
+        A.tail_c[3] = A.tail_c[2] + Lt / 16;
+        A.nchunks = (int)kf + 5;
+      }
+    }
+  }
   A.nbuf = P.nbuf;
   A.debug = std::getenv("EFGP_SORTED_DEBUG") ? std::atoi(std::getenv("EFGP_SORTED_DEBUG")) : 0;
   A.own = P.sorted_own && P.ntiles <= P.tiles_grid;

@@ -144,10 +144,14 @@ def test_fp32_weights_refused_below_1e_6():
         model(c, spread="sorted", weights="fp32")
 
 
-@pytest.mark.parametrize("weights", ["fp64", "fp32", "mixed"])
+@pytest.mark.parametrize("weights", ["fp64", "fp32", "mixed", "fp64-tail"])
 def test_sorted_chunks_ragged_and_overflow(weights, monkeypatch):
     # many chunks with a ragged tail (small chunk), and a point cloud concentrated in one tile so the
     # tile lists overflow into the direct RED path: SORTED equals GLOBAL to roundoff
+    # ("fp64-tail": the halving chunks at the end of a run, forced on at this small size)
+    if weights == "fp64-tail":
+        weights = "fp64"
+        monkeypatch.setenv("EFGP_SORTED_TAIL", "1")
     c = CONFIGS["c5"]
     rng = np.random.default_rng(7)
     x_u, y_u, _ = generate(c, N=300_001, q=1)
