@@ -21,7 +21,7 @@
 
 namespace efgp {
 
-// w_n = y_n / sigma_n^2; raise dflags[2] for sigma_n <= 0 or non-finite; min sigma_n into *minbits
+// w_n = y_n * (1 / sigma_n^2); raise dflags[2] for sigma_n <= 0 or non-finite; min sigma_n into *minbits
 // (for positive doubles the IEEE bit pattern is ordered like the value)
 __global__ void k_het_prep(const double *__restrict__ y, const double *__restrict__ sd, int64_t N,
                            double *__restrict__ w, unsigned long long *__restrict__ minbits, int *__restrict__ err,
@@ -32,8 +32,11 @@ __global__ void k_het_prep(const double *__restrict__ y, const double *__restric
     const double s = sd[i];
     const bool ok = s > 0.0 && isfinite(s);
     bad |= !ok;
-    w[i] = ok ? y[i] / (s * s) : 0.0;
-    if (iv) iv[i] = ok ? 1.0 / (s * s) : 0.0;
+    // y_n * rcp(sigma_n^2): one IEEE reciprocal and a product — the roundings of the SORTED kernel's
+    // pass 2, which forms the same two strengths from the raw (y_n, sigma_n)
+    const double r = ok ? __drcp_rn(s * s) : 0.0;
+    w[i] = ok ? y[i] * r : 0.0;
+    if (iv) iv[i] = r;
     if (ok) {
       const unsigned long long b = (unsigned long long)__double_as_longlong(s);
       lmin = b < lmin ? b : lmin;

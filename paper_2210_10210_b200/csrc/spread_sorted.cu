@@ -566,9 +566,8 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
         if (slot >= wlim[t]) {
           double yo = ys[j], wo = WGT ? s1s[j] : 1.0;
           if (WGT && A.wraw) {  // the strengths of pass 2, same roundings
-            const double v = wo * wo;
-            wo = 1.0 / v;
-            yo = yo / v;
+            wo = __drcp_rn(wo * wo);
+            yo = yo * wo;
           }
           spread_point_red<W>(xs2[j].x, xs2[j].y, yo, A.h, A.n1, A.poly_dev, A.g1, A.gy, wo);
         }
@@ -751,10 +750,9 @@ __device__ void accumulator_role(const FusedArgs &A, unsigned char *sm, int tid_
             es_reduce<W>(grid_t(h, rv.x, n1), s1);
             es_reduce<W>(grid_t(h, rv.y, n1), s2);
             double wz = rv.z, wy = rv.w;
-            if (wraw) {  // raw (sigma_n, y_n) -> strengths 1/sigma_n^2 and y_n/sigma_n^2 (k_het_prep's roundings)
-              const double v = rv.z * rv.z;
-              wz = 1.0 / v;
-              wy = rv.w / v;
+            if (wraw) {  // raw (sigma_n, y_n) -> strengths 1/sigma_n^2 and y_n/sigma_n^2 (k_het_prep's roundings: y_n * rcp(sigma_n^2))
+              wz = __drcp_rn(rv.z * rv.z);  // one IEEE reciprocal, then a product (k_het_prep: the same)
+              wy = rv.w * wz;
             }
             reinterpret_cast<double4 *>(st)[0] = make_double4(s1, s2, wz, wy);  // (s1, s2, w, y)
           } else if constexpr (MODE == kModeF64) {
