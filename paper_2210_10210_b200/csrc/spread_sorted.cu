@@ -328,15 +328,16 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
   // per tile, for this batch: the record offset of batch slot 0 in the tile's list buffer (segment
   // start + reserved base - slot base; a record index, < 2^31 by the host's check) and the slot bound
   // (slot < wlim <=> the record fits the segment): the copy-out's address is one add per point
-  int *woff = wloc + ntiles;                                          // ntiles
-  int *wlim = woff + ntiles;                                          // ntiles
+  int2 *wol = reinterpret_cast<int2 *>(wloc + ntiles);                // ntiles x (woff, wlim): one 8-byte load
   int *off = reinterpret_cast<int *>(sm + kBinWarps * wbytes);        // ntiles (CTA-shared)
   int *rowt = off + ntiles;                                           // S
   int *colt = rowt + A.S;                                             // S
   __shared__ __align__(8) uint64_t bar[kBinWarps][kWStages];
   for (int c = g; c < A.S; c += kBinThreads) {
-    rowt[c] = ((c / A.T1) * A.nt2) << 16 | (c % A.T1) * A.T2;
-    colt[c] = (c / A.T2) << 16 | (c % A.T2);
+    // (tile << 8 | cell-in-tile) split over the two tables: their SUM is the packed pair (the cell
+    // parts add to < T1 T2 <= 128: no carry into the tile bits), one add per point
+    rowt[c] = ((c / A.T1) * A.nt2) << 8 | (c % A.T1) * A.T2;
+    colt[c] = (c / A.T2) << 8 | (c % A.T2);
   }
   for (int t = g; t < ntiles; t += kBinThreads) off[t] = 0;
   for (int t = lane; t < ntiles; t += 32) wcnt[t] = 0;
@@ -472,9 +473,9 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       const double2 p = ok ? pv[q] : make_double2(0.0, 0.0);
       const int r = rowt[start_cell<W>(grid_t(A.h, p.x, A.n1)) - A.s_lo];
       const int c = colt[start_cell<W>(grid_t(A.h, p.y, A.n1)) - A.s_lo];
-      tk[q] = (in && ok) ? (((r >> 16) + (c >> 16)) << 8 | ((r & 0xFFFF) + (c & 0xFFFF))) : -1;
+      tk[q] = (in && ok) ? r + c : -1;
       EFGP_DCHECK(!(in && ok) || ((tk[q] >> 8) < ntiles && (tk[q] & 0xFF) < A.T1 * A.T2));
-      ci[q] = (r >> 16) + (c >> 16);
+      ci[q] = (r + c) >> 8;
     }
 #pragma unroll
     for (int q = 0; q < kWBatch / 32; ++q) rk[q] = tk[q] >= 0 ? atomicAdd(&wcnt[ci[q]], 1) : 0;
@@ -510,8 +511,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
         const int t = tb + u;
         if (t < te) {
           wloc[t] = run;
-          woff[t] = (t * G + (int)blockIdx.x) * A.segcap + wbv[u] - run;
-          wlim[t] = A.segcap - wbv[u] + run;
+          wol[t] = make_int2((t * G + (int)blockIdx.x) * A.segcap + wbv[u] - run, A.segcap - wbv[u] + run);
           wcnt[t] = 0;
           run += cnt[u];
         }
@@ -531,8 +531,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
         const int c = wcnt[t];
         wloc[t] = run;
         const int wb = c ? atomicAdd(&off[t], c) : 0;
-        woff[t] = (t * G + (int)blockIdx.x) * A.segcap + wb - run;
-        wlim[t] = A.segcap - wb + run;
+        wol[t] = make_int2((t * G + (int)blockIdx.x) * A.segcap + wb - run, A.segcap - wb + run);
         wcnt[t] = 0;
         run += c;
       }
@@ -549,12 +548,13 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     for (int slot = lane; slot < nv; slot += 32) {
       const int v = perm[slot];
       const int j = v & 0xFF, key = (v >> 8) & 0xFF, t = v >> 16;
-      EFGP_DCHECK(j < nb && t < ntiles && slot >= wloc[t] && woff[t] + slot >= (t * G + (int)blockIdx.x) * A.segcap);
+      const int2 ol = wol[t];
+      EFGP_DCHECK(j < nb && t < ntiles && slot >= wloc[t] && ol.x + slot >= (t * G + (int)blockIdx.x) * A.segcap);
       const double2 xx = xs2[j];
       const double yv = ys[j];
       const double s1v = WGT ? s1s[j] : 0.0;
-      if (slot < wlim[t])
-        st_v4(rec + (woff[t] + slot), xx.x, xx.y, WGT ? s1v : yv,
+      if (slot < ol.y)
+        st_v4(rec + (ol.x + slot), xx.x, xx.y, WGT ? s1v : yv,
               WGT ? yv : __longlong_as_double((long long)key));  // WGT: (x1, x2, w, y), start cell recomputed
       else
         ovf = true;
@@ -563,7 +563,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       for (int slot = lane; slot < nv; slot += 32) {  // kept out of the hot loop above
         const int v = perm[slot];
         const int j = v & 0xFF, t = v >> 16;
-        if (slot >= wlim[t]) {
+        if (slot >= wol[t].y) {
           double yo = ys[j], wo = WGT ? s1s[j] : 1.0;
           if (WGT && A.wraw) {  // the strengths of pass 2, same roundings
             wo = __drcp_rn(wo * wo);
