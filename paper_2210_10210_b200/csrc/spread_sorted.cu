@@ -488,6 +488,8 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     // reservations (shared atomics with a return value) issued back to back before any result is
     // used: a loop that used each atomic's result before issuing the next serialised kTper round trips
     int nv;
+    bool ovl = false;  // one of this lane's tiles overflows its segment in this batch (found here, per
+                       // tile, so the copy-out loop carries no per-record flag)
     if (tper <= kTper) {
       int cnt[kTper], wbv[kTper];
       int sum = 0;
@@ -505,6 +507,8 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       nv = __shfl_sync(0xffffffffu, incl, 31);
 #pragma unroll
       for (int u = 0; u < kTper; ++u) wbv[u] = cnt[u] ? atomicAdd(&off[tb + u], cnt[u]) : 0;
+#pragma unroll
+      for (int u = 0; u < kTper; ++u) ovl |= cnt[u] > 0 && wbv[u] + cnt[u] > A.segcap;
       int run = incl - sum;
 #pragma unroll
       for (int u = 0; u < kTper; ++u) {
@@ -531,6 +535,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
         const int c = wcnt[t];
         wloc[t] = run;
         const int wb = c ? atomicAdd(&off[t], c) : 0;
+        ovl |= c > 0 && wb + c > A.segcap;
         wol[t] = make_int2((t * G + (int)blockIdx.x) * A.segcap + wb - run, A.segcap - wb + run);
         wcnt[t] = 0;
         run += c;
@@ -543,7 +548,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       if (tk[q] >= 0) perm[wloc[tk[q] >> 8] + rk[q]] = (q * 32 + lane) | (tk[q] << 8);
     __syncwarp();
     BT(4);
-    bool ovf = false;
+    const bool any_ovf = __any_sync(0xffffffffu, ovl);
 #pragma unroll 4
     for (int slot = lane; slot < nv; slot += 32) {
       const int v = perm[slot];
@@ -553,13 +558,11 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       const double2 xx = xs2[j];
       const double yv = ys[j];
       const double s1v = WGT ? s1s[j] : 0.0;
-      if (slot < ol.y)
-        st_v4(rec + (ol.x + slot), xx.x, xx.y, WGT ? s1v : yv,
+      if (slot < ol.y)  // (record index >= 0: the unsigned sum widens in one instruction)
+        st_v4(rec + (unsigned)(ol.x + slot), xx.x, xx.y, WGT ? s1v : yv,
               WGT ? yv : __longlong_as_double((long long)key));  // WGT: (x1, x2, w, y), start cell recomputed
-      else
-        ovf = true;
     }
-    if (__any_sync(0xffffffffu, ovf)) {  // full segments (concentrated data): direct RED spreading,
+    if (any_ovf) {  // full segments (concentrated data): direct RED spreading,
       for (int slot = lane; slot < nv; slot += 32) {  // kept out of the hot loop above
         const int v = perm[slot];
         const int j = v & 0xFF, t = v >> 16;
