@@ -470,9 +470,11 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       bool ok = pv[q].x >= 0.0 && pv[q].x <= 1.0 && pv[q].y >= 0.0 && pv[q].y <= 1.0 && isfinite(yvv[q]);
       bad |= in && !ok;
       if (WGT) ok = ok && !((sdbad >> q) & 1u);  // a point with an invalid sigma_n is dropped (the fit fails)
-      const double2 p = ok ? pv[q] : make_double2(0.0, 0.0);
-      const int r = rowt[start_cell<W>(grid_t(A.h, p.x, A.n1)) - A.s_lo];
-      const int c = colt[start_cell<W>(grid_t(A.h, p.y, A.n1)) - A.s_lo];
+      // a rejected point keeps its coordinates; its (arbitrary) start cells are clamped into the tables
+      // (one unsigned min per dimension instead of four selects on the coordinates)
+      const unsigned smax = (unsigned)(A.S - 1);
+      const int r = rowt[min((unsigned)(start_cell<W>(grid_t(A.h, pv[q].x, A.n1)) - A.s_lo), smax)];
+      const int c = colt[min((unsigned)(start_cell<W>(grid_t(A.h, pv[q].y, A.n1)) - A.s_lo), smax)];
       tk[q] = (in && ok) ? r + c : -1;
       EFGP_DCHECK(!(in && ok) || ((tk[q] >> 8) < ntiles && (tk[q] & 0xFF) < A.T1 * A.T2));
       ci[q] = (r + c) >> 8;
