@@ -33,6 +33,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "efgp_internal.cuh"
 
@@ -492,11 +493,14 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
     int nv;
     bool ovl = false;  // one of this lane's tiles overflows its segment in this batch (found here, per
                        // tile, so the copy-out loop carries no per-record flag)
-    if (tper <= kTper) {
-      int cnt[kTper], wbv[kTper];
+    // (the trip count is a compile-time 6 or 8: c5's 169 tiles are 6 per lane, and two more predicated-off
+    // trips cost ~20 instructions per batch and lane in the role whose instruction count sets the pace)
+    auto scan_fixed = [&](auto kt) {
+      constexpr int KT = decltype(kt)::value;
+      int cnt[KT], wbv[KT];
       int sum = 0;
 #pragma unroll
-      for (int u = 0; u < kTper; ++u) {
+      for (int u = 0; u < KT; ++u) {
         cnt[u] = tb + u < te ? wcnt[tb + u] : 0;
         sum += cnt[u];
       }
@@ -508,12 +512,12 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       }
       nv = __shfl_sync(0xffffffffu, incl, 31);
 #pragma unroll
-      for (int u = 0; u < kTper; ++u) wbv[u] = cnt[u] ? atomicAdd(&off[tb + u], cnt[u]) : 0;
+      for (int u = 0; u < KT; ++u) wbv[u] = cnt[u] ? atomicAdd(&off[tb + u], cnt[u]) : 0;
 #pragma unroll
-      for (int u = 0; u < kTper; ++u) ovl |= cnt[u] > 0 && wbv[u] + cnt[u] > A.segcap;
+      for (int u = 0; u < KT; ++u) ovl |= cnt[u] > 0 && wbv[u] + cnt[u] > A.segcap;
       int run = incl - sum;
 #pragma unroll
-      for (int u = 0; u < kTper; ++u) {
+      for (int u = 0; u < KT; ++u) {
         const int t = tb + u;
         if (t < te) {
           wloc[t] = run;
@@ -522,6 +526,11 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
           run += cnt[u];
         }
       }
+    };
+    if (tper <= 6) {
+      scan_fixed(std::integral_constant<int, 6>{});
+    } else if (tper <= kTper) {
+      scan_fixed(std::integral_constant<int, kTper>{});
     } else {
       int sum = 0;
       for (int t = tb; t < te; ++t) sum += wcnt[t];
