@@ -210,6 +210,36 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 __device__ __forceinline__ void st_v4(double4 *p, double a, double b, double c, double d) {
   asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
+// shared-memory atomic add with a result, predicated (no branch around it): returns 0 without touching
+// memory when v == 0 / !pred.  The compiler's form of `v ? atomicAdd(p, v) : 0` is a BSSY / BRA / BSYNC
+// triple per atomic, which shows in the binner's per-batch chain.
+__device__ __forceinline__ int atoms_add_if_nz(int *p, int v) {
+  int r;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.s32 q, %2, 0;\n mov.s32 %0, 0;\n @q atom.shared.add.s32 %0, [%1], %2;\n}"
+      : "=r"(r)
+      : "r"(smem_u32(p)), "r"(v)
+      : "memory");
+  return r;
+}
+__device__ __forceinline__ int atoms_inc_if(int *p, bool pred) {
+  int r;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.s32 q, %2, 0;\n mov.s32 %0, 0;\n @q atom.shared.add.s32 %0, [%1], 1;\n}"
+      : "=r"(r)
+      : "r"(smem_u32(p)), "r"((int)pred)
+      : "memory");
+  return r;
+}
+// one step of an inclusive warp scan: x += (lane >= o ? x of lane - o : 0), the range test taken from the
+// shuffle's own predicate (no compare, no select, no predicate kept across the steps)
+__device__ __forceinline__ int scan_step_up(int x, int o) {
+  asm volatile(
+      "{\n .reg .pred q;\n .reg .s32 t;\n shfl.sync.up.b32 t|q, %0, %1, 0, 0xffffffff;\n @q add.s32 %0, %0, t;\n}"
+      : "+r"(x)
+      : "r"(o));
+  return x;
+}
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -481,7 +511,7 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       ci[q] = (r + c) >> 8;
     }
 #pragma unroll
-    for (int q = 0; q < kWBatch / 32; ++q) rk[q] = tk[q] >= 0 ? atomicAdd(&wcnt[ci[q]], 1) : 0;
+    for (int q = 0; q < kWBatch / 32; ++q) rk[q] = atoms_inc_if(&wcnt[ci[q]], tk[q] >= 0);  // (ci is a valid tile even for a rejected point)
     if (bad) atomicOr(A.err, 1);
     if (WGT && sdbad) atomicOr(A.err + 2, 1);
     __syncwarp();
@@ -506,13 +536,10 @@ __device__ void binner_role(const FusedArgs &A, unsigned char *sm, int g /* 0..1
       }
       int incl = sum;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
+      for (int o = 1; o < 32; o <<= 1) incl = scan_step_up(incl, o);
       nv = __shfl_sync(0xffffffffu, incl, 31);
 #pragma unroll
-      for (int u = 0; u < KT; ++u) wbv[u] = cnt[u] ? atomicAdd(&off[tb + u], cnt[u]) : 0;
+      for (int u = 0; u < KT; ++u) wbv[u] = atoms_add_if_nz(&off[tb + u], cnt[u]);
 #pragma unroll
       for (int u = 0; u < KT; ++u) ovl |= cnt[u] > 0 && wbv[u] + cnt[u] > A.segcap;
       int run = incl - sum;
