@@ -210,9 +210,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 __device__ __forceinline__ void st_v4(double4 *p, double a, double b, double c, double d) {
   asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
-// shared-memory atomic add with a result, predicated (no branch around it): returns 0 without touching
-// memory when v == 0 / !pred.  The compiler's form of `v ? atomicAdd(p, v) : 0` is a BSSY / BRA / BSYNC
-// triple per atomic, which shows in the binner's per-batch chain.
+// shared-memory atomic add with a result, skipped when v == 0 / !pred (returns 0 without touching memory).
+// Written as a predicated `atom.shared`; ptxas still emits the BSSY / BRA / BSYNC form around an ATOMS with
+// a result (same code as `v ? atomicAdd(p, v) : 0`), and unconditional atomics that add 0 measured slower
+// — kept as the one place where that choice is made.
 __device__ __forceinline__ int atoms_add_if_nz(int *p, int v) {
   int r;
   asm volatile(
